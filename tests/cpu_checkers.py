@@ -1,0 +1,258 @@
+"""ctypes bindings for the two CPU checkers (TEST INFRASTRUCTURE ONLY).
+
+  oracle()     -> oracle/liboracle.so       prefix ko_  (C restatement, oracle/ks_oracle.c)
+  reference()  -> oracle/_ref/libks_ref.so  prefix kr_  (the reference's own headers, unmodified)
+
+Both export the interface declared in oracle/ks_oracle_api.h, so one wrapper class drives
+either.  Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+ORACLE_DIR = ROOT / "oracle"
+
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+
+
+def _vec(a, n, dtype=np.float64):
+    out = np.ascontiguousarray(np.asarray(a, dtype=dtype).reshape(-1))
+    assert out.size == n, (out.size, n)
+    return out
+
+
+class CheckerError(RuntimeError):
+    pass
+
+
+class CpuChecker:
+    """One loaded checker library (`ko_` or `kr_` prefix)."""
+
+    def __init__(self, path: Path, prefix: str, kind: str):
+        self.kind = kind
+        self.path = Path(path)
+        self.lib = C.CDLL(str(path))
+        self.p = prefix
+        L = self.lib
+        VP = C.c_void_p
+
+        def fn(name, restype, *argtypes):
+            f = getattr(L, prefix + name)
+            f.restype = restype
+            f.argtypes = list(argtypes)
+            return f
+
+        self._last_error = fn("last_error", C.c_char_p)
+        self._create = fn("tsdf_create", VP, _f64p, C.c_int, C.c_int)
+        self._destroy = fn("tsdf_destroy", None, VP)
+        self._integrate = fn("integrate_depth", C.c_int, VP, _f32p, C.c_int, C.c_int, _f64p, _f64p, _f64p)
+        self._stamp_cuboid = fn("stamp_cuboid", C.c_int, VP, _f64p, _f64p, _f64p)
+        self._stamp_sphere = fn("stamp_sphere", C.c_int, VP, _f64p, C.c_double)
+        self._decay = fn("decay_weights", None, VP, C.c_int, C.c_int, _f64p, _f64p, _f64p)
+        self._recycle = fn("recycle_blocks", C.c_int, VP)
+        self._count = fn("allocated_block_count", C.c_int, VP)
+        self._available = fn("available", C.c_int, VP)
+        self._next_fresh = fn("next_fresh", C.c_int, VP)
+        self._slot_count = fn("slot_count", C.c_int, VP)
+        self._find = fn("find", C.c_int, VP, C.c_int, C.c_int, C.c_int)
+        self._free_list = fn("free_list", C.c_int, VP, _i32p, C.c_int)
+        self._export = fn("export_blocks", C.c_int, VP, _i32p, _i32p, C.c_int)
+        self._channels = fn("block_channels", None, VP, C.c_int, _f64p, _f64p, _f64p)
+        self._query_tsdf = fn("query_tsdf", None, VP, _f64p, C.c_int64, C.c_int, _f64p, _u8p)
+        self._seed_gather = fn("seed_gather", None, VP, _f64p, _i32p, C.c_double, _u8p)
+        self._seed_scatter = fn("seed_scatter", None, VP, _f64p, _i32p, C.c_double, _u8p)
+        self._propagate = fn("propagate", C.c_int, _u8p, C.c_int64, _i32p, C.c_double, _i32p, _f64p)
+        self._recover = fn("recover_signs", None, VP, _f64p, _i32p, C.c_double, C.c_int, _i32p, _f64p)
+        self._query_esdf = fn("query_esdf", None, _f64p, _i32p, C.c_double, C.c_int, _f64p, _f64p,
+                              C.c_int64, _f64p, _f64p, _u8p)
+
+    def last_error(self) -> str:
+        return (self._last_error() or b"").decode()
+
+    # --- TSDF ---------------------------------------------------------------------------
+    def make_tsdf(self, voxel_size=0.01, truncation=None, alpha_time=0.99, alpha_frustum=0.5,
+                  weight_threshold=0.5, capacity=8192, slot_count=0) -> "CheckerTsdf":
+        if truncation is None:
+            truncation = 4.0 * voxel_size
+        cfg = np.array([voxel_size, truncation, alpha_time, alpha_frustum, weight_threshold], np.float64)
+        handle = self._create(cfg, int(capacity), int(slot_count))
+        if not handle:
+            raise CheckerError(self.last_error())
+        return CheckerTsdf(self, handle, voxel_size, truncation, capacity)
+
+    # --- ESDF (stateless) ----------------------------------------------------------------
+    def propagate(self, mask, dims, voxel_size):
+        dims = _vec(dims, 3, np.int32)
+        mask = np.ascontiguousarray(mask, np.uint8).reshape(-1)
+        cells = int(dims[0]) * int(dims[1]) * int(dims[2])
+        site = np.empty((max(cells, 1), 3), np.int32)
+        dist = np.empty(max(cells, 1), np.float64)
+        has = self._propagate(mask, mask.size, dims, float(voxel_size), site, dist)
+        if has < 0:
+            raise CheckerError(self.last_error())
+        return bool(has), site[:cells], dist[:cells]
+
+    def query_esdf(self, origin, dims, voxel_size, has_sites, distance, points):
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        n = pts.shape[0]
+        d = np.empty(n, np.float64)
+        g = np.empty((n, 3), np.float64)
+        inside = np.empty(n, np.uint8)
+        self._query_esdf(_vec(origin, 3), _vec(dims, 3, np.int32), float(voxel_size), int(has_sites),
+                         np.ascontiguousarray(distance, np.float64), pts, n, d, g, inside)
+        return d, g, inside.astype(bool)
+
+
+class CheckerTsdf:
+    def __init__(self, lib: CpuChecker, handle, voxel_size, truncation, capacity):
+        self.lib = lib
+        self.h = handle
+        self.voxel_size = voxel_size
+        self.truncation = truncation
+        self.capacity = capacity
+
+    def close(self):
+        if self.h:
+            self.lib._destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def integrate_depth(self, depth, width, height, intr, pose_R, pose_t) -> int:
+        depth = np.ascontiguousarray(depth, np.float32).reshape(-1)
+        assert depth.size == width * height
+        k = self.lib._integrate(self.h, depth, width, height, _vec(intr, 4), _vec(pose_R, 9), _vec(pose_t, 3))
+        if k < 0:
+            raise CheckerError(self.lib.last_error())
+        return k
+
+    def stamp_cuboid(self, pose_R, pose_t, half_extents):
+        if self.lib._stamp_cuboid(self.h, _vec(pose_R, 9), _vec(pose_t, 3), _vec(half_extents, 3)) != 0:
+            raise CheckerError(self.lib.last_error())
+
+    def stamp_sphere(self, center, radius):
+        if self.lib._stamp_sphere(self.h, _vec(center, 3), float(radius)) != 0:
+            raise CheckerError(self.lib.last_error())
+
+    def decay_weights(self, width, height, intr, pose_R, pose_t):
+        self.lib._decay(self.h, width, height, _vec(intr, 4), _vec(pose_R, 9), _vec(pose_t, 3))
+
+    def recycle_blocks(self) -> int:
+        return self.lib._recycle(self.h)
+
+    def allocated_block_count(self) -> int:
+        return self.lib._count(self.h)
+
+    def available(self) -> int:
+        return self.lib._available(self.h)
+
+    def next_fresh(self) -> int:
+        return self.lib._next_fresh(self.h)
+
+    def slot_count(self) -> int:
+        return self.lib._slot_count(self.h)
+
+    def find(self, key) -> int:
+        return self.lib._find(self.h, int(key[0]), int(key[1]), int(key[2]))
+
+    def free_list(self):
+        out = np.empty(max(self.capacity, 1), np.int32)
+        n = self.lib._free_list(self.h, out, out.size)
+        return out[:n].copy()
+
+    def export_blocks(self):
+        """(keys[L,3], pool[L]) of live blocks in slot order."""
+        n = self.allocated_block_count()
+        keys = np.empty((max(n, 1), 3), np.int32)
+        pool = np.empty(max(n, 1), np.int32)
+        self.lib._export(self.h, keys, pool, n)
+        return keys[:n], pool[:n]
+
+    def block_channels(self, pool: int):
+        s = np.empty(512, np.float64)
+        w = np.empty(512, np.float64)
+        g = np.empty(512, np.float64)
+        self.lib._channels(self.h, int(pool), s, w, g)
+        return s, w, g
+
+    def blocks_by_key(self):
+        """dict key(tuple) -> (pool, sum, wt, geom), the by-key parity view."""
+        keys, pool = self.export_blocks()
+        return {tuple(int(c) for c in k): (int(p),) + self.block_channels(int(p)) for k, p in zip(keys, pool)}
+
+    def query_tsdf(self, points, geom_only=False):
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        n = pts.shape[0]
+        out = np.empty(n, np.float64)
+        valid = np.empty(n, np.uint8)
+        self.lib._query_tsdf(self.h, pts, n, int(geom_only), out, valid)
+        return out, valid.astype(bool)
+
+    def seed_gather(self, origin, dims, voxel_size):
+        dims = _vec(dims, 3, np.int32)
+        mask = np.empty(int(dims[0]) * int(dims[1]) * int(dims[2]), np.uint8)
+        self.lib._seed_gather(self.h, _vec(origin, 3), dims, float(voxel_size), mask)
+        return mask
+
+    def seed_scatter(self, origin, dims, voxel_size):
+        dims = _vec(dims, 3, np.int32)
+        mask = np.empty(int(dims[0]) * int(dims[1]) * int(dims[2]), np.uint8)
+        self.lib._seed_scatter(self.h, _vec(origin, 3), dims, float(voxel_size), mask)
+        return mask
+
+    def recover_signs(self, origin, dims, voxel_size, has_sites, site, distance):
+        out = np.array(distance, np.float64, copy=True).reshape(-1)
+        self.lib._recover(self.h, _vec(origin, 3), _vec(dims, 3, np.int32), float(voxel_size), int(has_sites),
+                          np.ascontiguousarray(site, np.int32).reshape(-1), out)
+        return out
+
+    def build_esdf(self, origin, dims, voxel_size, seeding="gather"):
+        """seed -> propagate -> recover_signs (esdf.hpp:323-327)."""
+        mask = (self.seed_gather if seeding == "gather" else self.seed_scatter)(origin, dims, voxel_size)
+        has, site, dist = self.lib.propagate(mask, dims, voxel_size)
+        dist = self.recover_signs(origin, dims, voxel_size, has, site, dist)
+        return mask, has, site, dist
+
+
+def build_checkers(quiet=True):
+    """(Re)build liboracle.so and, when /root/reference is mounted, _ref/libks_ref.so."""
+    subprocess.run(["make", "-C", str(ORACLE_DIR), "all"], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+_cache = {}
+
+
+def oracle() -> CpuChecker:
+    if "o" not in _cache:
+        path = ORACLE_DIR / "liboracle.so"
+        if not path.exists():
+            build_checkers()
+        _cache["o"] = CpuChecker(path, "ko_", "port")
+    return _cache["o"]
+
+
+def reference_available() -> bool:
+    return (ORACLE_DIR / "_ref" / "libks_ref.so").exists()
+
+
+def reference() -> CpuChecker:
+    if "r" not in _cache:
+        path = ORACLE_DIR / "_ref" / "libks_ref.so"
+        if not path.exists() and os.path.isdir("/root/reference"):
+            build_checkers()
+        _cache["r"] = CpuChecker(path, "kr_", "reference")
+    return _cache["r"]
