@@ -1,0 +1,195 @@
+/* ks_b200 -- C ABI of the B200-native perception hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference's header-only C++ API
+ *   /root/reference/proj/include/ks/sdf_world.hpp   (block-sparse TSDF)
+ *   /root/reference/proj/include/ks/esdf.hpp        (dense ESDF + query)
+ * Each entry point cites the reference function it replaces.  The reference has
+ * no FFI of its own (it is `inline` C++); include/ks_b200/ks.hpp re-exports the
+ * reference's ks:: names on top of this ABI and INTEGRATION.md shows the binding.
+ *
+ * Rules of the boundary
+ *   - plain pointers and sizes only; handles are opaque; no exceptions cross it.
+ *   - every call returns a ks_status; ks_last_error() holds the reference's
+ *     exception text for that status (thread-local).
+ *   - "_async" calls enqueue on the handle's stream and never synchronise, so a
+ *     whole update can be captured in one CUDA graph (ks_graph_*).  Their outcome
+ *     (blocks touched, pool exhaustion, ...) is collected by ks_tsdf_sync().
+ *   - there is no CPU fallback: without a CUDA device every compute call fails
+ *     with KS_ERR_CUDA.
+ *
+ * Conventions: rotations are row-major double[9], camera pose is camera-to-world;
+ * ESDF cell index = x + nx*(y + ny*z); a block's 512 voxels are lx + 8*(ly + 8*lz).
+ */
+#ifndef KS_B200_H
+#define KS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define KS_API
+#else
+#define KS_API __attribute__((visibility("default")))
+#endif
+
+typedef enum ks_status {
+  KS_OK = 0,
+  KS_ERR_INVALID = 1,        /* ks::ValidationError (bad config / frame / shape)          */
+  KS_ERR_POOL_EXHAUSTED = 2, /* ks::ValidationError "tsdf: pool exhausted, frame requires ..." */
+  KS_ERR_TABLE_FULL = 3,     /* ks::ValidationError "tsdf: hash table full"               */
+  KS_ERR_CUDA = 4,           /* CUDA runtime failure or no device                         */
+  KS_ERR_RANGE = 5,          /* block coordinate outside +-2^20 (packed-key limit)        */
+  KS_ERR_UNSUPPORTED = 6     /* grid larger than this build's tile limits                 */
+} ks_status;
+
+typedef struct ks_tsdf ks_tsdf;   /* ks::SparseTsdf  (sdf_world.hpp:206-210) */
+typedef struct ks_esdf ks_esdf;   /* ks::DenseEsdf   (esdf.hpp:58-64)        */
+typedef struct ks_graph ks_graph; /* an instantiated CUDA graph               */
+typedef void* ks_stream;          /* cudaStream_t                             */
+
+/* ks::TsdfConfig (sdf_world.hpp:38-54) */
+typedef struct ks_tsdf_config {
+  double voxel_size, truncation, alpha_time, alpha_frustum, weight_threshold;
+  int32_t capacity;   /* block pool size   */
+  int32_t slot_count; /* 0 -> 2 * capacity */
+} ks_tsdf_config;
+
+/* ks::DepthFrame minus the pixels (sdf_world.hpp:191-204) */
+typedef struct ks_camera {
+  int32_t width, height;
+  double fx, fy, cx, cy;
+  double pose_R[9], pose_t[3];
+} ks_camera;
+
+/* ks::EsdfConfig (esdf.hpp:35-54); seeding: 0 = scatter, 1 = gather */
+typedef struct ks_esdf_config {
+  double origin[3];
+  int32_t nx, ny, nz;
+  double voxel_size;
+  int32_t seeding;
+} ks_esdf_config;
+
+/* outcome of the TSDF operations enqueued since the previous ks_tsdf_sync() */
+typedef struct ks_tsdf_report {
+  int32_t status;          /* first ks_status hit, KS_OK otherwise                        */
+  int32_t blocks_touched;  /* return value of the last integrate_depth (sdf_world.hpp:388) */
+  int32_t required;        /* on KS_ERR_POOL_EXHAUSTED: new blocks the op needed           */
+  int32_t available;       /*                            free + fresh pool entries it had   */
+  int32_t live_blocks;     /* allocated_block_count (sdf_world.hpp:509)                    */
+  int32_t next_fresh;      /* BlockHashTable::next_fresh (sdf_world.hpp:112)               */
+  int32_t free_count;      /* BlockHashTable::free_list.size()                             */
+  int32_t recycled;        /* return value of the last recycle_blocks (sdf_world.hpp:474)  */
+} ks_tsdf_report;
+
+typedef struct ks_esdf_report {
+  int32_t status;
+  int32_t has_sites;       /* DenseEsdf::has_sites (esdf.hpp:62)       */
+  int32_t signs_recovered; /* DenseEsdf::signs_recovered (esdf.hpp:63) */
+  int64_t seed_count;      /* cells marked by the last seeding pass     */
+} ks_esdf_report;
+
+/* ---- library ------------------------------------------------------------- */
+KS_API const char* ks_last_error(void);
+KS_API const char* ks_version(void);
+KS_API int ks_device_count(void);
+/* kernels launched by this library since load (bench.py's gpu_launches) */
+KS_API int64_t ks_kernel_launch_count(void);
+
+/* ---- streams / graphs ------------------------------------------------------ */
+KS_API int ks_stream_create(ks_stream* out);
+KS_API int ks_stream_destroy(ks_stream s);
+KS_API int ks_stream_sync(ks_stream s);
+KS_API int ks_graph_begin_capture(ks_stream s);
+KS_API int ks_graph_end_capture(ks_stream s, ks_graph** out);
+KS_API int ks_graph_launch(ks_graph* g, ks_stream s);
+KS_API int ks_graph_node_count(ks_graph* g, int64_t* kernel_nodes, int64_t* all_nodes);
+KS_API void ks_graph_destroy(ks_graph* g);
+
+/* ---- TSDF ------------------------------------------------------------------ */
+/* make_tsdf_config (sdf_world.hpp:56-61) */
+KS_API int ks_tsdf_config_init(double voxel_size, ks_tsdf_config* out);
+/* make_tsdf (sdf_world.hpp:327-334); validate() texts preserved */
+KS_API int ks_tsdf_create(const ks_tsdf_config* config, ks_tsdf** out);
+KS_API void ks_tsdf_destroy(ks_tsdf* t);
+KS_API int ks_tsdf_set_stream(ks_tsdf* t, ks_stream s);
+KS_API ks_stream ks_tsdf_get_stream(const ks_tsdf* t);
+
+/* integrate_depth (sdf_world.hpp:340-389), blocking, host pixels.
+ * DepthFrame::validate texts preserved; *blocks_touched = return value. */
+KS_API int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float* depth_host,
+                                   int32_t* blocks_touched);
+/* the same in three capturable steps: copy a frame into the handle's pinned
+ * staging area (CPU only), enqueue its upload, enqueue the four phases */
+KS_API int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_host);
+KS_API int ks_tsdf_upload_frame_async(ks_tsdf* t);
+KS_API int ks_tsdf_integrate_async(ks_tsdf* t);
+
+/* stamp_primitive (sdf_world.hpp:394-444) */
+KS_API int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t[3],
+                                const double half_extents[3]);
+KS_API int ks_tsdf_stamp_sphere(ks_tsdf* t, const double center[3], double radius);
+KS_API int ks_tsdf_stamp_cuboid_async(ks_tsdf* t, const double pose_R[9], const double pose_t[3],
+                                      const double half_extents[3]);
+KS_API int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double radius);
+
+/* decay_weights (sdf_world.hpp:449-457), recycle_blocks (sdf_world.hpp:462-475) */
+KS_API int ks_tsdf_decay_weights(ks_tsdf* t, const ks_camera* cam);
+KS_API int ks_tsdf_decay_weights_async(ks_tsdf* t, const ks_camera* cam);
+KS_API int ks_tsdf_recycle_blocks(ks_tsdf* t, int32_t* recycled);
+
+/* wait for the handle's stream and collect the outcome of everything enqueued;
+ * returns report->status and sets ks_last_error() like the blocking calls */
+KS_API int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report);
+
+/* query_tsdf / query_tsdf_geom (sdf_world.hpp:500-507): n xyz triples in host
+ * memory -> value + has_value flag (std::optional) */
+KS_API int ks_tsdf_query(ks_tsdf* t, const double* points_host, int64_t n, int32_t geom_only,
+                         double* out_sdf, uint8_t* out_valid);
+/* allocated_block_count (sdf_world.hpp:509) */
+KS_API int ks_tsdf_allocated_block_count(ks_tsdf* t, int32_t* count);
+/* BlockHashTable::find (sdf_world.hpp:132-142) */
+KS_API int ks_tsdf_find(ks_tsdf* t, const int32_t key[3], int32_t* pool_index);
+/* parity dump of SparseTsdf::table / ::pool: live blocks in slot order */
+KS_API int ks_tsdf_export_blocks(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_index, int32_t max_blocks,
+                                 int32_t* count);
+/* VoxelBlock channels of the given pool entries: n x 512 doubles each */
+KS_API int ks_tsdf_download_blocks(ks_tsdf* t, const int32_t* pool_index, int32_t n, double* depth_sum,
+                                   double* depth_wt, double* geom_sdf);
+/* BlockHashTable::free_list, oldest first */
+KS_API int ks_tsdf_free_list(ks_tsdf* t, int32_t* out, int32_t max_out, int32_t* count);
+
+/* ---- ESDF ------------------------------------------------------------------ */
+/* EsdfConfig::validate (esdf.hpp:41-44) + device buffers for the grid */
+KS_API int ks_esdf_create(const ks_esdf_config* config, ks_esdf** out);
+KS_API void ks_esdf_destroy(ks_esdf* e);
+KS_API int ks_esdf_set_stream(ks_esdf* e, ks_stream s);
+
+/* build_esdf (esdf.hpp:323-327): seed -> propagate -> recover_signs */
+KS_API int ks_esdf_build(ks_esdf* e, const ks_tsdf* t);
+KS_API int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t);
+/* seed_gather / seed_scatter (esdf.hpp:102-122 / :73-98); mask_host may be NULL */
+KS_API int ks_esdf_seed(ks_esdf* e, const ks_tsdf* t, int32_t mode, uint8_t* mask_host);
+/* propagate (esdf.hpp:193-282) from a host mask (NULL: the mask left by ks_esdf_seed) */
+KS_API int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_len);
+/* recover_signs (esdf.hpp:288-320) on the field left by ks_esdf_propagate */
+KS_API int ks_esdf_recover_signs(ks_esdf* e, const ks_tsdf* t);
+KS_API int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report);
+
+/* DenseEsdf::site / ::distance (any pointer may be NULL).  d2 = squared integer
+ * site offset (exact), INT32_MAX when the grid has no sites. */
+KS_API int ks_esdf_download(ks_esdf* e, int32_t* site_xyz, double* distance, int32_t* d2);
+
+/* query (esdf.hpp:337-387) for n points: host buffers, blocking */
+KS_API int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, double* distance,
+                         double* gradient_xyz, uint8_t* inside);
+/* the same with device-resident buffers, enqueued on the handle's stream */
+KS_API int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, double* distance_dev,
+                                      double* gradient_dev, uint8_t* inside_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_B200_H */

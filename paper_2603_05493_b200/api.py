@@ -1,0 +1,524 @@
+"""Host-side mirror of the reference's ks:: perception API over the ks_b200 C ABI.
+
+Function names, argument meaning and error behaviour follow
+/root/reference/proj/include/ks/sdf_world.hpp and esdf.hpp:
+
+    make_tsdf_config, make_tsdf, integrate_depth, stamp_primitive, decay_weights, recycle_blocks,
+    query_tsdf, query_tsdf_geom, allocated_block_count, seed_gather, seed_scatter, propagate,
+    recover_signs, build_esdf, query
+
+Everything here is a thin ctypes call into libks_b200.so (include/ks_b200.h).  There is no CPU
+implementation: loading fails loudly when the library is missing, and every compute call fails with
+KS_ERR_CUDA when no device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libks_b200.so"
+
+KS_OK, KS_ERR_INVALID, KS_ERR_POOL_EXHAUSTED, KS_ERR_TABLE_FULL, KS_ERR_CUDA, KS_ERR_RANGE, KS_ERR_UNSUPPORTED = range(7)
+
+
+class ValidationError(RuntimeError):
+    """ks::ValidationError (core.hpp:36-39)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class TsdfConfigC(C.Structure):
+    _fields_ = [("voxel_size", C.c_double), ("truncation", C.c_double), ("alpha_time", C.c_double),
+                ("alpha_frustum", C.c_double), ("weight_threshold", C.c_double), ("capacity", C.c_int32),
+                ("slot_count", C.c_int32)]
+
+
+class CameraC(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("pose_R", C.c_double * 9), ("pose_t", C.c_double * 3)]
+
+
+class EsdfConfigC(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("voxel_size", C.c_double), ("seeding", C.c_int32)]
+
+
+class TsdfReportC(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("status", "blocks_touched", "required", "available", "live_blocks",
+                                          "next_fresh", "free_count", "recycled")]
+
+
+class EsdfReportC(C.Structure):
+    _fields_ = [("status", C.c_int32), ("has_sites", C.c_int32), ("signs_recovered", C.c_int32),
+                ("seed_count", C.c_int64)]
+
+
+_lib = None
+
+# every symbol include/ks_b200.h declares (tests check the .so exports exactly these)
+ABI_SYMBOLS = [
+    "ks_last_error", "ks_version", "ks_device_count", "ks_kernel_launch_count", "ks_stream_create",
+    "ks_stream_destroy", "ks_stream_sync", "ks_graph_begin_capture", "ks_graph_end_capture", "ks_graph_launch",
+    "ks_graph_node_count", "ks_graph_destroy", "ks_tsdf_config_init", "ks_tsdf_create", "ks_tsdf_destroy",
+    "ks_tsdf_set_stream", "ks_tsdf_get_stream", "ks_tsdf_integrate_depth", "ks_tsdf_stage_frame",
+    "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stamp_cuboid", "ks_tsdf_stamp_sphere",
+    "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_tsdf_decay_weights",
+    "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
+    "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
+    "ks_tsdf_free_list", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
+    "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync",
+    "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async",
+]
+
+
+def load_library() -> C.CDLL:
+    """Load libks_b200.so.  Fails loudly: there is no fallback implementation."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2603_05493_b200.build` "
+                          "(the perception path has no CPU implementation)")
+    lib = C.CDLL(str(LIB_PATH))
+    VP, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    sig = {
+        "ks_last_error": (C.c_char_p, []),
+        "ks_version": (C.c_char_p, []),
+        "ks_device_count": (C.c_int, []),
+        "ks_kernel_launch_count": (I64, []),
+        "ks_stream_create": (C.c_int, [P(VP)]),
+        "ks_stream_destroy": (C.c_int, [VP]),
+        "ks_stream_sync": (C.c_int, [VP]),
+        "ks_graph_begin_capture": (C.c_int, [VP]),
+        "ks_graph_end_capture": (C.c_int, [VP, P(VP)]),
+        "ks_graph_launch": (C.c_int, [VP, VP]),
+        "ks_graph_node_count": (C.c_int, [VP, P(I64), P(I64)]),
+        "ks_graph_destroy": (None, [VP]),
+        "ks_tsdf_config_init": (C.c_int, [D, P(TsdfConfigC)]),
+        "ks_tsdf_create": (C.c_int, [P(TsdfConfigC), P(VP)]),
+        "ks_tsdf_destroy": (None, [VP]),
+        "ks_tsdf_set_stream": (C.c_int, [VP, VP]),
+        "ks_tsdf_get_stream": (VP, [VP]),
+        "ks_tsdf_integrate_depth": (C.c_int, [VP, P(CameraC), VP, P(I32)]),
+        "ks_tsdf_stage_frame": (C.c_int, [VP, P(CameraC), VP]),
+        "ks_tsdf_upload_frame_async": (C.c_int, [VP]),
+        "ks_tsdf_integrate_async": (C.c_int, [VP]),
+        "ks_tsdf_stamp_cuboid": (C.c_int, [VP, VP, VP, VP]),
+        "ks_tsdf_stamp_sphere": (C.c_int, [VP, VP, D]),
+        "ks_tsdf_stamp_cuboid_async": (C.c_int, [VP, VP, VP, VP]),
+        "ks_tsdf_stamp_sphere_async": (C.c_int, [VP, VP, D]),
+        "ks_tsdf_decay_weights": (C.c_int, [VP, P(CameraC)]),
+        "ks_tsdf_decay_weights_async": (C.c_int, [VP, P(CameraC)]),
+        "ks_tsdf_recycle_blocks": (C.c_int, [VP, P(I32)]),
+        "ks_tsdf_sync": (C.c_int, [VP, P(TsdfReportC)]),
+        "ks_tsdf_query": (C.c_int, [VP, VP, I64, I32, VP, VP]),
+        "ks_tsdf_allocated_block_count": (C.c_int, [VP, P(I32)]),
+        "ks_tsdf_find": (C.c_int, [VP, VP, P(I32)]),
+        "ks_tsdf_export_blocks": (C.c_int, [VP, VP, VP, I32, P(I32)]),
+        "ks_tsdf_download_blocks": (C.c_int, [VP, VP, I32, VP, VP, VP]),
+        "ks_tsdf_free_list": (C.c_int, [VP, VP, I32, P(I32)]),
+        "ks_esdf_create": (C.c_int, [P(EsdfConfigC), P(VP)]),
+        "ks_esdf_destroy": (None, [VP]),
+        "ks_esdf_set_stream": (C.c_int, [VP, VP]),
+        "ks_esdf_build": (C.c_int, [VP, VP]),
+        "ks_esdf_build_async": (C.c_int, [VP, VP]),
+        "ks_esdf_seed": (C.c_int, [VP, VP, I32, VP]),
+        "ks_esdf_propagate": (C.c_int, [VP, VP, I64]),
+        "ks_esdf_recover_signs": (C.c_int, [VP, VP]),
+        "ks_esdf_sync": (C.c_int, [VP, P(EsdfReportC)]),
+        "ks_esdf_download": (C.c_int, [VP, VP, VP, VP]),
+        "ks_esdf_query": (C.c_int, [VP, VP, I64, VP, VP, VP]),
+        "ks_esdf_query_device_async": (C.c_int, [VP, VP, I64, VP, VP, VP]),
+    }
+    assert sorted(sig) == sorted(ABI_SYMBOLS)
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return (load_library().ks_last_error() or b"").decode()
+
+
+def _check(rc: int):
+    if rc == KS_OK:
+        return
+    msg = last_error()
+    if rc == KS_ERR_CUDA:
+        raise CudaError(msg)
+    raise ValidationError(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a, n=None) -> np.ndarray:
+    out = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    if n is not None:
+        assert out.size == n
+    return out
+
+
+def kernel_launch_count() -> int:
+    return int(load_library().ks_kernel_launch_count())
+
+
+# ---- value types mirroring the reference structs --------------------------------------------------
+
+@dataclass
+class TsdfConfig:  # sdf_world.hpp:38-54
+    voxel_size: float = 0.01
+    truncation: float = 0.04
+    alpha_time: float = 0.99
+    alpha_frustum: float = 0.5
+    weight_threshold: float = 0.5
+    capacity: int = 8192
+    slot_count: int = 0
+
+
+def make_tsdf_config(voxel_size: float) -> TsdfConfig:  # sdf_world.hpp:56-61
+    return TsdfConfig(voxel_size=voxel_size, truncation=4.0 * voxel_size)
+
+
+@dataclass
+class DepthFrame:  # sdf_world.hpp:191-204
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    pose_R: np.ndarray = field(default_factory=lambda: np.eye(3))
+    pose_t: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    depth: Optional[np.ndarray] = None
+
+    def camera(self) -> CameraC:
+        cam = CameraC(int(self.width), int(self.height), float(self.fx), float(self.fy), float(self.cx), float(self.cy))
+        cam.pose_R[:] = list(_f64(self.pose_R, 9))
+        cam.pose_t[:] = list(_f64(self.pose_t, 3))
+        return cam
+
+
+@dataclass
+class Cuboid:  # sdf_world.hpp:212-215
+    pose_R: np.ndarray
+    pose_t: np.ndarray
+    half_extents: np.ndarray
+
+
+@dataclass
+class SphereShape:  # sdf_world.hpp:217-220
+    center: np.ndarray
+    radius: float
+
+
+@dataclass
+class EsdfConfig:  # esdf.hpp:35-54
+    origin: Sequence[float] = (0.0, 0.0, 0.0)
+    nx: int = 1
+    ny: int = 1
+    nz: int = 1
+    voxel_size: float = 0.01
+    seeding: str = "gather"
+
+    def cell_count(self) -> int:
+        return int(self.nx) * int(self.ny) * int(self.nz)
+
+
+@dataclass
+class EsdfSample:  # esdf.hpp:329-333 (batched)
+    distance: np.ndarray
+    gradient: np.ndarray
+    inside: np.ndarray
+
+
+# ---- handles -------------------------------------------------------------------------------------
+
+class SparseTsdf:
+    """ks::SparseTsdf (sdf_world.hpp:206-210) living in HBM."""
+
+    def __init__(self, config: TsdfConfig, stream: Optional[int] = None):
+        self.lib = load_library()
+        self.config = config
+        c = TsdfConfigC(config.voxel_size, config.truncation, config.alpha_time, config.alpha_frustum,
+                        config.weight_threshold, int(config.capacity), int(config.slot_count))
+        h = C.c_void_p()
+        _check(self.lib.ks_tsdf_create(C.byref(c), C.byref(h)))
+        self.h = h
+        if stream is not None:
+            _check(self.lib.ks_tsdf_set_stream(self.h, C.c_void_p(stream)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ks_tsdf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # capturable pieces
+    def stage_frame(self, frame: DepthFrame):
+        depth = np.ascontiguousarray(frame.depth, np.float32).reshape(-1)
+        if depth.size != frame.width * frame.height:
+            raise ValidationError("depth frame: depth buffer size mismatch")  # sdf_world.hpp:200-201
+        cam = frame.camera()
+        _check(self.lib.ks_tsdf_stage_frame(self.h, C.byref(cam), _ptr(depth)))
+
+    def upload_frame_async(self):
+        _check(self.lib.ks_tsdf_upload_frame_async(self.h))
+
+    def integrate_async(self):
+        _check(self.lib.ks_tsdf_integrate_async(self.h))
+
+    def stamp_async(self, primitive):
+        if isinstance(primitive, Cuboid):
+            R, t, he = _f64(primitive.pose_R, 9), _f64(primitive.pose_t, 3), _f64(primitive.half_extents, 3)
+            _check(self.lib.ks_tsdf_stamp_cuboid_async(self.h, _ptr(R), _ptr(t), _ptr(he)))
+        else:
+            c = _f64(primitive.center, 3)
+            _check(self.lib.ks_tsdf_stamp_sphere_async(self.h, _ptr(c), float(primitive.radius)))
+
+    def sync(self) -> TsdfReportC:
+        rep = TsdfReportC()
+        _check(self.lib.ks_tsdf_sync(self.h, C.byref(rep)))
+        return rep
+
+    # parity views
+    def export_blocks(self) -> Tuple[np.ndarray, np.ndarray]:
+        n = C.c_int32()
+        _check(self.lib.ks_tsdf_export_blocks(self.h, None, None, 0, C.byref(n)))
+        keys = np.empty((max(n.value, 1), 3), np.int32)
+        pool = np.empty(max(n.value, 1), np.int32)
+        _check(self.lib.ks_tsdf_export_blocks(self.h, _ptr(keys), _ptr(pool), n.value, C.byref(n)))
+        return keys[:n.value], pool[:n.value]
+
+    def download_blocks(self, pools) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        pools = np.ascontiguousarray(pools, np.int32)
+        n = pools.size
+        s, w, g = (np.empty((max(n, 1), 512), np.float64) for _ in range(3))
+        _check(self.lib.ks_tsdf_download_blocks(self.h, _ptr(pools), n, _ptr(s), _ptr(w), _ptr(g)))
+        return s[:n], w[:n], g[:n]
+
+    def find(self, key) -> int:
+        k = np.ascontiguousarray(key, np.int32)
+        out = C.c_int32()
+        _check(self.lib.ks_tsdf_find(self.h, _ptr(k), C.byref(out)))
+        return out.value
+
+    def free_list(self) -> np.ndarray:
+        out = np.empty(max(self.config.capacity, 1), np.int32)
+        n = C.c_int32()
+        _check(self.lib.ks_tsdf_free_list(self.h, _ptr(out), out.size, C.byref(n)))
+        return out[:n.value].copy()
+
+
+class DenseEsdf:
+    """ks::DenseEsdf (esdf.hpp:58-64) living in HBM; site/distance are downloaded on demand."""
+
+    def __init__(self, config: EsdfConfig, stream: Optional[int] = None):
+        self.lib = load_library()
+        self.config = config
+        c = EsdfConfigC()
+        c.origin[:] = [float(v) for v in config.origin]
+        c.nx, c.ny, c.nz = int(config.nx), int(config.ny), int(config.nz)
+        c.voxel_size = float(config.voxel_size)
+        c.seeding = 1 if config.seeding == "gather" else 0
+        h = C.c_void_p()
+        _check(self.lib.ks_esdf_create(C.byref(c), C.byref(h)))
+        self.h = h
+        if stream is not None:
+            _check(self.lib.ks_esdf_set_stream(self.h, C.c_void_p(stream)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ks_esdf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def build_async(self, tsdf: SparseTsdf):
+        _check(self.lib.ks_esdf_build_async(self.h, tsdf.h))
+
+    def report(self) -> EsdfReportC:
+        rep = EsdfReportC()
+        _check(self.lib.ks_esdf_sync(self.h, C.byref(rep)))
+        return rep
+
+    @property
+    def has_sites(self) -> bool:
+        return bool(self.report().has_sites)
+
+    @property
+    def signs_recovered(self) -> bool:
+        return bool(self.report().signs_recovered)
+
+    def download(self, site=True, distance=True, d2=True):
+        n = self.config.cell_count()
+        s = np.empty((n, 3), np.int32) if site else None
+        d = np.empty(n, np.float64) if distance else None
+        q = np.empty(n, np.int32) if d2 else None
+        _check(self.lib.ks_esdf_download(self.h, _ptr(s), _ptr(d), _ptr(q)))
+        return s, d, q
+
+    @property
+    def site(self) -> np.ndarray:
+        return self.download(True, False, False)[0]
+
+    @property
+    def distance(self) -> np.ndarray:
+        return self.download(False, True, False)[1]
+
+
+# ---- the reference's free functions ------------------------------------------------------------------
+
+def make_tsdf(config: TsdfConfig, stream: Optional[int] = None) -> SparseTsdf:  # sdf_world.hpp:327-334
+    return SparseTsdf(config, stream)
+
+
+def integrate_depth(tsdf: SparseTsdf, frame: DepthFrame) -> int:  # sdf_world.hpp:340-389
+    depth = np.ascontiguousarray(frame.depth, np.float32).reshape(-1)
+    if depth.size != frame.width * frame.height and frame.width > 0 and frame.height > 0 and frame.fx > 0 and frame.fy > 0:
+        raise ValidationError("depth frame: depth buffer size mismatch")
+    cam = frame.camera()
+    touched = C.c_int32()
+    _check(tsdf.lib.ks_tsdf_integrate_depth(tsdf.h, C.byref(cam), _ptr(depth), C.byref(touched)))
+    return touched.value
+
+
+def stamp_primitive(tsdf: SparseTsdf, primitive) -> None:  # sdf_world.hpp:394-444
+    if isinstance(primitive, Cuboid):
+        R, t, he = _f64(primitive.pose_R, 9), _f64(primitive.pose_t, 3), _f64(primitive.half_extents, 3)
+        _check(tsdf.lib.ks_tsdf_stamp_cuboid(tsdf.h, _ptr(R), _ptr(t), _ptr(he)))
+    else:
+        c = _f64(primitive.center, 3)
+        _check(tsdf.lib.ks_tsdf_stamp_sphere(tsdf.h, _ptr(c), float(primitive.radius)))
+
+
+def decay_weights(tsdf: SparseTsdf, camera: DepthFrame) -> None:  # sdf_world.hpp:449-457
+    cam = camera.camera()
+    _check(tsdf.lib.ks_tsdf_decay_weights(tsdf.h, C.byref(cam)))
+
+
+def recycle_blocks(tsdf: SparseTsdf) -> int:  # sdf_world.hpp:462-475
+    n = C.c_int32()
+    _check(tsdf.lib.ks_tsdf_recycle_blocks(tsdf.h, C.byref(n)))
+    return n.value
+
+
+def _query_tsdf(tsdf: SparseTsdf, points, geom_only: bool):
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    out = np.empty(max(n, 1), np.float64)
+    valid = np.empty(max(n, 1), np.uint8)
+    _check(tsdf.lib.ks_tsdf_query(tsdf.h, _ptr(pts), n, int(geom_only), _ptr(out), _ptr(valid)))
+    return out[:n], valid[:n].astype(bool)
+
+
+def query_tsdf(tsdf: SparseTsdf, points):  # sdf_world.hpp:500-502 (batched: value, has_value)
+    return _query_tsdf(tsdf, points, False)
+
+
+def query_tsdf_geom(tsdf: SparseTsdf, points):  # sdf_world.hpp:505-507
+    return _query_tsdf(tsdf, points, True)
+
+
+def allocated_block_count(tsdf: SparseTsdf) -> int:  # sdf_world.hpp:509
+    n = C.c_int32()
+    _check(tsdf.lib.ks_tsdf_allocated_block_count(tsdf.h, C.byref(n)))
+    return n.value
+
+
+def _seed(tsdf: SparseTsdf, config: EsdfConfig, mode: int, esdf: Optional[DenseEsdf]):
+    e = esdf or DenseEsdf(config)
+    mask = np.empty(config.cell_count(), np.uint8)
+    _check(e.lib.ks_esdf_seed(e.h, tsdf.h, mode, _ptr(mask)))
+    return mask
+
+
+def seed_gather(tsdf: SparseTsdf, config: EsdfConfig, esdf: Optional[DenseEsdf] = None) -> np.ndarray:  # esdf.hpp:102-122
+    return _seed(tsdf, config, 1, esdf)
+
+
+def seed_scatter(tsdf: SparseTsdf, config: EsdfConfig, esdf: Optional[DenseEsdf] = None) -> np.ndarray:  # esdf.hpp:73-98
+    return _seed(tsdf, config, 0, esdf)
+
+
+def propagate(seeds: np.ndarray, config: EsdfConfig, esdf: Optional[DenseEsdf] = None) -> DenseEsdf:  # esdf.hpp:193-282
+    e = esdf or DenseEsdf(config)
+    mask = np.ascontiguousarray(seeds, np.uint8).reshape(-1)
+    _check(e.lib.ks_esdf_propagate(e.h, _ptr(mask), mask.size))
+    return e
+
+
+def recover_signs(esdf: DenseEsdf, tsdf: SparseTsdf) -> DenseEsdf:  # esdf.hpp:288-320
+    _check(esdf.lib.ks_esdf_recover_signs(esdf.h, tsdf.h))
+    return esdf
+
+
+def build_esdf(tsdf: SparseTsdf, config: EsdfConfig, esdf: Optional[DenseEsdf] = None) -> DenseEsdf:  # esdf.hpp:323-327
+    e = esdf or DenseEsdf(config)
+    _check(e.lib.ks_esdf_build(e.h, tsdf.h))
+    return e
+
+
+def query(esdf: DenseEsdf, points) -> EsdfSample:  # esdf.hpp:337-387, batched over points
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    d = np.empty(max(n, 1), np.float64)
+    g = np.empty((max(n, 1), 3), np.float64)
+    inside = np.empty(max(n, 1), np.uint8)
+    _check(esdf.lib.ks_esdf_query(esdf.h, _ptr(pts), n, _ptr(d), _ptr(g), _ptr(inside)))
+    return EsdfSample(d[:n], g[:n], inside[:n].astype(bool))
+
+
+# ---- CUDA graph helper ----------------------------------------------------------------------------
+
+class Graph:
+    """Capture a sequence of *_async calls issued on `stream` into one replayable CUDA graph."""
+
+    def __init__(self, stream: int):
+        self.lib = load_library()
+        self.stream = C.c_void_p(stream)
+        self.h = C.c_void_p()
+
+    def __enter__(self):
+        _check(self.lib.ks_graph_begin_capture(self.stream))
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        rc = self.lib.ks_graph_end_capture(self.stream, C.byref(self.h))
+        if exc_type is None:
+            _check(rc)
+        return False
+
+    def launch(self):
+        _check(self.lib.ks_graph_launch(self.h, self.stream))
+
+    def node_count(self) -> Tuple[int, int]:
+        k, a = C.c_int64(), C.c_int64()
+        _check(self.lib.ks_graph_node_count(self.h, C.byref(k), C.byref(a)))
+        return k.value, a.value
+
+    def close(self):
+        if self.h:
+            self.lib.ks_graph_destroy(self.h)
+            self.h = C.c_void_p()

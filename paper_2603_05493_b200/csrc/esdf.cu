@@ -1,0 +1,715 @@
+// Dense workspace ESDF on the device: seeding, exact EDT ("PBA+"), sign recovery and
+// batched trilinear queries.  Replaces /root/reference/proj/include/ks/esdf.hpp
+// behind the C ABI in include/ks_b200.h.  See DESIGN.md for layouts and byte counts.
+//
+// Device layout of the finished field (per cell, 8 bytes):
+//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites)
+//   d2s  : uint32  bit31 = negative, bits0-30 = squared integer site offset
+//                  (0x7FFFFFFF: no sites).  distance = sqrt((double)d2) * voxel_size
+//                  is formed on the fly, so queries see exactly the reference's doubles.
+// Both are stored y-fastest, index = y + ny*(x + nx*z): the x sweep runs with lane <-> y,
+// so its stores are coalesced; the download path converts back to the reference's
+// x-fastest order (esdf.hpp:48-50).
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "edt_core.cuh"
+
+namespace ksb {
+
+constexpr uint32_t kSiteNone = 0xFFFFFFFFu;
+constexpr uint32_t kD2None = 0x7FFFFFFFu;
+constexpr uint32_t kYzNone = 0xFFFFFFFFu;
+constexpr int kMaxDim = 1024;  // 10-bit site packing, uint16 stacks
+
+struct EsdfCtrl {
+  unsigned long long seed_count;
+  int signs_recovered;
+  int pad;
+};
+
+struct EsdfView {
+  int nx, ny, nz;
+  long long cells;
+  double origin[3];
+  double ve;
+  int* vox;      // [3][nx+ny+nz] TSDF voxel index of (cell centre + {0, +h, -h}) per axis position
+  double* ctr;   // [nx+ny+nz]    cell centre coordinate per axis position (esdf.hpp:51-53)
+  int* dir;      // dense block directory over the workspace: pool entry or -1
+  int dlo[3], dn[3];
+  long long dcount;
+  uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66)
+  uint16_t* near_z;  // [cells] x-fastest phase-1 result
+  uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
+  uint32_t* site;    // [cells] y-fastest
+  uint32_t* d2s;     // [cells] y-fastest
+  EsdfCtrl* ctrl;
+};
+
+__device__ __forceinline__ int axis_base(const EsdfView& E, int axis) { return axis == 0 ? 0 : (axis == 1 ? E.nx : E.nx + E.ny); }
+
+// pool entry of the TSDF block containing voxel (vx,vy,vz), via the workspace directory
+__device__ __forceinline__ int dir_lookup(const EsdfView& E, int vx, int vy, int vz) {
+  const int bx = (vx >> 3) - E.dlo[0], by = (vy >> 3) - E.dlo[1], bz = (vz >> 3) - E.dlo[2];
+  if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) return -1;
+  return E.dir[bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)];
+}
+__device__ __forceinline__ uint32_t digest_bit(const TsdfView& T, int pool, int plane, int vx, int vy, int vz) {
+  const int local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));  // local_index_of (sdf_world.hpp:274-280)
+  return (T.digest[static_cast<size_t>(pool) * kDigestWords + plane * 16 + (local >> 5)] >> (local & 31)) & 1u;
+}
+
+// ---- per-axis tables: every fp64 division of the seeding stage happens here, once per axis position ----
+__global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
+  const int total = E.nx + E.ny + E.nz;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int axis = i < E.nx ? 0 : (i < E.nx + E.ny ? 1 : 2);
+  const int k = i - axis_base(E, axis);
+  const double c = E.origin[axis] + (k + 0.5) * E.ve;  // EsdfConfig::cell_center (esdf.hpp:51-53)
+  const double h = 0.5 * E.ve;                         // esdf.hpp:106
+  E.ctr[i] = c;
+  E.vox[i] = voxel_index(c + 0.0, tsdf_voxel);
+  E.vox[total + i] = voxel_index(c + h, tsdf_voxel);
+  E.vox[2 * total + i] = voxel_index(c + (-h), tsdf_voxel);
+}
+
+__global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
+  const int bound = T.ctrl->next_fresh;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < bound; p += gridDim.x * blockDim.x) {
+    const uint64_t key = T.pool_key[p];
+    if (key == kKeyEmpty) continue;
+    int bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    bx -= E.dlo[0], by -= E.dlo[1], bz -= E.dlo[2];
+    if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
+    E.dir[bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)] = p;
+  }
+}
+
+// ---- seed_gather (esdf.hpp:102-122): 7-probe stencil per ESDF cell, bits instead of voxels ----
+__global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  bool seed = false;
+  if (idx < E.cells) {
+    const int x = static_cast<int>(idx % E.nx);
+    const int y = static_cast<int>((idx / E.nx) % E.ny);
+    const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
+    const int total = E.nx + E.ny + E.nz;
+    const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
+    const int xc = E.vox[ix], xp = E.vox[total + ix], xm = E.vox[2 * total + ix];
+    const int yc = E.vox[iy], yp = E.vox[total + iy], ym = E.vox[2 * total + iy];
+    const int zc = E.vox[iz], zp = E.vox[total + iz], zm = E.vox[2 * total + iz];
+    auto probe = [&](int vx, int vy, int vz) -> bool {
+      const int pool = dir_lookup(E, vx, vy, vz);
+      return pool >= 0 && digest_bit(T, pool, kSurface, vx, vy, vz) != 0;
+    };
+    seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
+           (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
+           (zm != zc && probe(xc, yc, zm));
+    E.mask[idx] = seed ? 1 : 0;
+  }
+  const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
+  if ((threadIdx.x & 31) == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
+}
+
+// ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
+__global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
+  const int bound = T.ctrl->next_fresh;
+  const int tid = threadIdx.x;
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  for (int pool = blockIdx.x; pool < bound; pool += gridDim.x) {
+    const uint64_t key = T.pool_key[pool];
+    if (key == kKeyEmpty) continue;
+    const uint32_t word = T.digest[static_cast<size_t>(pool) * kDigestWords + kSurface * 16 + (tid >> 5)];
+    if (!((word >> (tid & 31)) & 1u)) continue;
+    int bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    const double cx = (bx * kBlockEdge + lx + 0.5) * T.voxel, cy = (by * kBlockEdge + ly + 0.5) * T.voxel,
+                 cz = (bz * kBlockEdge + lz + 0.5) * T.voxel;
+    const int ex = static_cast<int>(floor((cx - E.origin[0]) / E.ve));
+    const int ey = static_cast<int>(floor((cy - E.origin[1]) / E.ve));
+    const int ez = static_cast<int>(floor((cz - E.origin[2]) / E.ve));
+    if (ex < 0 || ex >= E.nx || ey < 0 || ey >= E.ny || ez < 0 || ez >= E.nz) continue;
+    E.mask[ex + static_cast<long long>(E.nx) * (ey + static_cast<long long>(E.ny) * ez)] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
+  unsigned local = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < E.cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    local += E.mask[i] != 0;
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xFFFFFFFFu, local, d);
+  if ((threadIdx.x & 31) == 0 && local != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(local));
+}
+
+// ---- phase 1: nearest seed along z per (x, y) column (esdf.hpp:213-233) ----
+// The column's mask becomes a bit string in shared memory ([word][thread], conflict free);
+// every z then finds its nearest set bit with clz/ffs.
+__global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
+  extern __shared__ uint32_t s_words[];
+  const long long plane = static_cast<long long>(E.nx) * E.ny;
+  const long long col = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int nwords = (E.nz + 31) >> 5;
+  const int stride = blockDim.x;
+  uint32_t* words = s_words + threadIdx.x;
+  if (col >= plane) return;
+  uint32_t any = 0;
+  for (int w = 0; w < nwords; ++w) {
+    uint32_t bits = 0;
+    const int zend = min(32, E.nz - 32 * w);
+    for (int b = 0; b < zend; ++b) bits |= (E.mask[col + plane * (32 * w + b)] != 0 ? 1u : 0u) << b;
+    words[w * stride] = bits;
+    any |= bits;
+  }
+  if (any == 0) {
+    for (int z = 0; z < E.nz; ++z) E.near_z[col + plane * z] = edt::kNone;
+    return;
+  }
+  for (int z = 0; z < E.nz; ++z) E.near_z[col + plane * z] = edt::nearest_set_bit(words, stride, nwords, z);
+}
+
+// ---- phases 2 and 3: banded lower-envelope sweeps (esdf.hpp:236-280), see edt_core.cuh ----
+struct SweepSmem {
+  uint16_t *stk_s, *stk_t, *mark, *lo, *hi, *blast;
+};
+__device__ __forceinline__ edt::RowTile carve_tile(unsigned char* base, int n, int band, int bands, size_t in_bytes) {
+  edt::RowTile T;
+  unsigned char* p = base + in_bytes;
+  T.stk_s = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
+  T.stk_t = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
+  T.mark = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
+  T.lo = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(bands) * 64;
+  T.hi = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(bands) * 64;
+  T.blast = reinterpret_cast<uint16_t*>(p);
+  T.n = n, T.band = band, T.bands = bands;
+  return T;
+}
+static size_t sweep_smem_bytes(int n, int bands, int in_elem_bytes) {
+  return static_cast<size_t>(n) * 32 * in_elem_bytes + static_cast<size_t>(n) * 64 * 3 + static_cast<size_t>(bands) * 64 * 3;
+}
+
+struct SrcY {  // candidate at y = the column's nearest seed z (phase-1 output)
+  const uint16_t* zs;
+  int z;
+  __device__ __forceinline__ int r2(int pos, int row) const {
+    const uint16_t v = zs[edt::at(pos, row)];
+    if (v == edt::kNone) return -1;
+    const int d = z - static_cast<int>(v);
+    return d * d;
+  }
+};
+struct SrcX {  // candidate at x = phase 2's (site_y, site_z)
+  const uint32_t* yz;
+  int y0, z;
+  __device__ __forceinline__ int r2(int pos, int row) const {
+    const uint32_t v = yz[edt::at(pos, row)];
+    if (v == kYzNone) return -1;
+    const int dy = (y0 + row) - static_cast<int>(v & 0xFFFFu);
+    const int dz = z - static_cast<int>(v >> 16);
+    return dy * dy + dz * dz;
+  }
+};
+
+template <class Src>
+__device__ __forceinline__ void sweep_stages(const edt::RowTile& T, const Src& src, int warp, int lane) {
+  if (warp < T.bands) edt::build_band(T, src, warp, lane);
+  __syncthreads();
+  for (int j = 0; (1 << j) < T.bands; ++j) {
+    if (warp < T.bands && (warp & ((2 << j) - 1)) == 0) edt::merge_groups(T, src, warp, j, lane);
+    __syncthreads();
+  }
+  if (warp < T.bands) edt::mark_band(T, warp, lane);
+  __syncthreads();
+  if (warp < T.bands) edt::last_mark_of_band(T, warp, lane);
+  __syncthreads();
+}
+
+// grid = (ceil(nx/32), nz); block = 32 * bands.  lane <-> x, positions = y.
+__global__ void k_sweep_y(EsdfView E, int band, int bands) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = blockIdx.x * 32 + lane, z = blockIdx.y;
+  const int ny = E.ny;
+  uint16_t* zs = reinterpret_cast<uint16_t*>(s_raw);
+  const edt::RowTile T = carve_tile(s_raw, ny, band, bands, static_cast<size_t>(ny) * 64);
+  const long long zoff = static_cast<long long>(E.nx) * ny * z;
+  const int base = warp * band, end = min(base + band, ny);
+  if (warp < bands)
+    for (int y = base; y < end; ++y) zs[edt::at(y, lane)] = x < E.nx ? E.near_z[zoff + static_cast<long long>(E.nx) * y + x] : edt::kNone;
+  __syncwarp();
+  const SrcY src{zs, z};
+  sweep_stages(T, src, warp, lane);
+  if (warp < bands)
+    edt::colour_band(T, warp, lane, [&](int y, uint16_t win) {
+      if (x < E.nx)
+        E.yz[zoff + static_cast<long long>(E.nx) * y + x] =
+            win == edt::kNone ? kYzNone : (static_cast<uint32_t>(win) | static_cast<uint32_t>(zs[edt::at(win, lane)]) << 16);
+    });
+}
+
+// grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
+// The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
+// bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
+__global__ void k_sweep_x(EsdfView E, int band, int bands) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int y0 = blockIdx.x * 32, z = blockIdx.y;
+  const int nx = E.nx, ny = E.ny;
+  uint32_t* in = reinterpret_cast<uint32_t*>(s_raw);
+  const edt::RowTile T = carve_tile(s_raw, nx, band, bands, static_cast<size_t>(nx) * 128);
+  const long long zoff = static_cast<long long>(nx) * ny * z;
+  for (int r = warp; r < 32; r += nwarps) {
+    const bool live = y0 + r < ny;
+    const uint32_t* row = E.yz + zoff + static_cast<long long>(nx) * (y0 + r);
+    for (int x = lane; x < nx; x += 32) in[x * 32 + ((r + x) & 31)] = live ? row[x] : kYzNone;
+  }
+  __syncthreads();
+  for (int x = warp; x < nx; x += nwarps) {
+    const uint32_t v = in[x * 32 + ((lane + x) & 31)];
+    __syncwarp();
+    in[x * 32 + lane] = v;
+  }
+  __syncthreads();
+  const SrcX src{in, y0, z};
+  sweep_stages(T, src, warp, lane);
+  const int y = y0 + lane;
+  if (warp < bands)
+    edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
+      if (y >= ny) return;
+      const long long o = y + static_cast<long long>(ny) * (x + static_cast<long long>(nx) * z);
+      if (win == edt::kNone) {
+        E.site[o] = kSiteNone;
+        E.d2s[o] = kD2None;
+        return;
+      }
+      const uint32_t v = in[edt::at(win, lane)];
+      const int sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
+      const int dx = x - static_cast<int>(win), dy = y - sy, dz = z - sz;
+      E.site[o] = static_cast<uint32_t>(win) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+      E.d2s[o] = static_cast<uint32_t>(dx * dx + dy * dy + dz * dz);
+    });
+}
+
+// ---- recover_signs (esdf.hpp:288-320) ----
+__global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
+  const long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (o >= E.cells) return;
+  const uint32_t site = E.site[o];
+  if (site == kSiteNone) return;
+  const int y = static_cast<int>(o % E.ny);
+  const int x = static_cast<int>((o / E.ny) % E.nx);
+  const int z = static_cast<int>(o / (static_cast<long long>(E.ny) * E.nx));
+  const int sx = site & 1023, sy = (site >> 10) & 1023, sz = site >> 20;
+  const double* cx = E.ctr;
+  const double* cy = E.ctr + E.nx;
+  const double* cz = E.ctr + E.nx + E.ny;
+  const double qx = cx[x], qy = cy[y], qz = cz[z];
+  const double px = cx[sx], py = cy[sy], pz = cz[sz];
+  const double dx = qx - px, dy = qy - py, dz = qz - pz;
+  const double n2 = sum3(dx * dx, dy * dy, dz * dz);
+  bool negative = false, resolved = false;
+  if (n2 > 0.0) {
+    const double n = sqrt(n2);  // delta.normalized() = delta / sqrt(squaredNorm)
+    const double wx = px + E.ve * (dx / n), wy = py + E.ve * (dy / n), wz = pz + E.ve * (dz / n);
+    const int vx = voxel_index(wx, T.voxel), vy = voxel_index(wy, T.voxel), vz = voxel_index(wz, T.voxel);
+    const int pool = dir_lookup(E, vx, vy, vz);
+    if (pool >= 0 && digest_bit(T, pool, kGeomValid, vx, vy, vz)) {  // query_tsdf_geom has a value
+      negative = digest_bit(T, pool, kGeomNeg, vx, vy, vz) != 0;
+      resolved = true;
+    }
+  }
+  if (!resolved) {  // combined sdf at the query cell's own centre
+    const int total = E.nx + E.ny + E.nz;
+    (void)total;
+    const int vx = E.vox[x], vy = E.vox[E.nx + y], vz = E.vox[E.nx + E.ny + z];
+    const int pool = dir_lookup(E, vx, vy, vz);
+    if (pool >= 0 && digest_bit(T, pool, kCombValid, vx, vy, vz)) negative = digest_bit(T, pool, kCombNeg, vx, vy, vz) != 0;
+  }
+  if (negative) E.d2s[o] |= 0x80000000u;
+}
+
+// ---- query (esdf.hpp:337-387) ----
+__device__ __forceinline__ double cell_distance(const EsdfView& E, int x, int y, int z) {
+  const uint32_t v = E.d2s[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)];
+  const double d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;  // esdf.hpp:276-277
+  return (v & 0x80000000u) ? -d : d;
+}
+__global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restrict__ pts, long long n, double* __restrict__ dist,
+                                               double* __restrict__ grad, uint8_t* __restrict__ inside) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  const int dims[3] = {E.nx, E.ny, E.nz};
+  bool in = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) in = in && p[a] >= E.origin[a] && p[a] <= E.origin[a] + dims[a] * E.ve;
+  if (inside) inside[i] = in;
+  if (E.ctrl->seed_count == 0) {  // no sites: +inf, zero gradient (esdf.hpp:345)
+    dist[i] = CUDART_INF;
+    if (grad) grad[3 * i] = grad[3 * i + 1] = grad[3 * i + 2] = 0.0;
+    return;
+  }
+  int i0[3], i1[3];
+  double f[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] == 1) {
+      i0[a] = i1[a] = 0;
+      f[a] = 0.0;
+      continue;
+    }
+    const double s = (p[a] - E.origin[a]) / E.ve - 0.5;
+    const double hi = static_cast<double>(dims[a] - 1);
+    const double c = s < 0.0 ? 0.0 : (hi < s ? hi : s);  // std::clamp
+    const int ic = static_cast<int>(c);
+    i0[a] = ic < dims[a] - 2 ? ic : dims[a] - 2;
+    i1[a] = i0[a] + 1;
+    f[a] = c - i0[a];
+  }
+  const double c000 = cell_distance(E, i0[0], i0[1], i0[2]), c100 = cell_distance(E, i1[0], i0[1], i0[2]);
+  const double c010 = cell_distance(E, i0[0], i1[1], i0[2]), c110 = cell_distance(E, i1[0], i1[1], i0[2]);
+  const double c001 = cell_distance(E, i0[0], i0[1], i1[2]), c101 = cell_distance(E, i1[0], i0[1], i1[2]);
+  const double c011 = cell_distance(E, i0[0], i1[1], i1[2]), c111 = cell_distance(E, i1[0], i1[1], i1[2]);
+  const double fx = f[0], fy = f[1], fz = f[2];
+  const double c00 = c000 * (1 - fx) + c100 * fx, c10 = c010 * (1 - fx) + c110 * fx;
+  const double c01 = c001 * (1 - fx) + c101 * fx, c11 = c011 * (1 - fx) + c111 * fx;
+  const double c0 = c00 * (1 - fy) + c10 * fy, c1 = c01 * (1 - fy) + c11 * fy;
+  dist[i] = c0 * (1 - fz) + c1 * fz;
+  if (grad) {
+    const double inv = 1.0 / E.ve;
+    grad[3 * i] = ((c100 - c000) * (1 - fy) * (1 - fz) + (c110 - c010) * fy * (1 - fz) + (c101 - c001) * (1 - fy) * fz +
+                   (c111 - c011) * fy * fz) *
+                  inv;
+    grad[3 * i + 1] = ((c10 - c00) * (1 - fz) + (c11 - c01) * fz) * inv;
+    grad[3 * i + 2] = (c1 - c0) * inv;
+  }
+}
+
+// ---- export to the reference's DenseEsdf arrays (x-fastest; esdf.hpp:58-64) ----
+__global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ site_xyz, double* __restrict__ distance,
+                                                int* __restrict__ d2) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= E.cells) return;
+  const int x = static_cast<int>(idx % E.nx);
+  const int y = static_cast<int>((idx / E.nx) % E.ny);
+  const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
+  const long long o = y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z);
+  const uint32_t s = E.site[o], v = E.d2s[o];
+  if (site_xyz) {
+    site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
+    site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
+    site_xyz[3 * idx + 2] = s == kSiteNone ? -1 : static_cast<int>(s >> 20);
+  }
+  if (distance) {
+    double d = CUDART_INF;
+    if (s != kSiteNone) {
+      d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;
+      if (v & 0x80000000u) d = -d;
+    }
+    distance[idx] = d;
+  }
+  if (d2) d2[idx] = s == kSiteNone ? 0x7FFFFFFF : static_cast<int>(v & 0x7FFFFFFFu);
+}
+
+}  // namespace ksb
+
+using namespace ksb;
+
+struct ks_esdf {
+  ks_esdf_config cfg;
+  EsdfView view;
+  cudaStream_t stream;
+  bool own_stream;
+  cudaEvent_t dep;
+  EsdfCtrl* h_ctrl;  // pinned
+  double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
+  int band_y, bands_y, band_x, bands_x;
+  size_t smem_y, smem_x;
+  int sticky_err;
+};
+
+namespace ksb {
+
+static void pick_bands(int n, int& band, int& bands) {
+  int warps = std::min(16, std::max(1, (n + 23) / 24));
+  band = (n + warps - 1) / warps;
+  bands = (n + band - 1) / band;
+}
+
+static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
+  const TsdfView& T = tsdf_view(t);
+  if (e->bound_voxel == T.voxel) return KS_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(e->stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone)
+    return fail(KS_ERR_INVALID, "esdf: build once against this TSDF before capturing a graph");
+  EsdfView& E = e->view;
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  if (E.dir) cudaFree(E.dir);
+  E.dir = nullptr;
+  const int dims[3] = {E.nx, E.ny, E.nz};
+  E.dcount = 1;
+  for (int a = 0; a < 3; ++a) {
+    // every probe of seeding / sign recovery lies within one ESDF cell of the box
+    const int lo = (voxel_index(E.origin[a] - E.ve, T.voxel) >> 3) - 1;
+    const int hi = (voxel_index(E.origin[a] + (dims[a] + 1) * E.ve, T.voxel) >> 3) + 1;
+    E.dlo[a] = lo;
+    E.dn[a] = hi - lo + 1;
+    E.dcount *= E.dn[a];
+  }
+  if (E.dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
+  KS_CUDA(cudaMalloc(&E.dir, E.dcount * sizeof(int)));
+  const int total = E.nx + E.ny + E.nz;
+  KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  e->bound_voxel = T.voxel;
+  return KS_OK;
+}
+
+static int order_after(ks_esdf* e, const ks_tsdf* t) {
+  cudaStream_t ts = tsdf_stream(t);
+  if (ts == e->stream) return KS_OK;
+  KS_CUDA(cudaEventRecord(e->dep, ts));
+  KS_CUDA(cudaStreamWaitEvent(e->stream, e->dep, 0));
+  return KS_OK;
+}
+
+static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
+  EsdfView& E = e->view;
+  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, E.dcount * sizeof(int), e->stream));
+  KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+  return KS_OK;
+}
+
+static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode) {
+  EsdfView& E = e->view;
+  KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+  if (mode == 1) {
+    KS_LAUNCH(k_seed_gather, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
+  } else {
+    KS_CUDA(cudaMemsetAsync(E.mask, 0, E.cells, e->stream));
+    KS_LAUNCH(k_seed_scatter, 4 * kSmCount, 512, 0, e->stream, E, tsdf_view(t));
+    KS_LAUNCH(k_count_mask, 4 * kSmCount, 256, 0, e->stream, E);
+  }
+  return KS_OK;
+}
+
+static int propagate_async(ks_esdf* e) {
+  EsdfView& E = e->view;
+  const long long plane = static_cast<long long>(E.nx) * E.ny;
+  const int nwords = (E.nz + 31) / 32;
+  KS_LAUNCH(k_flood_z, static_cast<unsigned>((plane + 127) / 128), 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
+  KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
+  KS_LAUNCH(k_sweep_x, dim3((E.ny + 31) / 32, E.nz), 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+static int signs_async(ks_esdf* e, const ks_tsdf* t) {
+  EsdfView& E = e->view;
+  KS_LAUNCH(k_recover_signs, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
+  const int one = 1;
+  (void)one;
+  KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+}  // namespace ksb
+
+extern "C" {
+
+int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
+  if (!cfg || !out) return fail(KS_ERR_INVALID, "null argument");
+  *out = nullptr;
+  // EsdfConfig::validate (esdf.hpp:41-44)
+  if (cfg->nx < 1 || cfg->ny < 1 || cfg->nz < 1) return fail(KS_ERR_INVALID, "esdf: dims must be >= 1");
+  if (cfg->voxel_size <= 0.0) return fail(KS_ERR_INVALID, "esdf: voxel_size must be > 0");
+  int devices = 0;
+  if (cudaGetDeviceCount(&devices) != cudaSuccess || devices == 0)
+    return fail(KS_ERR_CUDA, "ks_b200: no CUDA device (this library has no CPU path)");
+  if (cfg->nx > kMaxDim || cfg->ny > kMaxDim || cfg->nz > kMaxDim)
+    return fail(KS_ERR_UNSUPPORTED, "esdf: dims above 1024 per axis are not supported by this build");
+  ks_esdf* e = new ks_esdf();
+  std::memset(static_cast<void*>(e), 0, sizeof(*e));
+  e->cfg = *cfg;
+  EsdfView& E = e->view;
+  E.nx = cfg->nx, E.ny = cfg->ny, E.nz = cfg->nz;
+  E.cells = static_cast<long long>(cfg->nx) * cfg->ny * cfg->nz;
+  for (int a = 0; a < 3; ++a) E.origin[a] = cfg->origin[a];
+  E.ve = cfg->voxel_size;
+  pick_bands(E.ny, e->band_y, e->bands_y);
+  pick_bands(E.nx, e->band_x, e->bands_x);
+  e->smem_y = sweep_smem_bytes(E.ny, e->bands_y, 2);
+  e->smem_x = sweep_smem_bytes(E.nx, e->bands_x, 4);
+  if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
+    delete e;
+    return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 900, nx <= 720)");
+  }
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  e->own_stream = true;
+  KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
+  const int total = E.nx + E.ny + E.nz;
+  KS_CUDA(cudaMalloc(&E.vox, 3 * total * sizeof(int)));
+  KS_CUDA(cudaMalloc(&E.ctr, total * sizeof(double)));
+  KS_CUDA(cudaMalloc(&E.mask, E.cells));
+  KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
+  KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.site, E.cells * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.d2s, E.cells * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
+  KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
+  KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.site, 0xFF, E.cells * sizeof(uint32_t), e->stream));  // no sites yet
+  KS_CUDA(cudaMemsetAsync(E.d2s, 0xFF, E.cells * sizeof(uint32_t), e->stream));
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  *out = e;
+  return KS_OK;
+}
+
+void ks_esdf_destroy(ks_esdf* e) {
+  if (!e) return;
+  cudaStreamSynchronize(e->stream);
+  EsdfView& E = e->view;
+  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.ctrl);
+  if (E.dir) cudaFree(E.dir);
+  cudaFreeHost(e->h_ctrl);
+  cudaEventDestroy(e->dep);
+  if (e->own_stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+int ks_esdf_set_stream(ks_esdf* e, ks_stream s) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->own_stream) cudaStreamDestroy(e->stream);
+  e->own_stream = false;
+  e->stream = static_cast<cudaStream_t>(s);
+  return KS_OK;
+}
+
+int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
+  if (!e || !t) return fail(KS_ERR_INVALID, "null argument");
+  int rc;
+  if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
+  if ((rc = order_after(e, t)) != KS_OK) return rc;
+  if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  if ((rc = seed_async(e, t, e->cfg.seeding)) != KS_OK) return rc;
+  if ((rc = propagate_async(e)) != KS_OK) return rc;
+  return signs_async(e, t);
+}
+
+int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  KS_CUDA(cudaMemcpyAsync(e->h_ctrl, e->view.ctrl, sizeof(EsdfCtrl), cudaMemcpyDeviceToHost, e->stream));
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  if (report) {
+    report->status = KS_OK;
+    report->has_sites = e->h_ctrl->seed_count > 0;
+    report->signs_recovered = e->h_ctrl->signs_recovered != 0;
+    report->seed_count = static_cast<int64_t>(e->h_ctrl->seed_count);
+  }
+  return KS_OK;
+}
+
+int ks_esdf_build(ks_esdf* e, const ks_tsdf* t) {
+  int rc = ks_esdf_build_async(e, t);
+  return rc != KS_OK ? rc : ks_esdf_sync(e, nullptr);
+}
+
+int ks_esdf_seed(ks_esdf* e, const ks_tsdf* t, int32_t mode, uint8_t* mask_host) {
+  if (!e || !t) return fail(KS_ERR_INVALID, "null argument");
+  int rc;
+  if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
+  if ((rc = order_after(e, t)) != KS_OK) return rc;
+  if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  if ((rc = seed_async(e, t, mode)) != KS_OK) return rc;
+  if (mask_host) KS_CUDA(cudaMemcpyAsync(mask_host, e->view.mask, e->view.cells, cudaMemcpyDeviceToHost, e->stream));
+  return ks_esdf_sync(e, nullptr);
+}
+
+int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_len) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  EsdfView& E = e->view;
+  if (mask_host) {
+    if (mask_len != E.cells) return fail(KS_ERR_INVALID, "esdf: seed mask size does not match grid");  // esdf.hpp:195-196
+    KS_CUDA(cudaMemcpyAsync(E.mask, mask_host, E.cells, cudaMemcpyHostToDevice, e->stream));
+    KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+    KS_LAUNCH(k_count_mask, 4 * kSmCount, 256, 0, e->stream, E);
+  } else {
+    KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 0, sizeof(int), e->stream));
+  }
+  int rc = propagate_async(e);
+  return rc != KS_OK ? rc : ks_esdf_sync(e, nullptr);
+}
+
+int ks_esdf_recover_signs(ks_esdf* e, const ks_tsdf* t) {
+  if (!e || !t) return fail(KS_ERR_INVALID, "null argument");
+  int rc;
+  if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
+  if ((rc = order_after(e, t)) != KS_OK) return rc;
+  if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  if ((rc = signs_async(e, t)) != KS_OK) return rc;
+  return ks_esdf_sync(e, nullptr);
+}
+
+int ks_esdf_download(ks_esdf* e, int32_t* site_xyz, double* distance, int32_t* d2) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  EsdfView& E = e->view;
+  int* d_site = nullptr;
+  double* d_dist = nullptr;
+  int* d_d2 = nullptr;
+  if (site_xyz) KS_CUDA(cudaMalloc(&d_site, E.cells * 3 * sizeof(int)));
+  if (distance) KS_CUDA(cudaMalloc(&d_dist, E.cells * sizeof(double)));
+  if (d2) KS_CUDA(cudaMalloc(&d_d2, E.cells * sizeof(int)));
+  KS_LAUNCH(k_export, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, d_site, d_dist, d_d2);
+  if (site_xyz) KS_CUDA(cudaMemcpyAsync(site_xyz, d_site, E.cells * 3 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  if (distance) KS_CUDA(cudaMemcpyAsync(distance, d_dist, E.cells * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  if (d2) KS_CUDA(cudaMemcpyAsync(d2, d_d2, E.cells * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d_site), cudaFree(d_dist), cudaFree(d_d2);
+  return KS_OK;
+}
+
+int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, double* distance_dev, double* gradient_dev,
+                               uint8_t* inside_dev) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  if (n <= 0) return KS_OK;
+  KS_LAUNCH(k_query, static_cast<unsigned>((n + 255) / 256), 256, 0, e->stream, e->view, points_dev, static_cast<long long>(n),
+            distance_dev, gradient_dev, inside_dev);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, double* distance, double* gradient_xyz, uint8_t* inside) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  if (n <= 0) return KS_OK;
+  double *d_pts = nullptr, *d_dist = nullptr, *d_grad = nullptr;
+  uint8_t* d_in = nullptr;
+  KS_CUDA(cudaMalloc(&d_pts, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_dist, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_grad, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_in, n));
+  KS_CUDA(cudaMemcpyAsync(d_pts, points_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  int rc = ks_esdf_query_device_async(e, d_pts, n, d_dist, d_grad, d_in);
+  if (rc == KS_OK) {
+    if (distance) KS_CUDA(cudaMemcpyAsync(distance, d_dist, n * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (gradient_xyz) KS_CUDA(cudaMemcpyAsync(gradient_xyz, d_grad, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (inside) KS_CUDA(cudaMemcpyAsync(inside, d_in, n, cudaMemcpyDeviceToHost, e->stream));
+    KS_CUDA(cudaStreamSynchronize(e->stream));
+  }
+  cudaFree(d_pts), cudaFree(d_dist), cudaFree(d_grad), cudaFree(d_in);
+  return rc;
+}
+
+}  // extern "C"

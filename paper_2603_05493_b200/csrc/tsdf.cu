@@ -1,0 +1,980 @@
+// Block-sparse TSDF on the device: hash/allocation, depth integration, primitive
+// stamping, decay/recycle, point lookup.  Replaces the TSDF half of
+// /root/reference/proj/include/ks/sdf_world.hpp behind the C ABI in
+// include/ks_b200.h.  See DESIGN.md for the HBM layout and kernel roster.
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ksb {
+
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
+struct FrameParams {  // per-frame inputs, staged in pinned memory and uploaded with the pixels
+  int width, height;
+  double fx, fy, cx, cy;
+  Rigid c2w, w2c;
+  int half_samples;  // sdf_world.hpp:348
+  double step;       // sdf_world.hpp:347
+};
+
+struct OpLists {  // scratch of the op in flight (discover -> rank -> commit -> apply)
+  uint64_t* key;       // [cap] unique blocks touched
+  int* pool;           // [cap] pool entry (filled by commit for new blocks)
+  uint32_t* slot;      // [cap] slot in the per-frame set to clear afterwards (kNoSlot for stamps)
+  int* fresh_idx;      // [cap] indices into key[] of blocks that must be allocated
+  int* fresh_rank;     // [cap] rank of that key among the new keys (lexicographic)
+  int cap;
+  uint64_t* fset;      // per-frame dedup set, open addressing
+  uint32_t fset_mask;  // slots - 1
+};
+
+struct Primitive {  // ks::Cuboid / ks::SphereShape (sdf_world.hpp:212-220)
+  int is_sphere;
+  Rigid inv;  // cuboid: pose.inverse()
+  double he[3];
+  double c[3];
+  double radius;
+};
+
+struct Frustum {  // block_in_frustum planes (sdf_world.hpp:296-301), camera frame
+  double n[5][3];
+  Rigid w2c;
+  double radius;
+};
+
+}  // namespace ksb
+
+using namespace ksb;
+
+struct ks_tsdf {
+  ks_tsdf_config cfg;
+  TsdfView view;
+  cudaStream_t stream;
+  bool own_stream;
+  TsdfCtrl* h_ctrl;  // pinned
+  // frame staging
+  FrameParams* h_frame;  // pinned
+  FrameParams* d_frame;
+  float* h_depth;  // pinned
+  float* d_depth;
+  size_t depth_cap;  // pixels
+  bool frame_staged;
+  OpLists lists;
+  int* d_flags;  // [capacity] recycle flags
+};
+
+namespace ksb {
+const TsdfView& tsdf_view(const ks_tsdf* t) { return t->view; }
+cudaStream_t tsdf_stream(const ks_tsdf* t) { return t->stream; }
+
+// ---- device helpers ---------------------------------------------------------------
+
+__device__ __forceinline__ bool depth_valid(float d) { return isfinite(d) && d > 0.0f; }  // sdf_world.hpp:203
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+// sdf_cuboid / sdf_sphere (sdf_world.hpp:224-233)
+__device__ __forceinline__ double prim_sdf(const Primitive& P, double x, double y, double z) {
+  if (P.is_sphere) {
+    const double dx = x - P.c[0], dy = y - P.c[1], dz = z - P.c[2];
+    return sqrt(sum3(dx * dx, dy * dy, dz * dz)) - P.radius;
+  }
+  double l[3];
+  rigid_apply(P.inv, x, y, z, l);
+  const double q0 = fabs(l[0]) - P.he[0], q1 = fabs(l[1]) - P.he[1], q2 = fabs(l[2]) - P.he[2];
+  const double o0 = q0 < 0.0 ? 0.0 : q0, o1 = q1 < 0.0 ? 0.0 : q1, o2 = q2 < 0.0 ? 0.0 : q2;  // cwiseMax(0.0)
+  double mx = q1 < q2 ? q2 : q1;
+  mx = q0 < mx ? mx : q0;
+  return sqrt(sum3(o0 * o0, o1 * o1, o2 * o2)) + (0.0 < mx ? 0.0 : mx);  // + std::min(maxCoeff, 0.0)
+}
+
+// Effective-sdf predicates of one voxel (query_channel, sdf_world.hpp:481-494;
+// seed_threshold, esdf.hpp:69) -> the five digest bits.
+__device__ __forceinline__ uint32_t voxel_bits(double sum, double wt, double geom, double seed_thr) {
+  const bool dv = wt > 0.0;
+  const bool gv = isfinite(geom);
+  double best = 0.0;
+  if (dv) best = sum / wt;
+  if (gv) best = dv ? (geom < best ? geom : best) : geom;  // std::min(best, geom)
+  const bool cv = dv || gv;
+  uint32_t bits = 0;
+  if (cv && fabs(best) < seed_thr) bits |= 1u << kSurface;
+  if (gv) bits |= 1u << kGeomValid;
+  if (gv && geom < 0.0) bits |= 1u << kGeomNeg;
+  if (cv) bits |= 1u << kCombValid;
+  if (cv && best < 0.0) bits |= 1u << kCombNeg;
+  return bits;
+}
+
+// One warp = 32 consecutive voxels = one word of each plane.
+__device__ __forceinline__ void store_digest(uint32_t* digest, int pool, int tid, uint32_t bits) {
+  const int word = tid >> 5, lane = tid & 31;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int p = 0; p < kDigestPlanes; ++p) {
+    const uint32_t w = __ballot_sync(0xFFFFFFFFu, (bits >> p) & 1u);
+    if (lane == p) mine = w;
+  }
+  if (lane < kDigestPlanes) digest[static_cast<size_t>(pool) * kDigestWords + lane * 16 + word] = mine;
+}
+
+__device__ __forceinline__ bool op_blocked(const TsdfView& T) {
+  const TsdfCtrl* c = T.ctrl;
+  // pool exhaustion (allocate_keys, sdf_world.hpp:315-318) and a table without room are both
+  // decided before anything is inserted, so a failing op leaves the world untouched
+  return c->abort_op != 0 || c->fresh > c->free_count + (T.capacity - c->next_fresh) || c->live + c->fresh > T.nslots;
+}
+
+// Record a block the op touches; new blocks also join the allocation list.
+__device__ __forceinline__ void note_block(const TsdfView& T, const OpLists& L, int bx, int by, int bz, uint32_t slot) {
+  const int pool = table_find(T, bx, by, bz);
+  const int idx = atomicAdd(&T.ctrl->touched, 1);
+  if (idx < L.cap) {
+    L.key[idx] = pack_key(bx, by, bz);
+    L.pool[idx] = pool;
+    L.slot[idx] = slot;
+  }
+  if (pool < 0) {
+    const int j = atomicAdd(&T.ctrl->fresh, 1);
+    if (j < L.cap) L.fresh_idx[j] = idx;
+  }
+}
+
+// ---- phase 1+2: block discovery along rays + dedup (sdf_world.hpp:346-361, :308-311) ----
+__global__ void __launch_bounds__(256) k_discover(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
+                                                  const float* __restrict__ depth) {
+  const FrameParams& F = *Fp;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= F.width * F.height) return;
+  const float d = depth[pix];
+  if (!depth_valid(d)) return;
+  const int px = pix % F.width, py = pix / F.width;
+  const double dd = static_cast<double>(d);
+  const double sx = (px - F.cx) * dd / F.fx, sy = (py - F.cy) * dd / F.fy, sz = dd;
+  double ux = sx, uy = sy, uz = sz;  // normalized()
+  {
+    const double z = sum3(sx * sx, sy * sy, sz * sz);
+    if (z > 0.0) {
+      const double n = sqrt(z);
+      ux = sx / n, uy = sy / n, uz = sz / n;
+    }
+  }
+  uint64_t prev = kKeyEmpty;
+  for (int s = -F.half_samples; s <= F.half_samples; ++s) {
+    double off = s * F.step;
+    off = off < -T.trunc ? -T.trunc : (T.trunc < off ? T.trunc : off);  // std::clamp
+    double w[3];
+    rigid_apply(F.c2w, sx + off * ux, sy + off * uy, sz + off * uz, w);
+    const int bx = voxel_index(w[0], T.voxel) >> 3, by = voxel_index(w[1], T.voxel) >> 3,
+              bz = voxel_index(w[2], T.voxel) >> 3;  // floor_div(v, 8) == arithmetic shift
+    if (!key_in_range(bx, by, bz)) {
+      T.ctrl->abort_op = 1;
+      continue;
+    }
+    const uint64_t key = pack_key(bx, by, bz);
+    if (key == prev) continue;
+    prev = key;
+    uint32_t i = static_cast<uint32_t>(mix64(key)) & L.fset_mask;
+    while (true) {
+      const uint64_t cur = L.fset[i];
+      if (cur == key) break;
+      if (cur == kKeyEmpty) {
+        const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long*>(&L.fset[i]), kKeyEmpty, key);
+        if (old == kKeyEmpty) {
+          note_block(T, L, bx, by, bz, i);
+          break;
+        }
+        if (old == key) break;
+      }
+      i = (i + 1) & L.fset_mask;
+    }
+  }
+}
+
+// ---- phase 3a: rank of every new key among the new keys (sorted order of allocate_keys) ----
+__global__ void __launch_bounds__(256) k_rank(TsdfView T, OpLists L) {
+  if (op_blocked(T)) return;
+  const int n = min(T.ctrl->fresh, L.cap);
+  __shared__ uint64_t tile[256];
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const int i = base + threadIdx.x;
+    const uint64_t mine = i < n ? L.key[L.fresh_idx[i]] : 0;
+    int rank = 0;
+    for (int t0 = 0; t0 < n; t0 += 256) {
+      const int j = t0 + threadIdx.x;
+      tile[threadIdx.x] = j < n ? L.key[L.fresh_idx[j]] : kKeyEmpty;
+      __syncthreads();
+      const int m = min(256, n - t0);
+#pragma unroll 8
+      for (int k = 0; k < m; ++k) rank += tile[k] < mine;
+      __syncthreads();
+    }
+    if (i < n) L.fresh_rank[i] = rank;
+  }
+}
+
+// ---- phase 3b: pool assignment (free list first, LIFO), warp-cooperative hash insert, block reset
+// (BlockHashTable::insert sdf_world.hpp:146-172, VoxelBlock::reset :70-74) ----
+__global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
+  if (op_blocked(T)) return;
+  const TsdfCtrl* c = T.ctrl;
+  const int n = min(c->fresh, L.cap);
+  const int free_count = c->free_count, next_fresh = c->next_fresh;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int idx = L.fresh_idx[i];
+    const uint64_t key = L.key[idx];
+    const int r = L.fresh_rank[i];
+    const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int bx, by, bz;
+      unpack_key(key, bx, by, bz);
+      const uint32_t nslots = static_cast<uint32_t>(T.nslots);
+      const uint32_t start = static_cast<uint32_t>(block_hash(bx, by, bz) % nslots);
+      bool done = false;
+      for (uint32_t base = 0; base < nslots && !done; base += 32) {
+        const uint32_t off = base + lane;
+        const bool active = off < nslots;
+        const uint32_t s = active ? (start + off) % nslots : 0;
+        const uint64_t k = active ? T.slot_key[s] : 0;
+        uint32_t open = __ballot_sync(0xFFFFFFFFu, active && (k == kKeyEmpty || k == kKeyTomb));
+        while (open != 0 && !done) {
+          const int first = __ffs(open) - 1;
+          int ok = 0;
+          if (lane == first) {
+            ok = atomicCAS(reinterpret_cast<unsigned long long*>(&T.slot_key[s]), k, key) == k;
+            if (ok) T.slot_pool[s] = pool;
+          }
+          done = __shfl_sync(0xFFFFFFFFu, ok, first) != 0;
+          open &= ~(1u << first);
+        }
+      }
+      if (lane == 0) {
+        if (done) {
+          T.pool_key[pool] = key;
+          L.pool[idx] = pool;
+        } else {
+          atomicCAS(&T.ctrl->err, 0, static_cast<int>(KS_ERR_TABLE_FULL));
+          T.ctrl->abort_op = 1;
+        }
+      }
+    }
+    // reset the block: sum = wt = 0, geom = +inf, digest = 0
+    double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
+    double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
+    for (int q = threadIdx.x; q < kBlockVoxels; q += blockDim.x) {
+      sw[q] = make_double2(0.0, 0.0);
+      g[q] = CUDART_INF;
+    }
+    if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
+  }
+}
+
+// ---- phase 4: voxel-centric projective integration (sdf_world.hpp:368-387) ----
+// One CTA per touched block, one thread per voxel: each thread owns its voxel,
+// so there are no atomics; {sum, wt} moves as one 16-byte access per thread.
+__global__ void __launch_bounds__(512) k_integrate(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
+                                                   const float* __restrict__ depth) {
+  __shared__ FrameParams F;
+  if (threadIdx.x < sizeof(FrameParams) / 4)
+    reinterpret_cast<uint32_t*>(&F)[threadIdx.x] = reinterpret_cast<const uint32_t*>(Fp)[threadIdx.x];
+  __syncthreads();
+  const int touched = min(T.ctrl->touched, L.cap);
+  const bool blocked = op_blocked(T);
+  const int tid = threadIdx.x;
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const double v = T.voxel, trunc = T.trunc;
+  for (int i = blockIdx.x; i < touched; i += gridDim.x) {
+    if (tid == 0 && L.slot[i] != kNoSlot) L.fset[L.slot[i]] = kKeyEmpty;  // leave the frame set clean
+    if (blocked) continue;
+    const int pool = L.pool[i];
+    int bx, by, bz;
+    unpack_key(L.key[i], bx, by, bz);
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+    double2 sw = T.sumwt[at];
+    const double geom = T.geom[at];
+    // voxel_center (sdf_world.hpp:265-272)
+    double c[3];
+    rigid_apply(F.w2c, (bx * kBlockEdge + lx + 0.5) * v, (by * kBlockEdge + ly + 0.5) * v,
+                (bz * kBlockEdge + lz + 0.5) * v, c);
+    if (c[2] > 0.0) {
+      const int px = static_cast<int>(lround(F.fx * c[0] / c[2] + F.cx));
+      const int py = static_cast<int>(lround(F.fy * c[1] / c[2] + F.cy));
+      if (px >= 0 && px < F.width && py >= 0 && py < F.height) {
+        const float d = __ldg(depth + static_cast<size_t>(py) * F.width + px);
+        if (depth_valid(d)) {
+          const double sd_raw = static_cast<double>(d) - c[2];
+          if (!(sd_raw < -trunc)) {
+            const double sd = trunc < sd_raw ? trunc : sd_raw;  // std::min(sd_raw, trunc)
+            const double cc = (F.fx * v / c[2]) * (F.fy * v / c[2]);
+            const double w = cc < 1.0 ? 1.0 : cc;  // std::max(c, 1.0)
+            sw.x += w * sd;
+            sw.y += w;
+            T.sumwt[at] = sw;
+          }
+        }
+      }
+    }
+    store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, geom, T.seed_thr));
+  }
+}
+
+// ---- stamp: candidate blocks in the primitive's padded AABB (sdf_world.hpp:421-434) ----
+struct BlockBox {
+  int lo[3], n[3];
+  long long count;
+};
+__global__ void __launch_bounds__(256) k_stamp_candidates(TsdfView T, OpLists L, Primitive P, BlockBox B, double reach) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < B.count;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int bx = B.lo[0] + static_cast<int>(i % B.n[0]);
+    const int by = B.lo[1] + static_cast<int>((i / B.n[0]) % B.n[1]);
+    const int bz = B.lo[2] + static_cast<int>(i / (static_cast<long long>(B.n[0]) * B.n[1]));
+    // block_center (sdf_world.hpp:282-286)
+    const double sd = prim_sdf(P, (bx * kBlockEdge + 0.5 * kBlockEdge) * T.voxel,
+                               (by * kBlockEdge + 0.5 * kBlockEdge) * T.voxel,
+                               (bz * kBlockEdge + 0.5 * kBlockEdge) * T.voxel);
+    if (!(fabs(sd) <= reach)) continue;
+    if (!key_in_range(bx, by, bz)) {
+      T.ctrl->abort_op = 1;
+      continue;
+    }
+    note_block(T, L, bx, by, bz, kNoSlot);
+  }
+}
+
+// ---- stamp: per-voxel min with the analytic distance (sdf_world.hpp:437-443) ----
+__global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Primitive P) {
+  if (op_blocked(T)) return;
+  const int touched = min(T.ctrl->touched, L.cap);
+  const int tid = threadIdx.x;
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const double v = T.voxel;
+  for (int i = blockIdx.x; i < touched; i += gridDim.x) {
+    const int pool = L.pool[i];
+    int bx, by, bz;
+    unpack_key(L.key[i], bx, by, bz);
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+    const double sd = prim_sdf(P, (bx * kBlockEdge + lx + 0.5) * v, (by * kBlockEdge + ly + 0.5) * v,
+                               (bz * kBlockEdge + lz + 0.5) * v);
+    double g = T.geom[at];
+    if (sd < g) {  // std::min(geom, sd)
+      g = sd;
+      T.geom[at] = g;
+    }
+    const double2 sw = T.sumwt[at];
+    store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
+  }
+}
+
+// ---- op tail: commit the counters, surface errors (allocate_keys :312-318) ----
+__global__ void k_finish(TsdfView T, int list_cap, int is_integrate) {
+  TsdfCtrl* c = T.ctrl;
+  const int avail = c->free_count + (T.capacity - c->next_fresh);
+  int status = 0;
+  if (c->abort_op) {
+    status = c->err != 0 ? c->err : static_cast<int>(KS_ERR_RANGE);
+  } else if (c->fresh > avail || c->touched > list_cap) {
+    status = KS_ERR_POOL_EXHAUSTED;
+    if (c->err == 0) {
+      c->err_required = c->fresh;
+      c->err_available = avail;
+    }
+  } else if (c->live + c->fresh > T.nslots) {
+    status = KS_ERR_TABLE_FULL;
+  } else {
+    const int from_free = min(c->fresh, c->free_count);
+    c->free_count -= from_free;
+    c->next_fresh += c->fresh - from_free;
+    c->live += c->fresh;
+  }
+  if (status != 0 && c->err == 0) c->err = status;
+  if (is_integrate) c->last_touched = status == 0 ? c->touched : -1;
+  c->touched = 0;
+  c->fresh = 0;
+  c->abort_op = 0;
+}
+
+// ---- decay_weights (sdf_world.hpp:449-457) ----
+__global__ void __launch_bounds__(512) k_decay(TsdfView T, Frustum Fr, double alpha_t, double alpha_f) {
+  const int bound = T.ctrl->next_fresh;
+  const int tid = threadIdx.x;
+  for (int pool = blockIdx.x; pool < bound; pool += gridDim.x) {
+    const uint64_t key = T.pool_key[pool];
+    if (key == kKeyEmpty) continue;
+    int bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    double c[3];
+    rigid_apply(Fr.w2c, (bx * kBlockEdge + 0.5 * kBlockEdge) * T.voxel, (by * kBlockEdge + 0.5 * kBlockEdge) * T.voxel,
+                (bz * kBlockEdge + 0.5 * kBlockEdge) * T.voxel, c);
+    bool inside = true;
+#pragma unroll
+    for (int p = 0; p < 5; ++p)
+      if (sum3(Fr.n[p][0] * c[0], Fr.n[p][1] * c[1], Fr.n[p][2] * c[2]) < -Fr.radius) inside = false;
+    double factor = alpha_t;
+    if (inside) factor *= alpha_f;
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+    double2 sw = T.sumwt[at];
+    sw.y *= factor;  // depth_sum is deliberately not scaled (sdf_world.hpp:455)
+    T.sumwt[at] = sw;
+    store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, T.geom[at], T.seed_thr));
+  }
+}
+
+// ---- recycle_blocks (sdf_world.hpp:462-475) ----
+// weight_total() is a sequential sum (sdf_world.hpp:75-79); it is compared with a
+// threshold, so the summation order is kept: one thread walks its block in order.
+__global__ void __launch_bounds__(128) k_recycle_flag(TsdfView T, int* flags, double threshold) {
+  const int bound = T.ctrl->next_fresh;
+  for (int pool = blockIdx.x * blockDim.x + threadIdx.x; pool < bound; pool += gridDim.x * blockDim.x) {
+    int flag = 0;
+    if (T.pool_key[pool] != kKeyEmpty) {
+      const double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
+      const double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
+      double total = 0.0;
+      bool has_geom = false;
+      for (int q = 0; q < kBlockVoxels; ++q) {
+        total += sw[q].y;
+        has_geom |= isfinite(g[q]);
+      }
+      flag = total < threshold && !has_geom;
+    }
+    flags[pool] = flag;
+  }
+}
+// Tombstone flagged blocks in SLOT order and append their pool entries to the free list
+// in that order (the reference's iteration order, sdf_world.hpp:464-472).
+__global__ void __launch_bounds__(1024) k_recycle_commit(TsdfView T, const int* flags) {
+  __shared__ int warp_sum[32];
+  __shared__ int s_base;
+  TsdfCtrl* c = T.ctrl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int s0 = 0; s0 < T.nslots; s0 += blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    int pool = -1, f = 0;
+    if (s < T.nslots) {
+      const uint64_t k = T.slot_key[s];
+      if (k != kKeyEmpty && k != kKeyTomb) {
+        pool = T.slot_pool[s];
+        f = flags[pool];
+      }
+    }
+    int incl = f;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int up = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += up;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = warp_sum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int up = __shfl_up_sync(0xFFFFFFFFu, w, d);
+        if (lane >= d) w += up;
+      }
+      warp_sum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int before = s_base + (warp > 0 ? warp_sum[warp - 1] : 0) + incl - f;
+    if (f) {
+      T.free_list[c->free_count + before] = pool;
+      T.slot_key[s] = kKeyTomb;
+      T.slot_pool[s] = -1;
+      T.pool_key[pool] = kKeyEmpty;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += warp_sum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    c->free_count += s_base;
+    c->live -= s_base;
+    c->last_recycled = s_base;
+  }
+}
+
+// ---- query_tsdf / query_tsdf_geom (sdf_world.hpp:481-507) ----
+__global__ void __launch_bounds__(256) k_query_tsdf(TsdfView T, const double* __restrict__ pts, long long n, int geom_only,
+                                                    double* __restrict__ out, uint8_t* __restrict__ valid) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int vx = voxel_index(pts[3 * i], T.voxel), vy = voxel_index(pts[3 * i + 1], T.voxel),
+            vz = voxel_index(pts[3 * i + 2], T.voxel);
+  const int pool = table_find(T, vx >> 3, vy >> 3, vz >> 3);
+  double best = 0.0;
+  bool have = false;
+  if (pool >= 0) {
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + ((vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7)));
+    const double2 sw = T.sumwt[at];
+    const double g = T.geom[at];
+    if (!geom_only && sw.y > 0.0) {
+      best = sw.x / sw.y;
+      have = true;
+    }
+    if (isfinite(g)) {
+      best = have ? (g < best ? g : best) : g;
+      have = true;
+    }
+  }
+  out[i] = have ? best : 0.0;
+  valid[i] = have;
+}
+
+__global__ void k_find(TsdfView T, int bx, int by, int bz, int* out) { *out = table_find(T, bx, by, bz); }
+
+__global__ void k_fill_u64(uint64_t* p, size_t n, uint64_t v) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// ---- host side ----------------------------------------------------------------------
+
+static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
+  const size_t want = std::max<size_t>(pixels * samples, 2 * static_cast<size_t>(t->cfg.capacity) + 1);
+  if (static_cast<size_t>(t->lists.cap) >= want && t->depth_cap >= pixels) return KS_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(t->stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone)
+    return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  OpLists& L = t->lists;
+  if (static_cast<size_t>(L.cap) < want) {
+    cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
+    L.cap = static_cast<int>(want);
+    KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
+    KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
+    KS_CUDA(cudaMalloc(&L.slot, want * sizeof(uint32_t)));
+    KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
+    KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
+    uint32_t slots = 1u << 16;
+    while (slots < 2 * want) slots <<= 1;
+    L.fset_mask = slots - 1;
+    KS_CUDA(cudaMalloc(&L.fset, static_cast<size_t>(slots) * sizeof(uint64_t)));
+    KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, L.fset, static_cast<size_t>(slots), kKeyEmpty);
+  }
+  if (t->depth_cap < pixels) {
+    if (t->h_depth) cudaFreeHost(t->h_depth);
+    if (t->d_depth) cudaFree(t->d_depth);
+    t->h_depth = nullptr, t->d_depth = nullptr;
+    KS_CUDA(cudaMallocHost(&t->h_depth, pixels * sizeof(float)));
+    KS_CUDA(cudaMalloc(&t->d_depth, pixels * sizeof(float)));
+    t->depth_cap = pixels;
+  }
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  return KS_OK;
+}
+
+static void run_allocation(ks_tsdf* t) {
+  KS_LAUNCH(k_rank, 2 * kSmCount, 256, 0, t->stream, t->view, t->lists);
+  KS_LAUNCH(k_commit, 4 * kSmCount, 256, 0, t->stream, t->view, t->lists);
+}
+
+static int report_status(const TsdfCtrl& c) {
+  switch (c.err) {
+    case KS_OK:
+      return KS_OK;
+    case KS_ERR_POOL_EXHAUSTED:
+      return fail(KS_ERR_POOL_EXHAUSTED, "tsdf: pool exhausted, frame requires " + std::to_string(c.err_required) +
+                                             " new blocks but only " + std::to_string(c.err_available) + " are available");
+    case KS_ERR_TABLE_FULL:
+      return fail(KS_ERR_TABLE_FULL, "tsdf: hash table full");
+    case KS_ERR_RANGE:
+      return fail(KS_ERR_RANGE, "tsdf: block coordinate outside the supported +-2^20 range");
+    default:
+      return fail(c.err, "tsdf: device error " + std::to_string(c.err));
+  }
+}
+
+static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], const double hi_in[3]) {
+  // AABB grown by the truncation band -> block range (sdf_world.hpp:418-425)
+  const double v = t->cfg.voxel_size, trunc = t->cfg.truncation;
+  BlockBox B;
+  B.count = 1;
+  for (int a = 0; a < 3; ++a) {
+    const double lo = lo_in[a] - trunc, hi = hi_in[a] + trunc;
+    const int blo = voxel_index(lo, v) >> 3, bhi = voxel_index(hi, v) >> 3;
+    B.lo[a] = blo;
+    B.n[a] = bhi - blo + 1;
+    if (B.n[a] < 1) B.n[a] = 0;
+    B.count *= B.n[a];
+  }
+  const double reach = trunc + 0.5 * kBlockEdge * v * std::sqrt(3.0);  // sdf_world.hpp:288-290, :425
+  if (B.count > 0) {
+    const int grid = static_cast<int>(std::min<long long>((B.count + 255) / 256, 8 * kSmCount));
+    KS_LAUNCH(k_stamp_candidates, grid, 256, 0, t->stream, t->view, t->lists, P, B, reach);
+  }
+  run_allocation(t);
+  KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
+  KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 0);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+}  // namespace ksb
+
+extern "C" {
+
+int ks_tsdf_config_init(double voxel_size, ks_tsdf_config* out) {
+  if (!out) return fail(KS_ERR_INVALID, "null config");
+  *out = ks_tsdf_config{voxel_size, 4.0 * voxel_size, 0.99, 0.5, 0.5, 8192, 0};  // sdf_world.hpp:39-45, :56-61
+  return KS_OK;
+}
+
+int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
+  if (!cfg || !out) return fail(KS_ERR_INVALID, "null argument");
+  *out = nullptr;
+  // TsdfConfig::validate (sdf_world.hpp:47-53)
+  if (cfg->voxel_size <= 0.0) return fail(KS_ERR_INVALID, "tsdf: voxel_size must be > 0");
+  if (cfg->truncation < cfg->voxel_size) return fail(KS_ERR_INVALID, "tsdf: truncation must be >= voxel_size");
+  if (!(cfg->alpha_time > 0.0 && cfg->alpha_time <= 1.0) || !(cfg->alpha_frustum > 0.0 && cfg->alpha_frustum <= 1.0))
+    return fail(KS_ERR_INVALID, "tsdf: decay factors must lie in (0, 1]");
+  if (cfg->capacity < 1) return fail(KS_ERR_INVALID, "tsdf: capacity must be >= 1");
+  int devices = 0;
+  if (cudaGetDeviceCount(&devices) != cudaSuccess || devices == 0)
+    return fail(KS_ERR_CUDA, "ks_b200: no CUDA device (this library has no CPU path)");
+
+  ks_tsdf* t = new ks_tsdf();
+  std::memset(static_cast<void*>(t), 0, sizeof(*t));
+  t->cfg = *cfg;
+  TsdfView& V = t->view;
+  V.capacity = cfg->capacity;
+  V.nslots = cfg->slot_count > 0 ? cfg->slot_count : 2 * cfg->capacity;  // BlockHashTable::init (sdf_world.hpp:115-120)
+  V.voxel = cfg->voxel_size;
+  V.trunc = cfg->truncation;
+  V.seed_thr = 0.9 * cfg->voxel_size;  // seed_threshold (esdf.hpp:69)
+  const size_t cap = static_cast<size_t>(cfg->capacity);
+  KS_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  t->own_stream = true;
+  KS_CUDA(cudaMalloc(&V.slot_key, V.nslots * sizeof(uint64_t)));
+  KS_CUDA(cudaMalloc(&V.slot_pool, V.nslots * sizeof(int)));
+  KS_CUDA(cudaMalloc(&V.free_list, cap * sizeof(int)));
+  KS_CUDA(cudaMalloc(&V.pool_key, cap * sizeof(uint64_t)));
+  KS_CUDA(cudaMalloc(&V.sumwt, cap * kBlockVoxels * sizeof(double2)));
+  KS_CUDA(cudaMalloc(&V.geom, cap * kBlockVoxels * sizeof(double)));
+  KS_CUDA(cudaMalloc(&V.digest, cap * kDigestWords * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&V.ctrl, sizeof(TsdfCtrl)));
+  KS_CUDA(cudaMalloc(&t->d_flags, cap * sizeof(int)));
+  KS_CUDA(cudaMallocHost(&t->h_ctrl, sizeof(TsdfCtrl)));
+  KS_CUDA(cudaMallocHost(&t->h_frame, sizeof(FrameParams)));
+  KS_CUDA(cudaMalloc(&t->d_frame, sizeof(FrameParams)));
+  KS_CUDA(cudaMemsetAsync(V.ctrl, 0, sizeof(TsdfCtrl), t->stream));
+  KS_CUDA(cudaMemsetAsync(V.slot_pool, 0xFF, V.nslots * sizeof(int), t->stream));
+  KS_CUDA(cudaMemsetAsync(V.digest, 0, cap * kDigestWords * sizeof(uint32_t), t->stream));
+  KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, V.slot_key, static_cast<size_t>(V.nslots), kKeyEmpty);
+  KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, V.pool_key, cap, kKeyEmpty);
+  std::memset(t->h_ctrl, 0, sizeof(TsdfCtrl));
+  int rc = ensure_lists(t, 0, 1);
+  if (rc != KS_OK) return rc;
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  *out = t;
+  return KS_OK;
+}
+
+void ks_tsdf_destroy(ks_tsdf* t) {
+  if (!t) return;
+  cudaStreamSynchronize(t->stream);
+  TsdfView& V = t->view;
+  cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.free_list), cudaFree(V.pool_key);
+  cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.ctrl), cudaFree(t->d_flags);
+  OpLists& L = t->lists;
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
+  cudaFreeHost(t->h_ctrl), cudaFreeHost(t->h_frame), cudaFree(t->d_frame);
+  if (t->h_depth) cudaFreeHost(t->h_depth);
+  if (t->d_depth) cudaFree(t->d_depth);
+  if (t->own_stream) cudaStreamDestroy(t->stream);
+  delete t;
+}
+
+int ks_tsdf_set_stream(ks_tsdf* t, ks_stream s) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  if (t->own_stream) cudaStreamDestroy(t->stream);
+  t->own_stream = false;
+  t->stream = static_cast<cudaStream_t>(s);
+  return KS_OK;
+}
+
+ks_stream ks_tsdf_get_stream(const ks_tsdf* t) { return t ? static_cast<ks_stream>(t->stream) : nullptr; }
+
+int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_host) {
+  if (!t || !cam) return fail(KS_ERR_INVALID, "null argument");
+  // DepthFrame::validate (sdf_world.hpp:197-202)
+  if (cam->width <= 0 || cam->height <= 0 || cam->fx <= 0.0 || cam->fy <= 0.0)
+    return fail(KS_ERR_INVALID, "depth frame: invalid intrinsics");
+  if (!depth_host) return fail(KS_ERR_INVALID, "depth frame: depth buffer size mismatch");
+  const double step = 4.0 * t->cfg.voxel_size;                                                  // sdf_world.hpp:347
+  const int hs = std::max(1, static_cast<int>(std::ceil(t->cfg.truncation / step)));            // sdf_world.hpp:348
+  const size_t pixels = static_cast<size_t>(cam->width) * cam->height;
+  int rc = ensure_lists(t, pixels, 2 * hs + 1);
+  if (rc != KS_OK) return rc;
+  FrameParams& F = *t->h_frame;
+  F.width = cam->width, F.height = cam->height;
+  F.fx = cam->fx, F.fy = cam->fy, F.cx = cam->cx, F.cy = cam->cy;
+  std::memcpy(F.c2w.r, cam->pose_R, sizeof F.c2w.r);
+  std::memcpy(F.c2w.t, cam->pose_t, sizeof F.c2w.t);
+  F.w2c = rigid_inverse(F.c2w);
+  F.half_samples = hs;
+  F.step = step;
+  std::memcpy(t->h_depth, depth_host, pixels * sizeof(float));
+  t->frame_staged = true;
+  return KS_OK;
+}
+
+int ks_tsdf_upload_frame_async(ks_tsdf* t) {
+  if (!t || !t->frame_staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
+  const size_t pixels = static_cast<size_t>(t->h_frame->width) * t->h_frame->height;
+  KS_CUDA(cudaMemcpyAsync(t->d_frame, t->h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
+  KS_CUDA(cudaMemcpyAsync(t->d_depth, t->h_depth, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
+  return KS_OK;
+}
+
+int ks_tsdf_integrate_async(ks_tsdf* t) {
+  if (!t || !t->frame_staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
+  const int pixels = t->h_frame->width * t->h_frame->height;
+  KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
+  run_allocation(t);
+  KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
+  KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 1);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  KS_CUDA(cudaMemcpyAsync(t->h_ctrl, t->view.ctrl, sizeof(TsdfCtrl), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  const TsdfCtrl c = *t->h_ctrl;
+  if (c.err != 0) {  // errors are sticky until collected
+    KS_CUDA(cudaMemsetAsync(&t->view.ctrl->err, 0, sizeof(int), t->stream));
+    KS_CUDA(cudaStreamSynchronize(t->stream));
+  }
+  if (report) {
+    report->status = c.err;
+    report->blocks_touched = c.last_touched;
+    report->required = c.err_required;
+    report->available = c.err_available;
+    report->live_blocks = c.live;
+    report->next_fresh = c.next_fresh;
+    report->free_count = c.free_count;
+    report->recycled = c.last_recycled;
+  }
+  return report_status(c);
+}
+
+int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float* depth_host, int32_t* blocks_touched) {
+  int rc = ks_tsdf_stage_frame(t, cam, depth_host);
+  if (rc != KS_OK) return rc;
+  if ((rc = ks_tsdf_upload_frame_async(t)) != KS_OK) return rc;
+  if ((rc = ks_tsdf_integrate_async(t)) != KS_OK) return rc;
+  ks_tsdf_report rep;
+  rc = ks_tsdf_sync(t, &rep);
+  if (blocks_touched) *blocks_touched = rc == KS_OK ? rep.blocks_touched : 0;
+  return rc;
+}
+
+int ks_tsdf_stamp_cuboid_async(ks_tsdf* t, const double pose_R[9], const double pose_t[3], const double he[3]) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(he[a]) || !std::isfinite(pose_t[a])) return fail(KS_ERR_INVALID, "stamp: non-finite cuboid");
+  Rigid pose;
+  std::memcpy(pose.r, pose_R, sizeof pose.r);
+  std::memcpy(pose.t, pose_t, sizeof pose.t);
+  Primitive P;
+  std::memset(&P, 0, sizeof P);
+  P.inv = rigid_inverse(pose);
+  for (int a = 0; a < 3; ++a) P.he[a] = he[a];
+  // AABB of the eight rotated corners (sdf_world.hpp:402-410)
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int corner = 0; corner < 8; ++corner) {
+    const double sx = (corner & 1) ? 1.0 : -1.0, sy = (corner & 2) ? 1.0 : -1.0, sz = (corner & 4) ? 1.0 : -1.0;
+    double w[3];
+    rigid_apply(pose, sx * he[0], sy * he[1], sz * he[2], w);
+    for (int a = 0; a < 3; ++a) {
+      if (w[a] < lo[a]) lo[a] = w[a];
+      if (hi[a] < w[a]) hi[a] = w[a];
+    }
+  }
+  return stamp_async(t, P, lo, hi);
+}
+
+int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double radius) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  if (!std::isfinite(center[0]) || !std::isfinite(center[1]) || !std::isfinite(center[2]) || !std::isfinite(radius))
+    return fail(KS_ERR_INVALID, "stamp: non-finite sphere");
+  Primitive P;
+  std::memset(&P, 0, sizeof P);
+  P.is_sphere = 1;
+  P.radius = radius;
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    P.c[a] = center[a];
+    lo[a] = center[a] - radius;  // sdf_world.hpp:415-416
+    hi[a] = center[a] + radius;
+  }
+  return stamp_async(t, P, lo, hi);
+}
+
+int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t[3], const double he[3]) {
+  int rc = ks_tsdf_stamp_cuboid_async(t, pose_R, pose_t, he);
+  return rc != KS_OK ? rc : ks_tsdf_sync(t, nullptr);
+}
+
+int ks_tsdf_stamp_sphere(ks_tsdf* t, const double center[3], double radius) {
+  int rc = ks_tsdf_stamp_sphere_async(t, center, radius);
+  return rc != KS_OK ? rc : ks_tsdf_sync(t, nullptr);
+}
+
+int ks_tsdf_decay_weights_async(ks_tsdf* t, const ks_camera* cam) {
+  if (!t || !cam) return fail(KS_ERR_INVALID, "null argument");
+  Frustum Fr;
+  Rigid pose;
+  std::memcpy(pose.r, cam->pose_R, sizeof pose.r);
+  std::memcpy(pose.t, cam->pose_t, sizeof pose.t);
+  Fr.w2c = rigid_inverse(pose);
+  Fr.radius = 0.5 * kBlockEdge * t->cfg.voxel_size * std::sqrt(3.0);
+  const double raw[5][3] = {{0.0, 0.0, 1.0},
+                            {cam->fx, 0.0, cam->cx},
+                            {-cam->fx, 0.0, cam->width - 1 - cam->cx},
+                            {0.0, cam->fy, cam->cy},
+                            {0.0, -cam->fy, cam->height - 1 - cam->cy}};
+  for (int p = 0; p < 5; ++p) {
+    double n[3] = {raw[p][0], raw[p][1], raw[p][2]};
+    if (p > 0) {  // .normalized(); the near plane is written as a literal unit vector
+      const double z = sum3(n[0] * n[0], n[1] * n[1], n[2] * n[2]);
+      if (z > 0.0) {
+        const double len = std::sqrt(z);
+        for (double& c : n) c = c / len;
+      }
+    }
+    for (int a = 0; a < 3; ++a) Fr.n[p][a] = n[a];
+  }
+  KS_LAUNCH(k_decay, 4 * kSmCount, 512, 0, t->stream, t->view, Fr, t->cfg.alpha_time, t->cfg.alpha_frustum);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+int ks_tsdf_decay_weights(ks_tsdf* t, const ks_camera* cam) {
+  int rc = ks_tsdf_decay_weights_async(t, cam);
+  return rc != KS_OK ? rc : ks_tsdf_sync(t, nullptr);
+}
+
+int ks_tsdf_recycle_blocks(ks_tsdf* t, int32_t* recycled) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  KS_LAUNCH(k_recycle_flag, 2 * kSmCount, 128, 0, t->stream, t->view, t->d_flags, t->cfg.weight_threshold);
+  KS_LAUNCH(k_recycle_commit, 1, 1024, 0, t->stream, t->view, t->d_flags);
+  KS_CUDA(cudaGetLastError());
+  ks_tsdf_report rep;
+  int rc = ks_tsdf_sync(t, &rep);
+  if (recycled) *recycled = rep.recycled;
+  return rc;
+}
+
+int ks_tsdf_query(ks_tsdf* t, const double* points_host, int64_t n, int32_t geom_only, double* out_sdf, uint8_t* out_valid) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  if (n <= 0) return KS_OK;
+  double *d_pts = nullptr, *d_out = nullptr;
+  uint8_t* d_valid = nullptr;
+  KS_CUDA(cudaMalloc(&d_pts, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_out, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_valid, n));
+  KS_CUDA(cudaMemcpyAsync(d_pts, points_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, t->stream));
+  KS_LAUNCH(k_query_tsdf, static_cast<unsigned>((n + 255) / 256), 256, 0, t->stream, t->view, d_pts, static_cast<long long>(n),
+            geom_only, d_out, d_valid);
+  KS_CUDA(cudaMemcpyAsync(out_sdf, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaMemcpyAsync(out_valid, d_valid, n, cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  cudaFree(d_pts), cudaFree(d_out), cudaFree(d_valid);
+  return KS_OK;
+}
+
+int ks_tsdf_allocated_block_count(ks_tsdf* t, int32_t* count) {
+  ks_tsdf_report rep;
+  int rc = ks_tsdf_sync(t, &rep);
+  if (count) *count = rep.live_blocks;
+  return rc;
+}
+
+int ks_tsdf_find(ks_tsdf* t, const int32_t key[3], int32_t* pool_index) {
+  if (!t || !key || !pool_index) return fail(KS_ERR_INVALID, "null argument");
+  int* d_out = nullptr;
+  KS_CUDA(cudaMalloc(&d_out, sizeof(int)));
+  KS_LAUNCH(k_find, 1, 1, 0, t->stream, t->view, key[0], key[1], key[2], d_out);
+  KS_CUDA(cudaMemcpyAsync(pool_index, d_out, sizeof(int), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  cudaFree(d_out);
+  return KS_OK;
+}
+
+int ks_tsdf_export_blocks(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_index, int32_t max_blocks, int32_t* count) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  const int n = t->view.nslots;
+  std::vector<uint64_t> keys(n);
+  std::vector<int> pools(n);
+  KS_CUDA(cudaMemcpyAsync(keys.data(), t->view.slot_key, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaMemcpyAsync(pools.data(), t->view.slot_pool, n * sizeof(int), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  int live = 0;
+  for (int s = 0; s < n; ++s) {
+    if (keys[s] == kKeyEmpty || keys[s] == kKeyTomb) continue;
+    if (live < max_blocks) {
+      int x, y, z;
+      unpack_key(keys[s], x, y, z);
+      if (keys_xyz) keys_xyz[3 * live] = x, keys_xyz[3 * live + 1] = y, keys_xyz[3 * live + 2] = z;
+      if (pool_index) pool_index[live] = pools[s];
+    }
+    ++live;
+  }
+  if (count) *count = live;
+  return KS_OK;
+}
+
+int ks_tsdf_download_blocks(ks_tsdf* t, const int32_t* pool_index, int32_t n, double* depth_sum, double* depth_wt,
+                            double* geom_sdf) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  std::vector<double2> sw(kBlockVoxels);
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  for (int i = 0; i < n; ++i) {
+    const int p = pool_index[i];
+    if (p < 0 || p >= t->cfg.capacity) return fail(KS_ERR_INVALID, "tsdf: pool index out of range");
+    KS_CUDA(cudaMemcpy(sw.data(), t->view.sumwt + static_cast<size_t>(p) * kBlockVoxels, kBlockVoxels * sizeof(double2),
+                       cudaMemcpyDeviceToHost));
+    for (int q = 0; q < kBlockVoxels; ++q) {
+      if (depth_sum) depth_sum[static_cast<size_t>(i) * kBlockVoxels + q] = sw[q].x;
+      if (depth_wt) depth_wt[static_cast<size_t>(i) * kBlockVoxels + q] = sw[q].y;
+    }
+    if (geom_sdf)
+      KS_CUDA(cudaMemcpy(geom_sdf + static_cast<size_t>(i) * kBlockVoxels, t->view.geom + static_cast<size_t>(p) * kBlockVoxels,
+                         kBlockVoxels * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return KS_OK;
+}
+
+int ks_tsdf_free_list(ks_tsdf* t, int32_t* out, int32_t max_out, int32_t* count) {
+  ks_tsdf_report rep;
+  int rc = ks_tsdf_sync(t, &rep);
+  if (rc != KS_OK) return rc;
+  const int n = std::min(rep.free_count, max_out);
+  if (n > 0 && out) KS_CUDA(cudaMemcpy(out, t->view.free_list, n * sizeof(int), cudaMemcpyDeviceToHost));
+  if (count) *count = rep.free_count;
+  return KS_OK;
+}
+
+}  // extern "C"
