@@ -160,6 +160,11 @@ KS_API int ks_tsdf_download_blocks(ks_tsdf* t, const int32_t* pool_index, int32_
                                    double* depth_wt, double* geom_sdf);
 /* BlockHashTable::free_list, oldest first */
 KS_API int ks_tsdf_free_list(ks_tsdf* t, int32_t* out, int32_t max_out, int32_t* count);
+/* measurement hook: when enabled, non-captured ops record CUDA events between their stages;
+ * out = device ms of {block discovery, allocation, voxel integration} of the last integrate and
+ * {candidates+allocation, voxel stamping} of the last stamp */
+KS_API int ks_tsdf_profile(ks_tsdf* t, int32_t enable);
+KS_API int ks_tsdf_stage_ms(ks_tsdf* t, float out[5]);
 
 /* ---- ESDF ------------------------------------------------------------------ */
 /* EsdfConfig::validate (esdf.hpp:41-44) + device buffers for the grid */
@@ -177,6 +182,10 @@ KS_API int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_
 /* recover_signs (esdf.hpp:288-320) on the field left by ks_esdf_propagate */
 KS_API int ks_esdf_recover_signs(ks_esdf* e, const ks_tsdf* t);
 KS_API int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report);
+/* measurement hook: device ms of {directory, seeding, z flood, y sweep, x sweep, sign recovery}
+ * of the last non-captured ks_esdf_build_async */
+KS_API int ks_esdf_profile(ks_esdf* e, int32_t enable);
+KS_API int ks_esdf_stage_ms(ks_esdf* e, float out[6]);
 
 /* DenseEsdf::site / ::distance (any pointer may be NULL).  d2 = squared integer
  * site offset (exact), INT32_MAX when the grid has no sites. */

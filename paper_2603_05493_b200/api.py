@@ -72,7 +72,7 @@ ABI_SYMBOLS = [
     "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_tsdf_decay_weights",
     "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
     "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
-    "ks_tsdf_free_list", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
+    "ks_tsdf_free_list", "ks_tsdf_profile", "ks_tsdf_stage_ms", "ks_esdf_profile", "ks_esdf_stage_ms", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
     "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync",
     "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async",
 ]
@@ -125,6 +125,10 @@ def load_library() -> C.CDLL:
         "ks_tsdf_export_blocks": (C.c_int, [VP, VP, VP, I32, P(I32)]),
         "ks_tsdf_download_blocks": (C.c_int, [VP, VP, I32, VP, VP, VP]),
         "ks_tsdf_free_list": (C.c_int, [VP, VP, I32, P(I32)]),
+        "ks_tsdf_profile": (C.c_int, [VP, I32]),
+        "ks_tsdf_stage_ms": (C.c_int, [VP, P(C.c_float)]),
+        "ks_esdf_profile": (C.c_int, [VP, I32]),
+        "ks_esdf_stage_ms": (C.c_int, [VP, P(C.c_float)]),
         "ks_esdf_create": (C.c_int, [P(EsdfConfigC), P(VP)]),
         "ks_esdf_destroy": (None, [VP]),
         "ks_esdf_set_stream": (C.c_int, [VP, VP]),
@@ -298,6 +302,15 @@ class SparseTsdf:
         _check(self.lib.ks_tsdf_sync(self.h, C.byref(rep)))
         return rep
 
+    def profile(self, enable=True):
+        _check(self.lib.ks_tsdf_profile(self.h, int(enable)))
+
+    def stage_ms(self):
+        """{discover, allocate, integrate} of the last integrate, {candidates+allocate, stamp} of the last stamp."""
+        out = (C.c_float * 5)()
+        _check(self.lib.ks_tsdf_stage_ms(self.h, out))
+        return dict(zip(("discover", "allocate", "integrate", "stamp_candidates", "stamp_blocks"), list(out)))
+
     # parity views
     def export_blocks(self) -> Tuple[np.ndarray, np.ndarray]:
         n = C.c_int32()
@@ -357,6 +370,14 @@ class DenseEsdf:
 
     def build_async(self, tsdf: SparseTsdf):
         _check(self.lib.ks_esdf_build_async(self.h, tsdf.h))
+
+    def profile(self, enable=True):
+        _check(self.lib.ks_esdf_profile(self.h, int(enable)))
+
+    def stage_ms(self):
+        out = (C.c_float * 6)()
+        _check(self.lib.ks_esdf_stage_ms(self.h, out))
+        return dict(zip(("directory", "seed", "flood_z", "sweep_y", "sweep_x", "signs"), list(out)))
 
     def report(self) -> EsdfReportC:
         rep = EsdfReportC()

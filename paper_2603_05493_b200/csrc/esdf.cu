@@ -433,6 +433,8 @@ struct ks_esdf {
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
   int sticky_err;
+  bool profile, profile_stages;
+  cudaEvent_t ev[7];
 };
 
 namespace ksb {
@@ -506,7 +508,9 @@ static int propagate_async(ks_esdf* e) {
   const long long plane = static_cast<long long>(E.nx) * E.ny;
   const int nwords = (E.nz + 31) / 32;
   KS_LAUNCH(k_flood_z, static_cast<unsigned>((plane + 127) / 128), 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
+  if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
+  if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   KS_LAUNCH(k_sweep_x, dim3((E.ny + 31) / 32, E.nz), 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -558,6 +562,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
+  for (cudaEvent_t& ev : e->ev) KS_CUDA(cudaEventCreate(&ev));
   const int total = E.nx + E.ny + E.nz;
   KS_CUDA(cudaMalloc(&E.vox, 3 * total * sizeof(int)));
   KS_CUDA(cudaMalloc(&E.ctr, total * sizeof(double)));
@@ -585,6 +590,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (E.dir) cudaFree(E.dir);
   cudaFreeHost(e->h_ctrl);
   cudaEventDestroy(e->dep);
+  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   if (e->own_stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -603,10 +609,43 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   int rc;
   if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
   if ((rc = order_after(e, t)) != KS_OK) return rc;
+  bool prof = e->profile;
+  if (prof) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(e->stream, &cap);
+    prof = cap == cudaStreamCaptureStatusNone;
+  }
+  e->profile_stages = prof;
+  if (prof) cudaEventRecord(e->ev[0], e->stream);
   if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  if (prof) cudaEventRecord(e->ev[1], e->stream);
   if ((rc = seed_async(e, t, e->cfg.seeding)) != KS_OK) return rc;
+  if (prof) cudaEventRecord(e->ev[2], e->stream);
   if ((rc = propagate_async(e)) != KS_OK) return rc;
-  return signs_async(e, t);
+  if (prof) cudaEventRecord(e->ev[5], e->stream);
+  rc = signs_async(e, t);
+  if (prof) cudaEventRecord(e->ev[6], e->stream);
+  e->profile_stages = false;
+  return rc;
+}
+
+int ks_esdf_profile(ks_esdf* e, int32_t enable) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  e->profile = enable != 0;
+  return KS_OK;
+}
+
+int ks_esdf_stage_ms(ks_esdf* e, float out[6]) {
+  if (!e || !out) return fail(KS_ERR_INVALID, "null argument");
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  for (int i = 0; i < 6; ++i) {
+    out[i] = 0.0f;
+    if (cudaEventElapsedTime(&out[i], e->ev[i], e->ev[i + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      out[i] = -1.0f;
+    }
+  }
+  return KS_OK;
 }
 
 int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {

@@ -68,6 +68,8 @@ struct ks_tsdf {
   bool frame_staged;
   OpLists lists;
   int* d_flags;  // [capacity] recycle flags
+  bool profile;
+  cudaEvent_t ev[7];  // integrate: 0..3, stamp: 4..6
 };
 
 namespace ksb {
@@ -603,7 +605,18 @@ static int report_status(const TsdfCtrl& c) {
   }
 }
 
+static bool profiling(ks_tsdf* t) {
+  if (!t->profile) return false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(t->stream, &cap);
+  return cap == cudaStreamCaptureStatusNone;
+}
+#define KS_MARK(t, i) \
+  if (prof) cudaEventRecord((t)->ev[i], (t)->stream)
+
 static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], const double hi_in[3]) {
+  const bool prof = profiling(t);
+  KS_MARK(t, 4);
   // AABB grown by the truncation band -> block range (sdf_world.hpp:418-425)
   const double v = t->cfg.voxel_size, trunc = t->cfg.truncation;
   BlockBox B;
@@ -622,8 +635,10 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
     KS_LAUNCH(k_stamp_candidates, grid, 256, 0, t->stream, t->view, t->lists, P, B, reach);
   }
   run_allocation(t);
+  KS_MARK(t, 5);
   KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
   KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 0);
+  KS_MARK(t, 6);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
@@ -672,6 +687,7 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   KS_CUDA(cudaMalloc(&V.digest, cap * kDigestWords * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&V.ctrl, sizeof(TsdfCtrl)));
   KS_CUDA(cudaMalloc(&t->d_flags, cap * sizeof(int)));
+  for (cudaEvent_t& ev : t->ev) KS_CUDA(cudaEventCreate(&ev));
   KS_CUDA(cudaMallocHost(&t->h_ctrl, sizeof(TsdfCtrl)));
   KS_CUDA(cudaMallocHost(&t->h_frame, sizeof(FrameParams)));
   KS_CUDA(cudaMalloc(&t->d_frame, sizeof(FrameParams)));
@@ -699,8 +715,29 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFreeHost(t->h_ctrl), cudaFreeHost(t->h_frame), cudaFree(t->d_frame);
   if (t->h_depth) cudaFreeHost(t->h_depth);
   if (t->d_depth) cudaFree(t->d_depth);
+  for (cudaEvent_t ev : t->ev) cudaEventDestroy(ev);
   if (t->own_stream) cudaStreamDestroy(t->stream);
   delete t;
+}
+
+int ks_tsdf_profile(ks_tsdf* t, int32_t enable) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  t->profile = enable != 0;
+  return KS_OK;
+}
+
+int ks_tsdf_stage_ms(ks_tsdf* t, float out[5]) {
+  if (!t || !out) return fail(KS_ERR_INVALID, "null argument");
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}};
+  for (int i = 0; i < 5; ++i) {
+    out[i] = 0.0f;
+    if (cudaEventElapsedTime(&out[i], t->ev[pairs[i][0]], t->ev[pairs[i][1]]) != cudaSuccess) {
+      cudaGetLastError();
+      out[i] = -1.0f;
+    }
+  }
+  return KS_OK;
 }
 
 int ks_tsdf_set_stream(ks_tsdf* t, ks_stream s) {
@@ -749,10 +786,15 @@ int ks_tsdf_upload_frame_async(ks_tsdf* t) {
 int ks_tsdf_integrate_async(ks_tsdf* t) {
   if (!t || !t->frame_staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
   const int pixels = t->h_frame->width * t->h_frame->height;
+  const bool prof = profiling(t);
+  KS_MARK(t, 0);
   KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
+  KS_MARK(t, 1);
   run_allocation(t);
+  KS_MARK(t, 2);
   KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
   KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 1);
+  KS_MARK(t, 3);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
