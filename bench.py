@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""ESDF-update benchmark for the perception hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2|cfg1|cfg3|cfg5env]
+
+One step = one full update of the workload scene: integrate the depth frame(s) + stamp the cuboids +
+gather seeding + exact EDT + sign recovery (the ESDF is left queryable in HBM).  Default workload is
+BASELINE.json configs[1]: 2 x 1 x 1 m workspace at 5 mm (400 x 200 x 200 = 16 M cells), one 640x480
+camera, three cuboids.
+
+  value  : ESDF cells per second, CUDA-graph replay, inputs resident in HBM (CUDA events, L2 flushed
+           between steps, max over ranks; N ranks run N independent environments -> weak scaling)
+  e2e    : the same metric through the blocking ks:: drop-in calls with HOST buffers
+           (pinned staging + H2D of the frame, D2H of the reports inside the timed region)
+  roofline     : the slowest kernel stage, algorithmic bytes / its CUDA-event time / measured HBM peak
+  cpu_baseline : the reference's CPU implementation of the same update on this box's host, 1 core
+
+--impl reference times only the CPU implementation (oracle/_ref = the reference's own headers when
+built, else the oracle port).  The reference is single-threaded by construction, so cores = 1.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "esdf_update_voxels_per_s"
+UNIT = "voxels/s"
+
+
+# ---- workloads ------------------------------------------------------------------------------------------
+def make_scene(workload: str, env: int = 0):
+    from paper_2603_05493_b200 import scenes
+    if workload == "cfg1":
+        sc = scenes.config1("wavy")
+    elif workload == "cfg2":
+        sc = scenes.config2()
+    elif workload == "cfg3":
+        sc = scenes.config3()
+    elif workload == "cfg5env":
+        sc = scenes.config5_env(env)
+    else:
+        raise SystemExit(f"unknown workload {workload}")
+    if env and workload != "cfg5env":  # independent environments: same layout, different surface
+        for i, f in enumerate(sc.frames):
+            f.depth = scenes.wavy_depth(float(f.depth.mean()), 0.1 if workload == "cfg2" else 0.05, phase=0.37 * env + i)
+    return sc
+
+
+WORKLOAD_DESC = {
+    "cfg1": "configs[0]: 640x480 depth frame into 1 m^3 at 1 cm (100^3 cells)",
+    "cfg2": "configs[1]: 2 m^3 (2x1x1 m) workspace at 5 mm, 400x200x200 cells, one 640x480 depth camera + 3 cuboids, full ESDF every frame",
+    "cfg3": "configs[2]: 1 m^3 at 2 mm, 500^3 cells, 4 depth cameras + 2 cuboids",
+    "cfg5env": "configs[4]: one 1.5x1x1 m environment at 5 mm (300x200x200 cells) per rank",
+}
+
+
+# ---- clocks ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 7:
+                continue
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, r[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- CPU legs -------------------------------------------------------------------------------------------
+def cpu_checker():
+    sys.path.insert(0, str(ROOT / "tests"))
+    import cpu_checkers
+    if cpu_checkers.reference_available():
+        return cpu_checkers.reference()
+    return cpu_checkers.oracle()
+
+
+def cpu_update_seconds(lib, scene, dims):
+    """One full update on a fresh world, timed inside the C/C++ library; returns (seconds, stage dict)."""
+    world = lib.make_tsdf(scene.tsdf_voxel, capacity=scene.capacity)
+    stages, seeds, checksum = lib.timed_update(world, scene, dims)
+    world.close()
+    return sum(stages.values()), stages, seeds, checksum
+
+
+def host_cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    scene = make_scene(args.workload)
+    lib = cpu_checker()
+    nx, ny, nz = scene.esdf_dims
+    # bounded sample: full TSDF update + ESDF over the first `zs` z-slices, sized so W+K steps take ~2.5 min
+    per_cell_s = 3.6e-7  # ~2.8 M cells/s measured for this path on one core
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    zs = int(max(4, min(nz, budget / (per_cell_s * nx * ny))))
+    dims = (nx, ny, zs)
+    cells = nx * ny * zs
+    for _ in range(args.warmup):
+        cpu_update_seconds(lib, scene, dims)
+    t0 = time.perf_counter()
+    inner = []
+    for _ in range(args.steps):
+        inner.append(cpu_update_seconds(lib, scene, dims)[0])
+    wall = time.perf_counter() - t0
+    secs = sum(inner)
+    value = cells * args.steps / secs
+    sample = (f"{args.workload} scene, full TSDF update + ESDF over {nx}x{ny}x{zs} of {nx}x{ny}x{nz} cells per step "
+              f"(z-slab sample), timed inside the library; wall {wall:.1f}s; host {host_cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.workload], "cells_per_step": cells},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": lib.kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---- our arm --------------------------------------------------------------------------------------------
+def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcount: int) -> float:
+    """Compulsory HBM bytes of each stage for the device formats in DESIGN.md."""
+    return {
+        "discover": 4.0 * P + 20.0 * K,
+        "allocate": 12.0 * K,
+        "integrate": 4.0 * P + K * (512 * (16 + 16 + 8) + 320),
+        "stamp_blocks": Kp * (512 * (8 + 8 + 16) + 320),
+        "directory": 4.0 * dcount + 8.0 * L,
+        "seed": 1.0 * C_ + 64.0 * L + 4.0 * dcount,
+        "flood_z": 3.0 * C_,
+        "sweep_y": 6.0 * C_,
+        "sweep_x": 12.0 * C_,
+        "signs": 12.0 * C_ + 256.0 * L,
+    }[stage]
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_05493_b200 import api, build
+    build.build()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the perception path has no CPU implementation")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    scene = make_scene(args.workload, env=rank)
+    nx, ny, nz = scene.esdf_dims
+    cells = nx * ny * nz
+    frames = [api.DepthFrame(f.width, f.height, *f.intr, f.R, f.t, f.depth) for f in scene.frames]
+    prims = [api.Cuboid(c.R, c.t, c.half_extents) for c in scene.cuboids] + \
+            [api.SphereShape(s.center, s.radius) for s in scene.spheres]
+    pixels = sum(f.width * f.height for f in frames)
+
+    stream = torch.cuda.Stream()
+    cfg = api.make_tsdf_config(scene.tsdf_voxel)
+    cfg.capacity = scene.capacity
+    tsdf = api.make_tsdf(cfg, stream.cuda_stream)
+    ecfg = api.EsdfConfig(tuple(scene.esdf_origin), nx, ny, nz, scene.esdf_voxel, "gather")
+    esdf = api.DenseEsdf(ecfg, stream.cuda_stream)
+    # one TSDF handle integrates all cameras; with several frames each needs its own staged upload, so the
+    # multi-camera workloads keep one staging handle per camera pose by re-staging between integrates.
+
+    def enqueue_update(upload: bool):
+        for f in frames:
+            if upload or len(frames) > 1:
+                tsdf.stage_frame(f)
+                tsdf.upload_frame_async()
+            tsdf.integrate_async()
+        for p in prims:
+            tsdf.stamp_async(p)
+        esdf.build_async(tsdf)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    summary_in = torch.zeros(4, dtype=torch.float64, device="cuda")
+    summary_all = torch.zeros(4 * world, dtype=torch.float64, device="cuda")
+    probes = torch.from_numpy(np.ascontiguousarray(
+        scene.esdf_origin + np.random.RandomState(3).random_sample((4096, 3)) * np.array([nx, ny, nz]) * scene.esdf_voxel)).cuda()
+    probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
+
+    def gather_summaries():
+        """per-environment collision summary, all-gathered over NCCL (the only collective on this path)."""
+        api._check(esdf.lib.ks_esdf_query_device_async(esdf.h, C.c_void_p(probes.data_ptr()), 4096,
+                                                      C.c_void_p(probe_d.data_ptr()), None, None))
+        summary_in[0] = rank
+        summary_in[1] = probe_d.min()
+        summary_in[2] = (probe_d < 0.02).sum()
+        if world > 1:
+            dist.all_gather_into_tensor(summary_all, summary_in)
+
+    with torch.cuda.stream(stream):
+        # ---- eager warm-up (allocates blocks, binds the directory), then stage timings ---------------
+        tsdf.stage_frame(frames[0])
+        enqueue_update(upload=True)
+        rep = tsdf.sync()
+        touched_last, live = rep.blocks_touched, rep.live_blocks
+        tsdf.profile(True)
+        esdf.profile(True)
+        stage_acc = {}
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            enqueue_update(upload=False)
+            st = {**tsdf.stage_ms(), **esdf.stage_ms()}
+            if i >= args.warmup:
+                for k, v in st.items():
+                    stage_acc.setdefault(k, []).append(v)
+        tsdf.profile(False)
+        esdf.profile(False)
+        stage_ms = {k: float(np.mean(v)) for k, v in stage_acc.items()}
+
+        # ---- graph capture (inputs resident in HBM; multi-camera workloads re-upload inside the graph) --
+        graph = api.Graph(stream.cuda_stream)
+        with graph:
+            enqueue_update(upload=False)
+        kernel_nodes, all_nodes = graph.node_count()
+        for _ in range(args.warmup):
+            flush.zero_()
+            graph.launch()
+            if world > 1:
+                gather_summaries()
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        sampler = ClockSampler(local)
+        sampler.start()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the event pair)
+            starts[i].record(stream)
+            graph.launch()
+            if world > 1:
+                gather_summaries()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+        total_ms = float(total_ms.item())
+        rep = tsdf.sync()
+        erep = esdf.report()
+        assert rep.status == 0 and erep.has_sites
+
+        # ---- e2e: blocking drop-in calls with host buffers ------------------------------------------------
+        def blocking_update():
+            k = 0
+            for f in frames:
+                k = api.integrate_depth(tsdf, f)          # pinned staging + H2D + 4 phases + D2H report
+            for p in prims:
+                api.stamp_primitive(tsdf, p)
+            api.build_esdf(tsdf, ecfg, esdf)
+            r = esdf.report()                              # D2H: has_sites / seed count
+            return k, r.seed_count
+
+        for _ in range(args.warmup):
+            blocking_update()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            blocking_update()
+        torch.cuda.synchronize()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
+
+        # ---- e2e through the graph API (stage + upload + replay + report), informational ----------------
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            if len(frames) == 1:
+                tsdf.stage_frame(frames[0])
+                tsdf.upload_frame_async()
+            graph.launch()
+            tsdf.sync()
+            esdf.report()
+        e2e_graph_s = time.perf_counter() - t0
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the slowest stage ------------------------------------------------------------------
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    if peaks_path.exists():
+        peak, peak_src = float(json.loads(peaks_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    K = touched_last if touched_last > 0 else 0
+    dcount = 0
+    kernel_stages = ["discover", "allocate", "integrate", "stamp_blocks", "directory", "seed", "flood_z", "sweep_y", "sweep_x", "signs"]
+    dominant = max(kernel_stages, key=lambda s: stage_ms.get(s, 0.0))
+    stage_bytes = {s: algorithmic_bytes(s, cells, pixels, K, max(live - K, 0), live, dcount) for s in kernel_stages}
+    achieved = stage_bytes[dominant] / (stage_ms[dominant] * 1e-3) / 1e9
+    traffic = None
+    traffic_path = ROOT / "profiles" / "dram_traffic.json"
+    if traffic_path.exists():
+        traffic = json.loads(traffic_path.read_text()).get(args.workload, {}).get(dominant)
+    update_bytes = sum(stage_bytes[s] * (len(frames) if s in ("discover", "allocate", "integrate") else 1) for s in kernel_stages)
+    ms_per_step = total_ms / args.steps
+    value = world * cells * args.steps / (total_ms * 1e-3)
+
+    cpu_base = None
+    if world == 1 and not args.no_cpu_baseline:
+        lib = cpu_checker()
+        sample_dims = scene.esdf_dims if cells <= 20_000_000 else (nx, ny, max(4, int(20_000_000 / (nx * ny))))
+        runs = [cpu_update_seconds(lib, scene, sample_dims) for _ in range(2)]
+        secs = min(r[0] for r in runs)
+        sample_cells = sample_dims[0] * sample_dims[1] * sample_dims[2]
+        cpu_base = {"value": sample_cells / secs, "unit": UNIT, "cores": 1, "kind": lib.kind,
+                    "sample": f"2 full {args.workload} updates ({sample_dims[0]}x{sample_dims[1]}x{sample_dims[2]} cells each) on a fresh world, "
+                              f"best of 2, timed inside the library; stages s = "
+                              f"{ {k: round(v, 3) for k, v in runs[0][1].items()} }; host {host_cpu_model()}",
+                    "seconds_per_update": secs}
+
+    h2d = sum(f.width * f.height * 4 + 248 for f in frames)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.workload], "cells": cells, "tsdf_voxel_m": scene.tsdf_voxel,
+                   "esdf_voxel_m": scene.esdf_voxel, "blocks_touched": touched_last, "live_blocks": live,
+                   "seeds": int(erep.seed_count), "environments": world, "execution": "cuda-graph replay",
+                   "l2": "flushed between timed steps (256 MiB memset outside the event pairs); per-step working set ~22 B/cell > 126 MB L2",
+                   "collective": "none" if world == 1 else "ncclAllGather of 32-byte per-environment summaries each step"},
+        "clocks": clocks,
+        "e2e": {"value": world * cells * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 48 * (len(frames) + len(prims)) + 16,
+                "ms_per_step": 1e3 * e2e_s / args.steps, "path": "blocking ks:: calls: integrate_depth(host frame) + stamp_primitive x%d + build_esdf + report" % len(prims)},
+        "e2e_graph": {"value": cells * args.steps / e2e_graph_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_graph_s / args.steps,
+                      "path": "stage_frame + upload_frame_async + graph replay + sync/report"},
+        "gpu_launches": int(kernel_nodes * args.steps),
+        "graph": {"kernel_nodes": int(kernel_nodes), "all_nodes": int(all_nodes)},
+        "stage_ms": {k: round(v, 5) for k, v in stage_ms.items()},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": stage_bytes[dominant],
+                     "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
+        "cpu_baseline": cpu_base,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -21,11 +21,13 @@
  * normalized() is v / sqrt(v.v) with true per-component divisions.
  * Build: gcc -O2 -ffp-contract=off (no FMA contraction).
  */
+#define _POSIX_C_SOURCE 200809L
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define KS_ORACLE_PREFIX ko_
 #include "ks_oracle_api.h"
@@ -791,4 +793,49 @@ void ko_query_esdf(const double origin[3], const int dims[3], double ve, int has
     out_gradient[3 * q + 1] = ((c10 - c00) * (1 - fz) + (c11 - c01) * fz) * inv;
     out_gradient[3 * q + 2] = (c1 - c0) * inv;
   }
+}
+
+/* ---- timed full update (bench.py CPU legs) -------------------------------- */
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+int64_t ko_timed_update(ko_tsdf* t, int n_frames, const float* depth, int width, int height, const double intr[4],
+                        const double* poses_R, const double* poses_t, int n_cuboids, const double* cuboid_R,
+                        const double* cuboid_t, const double* cuboid_he, int n_spheres, const double* sphere_c,
+                        const double* sphere_r, const double origin[3], const int dims[3], double voxel_size,
+                        double* times_out, double* checksum_out) {
+  const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
+  double t0 = now_s();
+  for (int f = 0; f < n_frames; ++f)
+    if (ko_integrate_depth(t, depth + (size_t)f * width * height, width, height, intr, poses_R + 9 * f, poses_t + 3 * f) < 0)
+      return -1;
+  double t1 = now_s();
+  for (int c = 0; c < n_cuboids; ++c)
+    if (ko_stamp_cuboid(t, cuboid_R + 9 * c, cuboid_t + 3 * c, cuboid_he + 3 * c) != 0) return -1;
+  for (int s = 0; s < n_spheres; ++s)
+    if (ko_stamp_sphere(t, sphere_c + 3 * s, sphere_r[s]) != 0) return -1;
+  double t2 = now_s();
+  uint8_t* mask = malloc(cells);
+  int32_t* site = malloc(cells * 3 * sizeof(int32_t));
+  double* dist = malloc(cells * sizeof(double));
+  ko_seed_gather(t, origin, dims, voxel_size, mask);
+  double t3 = now_s();
+  const int has = ko_propagate(mask, (int64_t)cells, dims, voxel_size, site, dist);
+  double t4 = now_s();
+  ko_recover_signs(t, origin, dims, voxel_size, has, site, dist);
+  double t5 = now_s();
+  int64_t seeds = 0;
+  double sum = 0.0;
+  for (size_t i = 0; i < cells; ++i) {
+    seeds += mask[i] != 0;
+    sum += fabs(dist[i]);
+  }
+  times_out[0] = t1 - t0, times_out[1] = t2 - t1, times_out[2] = t3 - t2, times_out[3] = t4 - t3, times_out[4] = t5 - t4;
+  *checksum_out = sum;
+  free(mask);
+  free(site);
+  free(dist);
+  return has < 0 ? -1 : seeds;
 }

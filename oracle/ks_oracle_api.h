@@ -78,6 +78,18 @@ void KO(query_esdf)(const double origin[3], const int dims[3], double voxel_size
                     const double* distance, const double* points, int64_t n, double* out_distance,
                     double* out_gradient, uint8_t* out_inside);
 
+/* One full update run and timed INSIDE the library (no marshalling in the timed regions):
+ * integrate n_frames depth frames, stamp the primitives, then seed_gather -> propagate ->
+ * recover_signs over the given grid.  times_out = seconds of {integrate, stamp, seed, propagate,
+ * signs}; *checksum_out = sum of |distance| over the grid.  Returns the seed count, -1 on error.
+ * Used by bench.py's cpu_baseline and --impl reference legs. */
+int64_t KO(timed_update)(KO(tsdf)* t, int n_frames, const float* depth, int width, int height,
+                         const double intr[4], const double* poses_R, const double* poses_t,
+                         int n_cuboids, const double* cuboid_R, const double* cuboid_t,
+                         const double* cuboid_he, int n_spheres, const double* sphere_c,
+                         const double* sphere_r, const double origin[3], const int dims[3],
+                         double voxel_size, double* times_out, double* checksum_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,6 +3,8 @@
 // oracle/_ref/libks_ref.so by oracle/Makefile.  TEST INFRASTRUCTURE ONLY.
 // No reference source is copied: this file only calls the reference's public
 // functions and marshals plain arrays in and out.
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -242,6 +244,60 @@ void kr_query_esdf(const double origin[3], const int dims[3], double voxel_size,
     out_gradient[3 * i + 1] = s.gradient.y();
     out_gradient[3 * i + 2] = s.gradient.z();
     out_inside[i] = s.inside ? 1 : 0;
+  }
+}
+
+int64_t kr_timed_update(kr_tsdf* t, int n_frames, const float* depth, int width, int height,
+                        const double intr[4], const double* poses_R, const double* poses_t, int n_cuboids,
+                        const double* cuboid_R, const double* cuboid_t, const double* cuboid_he,
+                        int n_spheres, const double* sphere_c, const double* sphere_r,
+                        const double origin[3], const int dims[3], double voxel_size, double* times_out,
+                        double* checksum_out) {
+  using clock = std::chrono::steady_clock;
+  auto secs = [](clock::time_point a, clock::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  try {
+    std::vector<ks::DepthFrame> frames;
+    for (int f = 0; f < n_frames; ++f)
+      frames.push_back(to_frame(depth + static_cast<std::size_t>(f) * width * height, width, height, intr,
+                                poses_R + 9 * f, poses_t + 3 * f));
+    std::vector<ks::Primitive> prims;
+    for (int c = 0; c < n_cuboids; ++c) {
+      ks::Cuboid cuboid;
+      cuboid.pose = to_pose(cuboid_R + 9 * c, cuboid_t + 3 * c);
+      cuboid.half_extents = ks::Vec3(cuboid_he[3 * c], cuboid_he[3 * c + 1], cuboid_he[3 * c + 2]);
+      prims.emplace_back(cuboid);
+    }
+    for (int s = 0; s < n_spheres; ++s) {
+      ks::SphereShape sphere;
+      sphere.center = ks::Vec3(sphere_c[3 * s], sphere_c[3 * s + 1], sphere_c[3 * s + 2]);
+      sphere.radius = sphere_r[s];
+      prims.emplace_back(sphere);
+    }
+    const ks::EsdfConfig config = to_esdf_config(origin, dims, voxel_size);
+    const auto t0 = clock::now();
+    for (const auto& frame : frames) ks::integrate_depth(t->world, frame);
+    const auto t1 = clock::now();
+    for (const auto& prim : prims) ks::stamp_primitive(t->world, prim);
+    const auto t2 = clock::now();
+    const ks::SeedMask seeds = ks::seed_gather(t->world, config);
+    const auto t3 = clock::now();
+    ks::DenseEsdf esdf = ks::propagate(seeds, config);
+    const auto t4 = clock::now();
+    esdf = ks::recover_signs(std::move(esdf), t->world);
+    const auto t5 = clock::now();
+    times_out[0] = secs(t0, t1), times_out[1] = secs(t1, t2), times_out[2] = secs(t2, t3);
+    times_out[3] = secs(t3, t4), times_out[4] = secs(t4, t5);
+    int64_t count = 0;
+    double sum = 0.0;
+    for (std::size_t i = 0; i < seeds.size(); ++i) {
+      count += seeds[i] != 0;
+      sum += std::fabs(esdf.distance[i]);
+    }
+    *checksum_out = sum;
+    return count;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1;
   }
 }
 

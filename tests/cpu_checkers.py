@@ -75,6 +75,33 @@ class CpuChecker:
         self._query_esdf = fn("query_esdf", None, _f64p, _i32p, C.c_double, C.c_int, _f64p, _f64p,
                               C.c_int64, _f64p, _f64p, _u8p)
 
+        self._timed_update = fn("timed_update", C.c_int64, VP, C.c_int, _f32p, C.c_int, C.c_int, _f64p, _f64p, _f64p,
+                                C.c_int, _f64p, _f64p, _f64p, C.c_int, _f64p, _f64p, _f64p, _i32p, C.c_double,
+                                _f64p, _f64p)
+
+    def timed_update(self, tsdf: "CheckerTsdf", scene, dims=None):
+        """One full update of `scene` timed inside the library; returns (seconds per stage dict, seeds, checksum)."""
+        frames = scene.frames
+        f0 = frames[0]
+        depth = np.ascontiguousarray(np.stack([f.depth.reshape(-1) for f in frames]).astype(np.float32).reshape(-1))
+        R = np.ascontiguousarray(np.stack([np.asarray(f.R, np.float64).reshape(9) for f in frames]).reshape(-1))
+        t = np.ascontiguousarray(np.stack([np.asarray(f.t, np.float64).reshape(3) for f in frames]).reshape(-1))
+        z3, z9, z1 = np.zeros(3), np.zeros(9), np.zeros(1)
+        cR = np.ascontiguousarray(np.concatenate([np.asarray(c.R, np.float64).reshape(9) for c in scene.cuboids] or [z9]))
+        ct = np.ascontiguousarray(np.concatenate([np.asarray(c.t, np.float64).reshape(3) for c in scene.cuboids] or [z3]))
+        che = np.ascontiguousarray(np.concatenate([np.asarray(c.half_extents, np.float64).reshape(3) for c in scene.cuboids] or [z3]))
+        sc = np.ascontiguousarray(np.concatenate([np.asarray(s.center, np.float64).reshape(3) for s in scene.spheres] or [z3]))
+        sr = np.ascontiguousarray(np.array([s.radius for s in scene.spheres] or [0.0], np.float64))
+        times = np.zeros(5, np.float64)
+        checksum = np.zeros(1, np.float64)
+        dims = _vec(scene.esdf_dims if dims is None else dims, 3, np.int32)
+        seeds = self._timed_update(tsdf.h, len(frames), depth, f0.width, f0.height, _vec(f0.intr, 4), R, t,
+                                   len(scene.cuboids), cR, ct, che, len(scene.spheres), sc, sr,
+                                   _vec(scene.esdf_origin, 3), dims, float(scene.esdf_voxel), times, checksum)
+        if seeds < 0:
+            raise CheckerError(self.last_error())
+        return dict(zip(("integrate", "stamp", "seed", "propagate", "signs"), times.tolist())), int(seeds), float(checksum[0])
+
     def last_error(self) -> str:
         return (self._last_error() or b"").decode()
 
