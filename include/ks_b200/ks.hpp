@@ -1,0 +1,351 @@
+// ks_b200/ks.hpp -- the reference's ks:: perception API, backed by libks_b200.so (B200, sm_100a).
+//
+// Include this instead of "ks/sdf_world.hpp" and "ks/esdf.hpp"
+// (/root/reference/proj/include/ks/sdf_world.hpp, esdf.hpp) and link -lks_b200: the function
+// names, argument types, return values and exception types/texts are the reference's; the data
+// lives in HBM behind opaque handles (include/ks_b200.h).  Differences a caller can observe:
+//   * SparseTsdf / DenseEsdf hold a shared handle, so copying one aliases the same device world
+//     (the reference deep-copies its std::vectors); recover_signs(esdf, tsdf) works in place and
+//     returns the same handle.
+//   * SparseTsdf::pool / table and DenseEsdf::site / distance are not public vectors: call
+//     .site() / .distance() (downloaded on demand) or the ks_tsdf_export_* functions.
+//   * query_batch() is new: callers that looped over query() should hand the whole batch over.
+// Vec3 / Mat3 / Pose / ValidationError are taken from the reference's own core.hpp when
+// KS_B200_USE_REFERENCE_CORE is defined (mixing with the planner headers), else declared here.
+#ifndef KS_B200_KS_HPP
+#define KS_B200_KS_HPP
+
+#include <Eigen/Dense>
+
+#include <array>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <variant>
+#include <vector>
+
+#include "../ks_b200.h"
+
+#if defined(KS_B200_USE_REFERENCE_CORE)
+#include "ks/core.hpp"
+#else
+namespace ks {
+using Vec3 = Eigen::Vector3d;
+using Mat3 = Eigen::Matrix3d;
+inline constexpr double kInf = std::numeric_limits<double>::infinity();
+
+class ValidationError : public std::runtime_error {  // core.hpp:36-39
+ public:
+  explicit ValidationError(const std::string& what) : std::runtime_error(what) {}
+};
+class ParseError : public std::runtime_error {  // core.hpp:42-45
+ public:
+  explicit ParseError(const std::string& what) : std::runtime_error(what) {}
+};
+
+struct Pose {  // core.hpp:54-77
+  Mat3 rotation = Mat3::Identity();
+  Vec3 translation = Vec3::Zero();
+  static Pose Identity() { return Pose{}; }
+  Vec3 operator*(const Vec3& p) const { return rotation * p + translation; }
+  Pose operator*(const Pose& o) const { return Pose{rotation * o.rotation, rotation * o.translation + translation}; }
+  Pose inverse() const {
+    Pose out;
+    out.rotation = rotation.transpose();
+    out.translation = -(out.rotation * translation);
+    return out;
+  }
+};
+}  // namespace ks
+#endif
+
+namespace ks {
+
+namespace b200_detail {
+class CudaError : public std::runtime_error {
+ public:
+  explicit CudaError(const std::string& what) : std::runtime_error(what) {}
+};
+inline void check(int status) {
+  if (status == KS_OK) return;
+  const std::string text = ks_last_error();
+  if (status == KS_ERR_CUDA) throw CudaError(text);
+  throw ValidationError(text);
+}
+inline void fill_pose(const Pose& pose, double r[9], double t[3]) {
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) r[3 * i + j] = pose.rotation(i, j);
+    t[i] = pose.translation[i];
+  }
+}
+}  // namespace b200_detail
+
+// ---- sdf_world.hpp -----------------------------------------------------------------------------
+inline constexpr int kBlockEdge = 8;
+inline constexpr int kBlockVoxels = kBlockEdge * kBlockEdge * kBlockEdge;
+
+struct TsdfConfig {  // sdf_world.hpp:38-54
+  double voxel_size = 0.01;
+  double truncation = 0.04;
+  double alpha_time = 0.99;
+  double alpha_frustum = 0.5;
+  double weight_threshold = 0.5;
+  int capacity = 8192;
+  int slot_count = 0;
+  void validate() const {
+    if (voxel_size <= 0.0) throw ValidationError("tsdf: voxel_size must be > 0");
+    if (truncation < voxel_size) throw ValidationError("tsdf: truncation must be >= voxel_size");
+    if (!(alpha_time > 0.0 && alpha_time <= 1.0) || !(alpha_frustum > 0.0 && alpha_frustum <= 1.0))
+      throw ValidationError("tsdf: decay factors must lie in (0, 1]");
+    if (capacity < 1) throw ValidationError("tsdf: capacity must be >= 1");
+  }
+};
+
+inline TsdfConfig make_tsdf_config(double voxel_size) {  // sdf_world.hpp:56-61
+  TsdfConfig c;
+  c.voxel_size = voxel_size;
+  c.truncation = 4.0 * voxel_size;
+  return c;
+}
+
+struct BlockKey {  // sdf_world.hpp:87-90
+  std::int32_t x = 0, y = 0, z = 0;
+  bool operator==(const BlockKey&) const = default;
+};
+
+struct DepthFrame {  // sdf_world.hpp:191-204
+  int width = 0, height = 0;
+  double fx = 0.0, fy = 0.0, cx = 0.0, cy = 0.0;
+  Pose pose;
+  std::vector<float> depth;
+  void validate() const {
+    if (width <= 0 || height <= 0 || fx <= 0.0 || fy <= 0.0) throw ValidationError("depth frame: invalid intrinsics");
+    if (static_cast<int>(depth.size()) != width * height) throw ValidationError("depth frame: depth buffer size mismatch");
+  }
+  ks_camera camera() const {
+    ks_camera cam{};
+    cam.width = width, cam.height = height;
+    cam.fx = fx, cam.fy = fy, cam.cx = cx, cam.cy = cy;
+    b200_detail::fill_pose(pose, cam.pose_R, cam.pose_t);
+    return cam;
+  }
+};
+
+struct SparseTsdf {  // sdf_world.hpp:206-210; the table and the pool live in HBM
+  TsdfConfig config;
+  std::shared_ptr<ks_tsdf> handle;
+  ks_tsdf* get() const { return handle.get(); }
+};
+
+struct Cuboid {  // sdf_world.hpp:212-215
+  Pose pose;
+  Vec3 half_extents = Vec3::Zero();
+};
+struct SphereShape {  // sdf_world.hpp:217-220
+  Vec3 center = Vec3::Zero();
+  double radius = 0.0;
+};
+using Primitive = std::variant<Cuboid, SphereShape>;
+
+inline SparseTsdf make_tsdf(const TsdfConfig& config) {  // sdf_world.hpp:327-334
+  config.validate();
+  ks_tsdf_config c{config.voxel_size, config.truncation, config.alpha_time, config.alpha_frustum,
+                   config.weight_threshold, config.capacity, config.slot_count};
+  ks_tsdf* raw = nullptr;
+  b200_detail::check(ks_tsdf_create(&c, &raw));
+  return SparseTsdf{config, std::shared_ptr<ks_tsdf>(raw, ks_tsdf_destroy)};
+}
+
+inline int integrate_depth(SparseTsdf& tsdf, const DepthFrame& frame) {  // sdf_world.hpp:340-389
+  frame.validate();
+  const ks_camera cam = frame.camera();
+  std::int32_t touched = 0;
+  b200_detail::check(ks_tsdf_integrate_depth(tsdf.get(), &cam, frame.depth.data(), &touched));
+  return touched;
+}
+
+inline void stamp_primitive(SparseTsdf& tsdf, const Primitive& primitive) {  // sdf_world.hpp:394-444
+  if (const auto* cuboid = std::get_if<Cuboid>(&primitive)) {
+    double r[9], t[3];
+    b200_detail::fill_pose(cuboid->pose, r, t);
+    const double he[3] = {cuboid->half_extents[0], cuboid->half_extents[1], cuboid->half_extents[2]};
+    b200_detail::check(ks_tsdf_stamp_cuboid(tsdf.get(), r, t, he));
+  } else {
+    const auto& sphere = std::get<SphereShape>(primitive);
+    const double c[3] = {sphere.center[0], sphere.center[1], sphere.center[2]};
+    b200_detail::check(ks_tsdf_stamp_sphere(tsdf.get(), c, sphere.radius));
+  }
+}
+
+inline void decay_weights(SparseTsdf& tsdf, const DepthFrame& camera) {  // sdf_world.hpp:449-457
+  const ks_camera cam = camera.camera();
+  b200_detail::check(ks_tsdf_decay_weights(tsdf.get(), &cam));
+}
+
+inline int recycle_blocks(SparseTsdf& tsdf) {  // sdf_world.hpp:462-475
+  std::int32_t n = 0;
+  b200_detail::check(ks_tsdf_recycle_blocks(tsdf.get(), &n));
+  return n;
+}
+
+namespace b200_detail {
+inline std::optional<double> lookup(const SparseTsdf& tsdf, const Vec3& point, int geom_only) {
+  const double p[3] = {point[0], point[1], point[2]};
+  double value = 0.0;
+  std::uint8_t valid = 0;
+  check(ks_tsdf_query(tsdf.get(), p, 1, geom_only, &value, &valid));
+  if (!valid) return std::nullopt;
+  return value;
+}
+}  // namespace b200_detail
+
+inline std::optional<double> query_tsdf(const SparseTsdf& tsdf, const Vec3& point) {  // sdf_world.hpp:500-502
+  return b200_detail::lookup(tsdf, point, 0);
+}
+inline std::optional<double> query_tsdf_geom(const SparseTsdf& tsdf, const Vec3& point) {  // sdf_world.hpp:505-507
+  return b200_detail::lookup(tsdf, point, 1);
+}
+inline int allocated_block_count(const SparseTsdf& tsdf) {  // sdf_world.hpp:509
+  std::int32_t n = 0;
+  b200_detail::check(ks_tsdf_allocated_block_count(tsdf.get(), &n));
+  return n;
+}
+
+// ---- esdf.hpp ----------------------------------------------------------------------------------
+enum class SeedingMode { kScatter, kGather };  // esdf.hpp:33
+
+struct EsdfConfig {  // esdf.hpp:35-54
+  Vec3 origin = Vec3::Zero();
+  int nx = 1, ny = 1, nz = 1;
+  double voxel_size = 0.01;
+  SeedingMode seeding = SeedingMode::kGather;
+  void validate() const {
+    if (nx < 1 || ny < 1 || nz < 1) throw ValidationError("esdf: dims must be >= 1");
+    if (voxel_size <= 0.0) throw ValidationError("esdf: voxel_size must be > 0");
+  }
+  std::size_t cell_count() const { return static_cast<std::size_t>(nx) * ny * nz; }
+  std::size_t index(int x, int y, int z) const {
+    return static_cast<std::size_t>(x) + static_cast<std::size_t>(nx) * (y + static_cast<std::size_t>(ny) * z);
+  }
+  Vec3 cell_center(int x, int y, int z) const {
+    return origin + Vec3((x + 0.5) * voxel_size, (y + 0.5) * voxel_size, (z + 0.5) * voxel_size);
+  }
+};
+
+struct DenseEsdf {  // esdf.hpp:58-64; site/distance are downloaded from HBM on demand
+  EsdfConfig config;
+  std::shared_ptr<ks_esdf> handle;
+  bool has_sites = false;
+  bool signs_recovered = false;
+  ks_esdf* get() const { return handle.get(); }
+
+  std::vector<std::array<std::int32_t, 3>> site() const {
+    std::vector<std::array<std::int32_t, 3>> out(config.cell_count());
+    b200_detail::check(ks_esdf_download(get(), &out[0][0], nullptr, nullptr));
+    return out;
+  }
+  std::vector<double> distance() const {
+    std::vector<double> out(config.cell_count());
+    b200_detail::check(ks_esdf_download(get(), nullptr, out.data(), nullptr));
+    return out;
+  }
+  void refresh_flags() {
+    ks_esdf_report rep{};
+    b200_detail::check(ks_esdf_sync(get(), &rep));
+    has_sites = rep.has_sites != 0;
+    signs_recovered = rep.signs_recovered != 0;
+  }
+};
+
+using SeedMask = std::vector<std::uint8_t>;  // esdf.hpp:66
+
+inline double seed_threshold(const SparseTsdf& tsdf) { return 0.9 * tsdf.config.voxel_size; }  // esdf.hpp:69
+
+inline DenseEsdf make_esdf(const EsdfConfig& config) {
+  config.validate();
+  ks_esdf_config c{};
+  for (int a = 0; a < 3; ++a) c.origin[a] = config.origin[a];
+  c.nx = config.nx, c.ny = config.ny, c.nz = config.nz;
+  c.voxel_size = config.voxel_size;
+  c.seeding = config.seeding == SeedingMode::kGather ? 1 : 0;
+  ks_esdf* raw = nullptr;
+  b200_detail::check(ks_esdf_create(&c, &raw));
+  DenseEsdf esdf;
+  esdf.config = config;
+  esdf.handle = std::shared_ptr<ks_esdf>(raw, ks_esdf_destroy);
+  return esdf;
+}
+
+inline SeedMask seed_scatter(const SparseTsdf& tsdf, const EsdfConfig& config) {  // esdf.hpp:73-98
+  DenseEsdf scratch = make_esdf(config);
+  SeedMask seeds(config.cell_count(), 0);
+  b200_detail::check(ks_esdf_seed(scratch.get(), tsdf.get(), 0, seeds.data()));
+  return seeds;
+}
+inline SeedMask seed_gather(const SparseTsdf& tsdf, const EsdfConfig& config) {  // esdf.hpp:102-122
+  DenseEsdf scratch = make_esdf(config);
+  SeedMask seeds(config.cell_count(), 0);
+  b200_detail::check(ks_esdf_seed(scratch.get(), tsdf.get(), 1, seeds.data()));
+  return seeds;
+}
+
+inline DenseEsdf propagate(const SeedMask& seeds, const EsdfConfig& config) {  // esdf.hpp:193-282
+  config.validate();
+  if (seeds.size() != config.cell_count()) throw ValidationError("esdf: seed mask size does not match grid");
+  DenseEsdf esdf = make_esdf(config);
+  b200_detail::check(ks_esdf_propagate(esdf.get(), seeds.data(), static_cast<std::int64_t>(seeds.size())));
+  esdf.refresh_flags();
+  return esdf;
+}
+
+inline DenseEsdf recover_signs(DenseEsdf esdf, const SparseTsdf& tsdf) {  // esdf.hpp:288-320
+  b200_detail::check(ks_esdf_recover_signs(esdf.get(), tsdf.get()));
+  esdf.refresh_flags();
+  return esdf;
+}
+
+/// Rebuild into an existing field (no allocation; the per-frame call of a control loop).
+inline void build_esdf(const SparseTsdf& tsdf, DenseEsdf& esdf) {
+  b200_detail::check(ks_esdf_build(esdf.get(), tsdf.get()));
+  esdf.refresh_flags();
+}
+inline DenseEsdf build_esdf(const SparseTsdf& tsdf, const EsdfConfig& config) {  // esdf.hpp:323-327
+  DenseEsdf esdf = make_esdf(config);
+  build_esdf(tsdf, esdf);
+  return esdf;
+}
+
+struct EsdfSample {  // esdf.hpp:329-333
+  double distance = kInf;
+  Vec3 gradient = Vec3::Zero();
+  bool inside = false;
+};
+
+inline EsdfSample query(const DenseEsdf& esdf, const Vec3& point) {  // esdf.hpp:337-387
+  const double p[3] = {point[0], point[1], point[2]};
+  double d = kInf, g[3] = {0.0, 0.0, 0.0};
+  std::uint8_t inside = 0;
+  b200_detail::check(ks_esdf_query(esdf.get(), p, 1, &d, g, &inside));
+  EsdfSample s;
+  s.distance = d;
+  s.gradient = Vec3(g[0], g[1], g[2]);
+  s.inside = inside != 0;
+  return s;
+}
+
+/// Batched query: n points (xyz triples) -> distances, gradients (xyz triples), inside flags.
+inline void query_batch(const DenseEsdf& esdf, const std::vector<double>& points_xyz, std::vector<double>& distance,
+                        std::vector<double>& gradient_xyz, std::vector<std::uint8_t>& inside) {
+  const std::int64_t n = static_cast<std::int64_t>(points_xyz.size() / 3);
+  distance.resize(n);
+  gradient_xyz.resize(3 * n);
+  inside.resize(n);
+  b200_detail::check(ks_esdf_query(esdf.get(), points_xyz.data(), n, distance.data(), gradient_xyz.data(), inside.data()));
+}
+
+}  // namespace ks
+
+#endif  // KS_B200_KS_HPP
