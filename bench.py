@@ -185,11 +185,11 @@ def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcou
         "integrate": 4.0 * P + K * (512 * (16 + 16 + 8) + 320),
         "stamp_blocks": Kp * (512 * (8 + 8 + 16) + 320),
         "directory": 4.0 * dcount + 8.0 * L,
-        "seed": 1.0 * C_ + 64.0 * L + 4.0 * dcount,
-        "flood_z": 3.0 * C_,
-        "sweep_y": 6.0 * C_,
-        "sweep_x": 12.0 * C_,
-        "signs": 12.0 * C_ + 256.0 * L,
+        "seed": C_ / 8.0 + C_ / 512.0 + 64.0 * L + 4.0 * dcount,   # bit mask out, brick flags + surface planes + directory in
+        "flood_z": C_ / 8.0 + 2.0 * C_,                               # bit mask in, nearest-z (u16) out
+        "sweep_y": 2.0 * C_ + 4.0 * C_,                               # u16 in, (site_y, site_z) u32 out
+        "sweep_x": 4.0 * C_ + 8.0 * C_ + 256.0 * L,                   # u32 in, site u32 + signed d2 u32 out, sign planes
+        "signs": 0.0,                                                 # fused into sweep_x
     }[stage]
 
 

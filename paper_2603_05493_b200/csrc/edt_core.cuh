@@ -37,10 +37,8 @@ constexpr uint16_t kNone = 0xFFFFu;
 struct RowTile {
   uint16_t* stk_s;  // [n][32]   stack entry: site position
   uint16_t* stk_t;  // [n][32]   stack entry: first position where it wins
-  uint16_t* mark;   // [n][32]   winner whose interval starts at this position, else kNone
   uint16_t* lo;     // [bands][32] first live stack slot of the band
   uint16_t* hi;     // [bands][32] one past the last live slot
-  uint16_t* blast;  // [bands][32] last mark inside the band's own position range
   int n;            // row length
   int band;         // positions per band
   int bands;        // ceil(n / band)
@@ -91,7 +89,6 @@ KS_HD void build_band(const RowTile& T, const Src& src, int b, int row) {
   int top = base;
   int l = 0, tl = 0, gl = 0;  // cached top entry
   for (int u = base; u < end; ++u) {
-    T.mark[at(u, row)] = kNone;
     const int gu = src.r2(u, row);
     if (gu < 0) continue;
     while (true) {
@@ -182,41 +179,55 @@ KS_HD void merge_groups(const RowTile& T, const Src& src, int b, int j, int row)
   }
 }
 
-// Stage 3: every surviving entry marks the position where its interval starts.
-KS_HD void mark_band(const RowTile& T, int b, int row) {
-  const int lo = T.lo[at(b, row)], hi = T.hi[at(b, row)];
-  for (int k = lo; k < hi; ++k) T.mark[at(T.stk_t[at(k, row)], row)] = T.stk_s[at(k, row)];
-}
-
-// Stage 4: last mark inside the band's own position range.
-KS_HD void last_mark_of_band(const RowTile& T, int b, int row) {
-  const int base = b * T.band;
-  const int end = base + T.band < T.n ? base + T.band : T.n;
-  uint16_t last = kNone;
-  for (int p = base; p < end; ++p) {
-    const uint16_t mk = T.mark[at(p, row)];
-    if (mk != kNone) last = mk;
-  }
-  T.blast[at(b, row)] = last;
-}
-
-// Stage 5: colour the band's positions; emit(pos, winner) with winner == kNone
-// when the row holds no candidate at all.
+// Stage 3: colour the band's own positions by walking the merged stack (the
+// concatenation of every band's live slots, starts strictly increasing).
+// emit(pos, winner) with winner == kNone when the row holds no candidate at all.
 template <class Emit>
 KS_HD void colour_band(const RowTile& T, int b, int row, Emit&& emit) {
   const int base = b * T.band;
   const int end = base + T.band < T.n ? base + T.band : T.n;
-  uint16_t cur = kNone;
-  for (int bb = b - 1; bb >= 0; --bb) {
-    const uint16_t v = T.blast[at(bb, row)];
-    if (v != kNone) {
-      cur = v;
-      break;
+  // last band whose first live entry starts at or before `base`
+  int cb = -1, clo = 0, chi = 0;
+  for (int bb = 0; bb < T.bands; ++bb) {
+    const int lo = T.lo[at(bb, row)], hi = T.hi[at(bb, row)];
+    if (lo == hi) continue;
+    if (static_cast<int>(T.stk_t[at(lo, row)]) > base) break;
+    cb = bb, clo = lo, chi = hi;
+  }
+  if (cb < 0) {  // the first live entry of a row always starts at 0, so the row is empty
+    for (int p = base; p < end; ++p) emit(p, kNone);
+    return;
+  }
+  // last entry of that band starting at or before `base` (binary search, starts ascending)
+  int k = clo;
+  {
+    int hi_k = chi - 1;
+    while (k < hi_k) {
+      const int mid = (k + hi_k + 1) >> 1;
+      if (static_cast<int>(T.stk_t[at(mid, row)]) <= base) k = mid;
+      else hi_k = mid - 1;
     }
   }
+  uint16_t cur = T.stk_s[at(k, row)];
+  // successor entry and its start
+  int nb = cb, nk = k + 1, next_t = T.n;
+  auto settle = [&]() {
+    while (nb < T.bands && nk >= chi) {
+      ++nb;
+      if (nb < T.bands) {
+        nk = T.lo[at(nb, row)];
+        chi = T.hi[at(nb, row)];
+      }
+    }
+    next_t = nb < T.bands ? static_cast<int>(T.stk_t[at(nk, row)]) : T.n;
+  };
+  settle();
   for (int p = base; p < end; ++p) {
-    const uint16_t mk = T.mark[at(p, row)];
-    if (mk != kNone) cur = mk;
+    while (next_t <= p) {
+      cur = T.stk_s[at(nk, row)];
+      ++nk;
+      settle();
+    }
     emit(p, cur);
   }
 }

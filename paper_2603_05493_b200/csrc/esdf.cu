@@ -33,17 +33,26 @@ struct EsdfCtrl {
   int pad;
 };
 
+// per-axis table rows (each [nx+ny+nz]): TSDF voxel index of (cell centre + offset)
+enum VoxRow { kVoxC = 0, kVoxPh = 1, kVoxMh = 2, kVoxPe = 3, kVoxMe = 4, kVoxRows = 5 };
+
 struct EsdfView {
   int nx, ny, nz;
   long long cells;
   double origin[3];
   double ve;
-  int* vox;      // [3][nx+ny+nz] TSDF voxel index of (cell centre + {0, +h, -h}) per axis position
+  float ratio;   // ve / tsdf voxel (fast-path sign probe)
+  int* vox;      // [kVoxRows][nx+ny+nz]: offsets {0, +ve/2, -ve/2, +ve, -ve} (esdf.hpp:106-108, :303)
   double* ctr;   // [nx+ny+nz]    cell centre coordinate per axis position (esdf.hpp:51-53)
+  float* qsf;    // [nx+ny+nz]    fractional part of centre / tsdf voxel
   int* dir;      // dense block directory over the workspace: pool entry or -1
   int dlo[3], dn[3];
   long long dcount;
-  uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66)
+  uint8_t* brick;    // [ceil(n/8)^3] 1 when a live TSDF block can be probed from the 8^3-cell brick
+  int bnx, bny, bnz;
+  uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66) -- API paths
+  uint32_t* mbits;   // [nz][ny][wpr] the same mask, one bit per cell -- fused build path
+  int wpr;           // words per x row
   uint16_t* near_z;  // [cells] x-fastest phase-1 result
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
   uint32_t* site;    // [cells] y-fastest
@@ -57,11 +66,17 @@ __device__ __forceinline__ int axis_base(const EsdfView& E, int axis) { return a
 __device__ __forceinline__ int dir_lookup(const EsdfView& E, int vx, int vy, int vz) {
   const int bx = (vx >> 3) - E.dlo[0], by = (vy >> 3) - E.dlo[1], bz = (vz >> 3) - E.dlo[2];
   if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) return -1;
-  return E.dir[bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)];
+  return __ldg(E.dir + (bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)));
+}
+__device__ __forceinline__ uint32_t digest_word(const TsdfView& T, int pool, int plane, int local) {
+  return __ldg(T.digest + (static_cast<size_t>(pool) * kDigestWords + plane * 16 + (local >> 5)));
+}
+__device__ __forceinline__ int local_index(int vx, int vy, int vz) {  // local_index_of (sdf_world.hpp:274-280)
+  return (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
 }
 __device__ __forceinline__ uint32_t digest_bit(const TsdfView& T, int pool, int plane, int vx, int vy, int vz) {
-  const int local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));  // local_index_of (sdf_world.hpp:274-280)
-  return (T.digest[static_cast<size_t>(pool) * kDigestWords + plane * 16 + (local >> 5)] >> (local & 31)) & 1u;
+  const int local = local_index(vx, vy, vz);
+  return (digest_word(T, pool, plane, local) >> (local & 31)) & 1u;
 }
 
 // ---- per-axis tables: every fp64 division of the seeding stage happens here, once per axis position ----
@@ -74,9 +89,14 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
   const double c = E.origin[axis] + (k + 0.5) * E.ve;  // EsdfConfig::cell_center (esdf.hpp:51-53)
   const double h = 0.5 * E.ve;                         // esdf.hpp:106
   E.ctr[i] = c;
-  E.vox[i] = voxel_index(c + 0.0, tsdf_voxel);
-  E.vox[total + i] = voxel_index(c + h, tsdf_voxel);
-  E.vox[2 * total + i] = voxel_index(c + (-h), tsdf_voxel);
+  E.vox[kVoxC * total + i] = voxel_index(c + 0.0, tsdf_voxel);
+  E.vox[kVoxPh * total + i] = voxel_index(c + h, tsdf_voxel);
+  E.vox[kVoxMh * total + i] = voxel_index(c + (-h), tsdf_voxel);
+  // sign probe one cell along an axis: site_centre + ve * (+-1) (esdf.hpp:303 with an axis-aligned delta)
+  E.vox[kVoxPe * total + i] = voxel_index(c + E.ve * 1.0, tsdf_voxel);
+  E.vox[kVoxMe * total + i] = voxel_index(c + E.ve * -1.0, tsdf_voxel);
+  const double q = c / tsdf_voxel;
+  E.qsf[i] = static_cast<float>(q - floor(q));
 }
 
 __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
@@ -92,14 +112,49 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
   }
 }
 
+// A brick is 8^3 ESDF cells.  It is active when any TSDF block that one of its cells' seven
+// probes can land in is live; inactive bricks hold no seed and are skipped by the gather.
+__global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
+  const int nb = E.bnx * E.bny * E.bnz;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const int b[3] = {i % E.bnx, (i / E.bnx) % E.bny, i / (E.bnx * E.bny)};
+  const int dims[3] = {E.nx, E.ny, E.nz};
+  const int total = E.nx + E.ny + E.nz;
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int first = 8 * b[a], last = min(8 * b[a] + 7, dims[a] - 1);
+    const int base = axis_base(E, a);
+    lo[a] = max((E.vox[kVoxMh * total + base + first] >> 3) - E.dlo[a], 0);
+    hi[a] = min((E.vox[kVoxPh * total + base + last] >> 3) - E.dlo[a], E.dn[a] - 1);
+  }
+  uint8_t any = 0;
+  for (int z = lo[2]; z <= hi[2] && !any; ++z)
+    for (int y = lo[1]; y <= hi[1] && !any; ++y)
+      for (int x = lo[0]; x <= hi[0]; ++x)
+        if (E.dir[x + E.dn[0] * (y + static_cast<long long>(E.dn[1]) * z)] >= 0) {
+          any = 1;
+          break;
+        }
+  E.brick[i] = any;
+}
+
 // ---- seed_gather (esdf.hpp:102-122): 7-probe stencil per ESDF cell, bits instead of voxels ----
+// One warp = 32 consecutive x cells of one (y, z) row.  kBits: the fused build writes one ballot
+// word per warp; the API path writes the reference's byte mask.
+template <bool kBits>
 __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
-  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long warp_id = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long rows = static_cast<long long>(E.ny) * E.nz;
+  if (warp_id >= rows * E.wpr) return;
+  const int xw = static_cast<int>(warp_id % E.wpr);
+  const long long row = warp_id / E.wpr;
+  const int y = static_cast<int>(row % E.ny), z = static_cast<int>(row / E.ny);
+  const int x = xw * 32 + lane;
   bool seed = false;
-  if (idx < E.cells) {
-    const int x = static_cast<int>(idx % E.nx);
-    const int y = static_cast<int>((idx / E.nx) % E.ny);
-    const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
+  if (x < E.nx && E.brick[(x >> 3) + E.bnx * ((y >> 3) + E.bny * (z >> 3))]) {
     const int total = E.nx + E.ny + E.nz;
     const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
     const int xc = E.vox[ix], xp = E.vox[total + ix], xm = E.vox[2 * total + ix];
@@ -112,10 +167,14 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
     seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
            (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
            (zm != zc && probe(xc, yc, zm));
-    E.mask[idx] = seed ? 1 : 0;
   }
   const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
-  if ((threadIdx.x & 31) == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
+  if (kBits) {
+    if (lane == 0) E.mbits[row * E.wpr + xw] = votes;
+  } else if (x < E.nx) {
+    E.mask[x + static_cast<long long>(E.nx) * row] = seed ? 1 : 0;
+  }
+  if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
 }
 
 // ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
@@ -150,8 +209,10 @@ __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
 }
 
 // ---- phase 1: nearest seed along z per (x, y) column (esdf.hpp:213-233) ----
-// The column's mask becomes a bit string in shared memory ([word][thread], conflict free);
-// every z then finds its nearest set bit with clz/ffs.
+// The column's seeds become a bit string in shared memory ([word][thread], conflict free); one
+// ascending sweep then tracks the last seed at/below z and the next one above it.
+// Ties keep the lower z (strict '<', esdf.hpp:229).
+template <bool kBits>
 __global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
   extern __shared__ uint32_t s_words[];
   const long long plane = static_cast<long long>(E.nx) * E.ny;
@@ -160,39 +221,118 @@ __global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
   const int stride = blockDim.x;
   uint32_t* words = s_words + threadIdx.x;
   if (col >= plane) return;
+  const int x = static_cast<int>(col % E.nx), y = static_cast<int>(col / E.nx);
   uint32_t any = 0;
   for (int w = 0; w < nwords; ++w) {
     uint32_t bits = 0;
     const int zend = min(32, E.nz - 32 * w);
-    for (int b = 0; b < zend; ++b) bits |= (E.mask[col + plane * (32 * w + b)] != 0 ? 1u : 0u) << b;
+    if (kBits) {
+      const uint32_t* src = E.mbits + (static_cast<long long>(32 * w) * E.ny + y) * E.wpr + (x >> 5);
+      const long long step = static_cast<long long>(E.ny) * E.wpr;
+#pragma unroll 8
+      for (int b = 0; b < zend; ++b) bits |= ((__ldg(src + b * step) >> (x & 31)) & 1u) << b;
+    } else {
+#pragma unroll 8
+      for (int b = 0; b < zend; ++b) bits |= (E.mask[col + plane * (32 * w + b)] != 0 ? 1u : 0u) << b;
+    }
     words[w * stride] = bits;
     any |= bits;
   }
+  uint16_t* out = E.near_z + col;
   if (any == 0) {
-    for (int z = 0; z < E.nz; ++z) E.near_z[col + plane * z] = edt::kNone;
+    for (int z = 0; z < E.nz; ++z) out[plane * z] = edt::kNone;
     return;
   }
-  for (int z = 0; z < E.nz; ++z) E.near_z[col + plane * z] = edt::nearest_set_bit(words, stride, nwords, z);
+  auto next_set = [&](int from) -> int {  // first set bit at position >= from, or -1
+    if (from >= E.nz) return -1;
+    int w = from >> 5;
+    uint32_t m = words[w * stride] & (0xFFFFFFFFu << (from & 31));
+    while (m == 0 && ++w < nwords) m = words[w * stride];
+    return m != 0 ? 32 * w + __ffs(static_cast<int>(m)) - 1 : -1;
+  };
+  int below = -1, above = next_set(0);
+  for (int z = 0; z < E.nz; ++z) {
+    if (z == above) {
+      below = z;
+      above = next_set(z + 1);
+    }
+    int pick;
+    if (below < 0) pick = above;  // `any` guarantees one of the two exists
+    else if (above < 0) pick = below;
+    else pick = (above - z) < (z - below) ? above : below;
+    out[plane * z] = static_cast<uint16_t>(pick);
+  }
+}
+
+// ---- sign of one cell given its site (recover_signs, esdf.hpp:295-313) ----
+// The reference probes the geometry channel at site_centre + ve * normalize(cell_centre - site_centre)
+// and reads floor(probe / v_tsdf) per axis.  Which TSDF voxel that is gets decided here by, per axis,
+//   delta == 0            : the probe coordinate IS the site centre           -> table row kVoxC
+//   only this axis != 0   : normalize() gives exactly +-1 (sqrt(d*d) == |d|)  -> table rows kVoxPe / kVoxMe
+//   otherwise             : fp32 estimate of the offset, accepted only when it is farther from a voxel
+//                           face than its error bound; else the reference's own fp64 sequence.
+// so the voxel index is always the one the reference computes.
+__device__ __forceinline__ bool cell_negative(const EsdfView& E, const TsdfView& T, int x, int y, int z, int sx, int sy, int sz) {
+  const int total = E.nx + E.ny + E.nz;
+  const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
+  const int jx = sx, jy = E.nx + sy, jz = E.nx + E.ny + sz;
+  const int dx = x - sx, dy = y - sy, dz = z - sz;
+  if ((dx | dy | dz) != 0) {  // delta.squaredNorm() > 0 (distinct cells have distinct centres)
+    int vx, vy, vz;
+    const int nonzero = (dx != 0) + (dy != 0) + (dz != 0);
+    if (nonzero == 1) {
+      vx = E.vox[(dx == 0 ? kVoxC : (dx > 0 ? kVoxPe : kVoxMe)) * total + jx];
+      vy = E.vox[(dy == 0 ? kVoxC : (dy > 0 ? kVoxPe : kVoxMe)) * total + jy];
+      vz = E.vox[(dz == 0 ? kVoxC : (dz > 0 ? kVoxPe : kVoxMe)) * total + jz];
+    } else {
+      const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+      const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
+      const float ox = E.qsf[jx] + fx * rinv, oy = E.qsf[jy] + fy * rinv, oz = E.qsf[jz] + fz * rinv;
+      const float tol = 4e-6f * (1.0f + E.ratio);
+      const float rx = rintf(ox), ry = rintf(oy), rz = rintf(oz);
+      const bool sure = (dx == 0 || fabsf(ox - rx) > tol) && (dy == 0 || fabsf(oy - ry) > tol) && (dz == 0 || fabsf(oz - rz) > tol);
+      if (sure) {
+        vx = E.vox[jx] + (dx == 0 ? 0 : __float2int_rd(ox));
+        vy = E.vox[jy] + (dy == 0 ? 0 : __float2int_rd(oy));
+        vz = E.vox[jz] + (dz == 0 ? 0 : __float2int_rd(oz));
+      } else {  // the reference's arithmetic, operation by operation
+        const double px = E.ctr[jx], py = E.ctr[jy], pz = E.ctr[jz];
+        const double ex = E.ctr[ix] - px, ey = E.ctr[iy] - py, ez = E.ctr[iz] - pz;
+        const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
+        vx = voxel_index(px + E.ve * (ex / n), T.voxel);
+        vy = voxel_index(py + E.ve * (ey / n), T.voxel);
+        vz = voxel_index(pz + E.ve * (ez / n), T.voxel);
+      }
+    }
+    const int pool = dir_lookup(E, vx, vy, vz);
+    if (pool >= 0) {
+      const int local = local_index(vx, vy, vz);
+      if ((digest_word(T, pool, kGeomValid, local) >> (local & 31)) & 1u)  // query_tsdf_geom has a value
+        return ((digest_word(T, pool, kGeomNeg, local) >> (local & 31)) & 1u) != 0;
+    }
+  }
+  // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
+  const int vx = E.vox[ix], vy = E.vox[iy], vz = E.vox[iz];
+  const int pool = dir_lookup(E, vx, vy, vz);
+  if (pool < 0) return false;
+  const int local = local_index(vx, vy, vz);
+  if (!((digest_word(T, pool, kCombValid, local) >> (local & 31)) & 1u)) return false;
+  return ((digest_word(T, pool, kCombNeg, local) >> (local & 31)) & 1u) != 0;
 }
 
 // ---- phases 2 and 3: banded lower-envelope sweeps (esdf.hpp:236-280), see edt_core.cuh ----
-struct SweepSmem {
-  uint16_t *stk_s, *stk_t, *mark, *lo, *hi, *blast;
-};
 __device__ __forceinline__ edt::RowTile carve_tile(unsigned char* base, int n, int band, int bands, size_t in_bytes) {
   edt::RowTile T;
   unsigned char* p = base + in_bytes;
   T.stk_s = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
   T.stk_t = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
-  T.mark = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(n) * 64;
   T.lo = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(bands) * 64;
-  T.hi = reinterpret_cast<uint16_t*>(p), p += static_cast<size_t>(bands) * 64;
-  T.blast = reinterpret_cast<uint16_t*>(p);
+  T.hi = reinterpret_cast<uint16_t*>(p);
   T.n = n, T.band = band, T.bands = bands;
   return T;
 }
 static size_t sweep_smem_bytes(int n, int bands, int in_elem_bytes) {
-  return static_cast<size_t>(n) * 32 * in_elem_bytes + static_cast<size_t>(n) * 64 * 3 + static_cast<size_t>(bands) * 64 * 3;
+  return static_cast<size_t>(n) * 32 * in_elem_bytes + static_cast<size_t>(n) * 64 * 2 + static_cast<size_t>(bands) * 64 * 2;
 }
 
 struct SrcY {  // candidate at y = the column's nearest seed z (phase-1 output)
@@ -225,10 +365,6 @@ __device__ __forceinline__ void sweep_stages(const edt::RowTile& T, const Src& s
     if (warp < T.bands && (warp & ((2 << j) - 1)) == 0) edt::merge_groups(T, src, warp, j, lane);
     __syncthreads();
   }
-  if (warp < T.bands) edt::mark_band(T, warp, lane);
-  __syncthreads();
-  if (warp < T.bands) edt::last_mark_of_band(T, warp, lane);
-  __syncthreads();
 }
 
 // grid = (ceil(nx/32), nz); block = 32 * bands.  lane <-> x, positions = y.
@@ -257,7 +393,9 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
 // The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
 // bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
-__global__ void k_sweep_x(EsdfView E, int band, int bands) {
+// kSigns fuses recover_signs into the store of the finished cell.
+template <bool kSigns>
+__global__ void k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * 32, z = blockIdx.y;
@@ -290,14 +428,16 @@ __global__ void k_sweep_x(EsdfView E, int band, int bands) {
         return;
       }
       const uint32_t v = in[edt::at(win, lane)];
-      const int sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
-      const int dx = x - static_cast<int>(win), dy = y - sy, dz = z - sz;
-      E.site[o] = static_cast<uint32_t>(win) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-      E.d2s[o] = static_cast<uint32_t>(dx * dx + dy * dy + dz * dz);
+      const int sx = win, sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
+      const int dx = x - sx, dy = y - sy, dz = z - sz;
+      uint32_t d2 = static_cast<uint32_t>(dx * dx + dy * dy + dz * dz);
+      if (kSigns && cell_negative(E, Tw, x, y, z, sx, sy, sz)) d2 |= 0x80000000u;
+      E.site[o] = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+      E.d2s[o] = d2;
     });
 }
 
-// ---- recover_signs (esdf.hpp:288-320) ----
+// ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API ----
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   const long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (o >= E.cells) return;
@@ -306,33 +446,7 @@ __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   const int y = static_cast<int>(o % E.ny);
   const int x = static_cast<int>((o / E.ny) % E.nx);
   const int z = static_cast<int>(o / (static_cast<long long>(E.ny) * E.nx));
-  const int sx = site & 1023, sy = (site >> 10) & 1023, sz = site >> 20;
-  const double* cx = E.ctr;
-  const double* cy = E.ctr + E.nx;
-  const double* cz = E.ctr + E.nx + E.ny;
-  const double qx = cx[x], qy = cy[y], qz = cz[z];
-  const double px = cx[sx], py = cy[sy], pz = cz[sz];
-  const double dx = qx - px, dy = qy - py, dz = qz - pz;
-  const double n2 = sum3(dx * dx, dy * dy, dz * dz);
-  bool negative = false, resolved = false;
-  if (n2 > 0.0) {
-    const double n = sqrt(n2);  // delta.normalized() = delta / sqrt(squaredNorm)
-    const double wx = px + E.ve * (dx / n), wy = py + E.ve * (dy / n), wz = pz + E.ve * (dz / n);
-    const int vx = voxel_index(wx, T.voxel), vy = voxel_index(wy, T.voxel), vz = voxel_index(wz, T.voxel);
-    const int pool = dir_lookup(E, vx, vy, vz);
-    if (pool >= 0 && digest_bit(T, pool, kGeomValid, vx, vy, vz)) {  // query_tsdf_geom has a value
-      negative = digest_bit(T, pool, kGeomNeg, vx, vy, vz) != 0;
-      resolved = true;
-    }
-  }
-  if (!resolved) {  // combined sdf at the query cell's own centre
-    const int total = E.nx + E.ny + E.nz;
-    (void)total;
-    const int vx = E.vox[x], vy = E.vox[E.nx + y], vz = E.vox[E.nx + E.ny + z];
-    const int pool = dir_lookup(E, vx, vy, vz);
-    if (pool >= 0 && digest_bit(T, pool, kCombValid, vx, vy, vz)) negative = digest_bit(T, pool, kCombNeg, vx, vy, vz) != 0;
-  }
-  if (negative) E.d2s[o] |= 0x80000000u;
+  if (cell_negative(E, T, x, y, z, site & 1023, (site >> 10) & 1023, site >> 20)) E.d2s[o] ^= 0x80000000u;
 }
 
 // ---- query (esdf.hpp:337-387) ----
@@ -468,6 +582,7 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   }
   if (E.dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
   KS_CUDA(cudaMalloc(&E.dir, E.dcount * sizeof(int)));
+  E.ratio = static_cast<float>(E.ve / T.voxel);
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
   KS_CUDA(cudaStreamSynchronize(e->stream));
@@ -487,14 +602,20 @@ static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
   KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, E.dcount * sizeof(int), e->stream));
   KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+  const int bricks = E.bnx * E.bny * E.bnz;
+  KS_LAUNCH(k_brick_active, (bricks + 127) / 128, 128, 0, e->stream, E);
   return KS_OK;
 }
 
-static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode) {
+// bits: gather straight into the bit-packed mask of the fused build (gather mode only)
+static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   EsdfView& E = e->view;
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
   if (mode == 1) {
-    KS_LAUNCH(k_seed_gather, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
+    const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;
+    const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+    if (bits) KS_LAUNCH(k_seed_gather<true>, grid, 256, 0, e->stream, E, tsdf_view(t));
+    else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
   } else {
     KS_CUDA(cudaMemsetAsync(E.mask, 0, E.cells, e->stream));
     KS_LAUNCH(k_seed_scatter, 4 * kSmCount, 512, 0, e->stream, E, tsdf_view(t));
@@ -503,15 +624,24 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode) {
   return KS_OK;
 }
 
-static int propagate_async(ks_esdf* e) {
+// bits: phase 1 reads the bit-packed mask; t != nullptr: sign recovery is fused into the x sweep
+static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   EsdfView& E = e->view;
   const long long plane = static_cast<long long>(E.nx) * E.ny;
   const int nwords = (E.nz + 31) / 32;
-  KS_LAUNCH(k_flood_z, static_cast<unsigned>((plane + 127) / 128), 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
+  const unsigned fgrid = static_cast<unsigned>((plane + 127) / 128);
+  if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
+  else KS_LAUNCH(k_flood_z<false>, fgrid, 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
-  KS_LAUNCH(k_sweep_x, dim3((E.ny + 31) / 32, E.nz), 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
+  const dim3 xgrid((E.ny + 31) / 32, E.nz);
+  if (t) {
+    KS_LAUNCH(k_sweep_x<true>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
+    KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
+  } else {
+    KS_LAUNCH(k_sweep_x<false>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
+  }
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
@@ -519,8 +649,6 @@ static int propagate_async(ks_esdf* e) {
 static int signs_async(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
   KS_LAUNCH(k_recover_signs, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
-  const int one = 1;
-  (void)one;
   KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -555,17 +683,23 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   e->smem_x = sweep_smem_bytes(E.nx, e->bands_x, 4);
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
     delete e;
-    return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 900, nx <= 720)");
+    return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
   for (cudaEvent_t& ev : e->ev) KS_CUDA(cudaEventCreate(&ev));
   const int total = E.nx + E.ny + E.nz;
-  KS_CUDA(cudaMalloc(&E.vox, 3 * total * sizeof(int)));
+  KS_CUDA(cudaMalloc(&E.vox, kVoxRows * total * sizeof(int)));
   KS_CUDA(cudaMalloc(&E.ctr, total * sizeof(double)));
+  KS_CUDA(cudaMalloc(&E.qsf, total * sizeof(float)));
+  E.bnx = (E.nx + 7) / 8, E.bny = (E.ny + 7) / 8, E.bnz = (E.nz + 7) / 8;
+  KS_CUDA(cudaMalloc(&E.brick, static_cast<size_t>(E.bnx) * E.bny * E.bnz));
+  E.wpr = (E.nx + 31) / 32;
+  KS_CUDA(cudaMalloc(&E.mbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
@@ -585,7 +719,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   cudaFreeHost(e->h_ctrl);
@@ -619,11 +753,11 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   if (prof) cudaEventRecord(e->ev[0], e->stream);
   if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
   if (prof) cudaEventRecord(e->ev[1], e->stream);
-  if ((rc = seed_async(e, t, e->cfg.seeding)) != KS_OK) return rc;
+  const bool bits = e->cfg.seeding == 1;
+  if ((rc = seed_async(e, t, e->cfg.seeding, bits)) != KS_OK) return rc;
   if (prof) cudaEventRecord(e->ev[2], e->stream);
-  if ((rc = propagate_async(e)) != KS_OK) return rc;
+  rc = propagate_async(e, bits, t);  // sign recovery rides in the x sweep
   if (prof) cudaEventRecord(e->ev[5], e->stream);
-  rc = signs_async(e, t);
   if (prof) cudaEventRecord(e->ev[6], e->stream);
   e->profile_stages = false;
   return rc;
@@ -672,7 +806,7 @@ int ks_esdf_seed(ks_esdf* e, const ks_tsdf* t, int32_t mode, uint8_t* mask_host)
   if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
   if ((rc = order_after(e, t)) != KS_OK) return rc;
   if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
-  if ((rc = seed_async(e, t, mode)) != KS_OK) return rc;
+  if ((rc = seed_async(e, t, mode, false)) != KS_OK) return rc;
   if (mask_host) KS_CUDA(cudaMemcpyAsync(mask_host, e->view.mask, e->view.cells, cudaMemcpyDeviceToHost, e->stream));
   return ks_esdf_sync(e, nullptr);
 }
@@ -688,7 +822,7 @@ int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_len) {
   } else {
     KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 0, sizeof(int), e->stream));
   }
-  int rc = propagate_async(e);
+  int rc = propagate_async(e, false, nullptr);
   return rc != KS_OK ? rc : ks_esdf_sync(e, nullptr);
 }
 

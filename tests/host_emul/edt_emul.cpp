@@ -14,16 +14,14 @@ using namespace ksb::edt;
 namespace {
 
 struct TileMem {
-  std::vector<uint16_t> s, t, mark, lo, hi, blast;
+  std::vector<uint16_t> s, t, lo, hi;
   RowTile view(int n, int band) {
     const int bands = (n + band - 1) / band;
     s.assign(static_cast<size_t>(n) * kRows, 0);
     t.assign(static_cast<size_t>(n) * kRows, 0);
-    mark.assign(static_cast<size_t>(n) * kRows, 0x1234);  // deliberately dirty
     lo.assign(static_cast<size_t>(bands) * kRows, 0);
     hi.assign(static_cast<size_t>(bands) * kRows, 0);
-    blast.assign(static_cast<size_t>(bands) * kRows, 0);
-    return RowTile{s.data(), t.data(), mark.data(), lo.data(), hi.data(), blast.data(), n, band, bands};
+    return RowTile{s.data(), t.data(), lo.data(), hi.data(), n, band, bands};
   }
 };
 
@@ -35,10 +33,6 @@ void run_tile(TileMem& mem, int n, int band, int rows, const Src& src, Emit&& em
   for (int j = 0; (1 << j) < T.bands; ++j)
     for (int b = 0; b < T.bands; b += (2 << j))
       for (int r = 0; r < rows; ++r) merge_groups(T, src, b, j, r);
-  for (int b = 0; b < T.bands; ++b)
-    for (int r = 0; r < rows; ++r) mark_band(T, b, r);
-  for (int b = 0; b < T.bands; ++b)
-    for (int r = 0; r < rows; ++r) last_mark_of_band(T, b, r);
   for (int b = 0; b < T.bands; ++b)
     for (int r = 0; r < rows; ++r)
       colour_band(T, b, r, [&](int pos, uint16_t win) { emit(pos, r, win); });
