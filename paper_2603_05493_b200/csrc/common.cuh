@@ -91,10 +91,14 @@ inline Rigid rigid_inverse(const Rigid& g) {
 constexpr int kBlockEdge = 8;     // sdf_world.hpp:35
 constexpr int kBlockVoxels = 512; // sdf_world.hpp:36
 
-// Per-block digest: five 512-bit planes kept in sync with the voxel data by every
-// mutating kernel, so the dense ESDF stages read bits instead of 24-byte voxels.
-enum DigestPlane { kSurface = 0, kGeomValid = 1, kGeomNeg = 2, kCombValid = 3, kCombNeg = 4, kDigestPlanes = 5 };
-constexpr int kDigestWords = kDigestPlanes * 16;  // uint32 words per block
+// Per-block digest, kept in sync with the voxel data by every mutating kernel, so the dense
+// ESDF stages read bits instead of 24-byte voxels.  80 uint32 words per block:
+//   [ 0,16)  surface plane : 1 bit / voxel, |effective sdf| < 0.9 v  (seed_threshold, esdf.hpp:69)
+//   [16,48)  geometry pair : 2 bits / voxel, bit0 = geom_sdf finite, bit1 = geom_sdf < 0
+//   [48,80)  combined pair : 2 bits / voxel, bit0 = query_tsdf has a value, bit1 = it is < 0
+enum VoxelBit { kSurface = 0, kGeomValid = 1, kGeomNeg = 2, kCombValid = 3, kCombNeg = 4 };
+constexpr int kDigestWords = 80;
+constexpr int kDigestGeom = 16, kDigestComb = 48;
 
 // ---- TSDF device view ------------------------------------------------------------
 struct TsdfCtrl {  // device control block, mirrored to pinned host memory on sync
@@ -116,6 +120,7 @@ struct TsdfView {
   double2* sumwt;       // [capacity*512] {depth_sum, depth_wt}
   double* geom;         // [capacity*512]
   uint32_t* digest;     // [capacity*kDigestWords]
+  uint8_t* pool_geom;   // [capacity] 1 when the block holds stamped geometry
   TsdfCtrl* ctrl;
   double voxel, trunc, seed_thr;
 };

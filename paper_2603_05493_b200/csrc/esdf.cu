@@ -33,12 +33,14 @@ struct EsdfCtrl {
   int pad;
 };
 
-// per-axis table rows (each [nx+ny+nz]): TSDF voxel index of (cell centre + offset)
+// per-axis table rows (each [nx+ny+nz]): TSDF voxel index of (cell centre + offset), stored
+// RELATIVE to the block directory's origin (minus 8*dlo), so `>> 3` is the directory coordinate
+// and `& 7` is still the voxel's position inside its block.
 enum VoxRow { kVoxC = 0, kVoxPh = 1, kVoxMh = 2, kVoxPe = 3, kVoxMe = 4, kVoxRows = 5 };
 
 struct EsdfView {
   int nx, ny, nz;
-  long long cells;
+  int cells;     // <= 2^30 (dims <= 1024), so 32-bit indexing throughout
   double origin[3];
   double ve;
   float ratio;   // ve / tsdf voxel (fast-path sign probe)
@@ -47,11 +49,12 @@ struct EsdfView {
   float* qsf;    // [nx+ny+nz]    fractional part of centre / tsdf voxel
   int* dir;      // dense block directory over the workspace: pool entry or -1
   int dlo[3], dn[3];
-  long long dcount;
+  int dcount;
   uint8_t* brick;    // [ceil(n/8)^3] 1 when a live TSDF block can be probed from the 8^3-cell brick
   int bnx, bny, bnz;
   uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66) -- API paths
   uint32_t* mbits;   // [nz][ny][wpr] the same mask, one bit per cell -- fused build path
+  uint32_t* gbits;   // [nz][ny][wpr] seed cells with stamped geometry within one cell (sign probes can resolve)
   int wpr;           // words per x row
   uint16_t* near_z;  // [cells] x-fastest phase-1 result
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
@@ -62,21 +65,21 @@ struct EsdfView {
 
 __device__ __forceinline__ int axis_base(const EsdfView& E, int axis) { return axis == 0 ? 0 : (axis == 1 ? E.nx : E.nx + E.ny); }
 
-// pool entry of the TSDF block containing voxel (vx,vy,vz), via the workspace directory
+// pool entry of the TSDF block containing directory-relative voxel (vx,vy,vz).  Every probe of
+// seeding / sign recovery lies within one ESDF cell of the box, which bind_tsdf() covers with a
+// one-block margin, so no bounds test is needed.
 __device__ __forceinline__ int dir_lookup(const EsdfView& E, int vx, int vy, int vz) {
-  const int bx = (vx >> 3) - E.dlo[0], by = (vy >> 3) - E.dlo[1], bz = (vz >> 3) - E.dlo[2];
-  if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) return -1;
-  return __ldg(E.dir + (bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)));
-}
-__device__ __forceinline__ uint32_t digest_word(const TsdfView& T, int pool, int plane, int local) {
-  return __ldg(T.digest + (static_cast<size_t>(pool) * kDigestWords + plane * 16 + (local >> 5)));
+  return __ldg(E.dir + ((vx >> 3) + E.dn[0] * ((vy >> 3) + E.dn[1] * (vz >> 3))));
 }
 __device__ __forceinline__ int local_index(int vx, int vy, int vz) {  // local_index_of (sdf_world.hpp:274-280)
   return (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
 }
-__device__ __forceinline__ uint32_t digest_bit(const TsdfView& T, int pool, int plane, int vx, int vy, int vz) {
-  const int local = local_index(vx, vy, vz);
-  return (digest_word(T, pool, plane, local) >> (local & 31)) & 1u;
+__device__ __forceinline__ uint32_t surface_bit(const TsdfView& T, int pool, int local) {
+  return (__ldg(T.digest + (pool * kDigestWords + (local >> 5))) >> (local & 31)) & 1u;
+}
+// 2-bit pair {has value, negative} of the geometry (kDigestGeom) or combined (kDigestComb) channel
+__device__ __forceinline__ uint32_t pair_bits(const TsdfView& T, int pool, int plane_base, int local) {
+  return (__ldg(T.digest + (pool * kDigestWords + plane_base + (local >> 4))) >> ((local & 15) * 2)) & 3u;
 }
 
 // ---- per-axis tables: every fp64 division of the seeding stage happens here, once per axis position ----
@@ -86,15 +89,16 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
   if (i >= total) return;
   const int axis = i < E.nx ? 0 : (i < E.nx + E.ny ? 1 : 2);
   const int k = i - axis_base(E, axis);
+  const int rel = 8 * E.dlo[axis];
   const double c = E.origin[axis] + (k + 0.5) * E.ve;  // EsdfConfig::cell_center (esdf.hpp:51-53)
   const double h = 0.5 * E.ve;                         // esdf.hpp:106
   E.ctr[i] = c;
-  E.vox[kVoxC * total + i] = voxel_index(c + 0.0, tsdf_voxel);
-  E.vox[kVoxPh * total + i] = voxel_index(c + h, tsdf_voxel);
-  E.vox[kVoxMh * total + i] = voxel_index(c + (-h), tsdf_voxel);
+  E.vox[kVoxC * total + i] = voxel_index(c + 0.0, tsdf_voxel) - rel;
+  E.vox[kVoxPh * total + i] = voxel_index(c + h, tsdf_voxel) - rel;
+  E.vox[kVoxMh * total + i] = voxel_index(c + (-h), tsdf_voxel) - rel;
   // sign probe one cell along an axis: site_centre + ve * (+-1) (esdf.hpp:303 with an axis-aligned delta)
-  E.vox[kVoxPe * total + i] = voxel_index(c + E.ve * 1.0, tsdf_voxel);
-  E.vox[kVoxMe * total + i] = voxel_index(c + E.ve * -1.0, tsdf_voxel);
+  E.vox[kVoxPe * total + i] = voxel_index(c + E.ve * 1.0, tsdf_voxel) - rel;
+  E.vox[kVoxMe * total + i] = voxel_index(c + E.ve * -1.0, tsdf_voxel) - rel;
   const double q = c / tsdf_voxel;
   E.qsf[i] = static_cast<float>(q - floor(q));
 }
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
     unpack_key(key, bx, by, bz);
     bx -= E.dlo[0], by -= E.dlo[1], bz -= E.dlo[2];
     if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
-    E.dir[bx + E.dn[0] * (by + static_cast<long long>(E.dn[1]) * bz)] = p;
+    E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
   }
 }
 
@@ -126,14 +130,14 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
   for (int a = 0; a < 3; ++a) {
     const int first = 8 * b[a], last = min(8 * b[a] + 7, dims[a] - 1);
     const int base = axis_base(E, a);
-    lo[a] = max((E.vox[kVoxMh * total + base + first] >> 3) - E.dlo[a], 0);
-    hi[a] = min((E.vox[kVoxPh * total + base + last] >> 3) - E.dlo[a], E.dn[a] - 1);
+    lo[a] = E.vox[kVoxMh * total + base + first] >> 3;
+    hi[a] = E.vox[kVoxPh * total + base + last] >> 3;
   }
   uint8_t any = 0;
   for (int z = lo[2]; z <= hi[2] && !any; ++z)
     for (int y = lo[1]; y <= hi[1] && !any; ++y)
       for (int x = lo[0]; x <= hi[0]; ++x)
-        if (E.dir[x + E.dn[0] * (y + static_cast<long long>(E.dn[1]) * z)] >= 0) {
+        if (E.dir[x + E.dn[0] * (y + E.dn[1] * z)] >= 0) {
           any = 1;
           break;
         }
@@ -142,18 +146,19 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
 
 // ---- seed_gather (esdf.hpp:102-122): 7-probe stencil per ESDF cell, bits instead of voxels ----
 // One warp = 32 consecutive x cells of one (y, z) row.  kBits: the fused build writes one ballot
-// word per warp; the API path writes the reference's byte mask.
+// word per warp (plus the "stamped geometry within one cell" plane used by the fused sign
+// recovery); the API path writes the reference's byte mask.
 template <bool kBits>
 __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
-  const long long warp_id = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  const long long rows = static_cast<long long>(E.ny) * E.nz;
+  const int rows = E.ny * E.nz;
   if (warp_id >= rows * E.wpr) return;
-  const int xw = static_cast<int>(warp_id % E.wpr);
-  const long long row = warp_id / E.wpr;
-  const int y = static_cast<int>(row % E.ny), z = static_cast<int>(row / E.ny);
+  const int xw = warp_id % E.wpr;
+  const int row = warp_id / E.wpr;
+  const int y = row % E.ny, z = row / E.ny;
   const int x = xw * 32 + lane;
-  bool seed = false;
+  bool seed = false, geom_near = false;
   if (x < E.nx && E.brick[(x >> 3) + E.bnx * ((y >> 3) + E.bny * (z >> 3))]) {
     const int total = E.nx + E.ny + E.nz;
     const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
@@ -162,17 +167,32 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
     const int zc = E.vox[iz], zp = E.vox[total + iz], zm = E.vox[2 * total + iz];
     auto probe = [&](int vx, int vy, int vz) -> bool {
       const int pool = dir_lookup(E, vx, vy, vz);
-      return pool >= 0 && digest_bit(T, pool, kSurface, vx, vy, vz) != 0;
+      return pool >= 0 && surface_bit(T, pool, local_index(vx, vy, vz)) != 0;
     };
     seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
            (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
            (zm != zc && probe(xc, yc, zm));
+    if (kBits && seed) {  // any stamped block a sign probe from this site can reach (centre +- ve per axis)?
+      const int bx0 = E.vox[kVoxMe * total + ix] >> 3, bx1 = E.vox[kVoxPe * total + ix] >> 3;
+      const int by0 = E.vox[kVoxMe * total + iy] >> 3, by1 = E.vox[kVoxPe * total + iy] >> 3;
+      const int bz0 = E.vox[kVoxMe * total + iz] >> 3, bz1 = E.vox[kVoxPe * total + iz] >> 3;
+      for (int bz = bz0; bz <= bz1; ++bz)
+        for (int by = by0; by <= by1; ++by)
+          for (int bx = bx0; bx <= bx1; ++bx) {
+            const int pool = __ldg(E.dir + (bx + E.dn[0] * (by + E.dn[1] * bz)));
+            if (pool >= 0 && T.pool_geom[pool]) geom_near = true;
+          }
+    }
   }
   const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
   if (kBits) {
-    if (lane == 0) E.mbits[row * E.wpr + xw] = votes;
+    const uint32_t gvotes = __ballot_sync(0xFFFFFFFFu, geom_near);
+    if (lane == 0) {
+      E.mbits[row * E.wpr + xw] = votes;
+      E.gbits[row * E.wpr + xw] = gvotes;
+    }
   } else if (x < E.nx) {
-    E.mask[x + static_cast<long long>(E.nx) * row] = seed ? 1 : 0;
+    E.mask[x + E.nx * row] = seed ? 1 : 0;
   }
   if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
 }
@@ -185,8 +205,7 @@ __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
   for (int pool = blockIdx.x; pool < bound; pool += gridDim.x) {
     const uint64_t key = T.pool_key[pool];
     if (key == kKeyEmpty) continue;
-    const uint32_t word = T.digest[static_cast<size_t>(pool) * kDigestWords + kSurface * 16 + (tid >> 5)];
-    if (!((word >> (tid & 31)) & 1u)) continue;
+    if (!surface_bit(T, pool, tid)) continue;
     int bx, by, bz;
     unpack_key(key, bx, by, bz);
     const double cx = (bx * kBlockEdge + lx + 0.5) * T.voxel, cy = (by * kBlockEdge + ly + 0.5) * T.voxel,
@@ -195,15 +214,13 @@ __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
     const int ey = static_cast<int>(floor((cy - E.origin[1]) / E.ve));
     const int ez = static_cast<int>(floor((cz - E.origin[2]) / E.ve));
     if (ex < 0 || ex >= E.nx || ey < 0 || ey >= E.ny || ez < 0 || ez >= E.nz) continue;
-    E.mask[ex + static_cast<long long>(E.nx) * (ey + static_cast<long long>(E.ny) * ez)] = 1;
+    E.mask[ex + E.nx * (ey + E.ny * ez)] = 1;
   }
 }
 
 __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
   unsigned local = 0;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < E.cells;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    local += E.mask[i] != 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.cells; i += gridDim.x * blockDim.x) local += E.mask[i] != 0;
   for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xFFFFFFFFu, local, d);
   if ((threadIdx.x & 31) == 0 && local != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(local));
 }
@@ -215,20 +232,20 @@ __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
 template <bool kBits>
 __global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
   extern __shared__ uint32_t s_words[];
-  const long long plane = static_cast<long long>(E.nx) * E.ny;
-  const long long col = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int plane = E.nx * E.ny;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int nwords = (E.nz + 31) >> 5;
   const int stride = blockDim.x;
   uint32_t* words = s_words + threadIdx.x;
   if (col >= plane) return;
-  const int x = static_cast<int>(col % E.nx), y = static_cast<int>(col / E.nx);
+  const int x = col % E.nx, y = col / E.nx;
   uint32_t any = 0;
   for (int w = 0; w < nwords; ++w) {
     uint32_t bits = 0;
     const int zend = min(32, E.nz - 32 * w);
     if (kBits) {
-      const uint32_t* src = E.mbits + (static_cast<long long>(32 * w) * E.ny + y) * E.wpr + (x >> 5);
-      const long long step = static_cast<long long>(E.ny) * E.wpr;
+      const uint32_t* src = E.mbits + ((32 * w) * E.ny + y) * E.wpr + (x >> 5);
+      const int step = E.ny * E.wpr;
 #pragma unroll 8
       for (int b = 0; b < zend; ++b) bits |= ((__ldg(src + b * step) >> (x & 31)) & 1u) << b;
     } else {
@@ -264,61 +281,91 @@ __global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
   }
 }
 
-// ---- sign of one cell given its site (recover_signs, esdf.hpp:295-313) ----
+// ---- sign of a cell given its site (recover_signs, esdf.hpp:295-313) ----
 // The reference probes the geometry channel at site_centre + ve * normalize(cell_centre - site_centre)
-// and reads floor(probe / v_tsdf) per axis.  Which TSDF voxel that is gets decided here by, per axis,
+// and reads floor(probe / v_tsdf) per axis.  Which TSDF voxel that is gets decided, per axis, by
 //   delta == 0            : the probe coordinate IS the site centre           -> table row kVoxC
 //   only this axis != 0   : normalize() gives exactly +-1 (sqrt(d*d) == |d|)  -> table rows kVoxPe / kVoxMe
 //   otherwise             : fp32 estimate of the offset, accepted only when it is farther from a voxel
 //                           face than its error bound; else the reference's own fp64 sequence.
-// so the voxel index is always the one the reference computes.
-__device__ __forceinline__ bool cell_negative(const EsdfView& E, const TsdfView& T, int x, int y, int z, int sx, int sy, int sz) {
-  const int total = E.nx + E.ny + E.nz;
-  const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
-  const int jx = sx, jy = E.nx + sy, jz = E.nx + E.ny + sz;
-  const int dx = x - sx, dy = y - sy, dz = z - sz;
-  if ((dx | dy | dz) != 0) {  // delta.squaredNorm() > 0 (distinct cells have distinct centres)
-    int vx, vy, vz;
-    const int nonzero = (dx != 0) + (dy != 0) + (dz != 0);
-    if (nonzero == 1) {
-      vx = E.vox[(dx == 0 ? kVoxC : (dx > 0 ? kVoxPe : kVoxMe)) * total + jx];
-      vy = E.vox[(dy == 0 ? kVoxC : (dy > 0 ? kVoxPe : kVoxMe)) * total + jy];
-      vz = E.vox[(dz == 0 ? kVoxC : (dz > 0 ? kVoxPe : kVoxMe)) * total + jz];
-    } else {
-      const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
-      const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
-      const float ox = E.qsf[jx] + fx * rinv, oy = E.qsf[jy] + fy * rinv, oz = E.qsf[jz] + fz * rinv;
-      const float tol = 4e-6f * (1.0f + E.ratio);
-      const float rx = rintf(ox), ry = rintf(oy), rz = rintf(oz);
-      const bool sure = (dx == 0 || fabsf(ox - rx) > tol) && (dy == 0 || fabsf(oy - ry) > tol) && (dz == 0 || fabsf(oz - rz) > tol);
-      if (sure) {
-        vx = E.vox[jx] + (dx == 0 ? 0 : __float2int_rd(ox));
-        vy = E.vox[jy] + (dy == 0 ? 0 : __float2int_rd(oy));
-        vz = E.vox[jz] + (dz == 0 ? 0 : __float2int_rd(oz));
-      } else {  // the reference's arithmetic, operation by operation
-        const double px = E.ctr[jx], py = E.ctr[jy], pz = E.ctr[jz];
-        const double ex = E.ctr[ix] - px, ey = E.ctr[iy] - py, ez = E.ctr[iz] - pz;
-        const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
-        vx = voxel_index(px + E.ve * (ex / n), T.voxel);
-        vy = voxel_index(py + E.ve * (ey / n), T.voxel);
-        vz = voxel_index(pz + E.ve * (ez / n), T.voxel);
-      }
-    }
-    const int pool = dir_lookup(E, vx, vy, vz);
-    if (pool >= 0) {
-      const int local = local_index(vx, vy, vz);
-      if ((digest_word(T, pool, kGeomValid, local) >> (local & 31)) & 1u)  // query_tsdf_geom has a value
-        return ((digest_word(T, pool, kGeomNeg, local) >> (local & 31)) & 1u) != 0;
+// so the voxel index is always the one the reference computes.  Two hints skip work without changing the
+// result: a site with no stamped block within reach cannot resolve a geometry probe (gbits), and a cell
+// in an inactive brick has no allocated block under its own centre (fallback lookup).
+struct SignProbe {
+  const EsdfView& E;
+  const TsdfView& T;
+  int total;
+  int y, z, iy, iz;
+  int own_vy, own_vz;   // the cell's own voxel (fallback lookup)
+  int brick_row;
+  // current site
+  int sx, sy, sz, jx, jy, jz;
+  int v0x, v0y, v0z;
+  float qx, qy, qz;
+  bool geom_near;
+
+  __device__ __forceinline__ SignProbe(const EsdfView& E_, const TsdfView& T_, int y_, int z_) : E(E_), T(T_) {
+    total = E.nx + E.ny + E.nz;
+    y = y_, z = z_;
+    iy = E.nx + y, iz = E.nx + E.ny + z;
+    own_vy = E.vox[iy], own_vz = E.vox[iz];
+    brick_row = E.bnx * ((y >> 3) + E.bny * (z >> 3));
+    sx = sy = sz = -1;
+    geom_near = true;
+  }
+  template <bool kHints>
+  __device__ __forceinline__ void set_site(int sx_, int sy_, int sz_) {
+    sx = sx_, sy = sy_, sz = sz_;
+    jx = sx, jy = E.nx + sy, jz = E.nx + E.ny + sz;
+    geom_near = !kHints || ((__ldg(E.gbits + ((sz * E.ny + sy) * E.wpr + (sx >> 5))) >> (sx & 31)) & 1u) != 0;
+    if (geom_near) {
+      v0x = E.vox[jx], v0y = E.vox[jy], v0z = E.vox[jz];
+      qx = E.qsf[jx], qy = E.qsf[jy], qz = E.qsf[jz];
     }
   }
-  // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
-  const int vx = E.vox[ix], vy = E.vox[iy], vz = E.vox[iz];
-  const int pool = dir_lookup(E, vx, vy, vz);
-  if (pool < 0) return false;
-  const int local = local_index(vx, vy, vz);
-  if (!((digest_word(T, pool, kCombValid, local) >> (local & 31)) & 1u)) return false;
-  return ((digest_word(T, pool, kCombNeg, local) >> (local & 31)) & 1u) != 0;
-}
+  template <bool kHints>
+  __device__ __forceinline__ bool negative(int x) const {
+    const int dx = x - sx, dy = y - sy, dz = z - sz;
+    if (geom_near && (dx | dy | dz) != 0) {  // delta.squaredNorm() > 0 (distinct cells have distinct centres)
+      int vx, vy, vz;
+      if ((dx != 0) + (dy != 0) + (dz != 0) == 1) {
+        vx = dx == 0 ? v0x : E.vox[(dx > 0 ? kVoxPe : kVoxMe) * total + jx];
+        vy = dy == 0 ? v0y : E.vox[(dy > 0 ? kVoxPe : kVoxMe) * total + jy];
+        vz = dz == 0 ? v0z : E.vox[(dz > 0 ? kVoxPe : kVoxMe) * total + jz];
+      } else {
+        const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+        const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
+        const float ox = qx + fx * rinv, oy = qy + fy * rinv, oz = qz + fz * rinv;
+        const float tol = 4e-6f * (1.0f + E.ratio);
+        const bool sure = (dx == 0 || fabsf(ox - rintf(ox)) > tol) && (dy == 0 || fabsf(oy - rintf(oy)) > tol) &&
+                          (dz == 0 || fabsf(oz - rintf(oz)) > tol);
+        if (sure) {
+          vx = v0x + (dx == 0 ? 0 : __float2int_rd(ox));
+          vy = v0y + (dy == 0 ? 0 : __float2int_rd(oy));
+          vz = v0z + (dz == 0 ? 0 : __float2int_rd(oz));
+        } else {  // the reference's arithmetic, operation by operation
+          const double px = E.ctr[jx], py = E.ctr[jy], pz = E.ctr[jz];
+          const double ex = E.ctr[x] - px, ey = E.ctr[iy] - py, ez = E.ctr[iz] - pz;
+          const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
+          vx = voxel_index(px + E.ve * (ex / n), T.voxel) - 8 * E.dlo[0];
+          vy = voxel_index(py + E.ve * (ey / n), T.voxel) - 8 * E.dlo[1];
+          vz = voxel_index(pz + E.ve * (ez / n), T.voxel) - 8 * E.dlo[2];
+        }
+      }
+      const int pool = dir_lookup(E, vx, vy, vz);
+      if (pool >= 0) {
+        const uint32_t g = pair_bits(T, pool, kDigestGeom, local_index(vx, vy, vz));
+        if (g & 1u) return (g & 2u) != 0;  // query_tsdf_geom has a value: its sign decides
+      }
+    }
+    // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
+    if (kHints && !E.brick[brick_row + (x >> 3)]) return false;
+    const int vx = E.vox[x];
+    const int pool = dir_lookup(E, vx, own_vy, own_vz);
+    if (pool < 0) return false;
+    return pair_bits(T, pool, kDigestComb, local_index(vx, own_vy, own_vz)) == 3u;
+  }
+};
 
 // ---- phases 2 and 3: banded lower-envelope sweeps (esdf.hpp:236-280), see edt_core.cuh ----
 __device__ __forceinline__ edt::RowTile carve_tile(unsigned char* base, int n, int band, int bands, size_t in_bytes) {
@@ -375,19 +422,24 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
   const int ny = E.ny;
   uint16_t* zs = reinterpret_cast<uint16_t*>(s_raw);
   const edt::RowTile T = carve_tile(s_raw, ny, band, bands, static_cast<size_t>(ny) * 64);
-  const long long zoff = static_cast<long long>(E.nx) * ny * z;
+  const int zoff = E.nx * ny * z + x;
   const int base = warp * band, end = min(base + band, ny);
   if (warp < bands)
-    for (int y = base; y < end; ++y) zs[edt::at(y, lane)] = x < E.nx ? E.near_z[zoff + static_cast<long long>(E.nx) * y + x] : edt::kNone;
+    for (int y = base; y < end; ++y) zs[edt::at(y, lane)] = x < E.nx ? E.near_z[zoff + E.nx * y] : edt::kNone;
   __syncwarp();
   const SrcY src{zs, z};
   sweep_stages(T, src, warp, lane);
-  if (warp < bands)
+  if (warp < bands) {
+    uint16_t last = edt::kNone;
+    uint32_t packed = kYzNone;
     edt::colour_band(T, warp, lane, [&](int y, uint16_t win) {
-      if (x < E.nx)
-        E.yz[zoff + static_cast<long long>(E.nx) * y + x] =
-            win == edt::kNone ? kYzNone : (static_cast<uint32_t>(win) | static_cast<uint32_t>(zs[edt::at(win, lane)]) << 16);
+      if (win != last) {
+        last = win;
+        packed = win == edt::kNone ? kYzNone : (static_cast<uint32_t>(win) | static_cast<uint32_t>(zs[edt::at(win, lane)]) << 16);
+      }
+      if (x < E.nx) E.yz[zoff + E.nx * y] = packed;
     });
+  }
 }
 
 // grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
@@ -395,17 +447,17 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
 // kSigns fuses recover_signs into the store of the finished cell.
 template <bool kSigns>
-__global__ void k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
+__global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * 32, z = blockIdx.y;
   const int nx = E.nx, ny = E.ny;
   uint32_t* in = reinterpret_cast<uint32_t*>(s_raw);
   const edt::RowTile T = carve_tile(s_raw, nx, band, bands, static_cast<size_t>(nx) * 128);
-  const long long zoff = static_cast<long long>(nx) * ny * z;
+  const int zoff = nx * ny * z;
   for (int r = warp; r < 32; r += nwarps) {
     const bool live = y0 + r < ny;
-    const uint32_t* row = E.yz + zoff + static_cast<long long>(nx) * (y0 + r);
+    const uint32_t* row = E.yz + zoff + nx * (y0 + r);
     for (int x = lane; x < nx; x += 32) in[x * 32 + ((r + x) & 31)] = live ? row[x] : kYzNone;
   }
   __syncthreads();
@@ -418,35 +470,48 @@ __global__ void k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   const SrcX src{in, y0, z};
   sweep_stages(T, src, warp, lane);
   const int y = y0 + lane;
-  if (warp < bands)
+  if (warp < bands && y < ny) {
+    SignProbe probe(E, Tw, kSigns ? y : 0, kSigns ? z : 0);
+    const int obase = y + ny * nx * z;
+    uint16_t last = edt::kNone;
+    uint32_t site = kSiteNone;
+    int r2w = 0, sx = 0;
     edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
-      if (y >= ny) return;
-      const long long o = y + static_cast<long long>(ny) * (x + static_cast<long long>(nx) * z);
+      const int o = obase + ny * x;
       if (win == edt::kNone) {
         E.site[o] = kSiteNone;
         E.d2s[o] = kD2None;
         return;
       }
-      const uint32_t v = in[edt::at(win, lane)];
-      const int sx = win, sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
-      const int dx = x - sx, dy = y - sy, dz = z - sz;
-      uint32_t d2 = static_cast<uint32_t>(dx * dx + dy * dy + dz * dz);
-      if (kSigns && cell_negative(E, Tw, x, y, z, sx, sy, sz)) d2 |= 0x80000000u;
-      E.site[o] = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+      if (win != last) {  // everything that only depends on the winning site
+        last = win;
+        const uint32_t v = in[edt::at(win, lane)];
+        const int sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
+        sx = win;
+        r2w = (y - sy) * (y - sy) + (z - sz) * (z - sz);
+        site = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+        if (kSigns) probe.template set_site<true>(sx, sy, sz);
+      }
+      uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
+      if (kSigns && probe.template negative<true>(x)) d2 |= 0x80000000u;
+      E.site[o] = site;
       E.d2s[o] = d2;
     });
+  }
 }
 
-// ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API ----
+// ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
-  const long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
   const uint32_t site = E.site[o];
   if (site == kSiteNone) return;
-  const int y = static_cast<int>(o % E.ny);
-  const int x = static_cast<int>((o / E.ny) % E.nx);
-  const int z = static_cast<int>(o / (static_cast<long long>(E.ny) * E.nx));
-  if (cell_negative(E, T, x, y, z, site & 1023, (site >> 10) & 1023, site >> 20)) E.d2s[o] ^= 0x80000000u;
+  const int y = o % E.ny;
+  const int x = (o / E.ny) % E.nx;
+  const int z = o / (E.ny * E.nx);
+  SignProbe probe(E, T, y, z);
+  probe.template set_site<false>(site & 1023, (site >> 10) & 1023, site >> 20);
+  if (probe.template negative<false>(x)) E.d2s[o] ^= 0x80000000u;
 }
 
 // ---- query (esdf.hpp:337-387) ----
@@ -571,17 +636,18 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   if (E.dir) cudaFree(E.dir);
   E.dir = nullptr;
   const int dims[3] = {E.nx, E.ny, E.nz};
-  E.dcount = 1;
+  long long dcount = 1;
   for (int a = 0; a < 3; ++a) {
     // every probe of seeding / sign recovery lies within one ESDF cell of the box
     const int lo = (voxel_index(E.origin[a] - E.ve, T.voxel) >> 3) - 1;
     const int hi = (voxel_index(E.origin[a] + (dims[a] + 1) * E.ve, T.voxel) >> 3) + 1;
     E.dlo[a] = lo;
     E.dn[a] = hi - lo + 1;
-    E.dcount *= E.dn[a];
+    dcount *= E.dn[a];
   }
-  if (E.dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
-  KS_CUDA(cudaMalloc(&E.dir, E.dcount * sizeof(int)));
+  if (dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
+  E.dcount = static_cast<int>(dcount);
+  KS_CUDA(cudaMalloc(&E.dir, static_cast<size_t>(E.dcount) * sizeof(int)));
   E.ratio = static_cast<float>(E.ve / T.voxel);
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
@@ -600,7 +666,7 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
 
 static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, E.dcount * sizeof(int), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * sizeof(int), e->stream));
   KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
   const int bricks = E.bnx * E.bny * E.bnz;
   KS_LAUNCH(k_brick_active, (bricks + 127) / 128, 128, 0, e->stream, E);
@@ -612,7 +678,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   EsdfView& E = e->view;
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
   if (mode == 1) {
-    const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;
+    const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;  // one warp per 32 x cells
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
     if (bits) KS_LAUNCH(k_seed_gather<true>, grid, 256, 0, e->stream, E, tsdf_view(t));
     else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
@@ -627,7 +693,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
 // bits: phase 1 reads the bit-packed mask; t != nullptr: sign recovery is fused into the x sweep
 static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   EsdfView& E = e->view;
-  const long long plane = static_cast<long long>(E.nx) * E.ny;
+  const int plane = E.nx * E.ny;
   const int nwords = (E.nz + 31) / 32;
   const unsigned fgrid = static_cast<unsigned>((plane + 127) / 128);
   if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
@@ -674,7 +740,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   e->cfg = *cfg;
   EsdfView& E = e->view;
   E.nx = cfg->nx, E.ny = cfg->ny, E.nz = cfg->nz;
-  E.cells = static_cast<long long>(cfg->nx) * cfg->ny * cfg->nz;
+  E.cells = cfg->nx * cfg->ny * cfg->nz;  // <= 2^30
   for (int a = 0; a < 3; ++a) E.origin[a] = cfg->origin[a];
   E.ve = cfg->voxel_size;
   pick_bands(E.ny, e->band_y, e->bands_y);
@@ -700,6 +766,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.brick, static_cast<size_t>(E.bnx) * E.bny * E.bnz));
   E.wpr = (E.nx + 31) / 32;
   KS_CUDA(cudaMalloc(&E.mbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.gbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
@@ -719,7 +786,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.mbits), cudaFree(E.gbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   cudaFreeHost(e->h_ctrl);

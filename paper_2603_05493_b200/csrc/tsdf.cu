@@ -122,16 +122,32 @@ __device__ __forceinline__ uint32_t voxel_bits(double sum, double wt, double geo
   return bits;
 }
 
-// One warp = 32 consecutive voxels = one word of each plane.
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {  // bit i -> bit 2i
+  v &= 0xFFFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+// One warp = 32 consecutive voxels = one surface word and two words of each 2-bit pair plane.
 __device__ __forceinline__ void store_digest(uint32_t* digest, int pool, int tid, uint32_t bits) {
   const int word = tid >> 5, lane = tid & 31;
-  uint32_t mine = 0;
-#pragma unroll
-  for (int p = 0; p < kDigestPlanes; ++p) {
-    const uint32_t w = __ballot_sync(0xFFFFFFFFu, (bits >> p) & 1u);
-    if (lane == p) mine = w;
+  const uint32_t surf = __ballot_sync(0xFFFFFFFFu, (bits >> kSurface) & 1u);
+  const uint32_t gv = __ballot_sync(0xFFFFFFFFu, (bits >> kGeomValid) & 1u);
+  const uint32_t gn = __ballot_sync(0xFFFFFFFFu, (bits >> kGeomNeg) & 1u);
+  const uint32_t cv = __ballot_sync(0xFFFFFFFFu, (bits >> kCombValid) & 1u);
+  const uint32_t cn = __ballot_sync(0xFFFFFFFFu, (bits >> kCombNeg) & 1u);
+  uint32_t* d = digest + static_cast<size_t>(pool) * kDigestWords;
+  if (lane == 0) d[word] = surf;
+  if (lane == 1 || lane == 2) {
+    const int half = lane - 1;
+    d[kDigestGeom + 2 * word + half] = spread16(gv >> (16 * half)) | (spread16(gn >> (16 * half)) << 1);
   }
-  if (lane < kDigestPlanes) digest[static_cast<size_t>(pool) * kDigestWords + lane * 16 + word] = mine;
+  if (lane == 3 || lane == 4) {
+    const int half = lane - 3;
+    d[kDigestComb + 2 * word + half] = spread16(cv >> (16 * half)) | (spread16(cn >> (16 * half)) << 1);
+  }
 }
 
 __device__ __forceinline__ bool op_blocked(const TsdfView& T) {
@@ -283,6 +299,7 @@ __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
       g[q] = CUDART_INF;
     }
     if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
+    if (threadIdx.x == 0) T.pool_geom[pool] = 0;
   }
 }
 
@@ -380,6 +397,7 @@ __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Pri
     }
     const double2 sw = T.sumwt[at];
     store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
+    if (tid == 0) T.pool_geom[pool] = 1;  // every voxel of a stamped block holds a finite distance
   }
 }
 
@@ -685,6 +703,8 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   KS_CUDA(cudaMalloc(&V.sumwt, cap * kBlockVoxels * sizeof(double2)));
   KS_CUDA(cudaMalloc(&V.geom, cap * kBlockVoxels * sizeof(double)));
   KS_CUDA(cudaMalloc(&V.digest, cap * kDigestWords * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&V.pool_geom, cap));
+  KS_CUDA(cudaMemsetAsync(V.pool_geom, 0, cap, t->stream));
   KS_CUDA(cudaMalloc(&V.ctrl, sizeof(TsdfCtrl)));
   KS_CUDA(cudaMalloc(&t->d_flags, cap * sizeof(int)));
   for (cudaEvent_t& ev : t->ev) KS_CUDA(cudaEventCreate(&ev));
@@ -709,7 +729,7 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaStreamSynchronize(t->stream);
   TsdfView& V = t->view;
   cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.free_list), cudaFree(V.pool_key);
-  cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.ctrl), cudaFree(t->d_flags);
+  cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
   cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
   cudaFreeHost(t->h_ctrl), cudaFreeHost(t->h_frame), cudaFree(t->d_frame);
