@@ -222,15 +222,12 @@ def run_ours(args):
     tsdf = api.make_tsdf(cfg, stream.cuda_stream)
     ecfg = api.EsdfConfig(tuple(scene.esdf_origin), nx, ny, nz, scene.esdf_voxel, "gather")
     esdf = api.DenseEsdf(ecfg, stream.cuda_stream)
-    # one TSDF handle integrates all cameras; with several frames each needs its own staged upload, so the
-    # multi-camera workloads keep one staging handle per camera pose by re-staging between integrates.
 
     def enqueue_update(upload: bool):
-        for f in frames:
-            if upload or len(frames) > 1:
-                tsdf.stage_frame(f)
-                tsdf.upload_frame_async()
-            tsdf.integrate_async()
+        for slot in range(len(frames)):  # one staging slot per camera
+            if upload:
+                tsdf.upload_frame_async(slot)
+            tsdf.integrate_async(slot)
         for p in prims:
             tsdf.stamp_async(p)
         esdf.build_async(tsdf)
@@ -254,7 +251,8 @@ def run_ours(args):
 
     with torch.cuda.stream(stream):
         # ---- eager warm-up (allocates blocks, binds the directory), then stage timings ---------------
-        tsdf.stage_frame(frames[0])
+        for slot, f in enumerate(frames):
+            tsdf.stage_frame(f, slot)
         enqueue_update(upload=True)
         rep = tsdf.sync()
         touched_last, live = rep.blocks_touched, rep.live_blocks
@@ -338,9 +336,9 @@ def run_ours(args):
         # ---- e2e through the graph API (stage + upload + replay + report), informational ----------------
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            if len(frames) == 1:
-                tsdf.stage_frame(frames[0])
-                tsdf.upload_frame_async()
+            for slot, f in enumerate(frames):
+                tsdf.stage_frame(f, slot)
+                tsdf.upload_frame_async(slot)
             graph.launch()
             tsdf.sync()
             esdf.report()

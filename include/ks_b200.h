@@ -126,6 +126,12 @@ KS_API int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float
 KS_API int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_host);
 KS_API int ks_tsdf_upload_frame_async(ks_tsdf* t);
 KS_API int ks_tsdf_integrate_async(ks_tsdf* t);
+/* the same with one staging slot per camera (0 .. KS_MAX_FRAME_SLOTS-1), so that a multi-camera
+ * update (repeated integrate_depth) is a single replayable graph; slot 0 is the one used above */
+#define KS_MAX_FRAME_SLOTS 8
+KS_API int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host);
+KS_API int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot);
+KS_API int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot);
 
 /* stamp_primitive (sdf_world.hpp:394-444) */
 KS_API int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t[3],

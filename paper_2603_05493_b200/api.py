@@ -68,7 +68,8 @@ ABI_SYMBOLS = [
     "ks_stream_destroy", "ks_stream_sync", "ks_graph_begin_capture", "ks_graph_end_capture", "ks_graph_launch",
     "ks_graph_node_count", "ks_graph_destroy", "ks_tsdf_config_init", "ks_tsdf_create", "ks_tsdf_destroy",
     "ks_tsdf_set_stream", "ks_tsdf_get_stream", "ks_tsdf_integrate_depth", "ks_tsdf_stage_frame",
-    "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stamp_cuboid", "ks_tsdf_stamp_sphere",
+    "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stage_frame_slot",
+    "ks_tsdf_upload_frame_slot_async", "ks_tsdf_integrate_slot_async", "ks_tsdf_stamp_cuboid", "ks_tsdf_stamp_sphere",
     "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_tsdf_decay_weights",
     "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
     "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
@@ -110,6 +111,9 @@ def load_library() -> C.CDLL:
         "ks_tsdf_integrate_depth": (C.c_int, [VP, P(CameraC), VP, P(I32)]),
         "ks_tsdf_stage_frame": (C.c_int, [VP, P(CameraC), VP]),
         "ks_tsdf_upload_frame_async": (C.c_int, [VP]),
+        "ks_tsdf_stage_frame_slot": (C.c_int, [VP, I32, P(CameraC), VP]),
+        "ks_tsdf_upload_frame_slot_async": (C.c_int, [VP, I32]),
+        "ks_tsdf_integrate_slot_async": (C.c_int, [VP, I32]),
         "ks_tsdf_integrate_async": (C.c_int, [VP]),
         "ks_tsdf_stamp_cuboid": (C.c_int, [VP, VP, VP, VP]),
         "ks_tsdf_stamp_sphere": (C.c_int, [VP, VP, D]),
@@ -276,18 +280,18 @@ class SparseTsdf:
             pass
 
     # capturable pieces
-    def stage_frame(self, frame: DepthFrame):
+    def stage_frame(self, frame: DepthFrame, slot: int = 0):
         depth = np.ascontiguousarray(frame.depth, np.float32).reshape(-1)
         if depth.size != frame.width * frame.height:
             raise ValidationError("depth frame: depth buffer size mismatch")  # sdf_world.hpp:200-201
         cam = frame.camera()
-        _check(self.lib.ks_tsdf_stage_frame(self.h, C.byref(cam), _ptr(depth)))
+        _check(self.lib.ks_tsdf_stage_frame_slot(self.h, slot, C.byref(cam), _ptr(depth)))
 
-    def upload_frame_async(self):
-        _check(self.lib.ks_tsdf_upload_frame_async(self.h))
+    def upload_frame_async(self, slot: int = 0):
+        _check(self.lib.ks_tsdf_upload_frame_slot_async(self.h, slot))
 
-    def integrate_async(self):
-        _check(self.lib.ks_tsdf_integrate_async(self.h))
+    def integrate_async(self, slot: int = 0):
+        _check(self.lib.ks_tsdf_integrate_slot_async(self.h, slot))
 
     def stamp_async(self, primitive):
         if isinstance(primitive, Cuboid):

@@ -56,16 +56,9 @@ KS_HD int floordiv_small(int num, int den) {
   int q = static_cast<int>(qf);
   if (static_cast<float>(q) > qf) --q;
 #endif
-  int rem = num - q * den;
-  while (rem < 0) {
-    --q;
-    rem += den;
-  }
-  while (rem >= den) {
-    ++q;
-    rem -= den;
-  }
-  return q;
+  // the estimate is within one of the true floor (|num| < 2^23, quotient error < 1): one exact step
+  const int rem = num - q * den;
+  return q + (rem >= den) - (rem < 0);
 }
 
 // First integer position where the parabola at u (offset gu) is strictly below

@@ -445,8 +445,9 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
 // The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
 // bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
-// kSigns fuses recover_signs into the store of the finished cell.
-template <bool kSigns>
+// kSigns: 0 = unsigned field (propagate), 1 = recover_signs fused into the store of the finished cell,
+// 2 = the same using the hint planes left by the bit-packed gather of this build.
+template <int kSigns>
 __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -490,10 +491,10 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
         sx = win;
         r2w = (y - sy) * (y - sy) + (z - sz) * (z - sz);
         site = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-        if (kSigns) probe.template set_site<true>(sx, sy, sz);
+        if (kSigns) probe.template set_site<kSigns == 2>(sx, sy, sz);
       }
       uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
-      if (kSigns && probe.template negative<true>(x)) d2 |= 0x80000000u;
+      if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
       E.site[o] = site;
       E.d2s[o] = d2;
     });
@@ -702,12 +703,14 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
-  if (t) {
-    KS_LAUNCH(k_sweep_x<true>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
-    KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
+  if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
+    KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
+  } else if (t) {
+    KS_LAUNCH(k_sweep_x<1>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
   } else {
-    KS_LAUNCH(k_sweep_x<false>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
+    KS_LAUNCH(k_sweep_x<0>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
   }
+  if (t) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
@@ -752,8 +755,9 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));

@@ -59,13 +59,15 @@ struct ks_tsdf {
   cudaStream_t stream;
   bool own_stream;
   TsdfCtrl* h_ctrl;  // pinned
-  // frame staging
-  FrameParams* h_frame;  // pinned
-  FrameParams* d_frame;
-  float* h_depth;  // pinned
-  float* d_depth;
-  size_t depth_cap;  // pixels
-  bool frame_staged;
+  // frame staging: one slot per camera, so a multi-camera update is one graph
+  struct FrameSlot {
+    FrameParams* h_frame;  // pinned
+    FrameParams* d_frame;
+    float* h_depth;  // pinned
+    float* d_depth;
+    size_t depth_cap;  // pixels
+    bool staged;
+  } slots[KS_MAX_FRAME_SLOTS];
   OpLists lists;
   int* d_flags;  // [capacity] recycle flags
   bool profile;
@@ -567,38 +569,52 @@ __global__ void k_fill_u64(uint64_t* p, size_t n, uint64_t v) {
 
 // ---- host side ----------------------------------------------------------------------
 
+static bool capturing(cudaStream_t stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  return cap != cudaStreamCaptureStatusNone;
+}
+
 static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
   const size_t want = std::max<size_t>(pixels * samples, 2 * static_cast<size_t>(t->cfg.capacity) + 1);
-  if (static_cast<size_t>(t->lists.cap) >= want && t->depth_cap >= pixels) return KS_OK;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(t->stream, &cap);
-  if (cap != cudaStreamCaptureStatusNone)
+  if (static_cast<size_t>(t->lists.cap) >= want) return KS_OK;
+  if (capturing(t->stream))
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  if (static_cast<size_t>(L.cap) < want) {
-    cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
-    L.cap = static_cast<int>(want);
-    KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
-    KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
-    KS_CUDA(cudaMalloc(&L.slot, want * sizeof(uint32_t)));
-    KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
-    KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
-    uint32_t slots = 1u << 16;
-    while (slots < 2 * want) slots <<= 1;
-    L.fset_mask = slots - 1;
-    KS_CUDA(cudaMalloc(&L.fset, static_cast<size_t>(slots) * sizeof(uint64_t)));
-    KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, L.fset, static_cast<size_t>(slots), kKeyEmpty);
-  }
-  if (t->depth_cap < pixels) {
-    if (t->h_depth) cudaFreeHost(t->h_depth);
-    if (t->d_depth) cudaFree(t->d_depth);
-    t->h_depth = nullptr, t->d_depth = nullptr;
-    KS_CUDA(cudaMallocHost(&t->h_depth, pixels * sizeof(float)));
-    KS_CUDA(cudaMalloc(&t->d_depth, pixels * sizeof(float)));
-    t->depth_cap = pixels;
-  }
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
+  L.cap = static_cast<int>(want);
+  KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
+  KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
+  KS_CUDA(cudaMalloc(&L.slot, want * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
+  KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
+  uint32_t slots = 1u << 16;
+  while (slots < 2 * want) slots <<= 1;
+  L.fset_mask = slots - 1;
+  KS_CUDA(cudaMalloc(&L.fset, static_cast<size_t>(slots) * sizeof(uint64_t)));
+  KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, L.fset, static_cast<size_t>(slots), kKeyEmpty);
   KS_CUDA(cudaStreamSynchronize(t->stream));
+  return KS_OK;
+}
+
+static int ensure_slot(ks_tsdf* t, int slot, size_t pixels) {
+  ks_tsdf::FrameSlot& S = t->slots[slot];
+  if (S.h_frame && S.depth_cap >= pixels) return KS_OK;
+  if (capturing(t->stream)) return fail(KS_ERR_INVALID, "tsdf: stage every camera slot once before capturing a graph");
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  if (!S.h_frame) {
+    KS_CUDA(cudaMallocHost(&S.h_frame, sizeof(FrameParams)));
+    KS_CUDA(cudaMalloc(&S.d_frame, sizeof(FrameParams)));
+  }
+  if (S.depth_cap < pixels) {
+    if (S.h_depth) cudaFreeHost(S.h_depth);
+    if (S.d_depth) cudaFree(S.d_depth);
+    S.h_depth = nullptr, S.d_depth = nullptr;
+    KS_CUDA(cudaMallocHost(&S.h_depth, pixels * sizeof(float)));
+    KS_CUDA(cudaMalloc(&S.d_depth, pixels * sizeof(float)));
+    S.depth_cap = pixels;
+  }
   return KS_OK;
 }
 
@@ -709,8 +725,6 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   KS_CUDA(cudaMalloc(&t->d_flags, cap * sizeof(int)));
   for (cudaEvent_t& ev : t->ev) KS_CUDA(cudaEventCreate(&ev));
   KS_CUDA(cudaMallocHost(&t->h_ctrl, sizeof(TsdfCtrl)));
-  KS_CUDA(cudaMallocHost(&t->h_frame, sizeof(FrameParams)));
-  KS_CUDA(cudaMalloc(&t->d_frame, sizeof(FrameParams)));
   KS_CUDA(cudaMemsetAsync(V.ctrl, 0, sizeof(TsdfCtrl), t->stream));
   KS_CUDA(cudaMemsetAsync(V.slot_pool, 0xFF, V.nslots * sizeof(int), t->stream));
   KS_CUDA(cudaMemsetAsync(V.digest, 0, cap * kDigestWords * sizeof(uint32_t), t->stream));
@@ -732,9 +746,13 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
   cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
-  cudaFreeHost(t->h_ctrl), cudaFreeHost(t->h_frame), cudaFree(t->d_frame);
-  if (t->h_depth) cudaFreeHost(t->h_depth);
-  if (t->d_depth) cudaFree(t->d_depth);
+  cudaFreeHost(t->h_ctrl);
+  for (ks_tsdf::FrameSlot& S : t->slots) {
+    if (S.h_frame) cudaFreeHost(S.h_frame);
+    if (S.d_frame) cudaFree(S.d_frame);
+    if (S.h_depth) cudaFreeHost(S.h_depth);
+    if (S.d_depth) cudaFree(S.d_depth);
+  }
   for (cudaEvent_t ev : t->ev) cudaEventDestroy(ev);
   if (t->own_stream) cudaStreamDestroy(t->stream);
   delete t;
@@ -771,18 +789,21 @@ int ks_tsdf_set_stream(ks_tsdf* t, ks_stream s) {
 
 ks_stream ks_tsdf_get_stream(const ks_tsdf* t) { return t ? static_cast<ks_stream>(t->stream) : nullptr; }
 
-int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_host) {
+int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host) {
   if (!t || !cam) return fail(KS_ERR_INVALID, "null argument");
+  if (slot < 0 || slot >= KS_MAX_FRAME_SLOTS) return fail(KS_ERR_INVALID, "tsdf: camera slot out of range");
   // DepthFrame::validate (sdf_world.hpp:197-202)
   if (cam->width <= 0 || cam->height <= 0 || cam->fx <= 0.0 || cam->fy <= 0.0)
     return fail(KS_ERR_INVALID, "depth frame: invalid intrinsics");
   if (!depth_host) return fail(KS_ERR_INVALID, "depth frame: depth buffer size mismatch");
-  const double step = 4.0 * t->cfg.voxel_size;                                                  // sdf_world.hpp:347
-  const int hs = std::max(1, static_cast<int>(std::ceil(t->cfg.truncation / step)));            // sdf_world.hpp:348
+  const double step = 4.0 * t->cfg.voxel_size;                                        // sdf_world.hpp:347
+  const int hs = std::max(1, static_cast<int>(std::ceil(t->cfg.truncation / step)));  // sdf_world.hpp:348
   const size_t pixels = static_cast<size_t>(cam->width) * cam->height;
   int rc = ensure_lists(t, pixels, 2 * hs + 1);
   if (rc != KS_OK) return rc;
-  FrameParams& F = *t->h_frame;
+  if ((rc = ensure_slot(t, slot, pixels)) != KS_OK) return rc;
+  ks_tsdf::FrameSlot& S = t->slots[slot];
+  FrameParams& F = *S.h_frame;
   F.width = cam->width, F.height = cam->height;
   F.fx = cam->fx, F.fy = cam->fy, F.cx = cam->cx, F.cy = cam->cy;
   std::memcpy(F.c2w.r, cam->pose_R, sizeof F.c2w.r);
@@ -790,34 +811,40 @@ int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_hos
   F.w2c = rigid_inverse(F.c2w);
   F.half_samples = hs;
   F.step = step;
-  std::memcpy(t->h_depth, depth_host, pixels * sizeof(float));
-  t->frame_staged = true;
+  std::memcpy(S.h_depth, depth_host, pixels * sizeof(float));
+  S.staged = true;
   return KS_OK;
 }
 
-int ks_tsdf_upload_frame_async(ks_tsdf* t) {
-  if (!t || !t->frame_staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
-  const size_t pixels = static_cast<size_t>(t->h_frame->width) * t->h_frame->height;
-  KS_CUDA(cudaMemcpyAsync(t->d_frame, t->h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
-  KS_CUDA(cudaMemcpyAsync(t->d_depth, t->h_depth, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
+int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot) {
+  if (!t || slot < 0 || slot >= KS_MAX_FRAME_SLOTS || !t->slots[slot].staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
+  ks_tsdf::FrameSlot& S = t->slots[slot];
+  const size_t pixels = static_cast<size_t>(S.h_frame->width) * S.h_frame->height;
+  KS_CUDA(cudaMemcpyAsync(S.d_frame, S.h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
+  KS_CUDA(cudaMemcpyAsync(S.d_depth, S.h_depth, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
   return KS_OK;
 }
 
-int ks_tsdf_integrate_async(ks_tsdf* t) {
-  if (!t || !t->frame_staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
-  const int pixels = t->h_frame->width * t->h_frame->height;
+int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) {
+  if (!t || slot < 0 || slot >= KS_MAX_FRAME_SLOTS || !t->slots[slot].staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
+  ks_tsdf::FrameSlot& S = t->slots[slot];
+  const int pixels = S.h_frame->width * S.h_frame->height;
   const bool prof = profiling(t);
   KS_MARK(t, 0);
-  KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
+  KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_MARK(t, 1);
   run_allocation(t);
   KS_MARK(t, 2);
-  KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, t->d_frame, t->d_depth);
+  KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 1);
   KS_MARK(t, 3);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
+
+int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_host) { return ks_tsdf_stage_frame_slot(t, 0, cam, depth_host); }
+int ks_tsdf_upload_frame_async(ks_tsdf* t) { return ks_tsdf_upload_frame_slot_async(t, 0); }
+int ks_tsdf_integrate_async(ks_tsdf* t) { return ks_tsdf_integrate_slot_async(t, 0); }
 
 int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
   if (!t) return fail(KS_ERR_INVALID, "null tsdf");
