@@ -69,9 +69,9 @@ WORKLOAD_DESC = {
 
 # ---- clocks ---------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is under this benchmark's load."""
 
-    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    QUERY = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
@@ -82,7 +82,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._pump, daemon=True).start()
         except OSError:
@@ -90,28 +90,39 @@ class ClockSampler:
 
     def _pump(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
 
-    def stop(self):
+    def stop(self, t_begin: float, t_end: float):
+        """Summarise the samples that arrived inside [t_begin, t_end] (the timed region)."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        time.sleep(0.05)
         self.proc.terminate()
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            if len(r) < 7:
-                continue
-            try:
-                sm.append(float(r[0]))
-                mx.append(float(r[1]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, r[3:7]):
-                if flag.lower().startswith("active"):
-                    reasons.add(name)
+
+        def summarise(rows):
+            sm, mx, reasons = [], [], set()
+            for _, r in rows:
+                if len(r) < 8:
+                    continue
+                try:
+                    sm.append(float(r[1]))
+                    mx.append(float(r[2]))
+                except ValueError:
+                    continue
+                for name, flag in zip(names, r[4:8]):
+                    if flag.lower().startswith("active"):
+                        reasons.add(name)
+            return sm, mx, reasons
+
+        inside = [row for row in self.rows if t_begin <= row[0] <= t_end]
+        sm, mx, reasons = summarise(inside)
+        window = "timed region"
+        if not sm:  # region shorter than the sampling period: fall back to every sample of the loaded phase
+            sm, mx, reasons = summarise(self.rows)
+            window = "warm-up + timed region"
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 # ---- CPU legs -------------------------------------------------------------------------------------------
@@ -275,7 +286,9 @@ def run_ours(args):
         with graph:
             enqueue_update(upload=False)
         kernel_nodes, all_nodes = graph.node_count()
-        for _ in range(args.warmup):
+        sampler = ClockSampler(local)
+        sampler.start()
+        for _ in range(max(args.warmup, 50)):  # also gives the clock sampler a loaded GPU to look at
             flush.zero_()
             graph.launch()
             if world > 1:
@@ -283,11 +296,10 @@ def run_ours(args):
         stream.synchronize()
         if world > 1:
             dist.barrier()
-        sampler = ClockSampler(local)
-        sampler.start()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         torch.cuda.synchronize()
+        t_begin = time.time()
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the event pair)
             starts[i].record(stream)
@@ -296,9 +308,10 @@ def run_ours(args):
                 gather_summaries()
             ends[i].record(stream)
         torch.cuda.synchronize()
+        t_end = time.time()
         if world > 1:
             dist.barrier()
-        clocks = sampler.stop()
+        clocks = sampler.stop(t_begin, t_end)
         per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -414,7 +427,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))

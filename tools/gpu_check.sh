@@ -7,7 +7,7 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
 echo "== pytest -m gpu"; timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 | tee $OUT/pytest_gpu.txt
-echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 3 2> $OUT/bench_err.txt | tee $OUT/bench.json
+echo "== bench ours"; timeout 900 python bench.py --steps 200 --warmup 5 2> $OUT/bench_err.txt | tee $OUT/bench.json
 tail -5 $OUT/bench_err.txt
 if [ "$SKIP_REF" != "1" ]; then
   echo "== bench reference"; timeout 900 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tee $OUT/bench_reference.json
