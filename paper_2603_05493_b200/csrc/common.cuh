@@ -107,7 +107,7 @@ struct TsdfCtrl {  // device control block, mirrored to pinned host memory on sy
   int touched, fresh;   // per-op counters (reset by the op's tail kernel)
   int abort_op;         // the op in flight hit KS_ERR_RANGE
   int last_touched, last_recycled;
-  int pad;
+  int arrivals;         // CTAs of the apply kernel that are done (the last one closes the op)
 };
 
 struct TsdfView {

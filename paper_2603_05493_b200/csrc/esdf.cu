@@ -197,6 +197,112 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
   if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
 }
 
+// The fused build's gather: one CTA per 8^3-cell brick, one thread per cell.  An inactive brick only
+// writes its zero bytes.  An active brick stages what its 512 x 7 probes can touch -- the per-axis
+// voxel tables (72 ints), the directory entries of the <= kStage blocks in reach and their surface
+// bit planes -- in shared memory, so a probe is two shared-memory reads.  Output: one byte per
+// (y, z) row of the brick in the bit-packed seed plane and in the geometry-near plane.
+constexpr int kStage = 64;
+__global__ void __launch_bounds__(512) k_seed_gather_bricks(EsdfView E, TsdfView T) {
+  __shared__ int s_tab[3][5][8];        // [axis][VoxRow][cell in brick]
+  __shared__ int s_lo[3], s_n[3];
+  __shared__ int s_pool[kStage];
+  __shared__ uint8_t s_geom[kStage];
+  __shared__ uint32_t s_plane[kStage][16];
+  const int brick = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int bx = brick % E.bnx, by = (brick / E.bnx) % E.bny, bz = brick / (E.bnx * E.bny);
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const int x = 8 * bx + lx, y = 8 * by + ly, z = 8 * bz + lz;
+  uint8_t* mrow = reinterpret_cast<uint8_t*>(E.mbits);
+  uint8_t* grow = reinterpret_cast<uint8_t*>(E.gbits);
+  const bool in_grid = x < E.nx && y < E.ny && z < E.nz;
+  const int out_byte = (y + E.ny * z) * (E.wpr * 4) + bx;  // byte bx of row (y, z): bits 8bx .. 8bx+7
+  if (!E.brick[brick]) {
+    if (lx == 0 && y < E.ny && z < E.nz) {
+      mrow[out_byte] = 0;
+      grow[out_byte] = 0;
+    }
+    return;
+  }
+  const int total = E.nx + E.ny + E.nz;
+  if (tid < 120) {  // 3 axes x 5 rows x 8 cells
+    const int a = tid / 40, r = (tid / 8) % 5, c = tid & 7;
+    const int dims[3] = {E.nx, E.ny, E.nz};
+    const int b0[3] = {8 * bx, 8 * by, 8 * bz};
+    const int pos = min(b0[a] + c, dims[a] - 1);
+    s_tab[a][r][c] = E.vox[r * total + axis_base(E, a) + pos];
+  }
+  __syncthreads();
+  if (tid < 3) {  // directory range reachable from this brick: [centre - ve, centre + ve] per axis
+    const int dims[3] = {E.nx, E.ny, E.nz};
+    const int b0[3] = {8 * bx, 8 * by, 8 * bz};
+    const int last = min(7, dims[tid] - 1 - b0[tid]);
+    const int lo = s_tab[tid][kVoxMe][0] >> 3, hi = s_tab[tid][kVoxPe][last] >> 3;
+    s_lo[tid] = lo;
+    s_n[tid] = hi - lo + 1;
+  }
+  __syncthreads();
+  const int n0 = s_n[0], n1 = s_n[1], n2 = s_n[2];
+  const int nblocks = n0 * n1 * n2;
+  const bool staged = nblocks <= kStage;
+  if (staged) {
+    if (tid < nblocks) {
+      const int cx = tid % n0, cy = (tid / n0) % n1, cz = tid / (n0 * n1);
+      const int pool = __ldg(E.dir + ((s_lo[0] + cx) + E.dn[0] * ((s_lo[1] + cy) + E.dn[1] * (s_lo[2] + cz))));
+      s_pool[tid] = pool;
+      s_geom[tid] = pool >= 0 ? T.pool_geom[pool] : 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < nblocks * 16; i += blockDim.x) {
+      const int pool = s_pool[i >> 4];
+      s_plane[i >> 4][i & 15] = pool >= 0 ? __ldg(T.digest + (pool * kDigestWords + (i & 15))) : 0u;
+    }
+    __syncthreads();
+  }
+  bool seed = false, geom_near = false;
+  if (in_grid) {
+    const int xc = s_tab[0][kVoxC][lx], xp = s_tab[0][kVoxPh][lx], xm = s_tab[0][kVoxMh][lx];
+    const int yc = s_tab[1][kVoxC][ly], yp = s_tab[1][kVoxPh][ly], ym = s_tab[1][kVoxMh][ly];
+    const int zc = s_tab[2][kVoxC][lz], zp = s_tab[2][kVoxPh][lz], zm = s_tab[2][kVoxMh][lz];
+    auto probe = [&](int vx, int vy, int vz) -> bool {
+      const int local = local_index(vx, vy, vz);
+      if (staged) {
+        const int b = ((vx >> 3) - s_lo[0]) + n0 * (((vy >> 3) - s_lo[1]) + n1 * ((vz >> 3) - s_lo[2]));
+        return (s_plane[b][local >> 5] >> (local & 31)) & 1u;
+      }
+      const int pool = dir_lookup(E, vx, vy, vz);
+      return pool >= 0 && surface_bit(T, pool, local) != 0;
+    };
+    seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
+           (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
+           (zm != zc && probe(xc, yc, zm));
+    if (seed) {  // any stamped block a sign probe from this site can reach (centre +- ve per axis)?
+      const int x0 = s_tab[0][kVoxMe][lx] >> 3, x1 = s_tab[0][kVoxPe][lx] >> 3;
+      const int y0 = s_tab[1][kVoxMe][ly] >> 3, y1 = s_tab[1][kVoxPe][ly] >> 3;
+      const int z0 = s_tab[2][kVoxMe][lz] >> 3, z1 = s_tab[2][kVoxPe][lz] >> 3;
+      for (int cz = z0; cz <= z1; ++cz)
+        for (int cy = y0; cy <= y1; ++cy)
+          for (int cx = x0; cx <= x1; ++cx) {
+            if (staged) {
+              geom_near |= s_geom[(cx - s_lo[0]) + n0 * ((cy - s_lo[1]) + n1 * (cz - s_lo[2]))] != 0;
+            } else {
+              const int pool = __ldg(E.dir + (cx + E.dn[0] * (cy + E.dn[1] * cz)));
+              geom_near |= pool >= 0 && T.pool_geom[pool];
+            }
+          }
+    }
+  }
+  // a warp is 4 rows (ly) of 8 x cells: byte k of the ballot belongs to row ly0 + k
+  const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
+  const uint32_t gvotes = __ballot_sync(0xFFFFFFFFu, geom_near);
+  if (lx == 0 && y < E.ny && z < E.nz) {
+    mrow[out_byte] = static_cast<uint8_t>(votes >> (lane & 24));
+    grow[out_byte] = static_cast<uint8_t>(gvotes >> (lane & 24));
+  }
+  if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
+}
+
 // ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
 __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
   const int bound = T.ctrl->next_fresh;
@@ -681,7 +787,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   if (mode == 1) {
     const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;  // one warp per 32 x cells
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-    if (bits) KS_LAUNCH(k_seed_gather<true>, grid, 256, 0, e->stream, E, tsdf_view(t));
+    if (bits) KS_LAUNCH(k_seed_gather_bricks, E.bnx * E.bny * E.bnz, 512, 0, e->stream, E, tsdf_view(t));
     else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
   } else {
     KS_CUDA(cudaMemsetAsync(E.mask, 0, E.cells, e->stream));
@@ -779,6 +885,8 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.mbits, 0, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.gbits, 0, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
   KS_CUDA(cudaMemsetAsync(E.site, 0xFF, E.cells * sizeof(uint32_t), e->stream));  // no sites yet
   KS_CUDA(cudaMemsetAsync(E.d2s, 0xFF, E.cells * sizeof(uint32_t), e->stream));
   KS_CUDA(cudaStreamSynchronize(e->stream));

@@ -29,7 +29,6 @@ struct OpLists {  // scratch of the op in flight (discover -> rank -> commit -> 
   int* pool;           // [cap] pool entry (filled by commit for new blocks)
   uint32_t* slot;      // [cap] slot in the per-frame set to clear afterwards (kNoSlot for stamps)
   int* fresh_idx;      // [cap] indices into key[] of blocks that must be allocated
-  int* fresh_rank;     // [cap] rank of that key among the new keys (lexicographic)
   int cap;
   uint64_t* fset;      // per-frame dedup set, open addressing
   uint32_t fset_mask;  // slots - 1
@@ -225,39 +224,29 @@ __global__ void __launch_bounds__(256) k_discover(TsdfView T, OpLists L, const F
   }
 }
 
-// ---- phase 3a: rank of every new key among the new keys (sorted order of allocate_keys) ----
-__global__ void __launch_bounds__(256) k_rank(TsdfView T, OpLists L) {
-  if (op_blocked(T)) return;
-  const int n = min(T.ctrl->fresh, L.cap);
-  __shared__ uint64_t tile[256];
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const int i = base + threadIdx.x;
-    const uint64_t mine = i < n ? L.key[L.fresh_idx[i]] : 0;
-    int rank = 0;
-    for (int t0 = 0; t0 < n; t0 += 256) {
-      const int j = t0 + threadIdx.x;
-      tile[threadIdx.x] = j < n ? L.key[L.fresh_idx[j]] : kKeyEmpty;
-      __syncthreads();
-      const int m = min(256, n - t0);
-#pragma unroll 8
-      for (int k = 0; k < m; ++k) rank += tile[k] < mine;
-      __syncthreads();
-    }
-    if (i < n) L.fresh_rank[i] = rank;
-  }
-}
-
-// ---- phase 3b: pool assignment (free list first, LIFO), warp-cooperative hash insert, block reset
-// (BlockHashTable::insert sdf_world.hpp:146-172, VoxelBlock::reset :70-74) ----
+// ---- phase 3: allocation.  One CTA per new block: its rank among the new keys (= its place in the
+// sorted order allocate_keys inserts in, sdf_world.hpp:308-322) is counted by the whole CTA, the pool
+// index follows (free list LIFO first, then fresh), warp 0 inserts the key with a warp-cooperative
+// probe (32 slots per step, ballot, one CAS; BlockHashTable::insert sdf_world.hpp:146-172) and the
+// CTA resets the block (VoxelBlock::reset :70-74). ----
 __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
   if (op_blocked(T)) return;
   const TsdfCtrl* c = T.ctrl;
   const int n = min(c->fresh, L.cap);
   const int free_count = c->free_count, next_fresh = c->next_fresh;
+  __shared__ int s_count[8];
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const int idx = L.fresh_idx[i];
     const uint64_t key = L.key[idx];
-    const int r = L.fresh_rank[i];
+    int below = 0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) below += L.key[L.fresh_idx[j]] < key;
+    for (int d = 16; d > 0; d >>= 1) below += __shfl_down_sync(0xFFFFFFFFu, below, d);
+    __syncthreads();  // s_count free again
+    if ((threadIdx.x & 31) == 0) s_count[threadIdx.x >> 5] = below;
+    __syncthreads();
+    int r = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) r += s_count[w];
     const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
@@ -302,6 +291,47 @@ __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
     }
     if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
     if (threadIdx.x == 0) T.pool_geom[pool] = 0;
+  }
+}
+
+// Op tail, run by the last CTA of the apply kernel: commit the counters or surface the error
+// (allocate_keys' all-or-nothing check, sdf_world.hpp:312-318) and reset the per-op state.
+__device__ void finish_op(const TsdfView& T, int list_cap, int is_integrate) {
+  TsdfCtrl* c = T.ctrl;
+  const int avail = c->free_count + (T.capacity - c->next_fresh);
+  int status = 0;
+  if (c->abort_op) {
+    status = c->err != 0 ? c->err : static_cast<int>(KS_ERR_RANGE);
+  } else if (c->fresh > avail || c->touched > list_cap) {
+    status = KS_ERR_POOL_EXHAUSTED;
+    if (c->err == 0) {
+      c->err_required = c->fresh;
+      c->err_available = avail;
+    }
+  } else if (c->live + c->fresh > T.nslots) {
+    status = KS_ERR_TABLE_FULL;
+  } else {
+    const int from_free = min(c->fresh, c->free_count);
+    c->free_count -= from_free;
+    c->next_fresh += c->fresh - from_free;
+    c->live += c->fresh;
+  }
+  if (status != 0 && c->err == 0) c->err = status;
+  if (is_integrate) c->last_touched = status == 0 ? c->touched : -1;
+  c->touched = 0;
+  c->fresh = 0;
+  c->abort_op = 0;
+}
+// Every CTA calls this after its last block; the final arrival runs finish_op.
+__device__ __forceinline__ void arrive_and_finish(const TsdfView& T, int list_cap, int is_integrate) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&T.ctrl->arrivals, 1) == static_cast<int>(gridDim.x) - 1) {
+      T.ctrl->arrivals = 0;
+      __threadfence();
+      finish_op(T, list_cap, is_integrate);
+    }
   }
 }
 
@@ -352,6 +382,7 @@ __global__ void __launch_bounds__(512) k_integrate(TsdfView T, OpLists L, const 
     }
     store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, geom, T.seed_thr));
   }
+  arrive_and_finish(T, L.cap, 1);
 }
 
 // ---- stamp: candidate blocks in the primitive's padded AABB (sdf_world.hpp:421-434) ----
@@ -380,8 +411,7 @@ __global__ void __launch_bounds__(256) k_stamp_candidates(TsdfView T, OpLists L,
 
 // ---- stamp: per-voxel min with the analytic distance (sdf_world.hpp:437-443) ----
 __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Primitive P) {
-  if (op_blocked(T)) return;
-  const int touched = min(T.ctrl->touched, L.cap);
+  const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
   const int tid = threadIdx.x;
   const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
   const double v = T.voxel;
@@ -401,34 +431,7 @@ __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Pri
     store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
     if (tid == 0) T.pool_geom[pool] = 1;  // every voxel of a stamped block holds a finite distance
   }
-}
-
-// ---- op tail: commit the counters, surface errors (allocate_keys :312-318) ----
-__global__ void k_finish(TsdfView T, int list_cap, int is_integrate) {
-  TsdfCtrl* c = T.ctrl;
-  const int avail = c->free_count + (T.capacity - c->next_fresh);
-  int status = 0;
-  if (c->abort_op) {
-    status = c->err != 0 ? c->err : static_cast<int>(KS_ERR_RANGE);
-  } else if (c->fresh > avail || c->touched > list_cap) {
-    status = KS_ERR_POOL_EXHAUSTED;
-    if (c->err == 0) {
-      c->err_required = c->fresh;
-      c->err_available = avail;
-    }
-  } else if (c->live + c->fresh > T.nslots) {
-    status = KS_ERR_TABLE_FULL;
-  } else {
-    const int from_free = min(c->fresh, c->free_count);
-    c->free_count -= from_free;
-    c->next_fresh += c->fresh - from_free;
-    c->live += c->fresh;
-  }
-  if (status != 0 && c->err == 0) c->err = status;
-  if (is_integrate) c->last_touched = status == 0 ? c->touched : -1;
-  c->touched = 0;
-  c->fresh = 0;
-  c->abort_op = 0;
+  arrive_and_finish(T, L.cap, 0);
 }
 
 // ---- decay_weights (sdf_world.hpp:449-457) ----
@@ -582,13 +585,12 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fset);
   L.cap = static_cast<int>(want);
   KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
   KS_CUDA(cudaMalloc(&L.slot, want * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
-  KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
   uint32_t slots = 1u << 16;
   while (slots < 2 * want) slots <<= 1;
   L.fset_mask = slots - 1;
@@ -618,10 +620,7 @@ static int ensure_slot(ks_tsdf* t, int slot, size_t pixels) {
   return KS_OK;
 }
 
-static void run_allocation(ks_tsdf* t) {
-  KS_LAUNCH(k_rank, 2 * kSmCount, 256, 0, t->stream, t->view, t->lists);
-  KS_LAUNCH(k_commit, 4 * kSmCount, 256, 0, t->stream, t->view, t->lists);
-}
+static void run_allocation(ks_tsdf* t) { KS_LAUNCH(k_commit, 4 * kSmCount, 256, 0, t->stream, t->view, t->lists); }
 
 static int report_status(const TsdfCtrl& c) {
   switch (c.err) {
@@ -671,7 +670,6 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
   run_allocation(t);
   KS_MARK(t, 5);
   KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
-  KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 0);
   KS_MARK(t, 6);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -745,7 +743,7 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.free_list), cudaFree(V.pool_key);
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fset);
   cudaFreeHost(t->h_ctrl);
   for (ks_tsdf::FrameSlot& S : t->slots) {
     if (S.h_frame) cudaFreeHost(S.h_frame);
@@ -836,7 +834,6 @@ int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) {
   run_allocation(t);
   KS_MARK(t, 2);
   KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
-  KS_LAUNCH(k_finish, 1, 1, 0, t->stream, t->view, t->lists.cap, 1);
   KS_MARK(t, 3);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
