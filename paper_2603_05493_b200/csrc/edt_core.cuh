@@ -75,40 +75,46 @@ KS_HD int cost(int t, int u, int gu) {
 }
 
 // Stage 1: band-local stack for one row.  Src::r2(pos,row) < 0 means "no candidate".
+// Written as ONE flat loop in which every iteration either pops the top or consumes the next
+// position: lanes (= rows) with different pop counts re-converge every iteration instead of
+// serialising a nested pop loop per position.
 template <class Src>
 KS_HD void build_band(const RowTile& T, const Src& src, int b, int row) {
   const int base = b * T.band;
   const int end = base + T.band < T.n ? base + T.band : T.n;
   int top = base;
   int l = 0, tl = 0, gl = 0;  // cached top entry
-  for (int u = base; u < end; ++u) {
-    const int gu = src.r2(u, row);
-    if (gu < 0) continue;
-    while (true) {
+  int u = base;
+  int gu = u < end ? src.r2(u, row) : -1;
+  while (u < end) {
+    bool advance = true;
+    if (gu >= 0) {
       if (top == base) {
         T.stk_s[at(top, row)] = static_cast<uint16_t>(u);
         T.stk_t[at(top, row)] = 0;
         l = u, tl = 0, gl = gu;
         ++top;
-        break;
-      }
-      if (cost(tl, l, gl) > cost(tl, u, gu)) {  // u strictly better where l starts: l never wins
+      } else if (cost(tl, l, gl) > cost(tl, u, gu)) {  // u strictly better where l starts: l never wins
         --top;
         if (top > base) {
           l = T.stk_s[at(top - 1, row)];
           tl = T.stk_t[at(top - 1, row)];
           gl = src.r2(l, row);
         }
-        continue;
+        advance = false;
+      } else {
+        const int w = takeover(l, gl, u, gu);
+        if (w < T.n) {
+          T.stk_s[at(top, row)] = static_cast<uint16_t>(u);
+          T.stk_t[at(top, row)] = static_cast<uint16_t>(w);
+          l = u, tl = w, gl = gu;
+          ++top;
+        }
       }
-      const int w = takeover(l, gl, u, gu);
-      if (w < T.n) {
-        T.stk_s[at(top, row)] = static_cast<uint16_t>(u);
-        T.stk_t[at(top, row)] = static_cast<uint16_t>(w);
-        l = u, tl = w, gl = gu;
-        ++top;
-      }
-      break;
+    }
+    if (advance) {
+      ++u;
+      gu = u < end ? src.r2(u, row) : -1;
     }
   }
   T.lo[at(b, row)] = static_cast<uint16_t>(base);

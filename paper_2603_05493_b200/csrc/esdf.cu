@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <vector>
 
@@ -30,7 +31,7 @@ constexpr int kMaxDim = 1024;  // 10-bit site packing, uint16 stacks
 struct EsdfCtrl {
   unsigned long long seed_count;
   int signs_recovered;
-  int pad;
+  int active_bricks;  // entries of EsdfView::active, rebuilt with the directory
 };
 
 // per-axis table rows (each [nx+ny+nz]): TSDF voxel index of (cell centre + offset), stored
@@ -51,6 +52,7 @@ struct EsdfView {
   int dlo[3], dn[3];
   int dcount;
   uint8_t* brick;    // [ceil(n/8)^3] 1 when a live TSDF block can be probed from the 8^3-cell brick
+  int* active;       // compacted ids of the active bricks (count in ctrl->active_bricks)
   int bnx, bny, bnz;
   uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66) -- API paths
   uint32_t* mbits;   // [nz][ny][wpr] the same mask, one bit per cell -- fused build path
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
           break;
         }
   E.brick[i] = any;
+  if (any) E.active[atomicAdd(&E.ctrl->active_bricks, 1)] = i;
 }
 
 // ---- seed_gather (esdf.hpp:102-122): 7-probe stencil per ESDF cell, bits instead of voxels ----
@@ -197,8 +200,8 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
   if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
 }
 
-// The fused build's gather: one CTA per 8^3-cell brick, one thread per cell.  An inactive brick only
-// writes its zero bytes.  An active brick stages what its 512 x 7 probes can touch -- the per-axis
+// The fused build's gather: a persistent grid walks the ACTIVE 8^3-cell bricks (one thread per cell);
+// the bit planes are cleared beforehand, so inactive bricks cost nothing.  A brick stages what its 512 x 7 probes can touch -- the per-axis
 // voxel tables (72 ints), the directory entries of the <= kStage blocks in reach and their surface
 // bit planes -- in shared memory, so a probe is two shared-memory reads.  Output: one byte per
 // (y, z) row of the brick in the bit-packed seed plane and in the geometry-near plane.
@@ -209,23 +212,19 @@ __global__ void __launch_bounds__(512) k_seed_gather_bricks(EsdfView E, TsdfView
   __shared__ int s_pool[kStage];
   __shared__ uint8_t s_geom[kStage];
   __shared__ uint32_t s_plane[kStage][16];
-  const int brick = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int bx = brick % E.bnx, by = (brick / E.bnx) % E.bny, bz = brick / (E.bnx * E.bny);
   const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
-  const int x = 8 * bx + lx, y = 8 * by + ly, z = 8 * bz + lz;
   uint8_t* mrow = reinterpret_cast<uint8_t*>(E.mbits);
   uint8_t* grow = reinterpret_cast<uint8_t*>(E.gbits);
+  const int total = E.nx + E.ny + E.nz;
+  const int n_active = E.ctrl->active_bricks;
+  for (int item = blockIdx.x; item < n_active; item += gridDim.x) {
+  const int brick = E.active[item];
+  const int bx = brick % E.bnx, by = (brick / E.bnx) % E.bny, bz = brick / (E.bnx * E.bny);
+  const int x = 8 * bx + lx, y = 8 * by + ly, z = 8 * bz + lz;
   const bool in_grid = x < E.nx && y < E.ny && z < E.nz;
   const int out_byte = (y + E.ny * z) * (E.wpr * 4) + bx;  // byte bx of row (y, z): bits 8bx .. 8bx+7
-  if (!E.brick[brick]) {
-    if (lx == 0 && y < E.ny && z < E.nz) {
-      mrow[out_byte] = 0;
-      grow[out_byte] = 0;
-    }
-    return;
-  }
-  const int total = E.nx + E.ny + E.nz;
+  __syncthreads();  // shared staging of the previous brick is no longer read
   if (tid < 120) {  // 3 axes x 5 rows x 8 cells
     const int a = tid / 40, r = (tid / 8) % 5, c = tid & 7;
     const int dims[3] = {E.nx, E.ny, E.nz};
@@ -301,6 +300,7 @@ __global__ void __launch_bounds__(512) k_seed_gather_bricks(EsdfView E, TsdfView
     grow[out_byte] = static_cast<uint8_t>(gvotes >> (lane & 24));
   }
   if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
+  }
 }
 
 // ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
@@ -773,6 +773,7 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
 
 static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
+  KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
   KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * sizeof(int), e->stream));
   KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
   const int bricks = E.bnx * E.bny * E.bnz;
@@ -783,12 +784,16 @@ static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
 // bits: gather straight into the bit-packed mask of the fused build (gather mode only)
 static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.ctrl, 0, offsetof(EsdfCtrl, active_bricks), e->stream));  // seed_count, signs_recovered
   if (mode == 1) {
     const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;  // one warp per 32 x cells
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-    if (bits) KS_LAUNCH(k_seed_gather_bricks, E.bnx * E.bny * E.bnz, 512, 0, e->stream, E, tsdf_view(t));
-    else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
+    if (bits) {
+      const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
+      KS_CUDA(cudaMemsetAsync(E.mbits, 0, plane_bytes, e->stream));
+      KS_CUDA(cudaMemsetAsync(E.gbits, 0, plane_bytes, e->stream));
+      KS_LAUNCH(k_seed_gather_bricks, std::min(E.bnx * E.bny * E.bnz, 4 * kSmCount), 512, 0, e->stream, E, tsdf_view(t));
+    } else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
   } else {
     KS_CUDA(cudaMemsetAsync(E.mask, 0, E.cells, e->stream));
     KS_LAUNCH(k_seed_scatter, 4 * kSmCount, 512, 0, e->stream, E, tsdf_view(t));
@@ -874,6 +879,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.qsf, total * sizeof(float)));
   E.bnx = (E.nx + 7) / 8, E.bny = (E.ny + 7) / 8, E.bnz = (E.nz + 7) / 8;
   KS_CUDA(cudaMalloc(&E.brick, static_cast<size_t>(E.bnx) * E.bny * E.bnz));
+  KS_CUDA(cudaMalloc(&E.active, static_cast<size_t>(E.bnx) * E.bny * E.bnz * sizeof(int)));
   E.wpr = (E.nx + 31) / 32;
   KS_CUDA(cudaMalloc(&E.mbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.gbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
@@ -898,7 +904,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.mbits), cudaFree(E.gbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.gbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   cudaFreeHost(e->h_ctrl);
