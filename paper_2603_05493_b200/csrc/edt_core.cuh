@@ -34,36 +34,17 @@ namespace edt {
 constexpr int kRows = 32;
 constexpr uint16_t kNone = 0xFFFFu;
 
-// Where a stack slot lives.  A slot number is a position-like index: band b owns slots
-// [b*band, b*band + band).
-//   TileLayout     : 32 rows per tile, lane <-> row, warp <-> band; arrays are [slot][32 rows], so
-//                    lane == shared-memory bank for every access.
-//   LaneBandLayout : one row per warp, lane <-> band; arrays are [slot within band][32 bands], so
-//                    every access a lane makes to its OWN band hits its own bank.
-struct TileLayout {
-  KS_HD int slot(int s, int /*band*/, int row) const { return s * kRows + row; }
-  KS_HD int meta(int band, int row) const { return band * kRows + row; }
-};
-struct LaneBandLayout {
-  int band_size;
-  KS_HD int slot(int s, int band, int /*row*/) const { return (s - band * band_size) * 32 + band; }
-  KS_HD int meta(int band, int /*row*/) const { return band; }
-};
-
-template <class Layout>
-struct RowTileT {
-  uint16_t* stk_s;  // stack entry: site position
-  uint16_t* stk_t;  // stack entry: first position where it wins
-  uint16_t* lo;     // per band: first live stack slot
-  uint16_t* hi;     // per band: one past the last live slot
+struct RowTile {
+  uint16_t* stk_s;  // [n][32]   stack entry: site position
+  uint16_t* stk_t;  // [n][32]   stack entry: first position where it wins
+  uint16_t* lo;     // [bands][32] first live stack slot of the band
+  uint16_t* hi;     // [bands][32] one past the last live slot
   int n;            // row length
   int band;         // positions per band
   int bands;        // ceil(n / band)
-  Layout L;
 };
-using RowTile = RowTileT<TileLayout>;
 
-KS_HD int at(int pos, int row) { return pos * kRows + row; }  // [position][32 rows] input tiles
+KS_HD int at(int pos, int row) { return pos * kRows + row; }
 
 // floor(num / den) for den > 0 and |num| < 2^23 (positions < 1024, r2 < 2^22):
 // one float divide plus an exact integer correction.
@@ -97,8 +78,8 @@ KS_HD int cost(int t, int u, int gu) {
 // Written as ONE flat loop in which every iteration either pops the top or consumes the next
 // position: lanes (= rows) with different pop counts re-converge every iteration instead of
 // serialising a nested pop loop per position.
-template <class Layout, class Src>
-KS_HD void build_band(const RowTileT<Layout>& T, const Src& src, int b, int row) {
+template <class Src>
+KS_HD void build_band(const RowTile& T, const Src& src, int b, int row) {
   const int base = b * T.band;
   const int end = base + T.band < T.n ? base + T.band : T.n;
   int top = base;
@@ -109,23 +90,23 @@ KS_HD void build_band(const RowTileT<Layout>& T, const Src& src, int b, int row)
     bool advance = true;
     if (gu >= 0) {
       if (top == base) {
-        T.stk_s[T.L.slot(top, b, row)] = static_cast<uint16_t>(u);
-        T.stk_t[T.L.slot(top, b, row)] = 0;
+        T.stk_s[at(top, row)] = static_cast<uint16_t>(u);
+        T.stk_t[at(top, row)] = 0;
         l = u, tl = 0, gl = gu;
         ++top;
       } else if (cost(tl, l, gl) > cost(tl, u, gu)) {  // u strictly better where l starts: l never wins
         --top;
         if (top > base) {
-          l = T.stk_s[T.L.slot(top - 1, b, row)];
-          tl = T.stk_t[T.L.slot(top - 1, b, row)];
+          l = T.stk_s[at(top - 1, row)];
+          tl = T.stk_t[at(top - 1, row)];
           gl = src.r2(l, row);
         }
         advance = false;
       } else {
         const int w = takeover(l, gl, u, gu);
         if (w < T.n) {
-          T.stk_s[T.L.slot(top, b, row)] = static_cast<uint16_t>(u);
-          T.stk_t[T.L.slot(top, b, row)] = static_cast<uint16_t>(w);
+          T.stk_s[at(top, row)] = static_cast<uint16_t>(u);
+          T.stk_t[at(top, row)] = static_cast<uint16_t>(w);
           l = u, tl = w, gl = gu;
           ++top;
         }
@@ -136,38 +117,36 @@ KS_HD void build_band(const RowTileT<Layout>& T, const Src& src, int b, int row)
       gu = u < end ? src.r2(u, row) : -1;
     }
   }
-  T.lo[T.L.meta(b, row)] = static_cast<uint16_t>(base);
-  T.hi[T.L.meta(b, row)] = static_cast<uint16_t>(top);
+  T.lo[at(b, row)] = static_cast<uint16_t>(base);
+  T.hi[at(b, row)] = static_cast<uint16_t>(top);
 }
 
 // Stage 2, round j: band b (b % (2<<j) == 0) merges group [b, b+2^j) with
 // [b+2^j, b+2^(j+1)).  Removes left tops / right bottoms that can never win and
 // fixes the start of the first surviving right entry.
-template <class Layout, class Src>
-KS_HD void merge_groups(const RowTileT<Layout>& T, const Src& src, int b, int j, int row) {
+template <class Src>
+KS_HD void merge_groups(const RowTile& T, const Src& src, int b, int j, int row) {
   const int m = b + (1 << j);
   if (m >= T.bands) return;
   const int e = b + (2 << j) < T.bands ? b + (2 << j) : T.bands;
-  auto LO = [&](int band) -> int { return T.lo[T.L.meta(band, row)]; };
-  auto HI = [&](int band) -> int { return T.hi[T.L.meta(band, row)]; };
   int lb = m - 1;
-  while (lb >= b && LO(lb) == HI(lb)) --lb;
+  while (lb >= b && T.lo[at(lb, row)] == T.hi[at(lb, row)]) --lb;
   if (lb < b) return;  // left group empty: right group's first entry already starts at 0
   int rb = m;
-  while (rb < e && LO(rb) == HI(rb)) ++rb;
+  while (rb < e && T.lo[at(rb, row)] == T.hi[at(rb, row)]) ++rb;
   if (rb >= e) return;
   while (true) {
-    const int li = HI(lb) - 1;
-    const int l = T.stk_s[T.L.slot(li, lb, row)], tl = T.stk_t[T.L.slot(li, lb, row)], gl = src.r2(l, row);
-    const int ri = LO(rb);
-    const int r = T.stk_s[T.L.slot(ri, rb, row)], gr = src.r2(r, row);
+    const int li = T.hi[at(lb, row)] - 1;
+    const int l = T.stk_s[at(li, row)], tl = T.stk_t[at(li, row)], gl = src.r2(l, row);
+    const int ri = T.lo[at(rb, row)];
+    const int r = T.stk_s[at(ri, row)], gr = src.r2(r, row);
     if (cost(tl, l, gl) > cost(tl, r, gr)) {  // left top never wins
-      T.hi[T.L.meta(lb, row)] = static_cast<uint16_t>(li);
-      if (li == LO(lb)) {
+      T.hi[at(lb, row)] = static_cast<uint16_t>(li);
+      if (li == T.lo[at(lb, row)]) {
         do --lb;
-        while (lb >= b && LO(lb) == HI(lb));
+        while (lb >= b && T.lo[at(lb, row)] == T.hi[at(lb, row)]);
         if (lb < b) {  // left exhausted: r heads the merged group
-          T.stk_t[T.L.slot(ri, rb, row)] = 0;
+          T.stk_t[at(ri, row)] = 0;
           break;
         }
       }
@@ -178,23 +157,23 @@ KS_HD void merge_groups(const RowTileT<Layout>& T, const Src& src, int b, int j,
     int t2 = T.n;
     {
       int ri2 = ri + 1, rb2 = rb;
-      if (ri2 == HI(rb)) {
+      if (ri2 == T.hi[at(rb, row)]) {
         do ++rb2;
-        while (rb2 < e && LO(rb2) == HI(rb2));
-        ri2 = rb2 < e ? LO(rb2) : -1;
+        while (rb2 < e && T.lo[at(rb2, row)] == T.hi[at(rb2, row)]);
+        ri2 = rb2 < e ? T.lo[at(rb2, row)] : -1;
       }
-      if (ri2 >= 0) t2 = T.stk_t[T.L.slot(ri2, rb2, row)];
+      if (ri2 >= 0) t2 = T.stk_t[at(ri2, row)];
     }
     if (w >= t2) {  // right bottom never wins: its successor (or the row end) comes first
-      T.lo[T.L.meta(rb, row)] = static_cast<uint16_t>(ri + 1);
-      if (ri + 1 == HI(rb)) {
+      T.lo[at(rb, row)] = static_cast<uint16_t>(ri + 1);
+      if (ri + 1 == T.hi[at(rb, row)]) {
         do ++rb;
-        while (rb < e && LO(rb) == HI(rb));
+        while (rb < e && T.lo[at(rb, row)] == T.hi[at(rb, row)]);
         if (rb >= e) break;  // right exhausted
       }
       continue;
     }
-    T.stk_t[T.L.slot(ri, rb, row)] = static_cast<uint16_t>(w);
+    T.stk_t[at(ri, row)] = static_cast<uint16_t>(w);
     break;
   }
 }
@@ -202,16 +181,16 @@ KS_HD void merge_groups(const RowTileT<Layout>& T, const Src& src, int b, int j,
 // Stage 3: colour the band's own positions by walking the merged stack (the
 // concatenation of every band's live slots, starts strictly increasing).
 // emit(pos, winner) with winner == kNone when the row holds no candidate at all.
-template <class Layout, class Emit>
-KS_HD void colour_band(const RowTileT<Layout>& T, int b, int row, Emit&& emit) {
+template <class Emit>
+KS_HD void colour_band(const RowTile& T, int b, int row, Emit&& emit) {
   const int base = b * T.band;
   const int end = base + T.band < T.n ? base + T.band : T.n;
   // last band whose first live entry starts at or before `base`
   int cb = -1, clo = 0, chi = 0;
   for (int bb = 0; bb < T.bands; ++bb) {
-    const int lo = T.lo[T.L.meta(bb, row)], hi = T.hi[T.L.meta(bb, row)];
+    const int lo = T.lo[at(bb, row)], hi = T.hi[at(bb, row)];
     if (lo == hi) continue;
-    if (static_cast<int>(T.stk_t[T.L.slot(lo, bb, row)]) > base) break;
+    if (static_cast<int>(T.stk_t[at(lo, row)]) > base) break;
     cb = bb, clo = lo, chi = hi;
   }
   if (cb < 0) {  // the first live entry of a row always starts at 0, so the row is empty
@@ -224,27 +203,27 @@ KS_HD void colour_band(const RowTileT<Layout>& T, int b, int row, Emit&& emit) {
     int hi_k = chi - 1;
     while (k < hi_k) {
       const int mid = (k + hi_k + 1) >> 1;
-      if (static_cast<int>(T.stk_t[T.L.slot(mid, cb, row)]) <= base) k = mid;
+      if (static_cast<int>(T.stk_t[at(mid, row)]) <= base) k = mid;
       else hi_k = mid - 1;
     }
   }
-  uint16_t cur = T.stk_s[T.L.slot(k, cb, row)];
+  uint16_t cur = T.stk_s[at(k, row)];
   // successor entry and its start
   int nb = cb, nk = k + 1, next_t = T.n;
   auto settle = [&]() {
     while (nb < T.bands && nk >= chi) {
       ++nb;
       if (nb < T.bands) {
-        nk = T.lo[T.L.meta(nb, row)];
-        chi = T.hi[T.L.meta(nb, row)];
+        nk = T.lo[at(nb, row)];
+        chi = T.hi[at(nb, row)];
       }
     }
-    next_t = nb < T.bands ? static_cast<int>(T.stk_t[T.L.slot(nk, nb, row)]) : T.n;
+    next_t = nb < T.bands ? static_cast<int>(T.stk_t[at(nk, row)]) : T.n;
   };
   settle();
   for (int p = base; p < end; ++p) {
     while (next_t <= p) {
-      cur = T.stk_s[T.L.slot(nk, nb, row)];
+      cur = T.stk_s[at(nk, row)];
       ++nk;
       settle();
     }

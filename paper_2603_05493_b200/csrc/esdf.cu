@@ -7,7 +7,9 @@
 //   d2s  : uint32  bit31 = negative, bits0-30 = squared integer site offset
 //                  (0x7FFFFFFF: no sites).  distance = sqrt((double)d2) * voxel_size
 //                  is formed on the fly, so queries see exactly the reference's doubles.
-// Both use the reference's cell order, index = x + nx*(y + ny*z) (esdf.hpp:48-50).
+// Both are stored y-fastest, index = y + ny*(x + nx*z): the x sweep runs with lane <-> y,
+// so its stores are coalesced; the download path converts back to the reference's
+// x-fastest order (esdf.hpp:48-50).
 #include <math_constants.h>
 
 #include <algorithm>
@@ -58,8 +60,8 @@ struct EsdfView {
   int wpr;           // words per x row
   uint16_t* near_z;  // [cells] x-fastest phase-1 result
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
-  uint32_t* site;    // [cells] x-fastest
-  uint32_t* d2s;     // [cells] x-fastest
+  uint32_t* site;    // [cells] y-fastest
+  uint32_t* d2s;     // [cells] y-fastest
   EsdfCtrl* ctrl;
 };
 
@@ -546,79 +548,62 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
   }
 }
 
-// Phase 3: one WARP per (y, z) row, lane <-> band of x positions, only __syncwarp between stages,
-// so every warp of the SM runs its own row independently (no CTA barrier anywhere).  Per warp in
-// shared memory: the row's candidates (4 B each, loaded coalesced), the band stacks in the
-// LaneBandLayout (each lane's own stack lives in its own bank), and the winners (2 B each); the last
-// loop walks the row coalesced again, forms site and d^2, recovers the sign and stores x-fastest.
-// kSigns: 0 = unsigned field (propagate), 1 = recover_signs fused into the store, 2 = the same using
-// the hint planes left by the brick gather of this build.
-struct SrcRow {
-  const uint32_t* in;
-  int y, z;
-  __device__ __forceinline__ int r2(int pos, int) const {
-    const uint32_t v = in[pos];
-    if (v == kYzNone) return -1;
-    const int dy = y - static_cast<int>(v & 0xFFFFu);
-    const int dz = z - static_cast<int>(v >> 16);
-    return dy * dy + dz * dz;
-  }
-};
-constexpr int kRowWarps = 4;
-static size_t sweep_rows_smem_per_warp(int n, int band) {
-  const size_t nx_pad = (static_cast<size_t>(n) + 31) / 32 * 32;
-  return 4 * nx_pad + 2 * (2 * static_cast<size_t>(band) * 32) + 2 * nx_pad + 2 * 64;
-}
+// grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
+// The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
+// bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
+// kSigns: 0 = unsigned field (propagate), 1 = recover_signs fused into the store of the finished cell,
+// 2 = the same using the hint planes left by the bit-packed gather of this build.
 template <int kSigns>
-__global__ void __launch_bounds__(kRowWarps * 32, 12) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands, int smem_per_warp) {
+__global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int y0 = blockIdx.x * 32, z = blockIdx.y;
   const int nx = E.nx, ny = E.ny;
-  const int nx_pad = (nx + 31) & ~31;
-  unsigned char* base = s_raw + static_cast<size_t>(warp) * smem_per_warp;
-  uint32_t* in = reinterpret_cast<uint32_t*>(base);
-  uint16_t* stk_s = reinterpret_cast<uint16_t*>(in + nx_pad);
-  uint16_t* stk_t = stk_s + band * 32;
-  uint16_t* outw = stk_t + band * 32;
-  uint16_t* lo = outw + nx_pad;
-  uint16_t* hi = lo + 32;
-  const edt::RowTileT<edt::LaneBandLayout> T{stk_s, stk_t, lo, hi, nx, band, bands, edt::LaneBandLayout{band}};
-  const int rows = ny * E.nz;
-  for (int row = blockIdx.x * kRowWarps + warp; row < rows; row += gridDim.x * kRowWarps) {
-    const int y = row % ny, z = row / ny;
-    const uint32_t* src_row = E.yz + row * nx;
-    for (int x = lane; x < nx; x += 32) in[x] = src_row[x];
+  uint32_t* in = reinterpret_cast<uint32_t*>(s_raw);
+  const edt::RowTile T = carve_tile(s_raw, nx, band, bands, static_cast<size_t>(nx) * 128);
+  const int zoff = nx * ny * z;
+  for (int r = warp; r < 32; r += nwarps) {
+    const bool live = y0 + r < ny;
+    const uint32_t* row = E.yz + zoff + nx * (y0 + r);
+    for (int x = lane; x < nx; x += 32) in[x * 32 + ((r + x) & 31)] = live ? row[x] : kYzNone;
+  }
+  __syncthreads();
+  for (int x = warp; x < nx; x += nwarps) {
+    const uint32_t v = in[x * 32 + ((lane + x) & 31)];
     __syncwarp();
-    const SrcRow src{in, y, z};
-    if (lane < bands) edt::build_band(T, src, lane, 0);
-    __syncwarp();
-    for (int j = 0; (1 << j) < bands; ++j) {
-      if (lane < bands && (lane & ((2 << j) - 1)) == 0) edt::merge_groups(T, src, lane, j, 0);
-      __syncwarp();
-    }
-    if (lane < bands) edt::colour_band(T, lane, 0, [&](int x, uint16_t win) { outw[x] = win; });
-    __syncwarp();
+    in[x * 32 + lane] = v;
+  }
+  __syncthreads();
+  const SrcX src{in, y0, z};
+  sweep_stages(T, src, warp, lane);
+  const int y = y0 + lane;
+  if (warp < bands && y < ny) {
     SignProbe probe(E, Tw, kSigns ? y : 0, kSigns ? z : 0);
-    for (int x = lane; x < nx; x += 32) {
-      const int o = row * nx + x;
-      const uint16_t win = outw[x];
+    const int obase = y + ny * nx * z;
+    uint16_t last = edt::kNone;
+    uint32_t site = kSiteNone;
+    int r2w = 0, sx = 0;
+    edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
+      const int o = obase + ny * x;
       if (win == edt::kNone) {
         E.site[o] = kSiteNone;
         E.d2s[o] = kD2None;
-        continue;
+        return;
       }
-      const uint32_t v = in[win];
-      const int sx = win, sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
-      const int dx = x - sx, dy = y - sy, dz = z - sz;
-      uint32_t d2 = static_cast<uint32_t>(dx * dx + dy * dy + dz * dz);
-      if (kSigns) {
-        probe.template set_site<kSigns == 2>(sx, sy, sz);
-        if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
+      if (win != last) {  // everything that only depends on the winning site
+        last = win;
+        const uint32_t v = in[edt::at(win, lane)];
+        const int sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
+        sx = win;
+        r2w = (y - sy) * (y - sy) + (z - sz) * (z - sz);
+        site = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+        if (kSigns) probe.template set_site<kSigns == 2>(sx, sy, sz);
       }
-      E.site[o] = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+      uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
+      if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
+      E.site[o] = site;
       E.d2s[o] = d2;
-    }
-    __syncwarp();
+    });
   }
 }
 
@@ -628,8 +613,8 @@ __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   if (o >= E.cells) return;
   const uint32_t site = E.site[o];
   if (site == kSiteNone) return;
-  const int x = o % E.nx;
-  const int y = (o / E.nx) % E.ny;
+  const int y = o % E.ny;
+  const int x = (o / E.ny) % E.nx;
   const int z = o / (E.ny * E.nx);
   SignProbe probe(E, T, y, z);
   probe.template set_site<false>(site & 1023, (site >> 10) & 1023, site >> 20);
@@ -638,7 +623,7 @@ __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
 
 // ---- query (esdf.hpp:337-387) ----
 __device__ __forceinline__ double cell_distance(const EsdfView& E, int x, int y, int z) {
-  const uint32_t v = E.d2s[x + E.nx * (y + E.ny * z)];
+  const uint32_t v = E.d2s[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)];
   const double d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;  // esdf.hpp:276-277
   return (v & 0x80000000u) ? -d : d;
 }
@@ -693,12 +678,16 @@ __global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restr
   }
 }
 
-// ---- export to the reference's DenseEsdf arrays (esdf.hpp:58-64): unpack, same cell order ----
+// ---- export to the reference's DenseEsdf arrays (x-fastest; esdf.hpp:58-64) ----
 __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ site_xyz, double* __restrict__ distance,
                                                 int* __restrict__ d2) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= E.cells) return;
-  const uint32_t s = E.site[idx], v = E.d2s[idx];
+  const int x = static_cast<int>(idx % E.nx);
+  const int y = static_cast<int>((idx / E.nx) % E.ny);
+  const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
+  const long long o = y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z);
+  const uint32_t s = E.site[o], v = E.d2s[o];
   if (site_xyz) {
     site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
     site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
@@ -728,8 +717,7 @@ struct ks_esdf {
   EsdfCtrl* h_ctrl;  // pinned
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
-  size_t smem_y, smem_x;  // smem_x is per warp of the row kernel
-  int grid_x;
+  size_t smem_y, smem_x;
   int sticky_err;
   bool profile, profile_stages;
   cudaEvent_t ev[7];
@@ -825,14 +813,13 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
-  const int xgrid = e->grid_x, xthreads = kRowWarps * 32, per_warp = static_cast<int>(e->smem_x);
-  const size_t xsmem = e->smem_x * kRowWarps;
+  const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
-    KS_LAUNCH(k_sweep_x<2>, xgrid, xthreads, xsmem, e->stream, E, tsdf_view(t), e->band_x, e->bands_x, per_warp);
+    KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
   } else if (t) {
-    KS_LAUNCH(k_sweep_x<1>, xgrid, xthreads, xsmem, e->stream, E, tsdf_view(t), e->band_x, e->bands_x, per_warp);
+    KS_LAUNCH(k_sweep_x<1>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
   } else {
-    KS_LAUNCH(k_sweep_x<0>, xgrid, xthreads, xsmem, e->stream, E, TsdfView{}, e->band_x, e->bands_x, per_warp);
+    KS_LAUNCH(k_sweep_x<0>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
   }
   if (t) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
@@ -871,26 +858,17 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   for (int a = 0; a < 3; ++a) E.origin[a] = cfg->origin[a];
   E.ve = cfg->voxel_size;
   pick_bands(E.ny, e->band_y, e->bands_y);
-  e->band_x = (E.nx + 31) / 32;  // lane <-> band: at most 32 bands, odd size (own-bank stacks)
-  if (e->band_x % 2 == 0) ++e->band_x;
-  e->bands_x = (E.nx + e->band_x - 1) / e->band_x;
+  pick_bands(E.nx, e->band_x, e->bands_x);
   e->smem_y = sweep_smem_bytes(E.ny, e->bands_y, 2);
-  e->smem_x = sweep_rows_smem_per_warp(E.nx, e->band_x);
-  {
-    const size_t per_cta = e->smem_x * kRowWarps;
-    const int ctas_per_sm = static_cast<int>(std::min<size_t>(16, (227 * 1024) / per_cta));
-    const int rows = E.ny * E.nz;
-    e->grid_x = std::max(1, std::min((rows + kRowWarps - 1) / kRowWarps, kSmCount * std::max(1, ctas_per_sm)));
-  }
-  if (e->smem_y > 227 * 1024 || e->smem_x * kRowWarps > 227 * 1024) {
+  e->smem_x = sweep_smem_bytes(E.nx, e->bands_x, 4);
+  if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
     delete e;
-    return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build");
+    return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  const int xsmem = static_cast<int>(e->smem_x * kRowWarps);
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, xsmem));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, xsmem));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, xsmem));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));

@@ -21,7 +21,7 @@ struct TileMem {
     t.assign(static_cast<size_t>(n) * kRows, 0);
     lo.assign(static_cast<size_t>(bands) * kRows, 0);
     hi.assign(static_cast<size_t>(bands) * kRows, 0);
-    return RowTile{s.data(), t.data(), lo.data(), hi.data(), n, band, bands, TileLayout{}};
+    return RowTile{s.data(), t.data(), lo.data(), hi.data(), n, band, bands};
   }
 };
 
@@ -36,20 +36,6 @@ void run_tile(TileMem& mem, int n, int band, int rows, const Src& src, Emit&& em
   for (int b = 0; b < T.bands; ++b)
     for (int r = 0; r < rows; ++r)
       colour_band(T, b, r, [&](int pos, uint16_t win) { emit(pos, r, win); });
-}
-
-// One row handled the way the warp-per-row x sweep does it: lane <-> band, LaneBandLayout.
-template <class Src, class Emit>
-void run_row_lanes(int n, const Src& src, Emit&& emit) {
-  int band = (n + 31) / 32;
-  if (band % 2 == 0) ++band;  // odd, as in the kernel
-  const int bands = (n + band - 1) / band;
-  std::vector<uint16_t> s(static_cast<size_t>(band) * 32, 0x7777), t(static_cast<size_t>(band) * 32, 0x7777), lo(32, 0), hi(32, 0);
-  RowTileT<LaneBandLayout> T{s.data(), t.data(), lo.data(), hi.data(), n, band, bands, LaneBandLayout{band}};
-  for (int b = 0; b < bands; ++b) build_band(T, src, b, 0);
-  for (int j = 0; (1 << j) < bands; ++j)
-    for (int b = 0; b < bands; b += (2 << j)) merge_groups(T, src, b, j, 0);
-  for (int b = 0; b < bands; ++b) colour_band(T, b, 0, [&](int pos, uint16_t win) { emit(pos, win); });
 }
 
 struct SrcY {  // phase 2: candidate at y is the column's nearest seed z
@@ -107,38 +93,6 @@ extern "C" int emul_propagate(const uint8_t* mask, int nx, int ny, int nz, int b
             win == kNone ? 0xFFFFFFFFu : (static_cast<uint32_t>(win) | static_cast<uint32_t>(zs_tile[at(win, r)]) << 16);
       });
     }
-  // phase 3, warp-per-row variant (band_x < 0 selects it)
-  if (band_x < 0) {
-    struct SrcRow {
-      const uint32_t* row;
-      int y, z;
-      int r2(int pos, int) const {
-        const uint32_t v = row[pos];
-        if (v == 0xFFFFFFFFu) return -1;
-        const int dy = y - static_cast<int>(v & 0xFFFFu), dz = z - static_cast<int>(v >> 16);
-        return dy * dy + dz * dz;
-      }
-    };
-    for (int z = 0; z < nz; ++z)
-      for (int y = 0; y < ny; ++y) {
-        const uint32_t* row = &yz[idx(0, y, z)];
-        SrcRow src{row, y, z};
-        run_row_lanes(nx, src, [&](int pos, uint16_t win) {
-          const size_t i = idx(pos, y, z);
-          if (win == kNone) {
-            site[3 * i] = site[3 * i + 1] = site[3 * i + 2] = -1;
-            d2[i] = 0x7FFFFFFF;
-            return;
-          }
-          const uint32_t v = row[win];
-          const int sx = win, sy = static_cast<int>(v & 0xFFFFu), sz = static_cast<int>(v >> 16);
-          site[3 * i] = sx, site[3 * i + 1] = sy, site[3 * i + 2] = sz;
-          const int dx = pos - sx, dy = y - sy, dz = z - sz;
-          d2[i] = dx * dx + dy * dy + dz * dz;
-        });
-      }
-    return 0;
-  }
   // phase 3
   std::vector<uint32_t> yz_tile(static_cast<size_t>(nx) * kRows);
   for (int z = 0; z < nz; ++z)
