@@ -200,106 +200,118 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
   if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
 }
 
-// The fused build's gather: a persistent grid walks the ACTIVE 8^3-cell bricks (one thread per cell);
-// the bit planes are cleared beforehand, so inactive bricks cost nothing.  A brick stages what its 512 x 7 probes can touch -- the per-axis
-// voxel tables (72 ints), the directory entries of the <= kStage blocks in reach and their surface
-// bit planes -- in shared memory, so a probe is two shared-memory reads.  Output: one byte per
-// (y, z) row of the brick in the bit-packed seed plane and in the geometry-near plane.
+// The fused build's gather: one WARP per active 8^3-cell brick (16 cells per lane), persistent grid
+// over the compacted active list; the bit planes are cleared beforehand, so inactive bricks cost
+// nothing.  A warp stages what its brick's 512 x 7 probes can touch -- the directory entries of the
+// <= kStage blocks in reach and the surface bit planes of the live ones -- in its own slice of shared
+// memory (only __syncwarp), so a probe is two shared-memory reads, and 48 bricks are in flight per SM.
+// Output: one byte per (y, z) row of the brick in the seed plane and in the geometry-near plane.
 constexpr int kStage = 64;
-__global__ void __launch_bounds__(512) k_seed_gather_bricks(EsdfView E, TsdfView T) {
-  __shared__ int s_tab[3][5][8];        // [axis][VoxRow][cell in brick]
-  __shared__ int s_lo[3], s_n[3];
-  __shared__ int s_pool[kStage];
-  __shared__ uint8_t s_geom[kStage];
-  __shared__ uint32_t s_plane[kStage][16];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+constexpr int kGatherWarps = 8;
+struct GatherStage {
+  int pool[kStage];
+  uint32_t plane[kStage][16];
+  uint8_t geom[kStage];
+};
+__global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfView E, TsdfView T) {
+  __shared__ GatherStage s_stage[kGatherWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  GatherStage& S = s_stage[warp];
   uint8_t* mrow = reinterpret_cast<uint8_t*>(E.mbits);
   uint8_t* grow = reinterpret_cast<uint8_t*>(E.gbits);
   const int total = E.nx + E.ny + E.nz;
+  const int* vox_x = E.vox;
+  const int* vox_y = E.vox + E.nx;
+  const int* vox_z = E.vox + E.nx + E.ny;
   const int n_active = E.ctrl->active_bricks;
-  for (int item = blockIdx.x; item < n_active; item += gridDim.x) {
-  const int brick = E.active[item];
-  const int bx = brick % E.bnx, by = (brick / E.bnx) % E.bny, bz = brick / (E.bnx * E.bny);
-  const int x = 8 * bx + lx, y = 8 * by + ly, z = 8 * bz + lz;
-  const bool in_grid = x < E.nx && y < E.ny && z < E.nz;
-  const int out_byte = (y + E.ny * z) * (E.wpr * 4) + bx;  // byte bx of row (y, z): bits 8bx .. 8bx+7
-  __syncthreads();  // shared staging of the previous brick is no longer read
-  if (tid < 120) {  // 3 axes x 5 rows x 8 cells
-    const int a = tid / 40, r = (tid / 8) % 5, c = tid & 7;
-    const int dims[3] = {E.nx, E.ny, E.nz};
-    const int b0[3] = {8 * bx, 8 * by, 8 * bz};
-    const int pos = min(b0[a] + c, dims[a] - 1);
-    s_tab[a][r][c] = E.vox[r * total + axis_base(E, a) + pos];
-  }
-  __syncthreads();
-  if (tid < 3) {  // directory range reachable from this brick: [centre - ve, centre + ve] per axis
-    const int dims[3] = {E.nx, E.ny, E.nz};
-    const int b0[3] = {8 * bx, 8 * by, 8 * bz};
-    const int last = min(7, dims[tid] - 1 - b0[tid]);
-    const int lo = s_tab[tid][kVoxMe][0] >> 3, hi = s_tab[tid][kVoxPe][last] >> 3;
-    s_lo[tid] = lo;
-    s_n[tid] = hi - lo + 1;
-  }
-  __syncthreads();
-  const int n0 = s_n[0], n1 = s_n[1], n2 = s_n[2];
-  const int nblocks = n0 * n1 * n2;
-  const bool staged = nblocks <= kStage;
-  if (staged) {
-    if (tid < nblocks) {
-      const int cx = tid % n0, cy = (tid / n0) % n1, cz = tid / (n0 * n1);
-      const int pool = __ldg(E.dir + ((s_lo[0] + cx) + E.dn[0] * ((s_lo[1] + cy) + E.dn[1] * (s_lo[2] + cz))));
-      s_pool[tid] = pool;
-      s_geom[tid] = pool >= 0 ? T.pool_geom[pool] : 0;
+  const int lx = lane & 7, lyq = lane >> 3;  // lane covers x = lx, y in {lyq, lyq + 4}, all 8 z of the brick
+  for (int item = blockIdx.x * kGatherWarps + warp; item < n_active; item += gridDim.x * kGatherWarps) {
+    const int brick = E.active[item];
+    const int bx = brick % E.bnx, by = (brick / E.bnx) % E.bny, bz = brick / (E.bnx * E.bny);
+    // block range in reach of the brick: [first centre - ve, last centre + ve] per axis (lanes 0..2 = axes)
+    int lo_a = 0, n_a = 1;
+    if (lane < 3) {
+      const int dim = lane == 0 ? E.nx : (lane == 1 ? E.ny : E.nz);
+      const int b0 = 8 * (lane == 0 ? bx : (lane == 1 ? by : bz));
+      const int first = axis_base(E, lane) + b0, last = axis_base(E, lane) + min(b0 + 7, dim - 1);
+      lo_a = E.vox[kVoxMe * total + first] >> 3;
+      n_a = (E.vox[kVoxPe * total + last] >> 3) - lo_a + 1;
     }
-    __syncthreads();
-    for (int i = tid; i < nblocks * 16; i += blockDim.x) {
-      const int pool = s_pool[i >> 4];
-      s_plane[i >> 4][i & 15] = pool >= 0 ? __ldg(T.digest + (pool * kDigestWords + (i & 15))) : 0u;
+    const int lo0 = __shfl_sync(0xFFFFFFFFu, lo_a, 0), lo1 = __shfl_sync(0xFFFFFFFFu, lo_a, 1), lo2 = __shfl_sync(0xFFFFFFFFu, lo_a, 2);
+    const int n0 = __shfl_sync(0xFFFFFFFFu, n_a, 0), n1 = __shfl_sync(0xFFFFFFFFu, n_a, 1), n2 = __shfl_sync(0xFFFFFFFFu, n_a, 2);
+    const int nblocks = n0 * n1 * n2;
+    const bool staged = nblocks <= kStage;
+    __syncwarp();  // the previous brick's staging is no longer read
+    if (staged) {
+      for (int i = lane; i < nblocks; i += 32) {
+        const int cx = i % n0, cy = (i / n0) % n1, cz = i / (n0 * n1);
+        const int pool = __ldg(E.dir + ((lo0 + cx) + E.dn[0] * ((lo1 + cy) + E.dn[1] * (lo2 + cz))));
+        S.pool[i] = pool;
+        S.geom[i] = pool >= 0 ? T.pool_geom[pool] : 0;
+      }
+      __syncwarp();
+      for (int i = lane; i < nblocks * 16; i += 32) {
+        const int pool = S.pool[i >> 4];
+        S.plane[i >> 4][i & 15] = pool >= 0 ? __ldg(T.digest + (pool * kDigestWords + (i & 15))) : 0u;
+      }
+      __syncwarp();
     }
-    __syncthreads();
-  }
-  bool seed = false, geom_near = false;
-  if (in_grid) {
-    const int xc = s_tab[0][kVoxC][lx], xp = s_tab[0][kVoxPh][lx], xm = s_tab[0][kVoxMh][lx];
-    const int yc = s_tab[1][kVoxC][ly], yp = s_tab[1][kVoxPh][ly], ym = s_tab[1][kVoxMh][ly];
-    const int zc = s_tab[2][kVoxC][lz], zp = s_tab[2][kVoxPh][lz], zm = s_tab[2][kVoxMh][lz];
+    const int x = 8 * bx + lx;
+    const bool x_ok = x < E.nx;
+    const int xi = min(x, E.nx - 1);
+    const int xc = vox_x[xi], xp = vox_x[total + xi], xm = vox_x[2 * total + xi];
+    const int gx0 = vox_x[kVoxMe * total + xi] >> 3, gx1 = vox_x[kVoxPe * total + xi] >> 3;
     auto probe = [&](int vx, int vy, int vz) -> bool {
       const int local = local_index(vx, vy, vz);
       if (staged) {
-        const int b = ((vx >> 3) - s_lo[0]) + n0 * (((vy >> 3) - s_lo[1]) + n1 * ((vz >> 3) - s_lo[2]));
-        return (s_plane[b][local >> 5] >> (local & 31)) & 1u;
+        const int b = ((vx >> 3) - lo0) + n0 * (((vy >> 3) - lo1) + n1 * ((vz >> 3) - lo2));
+        return (S.plane[b][local >> 5] >> (local & 31)) & 1u;
       }
       const int pool = dir_lookup(E, vx, vy, vz);
       return pool >= 0 && surface_bit(T, pool, local) != 0;
     };
-    seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
-           (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
-           (zm != zc && probe(xc, yc, zm));
-    if (seed) {  // any stamped block a sign probe from this site can reach (centre +- ve per axis)?
-      const int x0 = s_tab[0][kVoxMe][lx] >> 3, x1 = s_tab[0][kVoxPe][lx] >> 3;
-      const int y0 = s_tab[1][kVoxMe][ly] >> 3, y1 = s_tab[1][kVoxPe][ly] >> 3;
-      const int z0 = s_tab[2][kVoxMe][lz] >> 3, z1 = s_tab[2][kVoxPe][lz] >> 3;
-      for (int cz = z0; cz <= z1; ++cz)
-        for (int cy = y0; cy <= y1; ++cy)
-          for (int cx = x0; cx <= x1; ++cx) {
-            if (staged) {
-              geom_near |= s_geom[(cx - s_lo[0]) + n0 * ((cy - s_lo[1]) + n1 * (cz - s_lo[2]))] != 0;
-            } else {
-              const int pool = __ldg(E.dir + (cx + E.dn[0] * (cy + E.dn[1] * cz)));
-              geom_near |= pool >= 0 && T.pool_geom[pool];
-            }
+    unsigned seeds_here = 0;
+    for (int lz = 0; lz < 8; ++lz) {
+      const int z = 8 * bz + lz;
+      const int zi = min(z, E.nz - 1);
+      const int zc = vox_z[zi], zp = vox_z[total + zi], zm = vox_z[2 * total + zi];
+      const int gz0 = vox_z[kVoxMe * total + zi] >> 3, gz1 = vox_z[kVoxPe * total + zi] >> 3;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int y = 8 * by + lyq + 4 * h;
+        const int yi = min(y, E.ny - 1);
+        bool seed = false, geom_near = false;
+        if (x_ok && y < E.ny && z < E.nz) {
+          const int yc = vox_y[yi], yp = vox_y[total + yi], ym = vox_y[2 * total + yi];
+          seed = probe(xc, yc, zc) || (xp != xc && probe(xp, yc, zc)) || (xm != xc && probe(xm, yc, zc)) ||
+                 (yp != yc && probe(xc, yp, zc)) || (ym != yc && probe(xc, ym, zc)) || (zp != zc && probe(xc, yc, zp)) ||
+                 (zm != zc && probe(xc, yc, zm));
+          if (seed) {  // any stamped block a sign probe from this site can reach (centre +- ve per axis)?
+            const int gy0 = vox_y[kVoxMe * total + yi] >> 3, gy1 = vox_y[kVoxPe * total + yi] >> 3;
+            for (int cz = gz0; cz <= gz1; ++cz)
+              for (int cy = gy0; cy <= gy1; ++cy)
+                for (int cx = gx0; cx <= gx1; ++cx) {
+                  if (staged) {
+                    geom_near |= S.geom[(cx - lo0) + n0 * ((cy - lo1) + n1 * (cz - lo2))] != 0;
+                  } else {
+                    const int pool = __ldg(E.dir + (cx + E.dn[0] * (cy + E.dn[1] * cz)));
+                    geom_near |= pool >= 0 && T.pool_geom[pool];
+                  }
+                }
           }
+        }
+        // the ballot is 4 rows (y) of 8 x cells: byte k belongs to row lyq = k
+        const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
+        const uint32_t gvotes = __ballot_sync(0xFFFFFFFFu, geom_near);
+        if (lx == 0 && y < E.ny && z < E.nz) {
+          const int out_byte = (y + E.ny * z) * (E.wpr * 4) + bx;  // byte bx of row (y, z): bits 8bx .. 8bx+7
+          mrow[out_byte] = static_cast<uint8_t>(votes >> (8 * lyq));
+          grow[out_byte] = static_cast<uint8_t>(gvotes >> (8 * lyq));
+        }
+        seeds_here += __popc(votes);
+      }
     }
-  }
-  // a warp is 4 rows (ly) of 8 x cells: byte k of the ballot belongs to row ly0 + k
-  const uint32_t votes = __ballot_sync(0xFFFFFFFFu, seed);
-  const uint32_t gvotes = __ballot_sync(0xFFFFFFFFu, geom_near);
-  if (lx == 0 && y < E.ny && z < E.nz) {
-    mrow[out_byte] = static_cast<uint8_t>(votes >> (lane & 24));
-    grow[out_byte] = static_cast<uint8_t>(gvotes >> (lane & 24));
-  }
-  if (lane == 0 && votes != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(__popc(votes)));
+    if (lane == 0 && seeds_here != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(seeds_here));
   }
 }
 
@@ -792,7 +804,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
       KS_CUDA(cudaMemsetAsync(E.mbits, 0, plane_bytes, e->stream));
       KS_CUDA(cudaMemsetAsync(E.gbits, 0, plane_bytes, e->stream));
-      KS_LAUNCH(k_seed_gather_bricks, std::min(E.bnx * E.bny * E.bnz, 4 * kSmCount), 512, 0, e->stream, E, tsdf_view(t));
+      KS_LAUNCH(k_seed_gather_bricks, 6 * kSmCount, kGatherWarps * 32, 0, e->stream, E, tsdf_view(t));
     } else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
   } else {
     KS_CUDA(cudaMemsetAsync(E.mask, 0, E.cells, e->stream));
