@@ -204,6 +204,29 @@ KS_API int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, doubl
 KS_API int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, double* distance_dev,
                                       double* gradient_dev, uint8_t* inside_dev);
 
+/* ---- scene collision (SURVEY 8f "next": the consumer of query) ---------------- */
+/* CollisionReport / SceneTimestepReport scalars (collision.hpp:46-52, :161-168) */
+typedef struct ks_collision_report {
+  double max_penetration; /* <= 0 means free                         */
+  double cost;
+  int32_t worst_sphere;   /* -1 when nothing penetrates              */
+  int32_t reserved;
+} ks_collision_report;
+/* scene_collision_static (collision.hpp:130-152): one query per sphere, hinge cost and its
+ * gradient w.r.t. the centres (n xyz triples, may be NULL).  Host buffers, blocking. */
+KS_API int ks_esdf_scene_collision_static(ks_esdf* e, const double* centers_host, const double* radii_host,
+                                          int64_t n, double activation_margin, ks_collision_report* report,
+                                          double* gradient_xyz_host);
+/* scene_collision (collision.hpp:177-239): swept spheres over `timesteps` x `spheres` centres
+ * with CHOMP speed weighting; reports[timesteps]; the gradients are timesteps x spheres xyz
+ * triples (next_center_gradient of the last timestep is zero).  Fails with the reference's
+ * "scene_collision: esdf signs not recovered" on an unsigned field. */
+KS_API int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host, const double* radii_host,
+                                         const double* velocities_host, int32_t timesteps, int32_t spheres,
+                                         double activation_margin, double dt, int32_t max_checks,
+                                         ks_collision_report* reports, double* center_gradient,
+                                         double* next_center_gradient, double* velocity_gradient);
+
 #ifdef __cplusplus
 }
 #endif

@@ -795,6 +795,115 @@ void ko_query_esdf(const double origin[3], const int dims[3], double ve, int has
   }
 }
 
+/* ---- scene collision (collision.hpp:30-44, :130-239) ------------------------- */
+static double hinge_cost(double clearance, double margin) { /* :30-37 */
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) {
+    const double gap = margin - clearance;
+    return gap * gap / (2.0 * margin);
+  }
+  return 0.5 * margin - clearance;
+}
+static double hinge_slope(double clearance, double margin) { /* :40-44 */
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) return -(margin - clearance) / margin;
+  return -1.0;
+}
+static void query_one(const double origin[3], const int dims[3], double ve, int has_sites, const double* distance,
+                      vec3 p, double* d, vec3* g) {
+  uint8_t inside;
+  ko_query_esdf(origin, dims, ve, has_sites, distance, p.v, 1, d, g->v, &inside);
+}
+void ko_scene_collision_static(const double origin[3], const int dims[3], double ve, int has_sites,
+                               const double* distance, const double* centers, const double* radii, int64_t n,
+                               double margin, double* report3, double* gradient) {
+  double max_pen = 0.0, total = 0.0;
+  int worst = -1;
+  for (int64_t s = 0; s < n; ++s) {
+    double d;
+    vec3 g;
+    query_one(origin, dims, ve, has_sites, distance, mk(centers[3 * s], centers[3 * s + 1], centers[3 * s + 2]), &d, &g);
+    const double clearance = d - radii[s];
+    const double pen = -clearance;
+    if (pen > max_pen) {
+      max_pen = pen;
+      worst = (int)s;
+    }
+    const double cost = hinge_cost(clearance, margin);
+    total += cost;
+    gradient[3 * s] = gradient[3 * s + 1] = gradient[3 * s + 2] = 0.0;
+    if (cost > 0.0) {
+      const double slope = hinge_slope(clearance, margin);
+      for (int a = 0; a < 3; ++a) gradient[3 * s + a] += slope * g.v[a];
+    }
+  }
+  report3[0] = max_pen;
+  report3[1] = worst;
+  report3[2] = total;
+}
+void ko_scene_collision_swept(const double origin[3], const int dims[3], double ve, int has_sites,
+                              const double* distance, const double* centers, const double* radii,
+                              const double* velocities, int timesteps, int spheres, double margin, double dt,
+                              int max_checks, double* reports, double* center_gradient,
+                              double* next_center_gradient, double* velocity_gradient) {
+  const double min_step = ve;
+  for (int t = 0; t < timesteps; ++t) {
+    const int has_next = t + 1 < timesteps;
+    double max_pen = 0.0, total = 0.0;
+    int worst = -1;
+    for (int s = 0; s < spheres; ++s) {
+      const size_t at = ((size_t)t * spheres + s) * 3;
+      const vec3 start = mk(centers[at], centers[at + 1], centers[at + 2]);
+      vec3 segment = mk(0.0, 0.0, 0.0);
+      if (has_next) {
+        const size_t nx = at + (size_t)spheres * 3;
+        segment = sub(mk(centers[nx], centers[nx + 1], centers[nx + 2]), start);
+      }
+      const double length = sqrt(sqnorm(segment));
+      const vec3 vel = mk(velocities[at], velocities[at + 1], velocities[at + 2]);
+      const double speed = sqrt(sqnorm(vel));
+      const double weight = speed * dt;
+      double hinge_sum = 0.0, lambda = 0.0;
+      vec3 start_grad = mk(0.0, 0.0, 0.0), next_grad = mk(0.0, 0.0, 0.0);
+      for (int check = 0; check < max_checks; ++check) {
+        const double frac = length > 0.0 ? lambda / length : 0.0;
+        const vec3 x = mk(start.v[0] + frac * segment.v[0], start.v[1] + frac * segment.v[1], start.v[2] + frac * segment.v[2]);
+        double d;
+        vec3 g;
+        query_one(origin, dims, ve, has_sites, distance, x, &d, &g);
+        const double clearance = d - radii[s];
+        if (-clearance > max_pen) {
+          max_pen = -clearance;
+          worst = s;
+        }
+        hinge_sum += hinge_cost(clearance, margin);
+        const double slope = hinge_slope(clearance, margin);
+        if (slope != 0.0) {
+          for (int a = 0; a < 3; ++a) {
+            const double gx = slope * g.v[a];
+            start_grad.v[a] += (1.0 - frac) * gx;
+            next_grad.v[a] += frac * gx;
+          }
+        }
+        if (!has_next) break;
+        const double advance = clearance < min_step ? min_step : clearance; /* std::max(clearance, min_step) */
+        lambda += advance;
+        if (lambda >= length) break;
+      }
+      total += weight * hinge_sum;
+      for (int a = 0; a < 3; ++a) {
+        center_gradient[at + a] = 0.0 + weight * start_grad.v[a];
+        if (has_next) next_center_gradient[at + a] = 0.0 + weight * next_grad.v[a];
+        velocity_gradient[at + a] = 0.0;
+        if (speed > 1e-12) velocity_gradient[at + a] += hinge_sum * dt * (vel.v[a] / speed);
+      }
+    }
+    reports[3 * t] = max_pen;
+    reports[3 * t + 1] = worst;
+    reports[3 * t + 2] = total;
+  }
+}
+
 /* ---- timed full update (bench.py CPU legs) -------------------------------- */
 static double now_s(void) {
   struct timespec ts;

@@ -78,6 +78,21 @@ void KO(query_esdf)(const double origin[3], const int dims[3], double voxel_size
                     const double* distance, const double* points, int64_t n, double* out_distance,
                     double* out_gradient, uint8_t* out_inside);
 
+/* scene_collision_static (collision.hpp:130-152): one query per sphere.
+ * report3 = {max_penetration, worst sphere index (-1 if none), cost}; gradient = n xyz triples. */
+void KO(scene_collision_static)(const double origin[3], const int dims[3], double voxel_size, int has_sites,
+                                const double* distance, const double* centers, const double* radii,
+                                int64_t n, double activation_margin, double* report3, double* gradient);
+/* scene_collision (collision.hpp:177-239): swept spheres over `timesteps` x `spheres` centres.
+ * reports = timesteps x {max_penetration, worst sphere, cost}; the three gradients are
+ * timesteps x spheres xyz triples (next_gradient of the last timestep is left untouched). */
+void KO(scene_collision_swept)(const double origin[3], const int dims[3], double voxel_size, int has_sites,
+                               const double* distance, const double* centers, const double* radii,
+                               const double* velocities, int timesteps, int spheres,
+                               double activation_margin, double dt, int max_checks, double* reports,
+                               double* center_gradient, double* next_center_gradient,
+                               double* velocity_gradient);
+
 /* One full update run and timed INSIDE the library (no marshalling in the timed regions):
  * integrate n_frames depth frames, stamp the primitives, then seed_gather -> propagate ->
  * recover_signs over the given grid.  times_out = seconds of {integrate, stamp, seed, propagate,

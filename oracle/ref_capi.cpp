@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "ks/collision.hpp"
 #include "ks/esdf.hpp"
 #include "ks/sdf_world.hpp"
 
@@ -244,6 +245,61 @@ void kr_query_esdf(const double origin[3], const int dims[3], double voxel_size,
     out_gradient[3 * i + 1] = s.gradient.y();
     out_gradient[3 * i + 2] = s.gradient.z();
     out_inside[i] = s.inside ? 1 : 0;
+  }
+}
+
+void kr_scene_collision_static(const double origin[3], const int dims[3], double voxel_size, int has_sites,
+                               const double* distance, const double* centers, const double* radii, int64_t n,
+                               double activation_margin, double* report3, double* gradient) {
+  ks::DenseEsdf esdf;
+  esdf.config = to_esdf_config(origin, dims, voxel_size);
+  esdf.has_sites = has_sites != 0;
+  esdf.distance.assign(distance, distance + esdf.config.cell_count());
+  std::vector<ks::Vec3> c(n);
+  for (int64_t i = 0; i < n; ++i) c[i] = ks::Vec3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+  const ks::CollisionReport rep =
+      ks::scene_collision_static(esdf, std::span<const ks::Vec3>(c), std::span<const double>(radii, n), activation_margin);
+  report3[0] = rep.max_penetration;
+  report3[1] = rep.worst_first;
+  report3[2] = rep.cost;
+  for (int64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) gradient[3 * i + a] = rep.gradient[i][a];
+}
+
+void kr_scene_collision_swept(const double origin[3], const int dims[3], double voxel_size, int has_sites,
+                              const double* distance, const double* centers, const double* radii,
+                              const double* velocities, int timesteps, int spheres, double activation_margin,
+                              double dt, int max_checks, double* reports, double* center_gradient,
+                              double* next_center_gradient, double* velocity_gradient) {
+  ks::DenseEsdf esdf;
+  esdf.config = to_esdf_config(origin, dims, voxel_size);
+  esdf.has_sites = has_sites != 0;
+  esdf.signs_recovered = true;
+  esdf.distance.assign(distance, distance + esdf.config.cell_count());
+  std::vector<std::vector<ks::Vec3>> c(timesteps), v(timesteps);
+  for (int t = 0; t < timesteps; ++t)
+    for (int s = 0; s < spheres; ++s) {
+      const std::size_t at = (static_cast<std::size_t>(t) * spheres + s) * 3;
+      c[t].emplace_back(centers[at], centers[at + 1], centers[at + 2]);
+      v[t].emplace_back(velocities[at], velocities[at + 1], velocities[at + 2]);
+    }
+  ks::SceneCollisionConfig config;
+  config.activation_margin = activation_margin;
+  config.dt = dt;
+  config.max_checks = max_checks;
+  const auto reps = ks::scene_collision(esdf, c, std::span<const double>(radii, spheres), v, config);
+  for (int t = 0; t < timesteps; ++t) {
+    reports[3 * t] = reps[t].max_penetration;
+    reports[3 * t + 1] = reps[t].worst_sphere;
+    reports[3 * t + 2] = reps[t].cost;
+    for (int s = 0; s < spheres; ++s) {
+      const std::size_t at = (static_cast<std::size_t>(t) * spheres + s) * 3;
+      for (int a = 0; a < 3; ++a) {
+        center_gradient[at + a] = reps[t].center_gradient[s][a];
+        velocity_gradient[at + a] = reps[t].velocity_gradient[s][a];
+        if (t + 1 < timesteps) next_center_gradient[at + a] = reps[t].next_center_gradient[s][a];
+      }
+    }
   }
 }
 

@@ -55,6 +55,10 @@ class TsdfReportC(C.Structure):
                                           "next_fresh", "free_count", "recycled")]
 
 
+class CollisionReportC(C.Structure):
+    _fields_ = [("max_penetration", C.c_double), ("cost", C.c_double), ("worst_sphere", C.c_int32), ("reserved", C.c_int32)]
+
+
 class EsdfReportC(C.Structure):
     _fields_ = [("status", C.c_int32), ("has_sites", C.c_int32), ("signs_recovered", C.c_int32),
                 ("seed_count", C.c_int64)]
@@ -75,7 +79,8 @@ ABI_SYMBOLS = [
     "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
     "ks_tsdf_free_list", "ks_tsdf_profile", "ks_tsdf_stage_ms", "ks_esdf_profile", "ks_esdf_stage_ms", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
     "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync",
-    "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async",
+    "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async", "ks_esdf_scene_collision_static",
+    "ks_esdf_scene_collision_swept",
 ]
 
 
@@ -145,6 +150,8 @@ def load_library() -> C.CDLL:
         "ks_esdf_download": (C.c_int, [VP, VP, VP, VP]),
         "ks_esdf_query": (C.c_int, [VP, VP, I64, VP, VP, VP]),
         "ks_esdf_query_device_async": (C.c_int, [VP, VP, I64, VP, VP, VP]),
+        "ks_esdf_scene_collision_static": (C.c_int, [VP, VP, VP, I64, D, P(CollisionReportC), VP]),
+        "ks_esdf_scene_collision_swept": (C.c_int, [VP, VP, VP, VP, I32, I32, D, D, I32, P(CollisionReportC), VP, VP, VP]),
     }
     assert sorted(sig) == sorted(ABI_SYMBOLS)
     for name, (res, args) in sig.items():
@@ -513,6 +520,44 @@ def query(esdf: DenseEsdf, points) -> EsdfSample:  # esdf.hpp:337-387, batched o
     inside = np.empty(max(n, 1), np.uint8)
     _check(esdf.lib.ks_esdf_query(esdf.h, _ptr(pts), n, _ptr(d), _ptr(g), _ptr(inside)))
     return EsdfSample(d[:n], g[:n], inside[:n].astype(bool))
+
+
+@dataclass
+class CollisionReport:  # collision.hpp:46-52 (scene part)
+    max_penetration: float
+    worst_first: int
+    cost: float
+    gradient: np.ndarray
+
+
+def scene_collision_static(esdf: DenseEsdf, centers, radii, activation_margin: float = 0.025) -> CollisionReport:
+    """collision.hpp:130-152"""
+    c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+    r = np.ascontiguousarray(radii, np.float64).reshape(-1)
+    if c.shape[0] != r.size:
+        raise ValidationError("scene_collision: center/radius count mismatch")
+    rep = CollisionReportC()
+    grad = np.zeros((max(r.size, 1), 3), np.float64)
+    _check(esdf.lib.ks_esdf_scene_collision_static(esdf.h, _ptr(c), _ptr(r), r.size, float(activation_margin), C.byref(rep), _ptr(grad)))
+    return CollisionReport(rep.max_penetration, rep.worst_sphere, rep.cost, grad[:r.size])
+
+
+def scene_collision(esdf: DenseEsdf, centers, radii, velocities, activation_margin=0.025, dt=1.0, max_checks=10000):
+    """collision.hpp:177-239 -> (reports[T] as (max_penetration, worst_sphere, cost) array, center, next, velocity gradients)"""
+    c = np.ascontiguousarray(centers, np.float64)
+    v = np.ascontiguousarray(velocities, np.float64)
+    if c.shape[0] != v.shape[0]:
+        raise ValidationError("scene_collision: centers/velocities timestep mismatch")
+    T, S = c.shape[0], c.shape[1]
+    r = np.ascontiguousarray(radii, np.float64).reshape(-1)
+    if r.size != S or v.shape[1] != S:
+        raise ValidationError("scene_collision: sphere count mismatch at timestep")
+    reps = (CollisionReportC * T)()
+    g0, g1, g2 = (np.zeros((T, S, 3), np.float64) for _ in range(3))
+    _check(esdf.lib.ks_esdf_scene_collision_swept(esdf.h, _ptr(c), _ptr(r), _ptr(v), T, S, float(activation_margin), float(dt),
+                                                  int(max_checks), reps, _ptr(g0), _ptr(g1), _ptr(g2)))
+    out = np.array([[x.max_penetration, x.worst_sphere, x.cost] for x in reps], np.float64)
+    return out, g0, g1, g2
 
 
 # ---- CUDA graph helper ----------------------------------------------------------------------------

@@ -51,7 +51,8 @@ struct EsdfView {
   int* dir;      // dense block directory over the workspace: pool entry or -1
   int dlo[3], dn[3];
   int dcount;
-  uint8_t* brick;    // [ceil(n/8)^3] 1 when a live TSDF block can be probed from the 8^3-cell brick
+  uint8_t* pool_surf;  // [tsdf capacity] 1 when the block's surface plane is not empty (rebuilt with the directory)
+  uint8_t* brick;    // [ceil(n/8)^3] bit0: a live TSDF block lies in the brick's probe reach; bit1: one with surface voxels
   int* active;       // compacted ids of the active bricks (count in ctrl->active_bricks)
   int bnx, bny, bnz;
   uint8_t* mask;     // [cells] x-fastest seed mask (SeedMask, esdf.hpp:66) -- API paths
@@ -115,11 +116,17 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
     bx -= E.dlo[0], by -= E.dlo[1], bz -= E.dlo[2];
     if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
     E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
+    uint32_t any = 0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) any |= T.digest[p * kDigestWords + w];
+    E.pool_surf[p] = any != 0;
   }
 }
 
-// A brick is 8^3 ESDF cells.  It is active when any TSDF block that one of its cells' seven
-// probes can land in is live; inactive bricks hold no seed and are skipped by the gather.
+// A brick is 8^3 ESDF cells.  bit0: some TSDF block that one of its cells' seven probes can land in
+// is live (a cell outside such a brick has no allocated block under its own centre -- the sign
+// fallback's shortcut).  bit1: one of those blocks holds surface voxels; only these bricks can
+// contain seeds, so only they go on the gather's work list.
 __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
   const int nb = E.bnx * E.bny * E.bnz;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,16 +142,15 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
     lo[a] = E.vox[kVoxMh * total + base + first] >> 3;
     hi[a] = E.vox[kVoxPh * total + base + last] >> 3;
   }
-  uint8_t any = 0;
-  for (int z = lo[2]; z <= hi[2] && !any; ++z)
-    for (int y = lo[1]; y <= hi[1] && !any; ++y)
-      for (int x = lo[0]; x <= hi[0]; ++x)
-        if (E.dir[x + E.dn[0] * (y + E.dn[1] * z)] >= 0) {
-          any = 1;
-          break;
-        }
-  E.brick[i] = any;
-  if (any) E.active[atomicAdd(&E.ctrl->active_bricks, 1)] = i;
+  uint8_t flags = 0;
+  for (int z = lo[2]; z <= hi[2] && flags != 3; ++z)
+    for (int y = lo[1]; y <= hi[1] && flags != 3; ++y)
+      for (int x = lo[0]; x <= hi[0] && flags != 3; ++x) {
+        const int pool = E.dir[x + E.dn[0] * (y + E.dn[1] * z)];
+        if (pool >= 0) flags |= E.pool_surf[pool] ? 3 : 1;
+      }
+  E.brick[i] = flags;
+  if (flags & 2) E.active[atomicAdd(&E.ctrl->active_bricks, 1)] = i;
 }
 
 // ---- seed_gather (esdf.hpp:102-122): 7-probe stencil per ESDF cell, bits instead of voxels ----
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
   const int y = row % E.ny, z = row / E.ny;
   const int x = xw * 32 + lane;
   bool seed = false, geom_near = false;
-  if (x < E.nx && E.brick[(x >> 3) + E.bnx * ((y >> 3) + E.bny * (z >> 3))]) {
+  if (x < E.nx && (E.brick[(x >> 3) + E.bnx * ((y >> 3) + E.bny * (z >> 3))] & 2)) {
     const int total = E.nx + E.ny + E.nz;
     const int ix = x, iy = E.nx + y, iz = E.nx + E.ny + z;
     const int xc = E.vox[ix], xp = E.vox[total + ix], xm = E.vox[2 * total + ix];
@@ -344,36 +350,45 @@ __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
 }
 
 // ---- phase 1: nearest seed along z per (x, y) column (esdf.hpp:213-233) ----
-// The column's seeds become a bit string in shared memory ([word][thread], conflict free); one
-// ascending sweep then tracks the last seed at/below z and the next one above it.
-// Ties keep the lower z (strict '<', esdf.hpp:229).
+// One warp per 32 consecutive x columns of one y.  The column's seeds become a bit string (bit z)
+// in shared memory ([word][lane], conflict free); one ascending sweep then tracks the last seed
+// at/below z and the next one above it.  Ties keep the lower z (strict '<', esdf.hpp:229).
+// kBits: the mask is the x-packed bit plane of the fused build; a 32(z) x 32(x) bit tile is
+// transposed with one load per lane and 32 ballots.  Otherwise it is the reference's byte mask.
+constexpr int kFloodWarps = 4;
 template <bool kBits>
-__global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
+__global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
   extern __shared__ uint32_t s_words[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int plane = E.nx * E.ny;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int nwords = (E.nz + 31) >> 5;
-  const int stride = blockDim.x;
-  uint32_t* words = s_words + threadIdx.x;
-  if (col >= plane) return;
-  const int x = col % E.nx, y = col / E.nx;
+  const int gw = blockIdx.x * kFloodWarps + warp;
+  if (gw >= E.wpr * E.ny) return;
+  const int xw = gw % E.wpr, y = gw / E.wpr;
+  const int x = xw * 32 + lane;
+  uint32_t* words = s_words + warp * (nwords * 32) + lane;  // words[w * 32]
   uint32_t any = 0;
   for (int w = 0; w < nwords; ++w) {
     uint32_t bits = 0;
-    const int zend = min(32, E.nz - 32 * w);
     if (kBits) {
-      const uint32_t* src = E.mbits + ((32 * w) * E.ny + y) * E.wpr + (x >> 5);
-      const int step = E.ny * E.wpr;
-#pragma unroll 8
-      for (int b = 0; b < zend; ++b) bits |= ((__ldg(src + b * step) >> (x & 31)) & 1u) << b;
-    } else {
+      const int z = 32 * w + lane;
+      const uint32_t mine = z < E.nz ? __ldg(E.mbits + (z * E.ny + y) * E.wpr + xw) : 0u;  // 32 x-bits of row (y, z)
+#pragma unroll
+      for (int xb = 0; xb < 32; ++xb) {
+        const uint32_t col = __ballot_sync(0xFFFFFFFFu, (mine >> xb) & 1u);  // column xb: bit z
+        if (lane == xb) bits = col;
+      }
+    } else if (x < E.nx) {
+      const int zend = min(32, E.nz - 32 * w);
+      const int col = y * E.nx + x;
 #pragma unroll 8
       for (int b = 0; b < zend; ++b) bits |= (E.mask[col + plane * (32 * w + b)] != 0 ? 1u : 0u) << b;
     }
-    words[w * stride] = bits;
+    words[w * 32] = bits;
     any |= bits;
   }
-  uint16_t* out = E.near_z + col;
+  if (x >= E.nx) return;
+  uint16_t* out = E.near_z + y * E.nx + x;
   if (any == 0) {
     for (int z = 0; z < E.nz; ++z) out[plane * z] = edt::kNone;
     return;
@@ -381,8 +396,8 @@ __global__ void __launch_bounds__(128) k_flood_z(EsdfView E) {
   auto next_set = [&](int from) -> int {  // first set bit at position >= from, or -1
     if (from >= E.nz) return -1;
     int w = from >> 5;
-    uint32_t m = words[w * stride] & (0xFFFFFFFFu << (from & 31));
-    while (m == 0 && ++w < nwords) m = words[w * stride];
+    uint32_t m = words[w * 32] & (0xFFFFFFFFu << (from & 31));
+    while (m == 0 && ++w < nwords) m = words[w * 32];
     return m != 0 ? 32 * w + __ffs(static_cast<int>(m)) - 1 : -1;
   };
   int below = -1, above = next_set(0);
@@ -477,7 +492,7 @@ struct SignProbe {
       }
     }
     // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
-    if (kHints && !E.brick[brick_row + (x >> 3)]) return false;
+    if (kHints && !(E.brick[brick_row + (x >> 3)] & 1)) return false;
     const int vx = E.vox[x];
     const int pool = dir_lookup(E, vx, own_vy, own_vz);
     if (pool < 0) return false;
@@ -639,21 +654,15 @@ __device__ __forceinline__ double cell_distance(const EsdfView& E, int x, int y,
   const double d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;  // esdf.hpp:276-277
   return (v & 0x80000000u) ? -d : d;
 }
-__global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restrict__ pts, long long n, double* __restrict__ dist,
-                                               double* __restrict__ grad, uint8_t* __restrict__ inside) {
-  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+// One point: distance, gradient (may be null), inside flag.
+__device__ __forceinline__ void query_point(const EsdfView& E, const double p[3], double& dist, double grad[3], bool& in) {
   const int dims[3] = {E.nx, E.ny, E.nz};
-  bool in = true;
+  in = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) in = in && p[a] >= E.origin[a] && p[a] <= E.origin[a] + dims[a] * E.ve;
-  if (inside) inside[i] = in;
-  if (E.ctrl->seed_count == 0) {  // no sites: +inf, zero gradient (esdf.hpp:345)
-    dist[i] = CUDART_INF;
-    if (grad) grad[3 * i] = grad[3 * i + 1] = grad[3 * i + 2] = 0.0;
-    return;
-  }
+  dist = CUDART_INF;
+  grad[0] = grad[1] = grad[2] = 0.0;
+  if (E.ctrl->seed_count == 0) return;  // no sites: +inf, zero gradient (esdf.hpp:345)
   int i0[3], i1[3];
   double f[3];
 #pragma unroll
@@ -679,14 +688,152 @@ __global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restr
   const double c00 = c000 * (1 - fx) + c100 * fx, c10 = c010 * (1 - fx) + c110 * fx;
   const double c01 = c001 * (1 - fx) + c101 * fx, c11 = c011 * (1 - fx) + c111 * fx;
   const double c0 = c00 * (1 - fy) + c10 * fy, c1 = c01 * (1 - fy) + c11 * fy;
-  dist[i] = c0 * (1 - fz) + c1 * fz;
-  if (grad) {
-    const double inv = 1.0 / E.ve;
-    grad[3 * i] = ((c100 - c000) * (1 - fy) * (1 - fz) + (c110 - c010) * fy * (1 - fz) + (c101 - c001) * (1 - fy) * fz +
-                   (c111 - c011) * fy * fz) *
-                  inv;
-    grad[3 * i + 1] = ((c10 - c00) * (1 - fz) + (c11 - c01) * fz) * inv;
-    grad[3 * i + 2] = (c1 - c0) * inv;
+  dist = c0 * (1 - fz) + c1 * fz;
+  const double inv = 1.0 / E.ve;
+  grad[0] = ((c100 - c000) * (1 - fy) * (1 - fz) + (c110 - c010) * fy * (1 - fz) + (c101 - c001) * (1 - fy) * fz +
+             (c111 - c011) * fy * fz) *
+            inv;
+  grad[1] = ((c10 - c00) * (1 - fz) + (c11 - c01) * fz) * inv;
+  grad[2] = (c1 - c0) * inv;
+}
+
+__global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restrict__ pts, long long n, double* __restrict__ dist,
+                                               double* __restrict__ grad, uint8_t* __restrict__ inside) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  double d, g[3];
+  bool in;
+  query_point(E, p, d, g, in);
+  dist[i] = d;
+  if (inside) inside[i] = in;
+  if (grad) grad[3 * i] = g[0], grad[3 * i + 1] = g[1], grad[3 * i + 2] = g[2];
+}
+
+// ---- scene collision (collision.hpp:30-44, :130-239) ----
+__device__ __forceinline__ double hinge_cost(double clearance, double margin) {  // collision.hpp:30-37
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) {
+    const double gap = margin - clearance;
+    return gap * gap / (2.0 * margin);
+  }
+  return 0.5 * margin - clearance;
+}
+__device__ __forceinline__ double hinge_slope(double clearance, double margin) {  // collision.hpp:40-44
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) return -(margin - clearance) / margin;
+  return -1.0;
+}
+
+// scene_collision_static (collision.hpp:130-152): one thread per sphere -> penetration, cost, gradient
+__global__ void __launch_bounds__(256) k_collision_static(EsdfView E, const double* __restrict__ centers,
+                                                          const double* __restrict__ radii, int n, double margin,
+                                                          double* __restrict__ pen, double* __restrict__ cost,
+                                                          double* __restrict__ grad) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double p[3] = {centers[3 * s], centers[3 * s + 1], centers[3 * s + 2]};
+  double d, g[3];
+  bool in;
+  query_point(E, p, d, g, in);
+  const double clearance = d - radii[s];
+  pen[s] = -clearance;
+  const double c = hinge_cost(clearance, margin);
+  cost[s] = c;
+  double out[3] = {0.0, 0.0, 0.0};
+  if (c > 0.0) {
+    const double slope = hinge_slope(clearance, margin);
+    for (int a = 0; a < 3; ++a) out[a] += slope * g[a];
+  }
+  if (grad) grad[3 * s] = out[0], grad[3 * s + 1] = out[1], grad[3 * s + 2] = out[2];
+}
+
+// scene_collision (collision.hpp:177-239): one thread per (timestep, sphere) walks its segment
+__global__ void __launch_bounds__(128) k_collision_swept(EsdfView E, const double* __restrict__ centers,
+                                                         const double* __restrict__ radii, const double* __restrict__ vel,
+                                                         int timesteps, int spheres, double margin, double dt, int max_checks,
+                                                         double* __restrict__ pen, double* __restrict__ cost,
+                                                         double* __restrict__ g_center, double* __restrict__ g_next,
+                                                         double* __restrict__ g_vel) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= timesteps * spheres) return;
+  const int t = i / spheres, s = i % spheres;
+  const bool has_next = t + 1 < timesteps;
+  const size_t at = static_cast<size_t>(i) * 3;
+  const double start[3] = {centers[at], centers[at + 1], centers[at + 2]};
+  double seg[3] = {0.0, 0.0, 0.0};
+  if (has_next) {
+    const size_t nx = at + static_cast<size_t>(spheres) * 3;
+    for (int a = 0; a < 3; ++a) seg[a] = centers[nx + a] - start[a];
+  }
+  const double length = sqrt(sum3(seg[0] * seg[0], seg[1] * seg[1], seg[2] * seg[2]));
+  const double v[3] = {vel[at], vel[at + 1], vel[at + 2]};
+  const double speed = sqrt(sum3(v[0] * v[0], v[1] * v[1], v[2] * v[2]));
+  const double weight = speed * dt;
+  const double radius = radii[s];
+  double hinge_sum = 0.0, lambda = 0.0, max_pen = 0.0;
+  double sg[3] = {0.0, 0.0, 0.0}, ng[3] = {0.0, 0.0, 0.0};
+  for (int check = 0; check < max_checks; ++check) {
+    const double frac = length > 0.0 ? lambda / length : 0.0;
+    const double x[3] = {start[0] + frac * seg[0], start[1] + frac * seg[1], start[2] + frac * seg[2]};
+    double d, g[3];
+    bool in;
+    query_point(E, x, d, g, in);
+    const double clearance = d - radius;
+    if (-clearance > max_pen) max_pen = -clearance;
+    hinge_sum += hinge_cost(clearance, margin);
+    const double slope = hinge_slope(clearance, margin);
+    if (slope != 0.0) {
+      for (int a = 0; a < 3; ++a) {
+        const double gx = slope * g[a];
+        sg[a] += (1.0 - frac) * gx;
+        ng[a] += frac * gx;
+      }
+    }
+    if (!has_next) break;
+    lambda += clearance < E.ve ? E.ve : clearance;  // std::max(clearance, min_step)
+    if (lambda >= length) break;
+  }
+  pen[i] = max_pen;
+  cost[i] = weight * hinge_sum;
+  for (int a = 0; a < 3; ++a) {
+    g_center[at + a] = 0.0 + weight * sg[a];
+    if (has_next) g_next[at + a] = 0.0 + weight * ng[a];
+    g_vel[at + a] = speed > 1e-12 ? 0.0 + hinge_sum * dt * (v[a] / speed) : 0.0;
+  }
+}
+
+// Per group of `width` entries: report {max penetration (>0, first index on ties, else 0 / -1), cost sum}.
+// One CTA per group; the sum is a fixed-shape tree (deterministic; last-bit differences from the
+// reference's left-to-right sum are covered by the 1e-12 relative tolerance stated in the tests).
+__global__ void __launch_bounds__(256) k_collision_reduce(const double* __restrict__ pen, const double* __restrict__ cost, int width,
+                                                          double* __restrict__ report3) {
+  __shared__ double s_pen[256], s_cost[256];
+  __shared__ int s_idx[256];
+  const int group = blockIdx.x, tid = threadIdx.x;
+  const double* gp = pen + static_cast<size_t>(group) * width;
+  const double* gc = cost + static_cast<size_t>(group) * width;
+  double best = 0.0, total = 0.0;
+  int best_i = -1;
+  for (int i = tid; i < width; i += blockDim.x) {
+    if (gp[i] > best) best = gp[i], best_i = i;  // strict: lowest index among this thread's equals
+    total += gc[i];
+  }
+  s_pen[tid] = best, s_idx[tid] = best_i, s_cost[tid] = total;
+  __syncthreads();
+  for (int d = 128; d > 0; d >>= 1) {
+    if (tid < d) {
+      const double op = s_pen[tid + d];
+      const int oi = s_idx[tid + d];
+      if (oi >= 0 && (op > s_pen[tid] || (op == s_pen[tid] && (s_idx[tid] < 0 || oi < s_idx[tid])))) s_pen[tid] = op, s_idx[tid] = oi;
+      s_cost[tid] += s_cost[tid + d];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    report3[3 * group] = s_pen[0];
+    report3[3 * group + 1] = s_idx[0];
+    report3[3 * group + 2] = s_cost[0];
   }
 }
 
@@ -767,6 +914,9 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   if (dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
   E.dcount = static_cast<int>(dcount);
   KS_CUDA(cudaMalloc(&E.dir, static_cast<size_t>(E.dcount) * sizeof(int)));
+  if (E.pool_surf) cudaFree(E.pool_surf);
+  E.pool_surf = nullptr;
+  KS_CUDA(cudaMalloc(&E.pool_surf, static_cast<size_t>(T.capacity)));
   E.ratio = static_cast<float>(E.ve / T.voxel);
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
@@ -819,9 +969,11 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   EsdfView& E = e->view;
   const int plane = E.nx * E.ny;
   const int nwords = (E.nz + 31) / 32;
-  const unsigned fgrid = static_cast<unsigned>((plane + 127) / 128);
-  if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
-  else KS_LAUNCH(k_flood_z<false>, fgrid, 128, nwords * 128 * sizeof(uint32_t), e->stream, E);
+  const unsigned fgrid = static_cast<unsigned>((E.wpr * E.ny + kFloodWarps - 1) / kFloodWarps);
+  const size_t fsmem = static_cast<size_t>(nwords) * 32 * kFloodWarps * sizeof(uint32_t);
+  (void)plane;
+  if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
+  else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
@@ -919,6 +1071,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.gbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
+  if (E.pool_surf) cudaFree(E.pool_surf);
   cudaFreeHost(e->h_ctrl);
   cudaEventDestroy(e->dep);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
@@ -1058,6 +1211,77 @@ int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, 
   KS_LAUNCH(k_query, static_cast<unsigned>((n + 255) / 256), 256, 0, e->stream, e->view, points_dev, static_cast<long long>(n),
             distance_dev, gradient_dev, inside_dev);
   KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+int ks_esdf_scene_collision_static(ks_esdf* e, const double* centers_host, const double* radii_host, int64_t n,
+                                   double activation_margin, ks_collision_report* report, double* gradient_xyz_host) {
+  if (!e || !report) return fail(KS_ERR_INVALID, "null argument");
+  report->max_penetration = 0.0, report->worst_sphere = -1, report->cost = 0.0;
+  if (n <= 0) return KS_OK;
+  if (n > (1 << 30)) return fail(KS_ERR_INVALID, "scene_collision: too many spheres");
+  double *d_c = nullptr, *d_r = nullptr, *d_pen = nullptr, *d_cost = nullptr, *d_grad = nullptr, *d_rep = nullptr;
+  KS_CUDA(cudaMalloc(&d_c, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_r, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_pen, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_cost, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_grad, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_rep, 3 * sizeof(double)));
+  KS_CUDA(cudaMemcpyAsync(d_c, centers_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  KS_CUDA(cudaMemcpyAsync(d_r, radii_host, n * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  KS_LAUNCH(k_collision_static, static_cast<unsigned>((n + 255) / 256), 256, 0, e->stream, e->view, d_c, d_r, static_cast<int>(n),
+            activation_margin, d_pen, d_cost, d_grad);
+  KS_LAUNCH(k_collision_reduce, 1, 256, 0, e->stream, d_pen, d_cost, static_cast<int>(n), d_rep);
+  double rep[3];
+  KS_CUDA(cudaMemcpyAsync(rep, d_rep, sizeof rep, cudaMemcpyDeviceToHost, e->stream));
+  if (gradient_xyz_host)
+    KS_CUDA(cudaMemcpyAsync(gradient_xyz_host, d_grad, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d_c), cudaFree(d_r), cudaFree(d_pen), cudaFree(d_cost), cudaFree(d_grad), cudaFree(d_rep);
+  report->max_penetration = rep[0], report->worst_sphere = static_cast<int32_t>(rep[1]), report->cost = rep[2];
+  return KS_OK;
+}
+
+int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host, const double* radii_host,
+                                  const double* velocities_host, int32_t timesteps, int32_t spheres, double activation_margin,
+                                  double dt, int32_t max_checks, ks_collision_report* reports, double* center_gradient,
+                                  double* next_center_gradient, double* velocity_gradient) {
+  if (!e || !reports) return fail(KS_ERR_INVALID, "null argument");
+  if (timesteps <= 0 || spheres <= 0) return KS_OK;
+  ks_esdf_report st;
+  int rc = ks_esdf_sync(e, &st);
+  if (rc != KS_OK) return rc;
+  if (!st.signs_recovered) return fail(KS_ERR_INVALID, "scene_collision: esdf signs not recovered");  // collision.hpp:181
+  const size_t n = static_cast<size_t>(timesteps) * spheres;
+  double *d_c = nullptr, *d_r = nullptr, *d_v = nullptr, *d_pen = nullptr, *d_cost = nullptr, *d_g = nullptr, *d_rep = nullptr;
+  KS_CUDA(cudaMalloc(&d_c, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_v, n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_r, spheres * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_pen, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_cost, n * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_g, 3 * n * 3 * sizeof(double)));
+  KS_CUDA(cudaMalloc(&d_rep, static_cast<size_t>(timesteps) * 3 * sizeof(double)));
+  KS_CUDA(cudaMemsetAsync(d_g, 0, 3 * n * 3 * sizeof(double), e->stream));
+  KS_CUDA(cudaMemcpyAsync(d_c, centers_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  KS_CUDA(cudaMemcpyAsync(d_v, velocities_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  KS_CUDA(cudaMemcpyAsync(d_r, radii_host, spheres * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  KS_LAUNCH(k_collision_swept, static_cast<unsigned>((n + 127) / 128), 128, 0, e->stream, e->view, d_c, d_r, d_v, timesteps, spheres,
+            activation_margin, dt, max_checks, d_pen, d_cost, d_g, d_g + n * 3, d_g + 2 * n * 3);
+  KS_LAUNCH(k_collision_reduce, timesteps, 256, 0, e->stream, d_pen, d_cost, spheres, d_rep);
+  std::vector<double> rep(static_cast<size_t>(timesteps) * 3);
+  KS_CUDA(cudaMemcpyAsync(rep.data(), d_rep, rep.size() * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  if (center_gradient) KS_CUDA(cudaMemcpyAsync(center_gradient, d_g, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  if (next_center_gradient)
+    KS_CUDA(cudaMemcpyAsync(next_center_gradient, d_g + n * 3, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  if (velocity_gradient)
+    KS_CUDA(cudaMemcpyAsync(velocity_gradient, d_g + 2 * n * 3, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d_c), cudaFree(d_v), cudaFree(d_r), cudaFree(d_pen), cudaFree(d_cost), cudaFree(d_g), cudaFree(d_rep);
+  for (int t = 0; t < timesteps; ++t) {
+    reports[t].max_penetration = rep[3 * t];
+    reports[t].worst_sphere = static_cast<int32_t>(rep[3 * t + 1]);
+    reports[t].cost = rep[3 * t + 2];
+  }
   return KS_OK;
 }
 

@@ -79,6 +79,35 @@ class CpuChecker:
                                 C.c_int, _f64p, _f64p, _f64p, C.c_int, _f64p, _f64p, _f64p, _i32p, C.c_double,
                                 _f64p, _f64p)
 
+        self._coll_static = fn("scene_collision_static", None, _f64p, _i32p, C.c_double, C.c_int, _f64p, _f64p, _f64p,
+                               C.c_int64, C.c_double, _f64p, _f64p)
+        self._coll_swept = fn("scene_collision_swept", None, _f64p, _i32p, C.c_double, C.c_int, _f64p, _f64p, _f64p,
+                              _f64p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _f64p, _f64p, _f64p, _f64p)
+
+    def scene_collision_static(self, origin, dims, voxel_size, has_sites, distance, centers, radii, margin=0.025):
+        """collision.hpp:130-152 -> (max_penetration, worst_sphere, cost, gradient[n,3])"""
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        r = np.ascontiguousarray(radii, np.float64).reshape(-1)
+        rep = np.zeros(3, np.float64)
+        grad = np.zeros((max(len(r), 1), 3), np.float64)
+        self._coll_static(_vec(origin, 3), _vec(dims, 3, np.int32), float(voxel_size), int(has_sites),
+                          np.ascontiguousarray(distance, np.float64), c, r, len(r), float(margin), rep, grad)
+        return float(rep[0]), int(rep[1]), float(rep[2]), grad[:len(r)]
+
+    def scene_collision_swept(self, origin, dims, voxel_size, has_sites, distance, centers, radii, velocities,
+                              margin=0.025, dt=1.0, max_checks=10000):
+        """collision.hpp:177-239 -> (reports[T,3], center_grad, next_grad, velocity_grad), each [T,S,3]"""
+        c = np.ascontiguousarray(centers, np.float64)
+        T, S = c.shape[0], c.shape[1]
+        v = np.ascontiguousarray(velocities, np.float64).reshape(T, S, 3)
+        r = np.ascontiguousarray(radii, np.float64).reshape(S)
+        rep = np.zeros((T, 3), np.float64)
+        g0, g1, g2 = (np.zeros((T, S, 3), np.float64) for _ in range(3))
+        self._coll_swept(_vec(origin, 3), _vec(dims, 3, np.int32), float(voxel_size), int(has_sites),
+                         np.ascontiguousarray(distance, np.float64), c.reshape(-1), r, v.reshape(-1), T, S, float(margin),
+                         float(dt), int(max_checks), rep.reshape(-1), g0.reshape(-1), g1.reshape(-1), g2.reshape(-1))
+        return rep, g0, g1, g2
+
     def timed_update(self, tsdf: "CheckerTsdf", scene, dims=None):
         """One full update of `scene` timed inside the library; returns (seconds per stage dict, seeds, checksum)."""
         frames = scene.frames

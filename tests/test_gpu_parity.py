@@ -368,3 +368,45 @@ def test_graph_replay_equals_eager_calls(oracle_lib):
     site, dist, _ = e.download(d2=False)
     assert np.array_equal(site, site0) and np.array_equal(dist, dist0)
     g.close()
+
+
+# ---- scene collision ("next" row: the consumer of query) ----------------------------------------------
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_scene_collision_against_oracle(oracle_lib, seed):
+    """Penetration, worst sphere and every gradient identical; the cost SUM is a fixed-shape tree on the GPU
+    and a left-to-right sum in the reference, so it is held to 1e-12 relative."""
+    scene = scenes.small_scene(seed, dims=(36, 30, 26))
+    tsdf, _ = gpu_world(scene)
+    cpu, _ = cpu_world(oracle_lib, scene)
+    cfg = esdf_config(scene)
+    e = api.build_esdf(tsdf, cfg)
+    _, has0, _, dist0 = cpu.build_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel)
+    rng = np.random.RandomState(seed)
+    ext = np.array(scene.esdf_dims) * scene.esdf_voxel
+    S, T = 300, 6
+    centers = scene.esdf_origin + (rng.random_sample((T, S, 3)) * 1.1 - 0.05) * ext
+    centers[1:] = centers[0] + np.cumsum(rng.normal(0, 0.05, (T - 1, S, 3)), 0)
+    vel = rng.normal(0, 0.3, (T, S, 3))
+    vel[2, :5] = 0.0
+    radii = 0.02 + rng.random_sample(S) * 0.08
+
+    want = oracle_lib.scene_collision_static(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel, has0, dist0, centers[0], radii)
+    got = api.scene_collision_static(e, centers[0], radii)
+    assert got.max_penetration == want[0] and got.worst_first == want[1] and want[1] >= 0
+    assert abs(got.cost - want[2]) <= 1e-12 * abs(want[2])
+    assert same_bits(got.gradient, want[3])
+
+    rep0, c0, n0, v0 = oracle_lib.scene_collision_swept(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel, has0, dist0,
+                                                        centers, radii, vel, dt=0.1)
+    rep, c1, n1, v1 = api.scene_collision(e, centers, radii, vel, dt=0.1)
+    assert np.array_equal(rep[:, :2], rep0[:, :2])
+    np.testing.assert_allclose(rep[:, 2], rep0[:, 2], rtol=1e-12, atol=0)
+    assert same_bits(c1, c0) and same_bits(n1, n0) and same_bits(v1, v0)
+    assert rep0[:, 2].sum() > 0
+
+    with pytest.raises(api.ValidationError, match="scene_collision: center/radius count mismatch"):
+        api.scene_collision_static(e, centers[0], radii[:-1])
+    unsigned = api.propagate(np.ones(8, np.uint8), api.EsdfConfig(nx=2, ny=2, nz=2))
+    with pytest.raises(api.ValidationError, match="scene_collision: esdf signs not recovered"):
+        api.scene_collision(unsigned, centers[:, :1], radii[:1], vel[:, :1])

@@ -101,3 +101,36 @@ def test_propagate_random_grids_with_ties(oracle_lib, reference_lib):
         ha, sa, da = oracle_lib.propagate(mask, dims, 0.02)
         hb, sb, db = reference_lib.propagate(mask, dims, 0.02)
         assert ha == hb and np.array_equal(sa, sb) and _same_bits(da, db)
+
+
+def _collision_case(lib, seed):
+    sc = scenes.small_scene(seed, dims=(36, 30, 26))
+    w = lib.make_tsdf(sc.tsdf_voxel, capacity=sc.capacity)
+    for f in sc.frames:
+        w.integrate_depth(f.depth, f.width, f.height, f.intr, f.R, f.t)
+    for c in sc.cuboids:
+        w.stamp_cuboid(c.R, c.t, c.half_extents)
+    for s in sc.spheres:
+        w.stamp_sphere(s.center, s.radius)
+    _, has, _, dist = w.build_esdf(sc.esdf_origin, sc.esdf_dims, sc.esdf_voxel)
+    rng = np.random.RandomState(seed)
+    ext = np.array(sc.esdf_dims) * sc.esdf_voxel
+    S, T = 40, 6
+    centers = sc.esdf_origin + (rng.random_sample((T, S, 3)) * 1.1 - 0.05) * ext
+    centers[1:] = centers[0] + np.cumsum(rng.normal(0, 0.05, (T - 1, S, 3)), 0)
+    vel = rng.normal(0, 0.3, (T, S, 3))
+    vel[2, :5] = 0.0
+    radii = 0.02 + rng.random_sample(S) * 0.08
+    static = lib.scene_collision_static(sc.esdf_origin, sc.esdf_dims, sc.esdf_voxel, has, dist, centers[0], radii)
+    swept = lib.scene_collision_swept(sc.esdf_origin, sc.esdf_dims, sc.esdf_voxel, has, dist, centers, radii, vel, dt=0.1)
+    return static, swept
+
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_scene_collision_is_identical(oracle_lib, reference_lib, seed):
+    (a_static, a_swept), (b_static, b_swept) = _collision_case(oracle_lib, seed), _collision_case(reference_lib, seed)
+    assert a_static[:3] == b_static[:3] and _same_bits(a_static[3], b_static[3])
+    assert a_static[2] > 0 and a_static[1] >= 0          # the fixture does collide
+    for x, y in zip(a_swept, b_swept):
+        assert _same_bits(x, y)
+    assert a_swept[0][:, 2].sum() > 0
