@@ -113,6 +113,7 @@ struct TsdfCtrl {  // device control block, mirrored to pinned host memory on sy
 struct TsdfView {
   uint64_t* slot_key;   // [nslots]  packed key | kKeyEmpty | kKeyTomb
   int* slot_pool;       // [nslots]
+  uint32_t* slot_claim; // [nslots]  rank holding the slot while an allocation is in flight, else 0xFFFFFFFF
   int nslots;
   int capacity;
   int* free_list;       // [capacity] oldest first

@@ -29,6 +29,8 @@ struct OpLists {  // scratch of the op in flight (discover -> rank -> commit -> 
   int* pool;           // [cap] pool entry (filled by commit for new blocks)
   uint32_t* slot;      // [cap] slot in the per-frame set to clear afterwards (kNoSlot for stamps)
   int* fresh_idx;      // [cap] indices into key[] of blocks that must be allocated
+  int* fresh_rank;     // [cap] rank of that key among the new keys (lexicographic = insertion order)
+  uint64_t* rank_key;  // [cap] key of each rank (published before the key claims any slot)
   int cap;
   uint64_t* fset;      // per-frame dedup set, open addressing
   uint32_t fset_mask;  // slots - 1
@@ -224,11 +226,74 @@ __global__ void __launch_bounds__(256) k_discover(TsdfView T, OpLists L, const F
   }
 }
 
+// Slot placement identical to the reference's sequential insertion (BlockHashTable::insert,
+// sdf_world.hpp:146-172, called in sorted key order by allocate_keys :319-322).  Sequentially, key
+// number r lands on the first slot of its probe chain that is Empty or Tombstone and not already
+// taken by a key of lower rank (the remembered first tombstone IS that slot whenever one precedes
+// the first Empty).  Here every new key claims slots in T.slot_claim with atomicMin(rank): a lower
+// rank displaces a higher one, and the displaced key carries on down its chain.  The fixed point is
+// the sequential layout, whatever the interleaving.  The table itself (slot_key) is not touched
+// until every claim has settled; finalize_slots() then writes the keys.
+constexpr uint32_t kNoClaim = 0xFFFFFFFFu;
+__device__ void claim_slot(const TsdfView& T, uint64_t key, uint32_t rank, const uint64_t* rank_key, int lane) {
+  const uint32_t nslots = static_cast<uint32_t>(T.nslots);
+  int bx, by, bz;
+  unpack_key(key, bx, by, bz);
+  uint32_t pos = static_cast<uint32_t>(block_hash(bx, by, bz) % nslots);
+  uint32_t walked = 0;
+  while (walked < 2 * nslots) {  // warp-cooperative: 32 slots per step
+    const uint32_t sidx = (pos + lane) % nslots;
+    const uint64_t k = T.slot_key[sidx];
+    const bool open = (k == kKeyEmpty || k == kKeyTomb) && __ldcg(&T.slot_claim[sidx]) > rank;  // L2: claims move under us
+    const uint32_t vote = __ballot_sync(0xFFFFFFFFu, open);
+    if (vote == 0) {
+      pos = (pos + 32) % nslots;
+      walked += 32;
+      continue;
+    }
+    const int first = __ffs(vote) - 1;
+    const uint32_t target = (pos + first) % nslots;
+    uint32_t old = 0;
+    if (lane == 0) old = atomicMin(&T.slot_claim[target], rank);
+    old = __shfl_sync(0xFFFFFFFFu, old, 0);
+    if (old > rank) {
+      if (old == kNoClaim) return;  // placed
+      // we displaced the key of rank `old`: it continues from the next slot of ITS chain (same slots onward)
+      rank = old;
+      key = __ldcg(&rank_key[old]);  // published (fence) before rank `old` could appear in a claim
+    }
+    // else: a lower rank got there first; either way carry on after this slot
+    pos = (target + 1) % nslots;
+    walked += first + 1;
+  }
+}
+// Write the settled claims into the table: run by the op's apply kernel before it touches voxels.
+__device__ void finalize_slots(const TsdfView& T, const OpLists& L, int n_fresh) {
+  const uint32_t nslots = static_cast<uint32_t>(T.nslots);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_fresh; i += gridDim.x * blockDim.x) {
+    const int idx = L.fresh_idx[i];
+    const uint64_t key = L.key[idx];
+    const uint32_t rank = static_cast<uint32_t>(L.fresh_rank[i]);
+    int bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    uint32_t pos = static_cast<uint32_t>(block_hash(bx, by, bz) % nslots);
+    for (uint32_t probe = 0; probe < nslots; ++probe) {
+      if (T.slot_claim[pos] == rank) {
+        T.slot_key[pos] = key;
+        T.slot_pool[pos] = L.pool[idx];
+        T.slot_claim[pos] = kNoClaim;
+        break;
+      }
+      pos = pos + 1 == nslots ? 0 : pos + 1;
+    }
+  }
+}
+
 // ---- phase 3: allocation.  One CTA per new block: its rank among the new keys (= its place in the
 // sorted order allocate_keys inserts in, sdf_world.hpp:308-322) is counted by the whole CTA, the pool
-// index follows (free list LIFO first, then fresh), warp 0 inserts the key with a warp-cooperative
-// probe (32 slots per step, ballot, one CAS; BlockHashTable::insert sdf_world.hpp:146-172) and the
-// CTA resets the block (VoxelBlock::reset :70-74). ----
+// index follows (free list LIFO first, then fresh), warp 0 claims the key's slot with a
+// warp-cooperative probe (32 slots per step, ballot, one atomicMin; see claim_slot) and the CTA
+// resets the block (VoxelBlock::reset :70-74). ----
 __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
   if (op_blocked(T)) return;
   const TsdfCtrl* c = T.ctrl;
@@ -250,37 +315,15 @@ __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
     const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      int bx, by, bz;
-      unpack_key(key, bx, by, bz);
-      const uint32_t nslots = static_cast<uint32_t>(T.nslots);
-      const uint32_t start = static_cast<uint32_t>(block_hash(bx, by, bz) % nslots);
-      bool done = false;
-      for (uint32_t base = 0; base < nslots && !done; base += 32) {
-        const uint32_t off = base + lane;
-        const bool active = off < nslots;
-        const uint32_t s = active ? (start + off) % nslots : 0;
-        const uint64_t k = active ? T.slot_key[s] : 0;
-        uint32_t open = __ballot_sync(0xFFFFFFFFu, active && (k == kKeyEmpty || k == kKeyTomb));
-        while (open != 0 && !done) {
-          const int first = __ffs(open) - 1;
-          int ok = 0;
-          if (lane == first) {
-            ok = atomicCAS(reinterpret_cast<unsigned long long*>(&T.slot_key[s]), k, key) == k;
-            if (ok) T.slot_pool[s] = pool;
-          }
-          done = __shfl_sync(0xFFFFFFFFu, ok, first) != 0;
-          open &= ~(1u << first);
-        }
-      }
       if (lane == 0) {
-        if (done) {
-          T.pool_key[pool] = key;
-          L.pool[idx] = pool;
-        } else {
-          atomicCAS(&T.ctrl->err, 0, static_cast<int>(KS_ERR_TABLE_FULL));
-          T.ctrl->abort_op = 1;
-        }
+        L.fresh_rank[i] = r;
+        L.rank_key[r] = key;
+        L.pool[idx] = pool;
+        T.pool_key[pool] = key;
+        __threadfence();  // the key of a rank is visible before that rank can be seen in a claim
       }
+      __syncwarp();
+      claim_slot(T, key, static_cast<uint32_t>(r), L.rank_key, lane);
     }
     // reset the block: sum = wt = 0, geom = +inf, digest = 0
     double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
@@ -346,6 +389,7 @@ __global__ void __launch_bounds__(512) k_integrate(TsdfView T, OpLists L, const 
   __syncthreads();
   const int touched = min(T.ctrl->touched, L.cap);
   const bool blocked = op_blocked(T);
+  if (!blocked) finalize_slots(T, L, min(T.ctrl->fresh, L.cap));
   const int tid = threadIdx.x;
   const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
   const double v = T.voxel, trunc = T.trunc;
@@ -412,6 +456,7 @@ __global__ void __launch_bounds__(256) k_stamp_candidates(TsdfView T, OpLists L,
 // ---- stamp: per-voxel min with the analytic distance (sdf_world.hpp:437-443) ----
 __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Primitive P) {
   const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
+  if (!op_blocked(T)) finalize_slots(T, L, min(T.ctrl->fresh, L.cap));
   const int tid = threadIdx.x;
   const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
   const double v = T.voxel;
@@ -585,12 +630,14 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
   L.cap = static_cast<int>(want);
   KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
   KS_CUDA(cudaMalloc(&L.slot, want * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
+  KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
+  KS_CUDA(cudaMalloc(&L.rank_key, want * sizeof(uint64_t)));
   uint32_t slots = 1u << 16;
   while (slots < 2 * want) slots <<= 1;
   L.fset_mask = slots - 1;
@@ -712,6 +759,8 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   t->own_stream = true;
   KS_CUDA(cudaMalloc(&V.slot_key, V.nslots * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&V.slot_pool, V.nslots * sizeof(int)));
+  KS_CUDA(cudaMalloc(&V.slot_claim, V.nslots * sizeof(uint32_t)));
+  KS_CUDA(cudaMemsetAsync(V.slot_claim, 0xFF, V.nslots * sizeof(uint32_t), t->stream));
   KS_CUDA(cudaMalloc(&V.free_list, cap * sizeof(int)));
   KS_CUDA(cudaMalloc(&V.pool_key, cap * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&V.sumwt, cap * kBlockVoxels * sizeof(double2)));
@@ -740,10 +789,10 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   if (!t) return;
   cudaStreamSynchronize(t->stream);
   TsdfView& V = t->view;
-  cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.free_list), cudaFree(V.pool_key);
+  cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.slot_claim), cudaFree(V.free_list), cudaFree(V.pool_key);
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
   cudaFreeHost(t->h_ctrl);
   for (ks_tsdf::FrameSlot& S : t->slots) {
     if (S.h_frame) cudaFreeHost(S.h_frame);

@@ -53,6 +53,7 @@ def assert_world_parity(gpu: api.SparseTsdf, cpu, exact_pool=True, rtol=1e-5):
     assert set(g) == set(c), "live key sets differ"
     if exact_pool:
         assert g == c, "key -> pool assignment differs"
+        assert np.array_equal(gk, ck) and np.array_equal(gp, cp), "hash slot order differs from sequential insertion"
     keys = sorted(g)
     gs, gw, gg = gpu.download_blocks([g[k] for k in keys])
     bit_exact = True
