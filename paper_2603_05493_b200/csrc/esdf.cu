@@ -3,7 +3,8 @@
 // behind the C ABI in include/ks_b200.h.  See DESIGN.md for layouts and byte counts.
 //
 // Device layout of the finished field (per cell, 8 bytes):
-//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites)
+//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites; bit 31 is scratch
+//                  between the x sweep and the sign pass)
 //   d2s  : uint32  bit31 = negative, bits0-30 = squared integer site offset
 //                  (0x7FFFFFFF: no sites).  distance = sqrt((double)d2) * voxel_size
 //                  is formed on the fly, so queries see exactly the reference's doubles.
@@ -553,8 +554,12 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
 // bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
 // Writes the unsigned field; recover_signs is a separate full-occupancy pass (its dependent global
-// lookups would stall warps that are pinned here by the tile's shared memory: measured 122 us fused
-// against the pass below).
+// lookups would stall warps that are pinned here by the tile's shared memory).  With kMark the store
+// also classifies the cell for that pass using the hint planes of this build: a cell needs sign work
+// only if its site has stamped geometry in reach (and is not the cell itself) or a live block may lie
+// under its own centre; such cells get bit 31 of `site` set ("sign pending"), all others are exterior.
+constexpr uint32_t kSignPending = 0x80000000u;
+template <bool kMark>
 __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -583,6 +588,10 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int b
     uint16_t last = edt::kNone;
     uint32_t site = kSiteNone;
     int r2w = 0, sx = 0;
+    bool near = false;        // site has stamped geometry in reach
+    int brick_x = -1;         // brick column of the cached flag below
+    bool brick_live = false;  // a live block may lie under this cell's own centre
+    const uint8_t* brick_row = E.brick + E.bnx * ((y >> 3) + E.bny * (z >> 3));
     edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
       const int o = obase + ny * x;
       if (win == edt::kNone) {
@@ -597,25 +606,45 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int b
         sx = win;
         r2w = (y - sy) * (y - sy) + (z - sz) * (z - sz);
         site = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+        if (kMark) near = ((__ldg(E.gbits + ((sz * ny + sy) * E.wpr + (sx >> 5))) >> (sx & 31)) & 1u) != 0;
       }
-      E.site[o] = site;
-      E.d2s[o] = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
+      const uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
+      uint32_t word = site;
+      if (kMark) {
+        if ((x >> 3) != brick_x) {
+          brick_x = x >> 3;
+          brick_live = (brick_row[brick_x] & 1) != 0;
+        }
+        if ((near && d2 != 0) || brick_live) word |= kSignPending;
+      }
+      E.site[o] = word;
+      E.d2s[o] = d2;
     });
   }
 }
 
-// ---- recover_signs (esdf.hpp:288-320): one thread per cell of the y-fastest field ----
-// Cells that resolve to "exterior" never touch d2s; the others flip its sign bit.
-template <bool kHints>
+// ---- recover_signs (esdf.hpp:288-320): grid = (ceil(ny/256), x chunks, nz); thread <-> y of the
+// y-fastest field, looping over its chunk of x.  kPending: only cells the x sweep marked are looked at
+// (everything else is exterior); cells that resolve to "exterior" never touch d2s, the others flip its
+// sign bit.
+constexpr int kSignChunks = 8;
+template <bool kPending>
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= E.cells) return;
-  const uint32_t site = E.site[o];
-  if (site == kSiteNone) return;
-  const int y = o % E.ny;
-  const int x = (o / E.ny) % E.nx;
-  const int z = o / (E.ny * E.nx);
-  if (cell_negative<kHints>(E, T, x, y, z, site & 1023, (site >> 10) & 1023, site >> 20)) E.d2s[o] ^= 0x80000000u;
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  const int z = blockIdx.z;
+  if (y >= E.ny) return;
+  const int per = (E.nx + kSignChunks - 1) / kSignChunks;
+  const int x_end = min(E.nx, (static_cast<int>(blockIdx.y) + 1) * per);
+  for (int x = blockIdx.y * per; x < x_end; ++x) {
+    const int o = y + E.ny * (x + E.nx * z);
+    const uint32_t site = E.site[o];
+    if (site == kSiteNone) continue;
+    if (kPending) {
+      if (!(site & kSignPending)) continue;
+      E.site[o] = site & ~kSignPending;
+    }
+    if (cell_negative<kPending>(E, T, x, y, z, site & 1023, (site >> 10) & 1023, (site >> 20) & 1023)) E.d2s[o] ^= 0x80000000u;
+  }
 }
 
 // ---- query (esdf.hpp:337-387) ----
@@ -820,7 +849,7 @@ __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ si
   if (site_xyz) {
     site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
     site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
-    site_xyz[3 * idx + 2] = s == kSiteNone ? -1 : static_cast<int>(s >> 20);
+    site_xyz[3 * idx + 2] = s == kSiteNone ? -1 : static_cast<int>((s >> 20) & 1023);
   }
   if (distance) {
     double d = CUDART_INF;
@@ -950,11 +979,14 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
-  KS_LAUNCH(k_sweep_x, dim3((E.ny + 31) / 32, E.nz), 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
-  if (t) {  // hint planes are fresh only when this build gathered into the bit planes
+  const dim3 xgrid((E.ny + 31) / 32, E.nz);
+  const bool mark = t && bits;  // hint planes are fresh only when this build gathered into the bit planes
+  if (mark) KS_LAUNCH(k_sweep_x<true>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
+  else KS_LAUNCH(k_sweep_x<false>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
+  if (t) {
     if (e->profile_stages) cudaEventRecord(e->ev[5], e->stream);
-    const unsigned sgrid = static_cast<unsigned>((E.cells + 255) / 256);
-    if (bits) KS_LAUNCH(k_recover_signs<true>, sgrid, 256, 0, e->stream, E, tsdf_view(t));
+    const dim3 sgrid((E.ny + 255) / 256, kSignChunks, E.nz);
+    if (mark) KS_LAUNCH(k_recover_signs<true>, sgrid, 256, 0, e->stream, E, tsdf_view(t));
     else KS_LAUNCH(k_recover_signs<false>, sgrid, 256, 0, e->stream, E, tsdf_view(t));
     KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   }
@@ -964,7 +996,7 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
 
 static int signs_async(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
-  KS_LAUNCH(k_recover_signs<false>, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
+  KS_LAUNCH(k_recover_signs<false>, dim3((E.ny + 255) / 256, kSignChunks, E.nz), 256, 0, e->stream, E, tsdf_view(t));
   KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -1002,7 +1034,8 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
