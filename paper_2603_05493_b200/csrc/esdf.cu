@@ -623,28 +623,39 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int b
   }
 }
 
-// ---- recover_signs (esdf.hpp:288-320): grid = (ceil(ny/256), x chunks, nz); thread <-> y of the
-// y-fastest field, looping over its chunk of x.  kPending: only cells the x sweep marked are looked at
-// (everything else is exterior); cells that resolve to "exterior" never touch d2s, the others flip its
-// sign bit.
-constexpr int kSignChunks = 8;
+// ---- recover_signs (esdf.hpp:288-320): one thread per cell of the y-fastest field ----
+// kPending: only cells the x sweep marked are looked at (everything else is exterior); cells that
+// resolve to "exterior" never touch d2s, the others flip its sign bit.  The cell index is decoded with
+// multiply-shift divisions: for d <= 1024 and v <= 2^30, v / d == (v * ceil(2^s / d)) >> s with
+// s = 31 + ceil(log2 d) (the multiplier stays below 2^33, the product below 2^63).
+struct DivMagic {
+  unsigned long long mul;
+  int shift;
+};
+static DivMagic make_div_magic(int d) {
+  int log2d = 1;
+  while ((1 << log2d) < d) ++log2d;
+  const int shift = 31 + log2d;
+  return DivMagic{((1ull << shift) + d - 1) / d, shift};
+}
+__device__ __forceinline__ int div_magic(int v, DivMagic m) {
+  return static_cast<int>((static_cast<unsigned long long>(static_cast<unsigned>(v)) * m.mul) >> m.shift);
+}
 template <bool kPending>
-__global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  const int z = blockIdx.z;
-  if (y >= E.ny) return;
-  const int per = (E.nx + kSignChunks - 1) / kSignChunks;
-  const int x_end = min(E.nx, (static_cast<int>(blockIdx.y) + 1) * per);
-  for (int x = blockIdx.y * per; x < x_end; ++x) {
-    const int o = y + E.ny * (x + E.nx * z);
-    const uint32_t site = E.site[o];
-    if (site == kSiteNone) continue;
-    if (kPending) {
-      if (!(site & kSignPending)) continue;
-      E.site[o] = site & ~kSignPending;
-    }
-    if (cell_negative<kPending>(E, T, x, y, z, site & 1023, (site >> 10) & 1023, (site >> 20) & 1023)) E.d2s[o] ^= 0x80000000u;
+__global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T, DivMagic magic_ny, DivMagic magic_nx) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= E.cells) return;
+  const uint32_t site = E.site[o];
+  if (site == kSiteNone) return;
+  if (kPending) {
+    if (!(site & kSignPending)) return;
+    E.site[o] = site & ~kSignPending;
   }
+  const int q = div_magic(o, magic_ny);
+  const int y = o - q * E.ny;
+  const int z = div_magic(q, magic_nx);
+  const int x = q - z * E.nx;
+  if (cell_negative<kPending>(E, T, x, y, z, site & 1023, (site >> 10) & 1023, (site >> 20) & 1023)) E.d2s[o] ^= 0x80000000u;
 }
 
 // ---- query (esdf.hpp:337-387) ----
@@ -985,9 +996,10 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   else KS_LAUNCH(k_sweep_x<false>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
   if (t) {
     if (e->profile_stages) cudaEventRecord(e->ev[5], e->stream);
-    const dim3 sgrid((E.ny + 255) / 256, kSignChunks, E.nz);
-    if (mark) KS_LAUNCH(k_recover_signs<true>, sgrid, 256, 0, e->stream, E, tsdf_view(t));
-    else KS_LAUNCH(k_recover_signs<false>, sgrid, 256, 0, e->stream, E, tsdf_view(t));
+    const unsigned sgrid = static_cast<unsigned>((E.cells + 255) / 256);
+    const DivMagic mny = make_div_magic(E.ny), mnx = make_div_magic(E.nx);
+    if (mark) KS_LAUNCH(k_recover_signs<true>, sgrid, 256, 0, e->stream, E, tsdf_view(t), mny, mnx);
+    else KS_LAUNCH(k_recover_signs<false>, sgrid, 256, 0, e->stream, E, tsdf_view(t), mny, mnx);
     KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   }
   KS_CUDA(cudaGetLastError());
@@ -996,7 +1008,8 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
 
 static int signs_async(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
-  KS_LAUNCH(k_recover_signs<false>, dim3((E.ny + 255) / 256, kSignChunks, E.nz), 256, 0, e->stream, E, tsdf_view(t));
+  KS_LAUNCH(k_recover_signs<false>, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t),
+            make_div_magic(E.ny), make_div_magic(E.nx));
   KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
