@@ -199,8 +199,8 @@ def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcou
         "seed": C_ / 8.0 + C_ / 512.0 + 64.0 * L + 4.0 * dcount,   # bit mask out, brick flags + surface planes + directory in
         "flood_z": C_ / 8.0 + 2.0 * C_,                               # bit mask in, nearest-z (u16) out
         "sweep_y": 2.0 * C_ + 4.0 * C_,                               # u16 in, (site_y, site_z) u32 out
-        "sweep_x": 4.0 * C_ + 8.0 * C_,                               # u32 in, site u32 + d2 u32 out
-        "signs": 4.0 * C_ + C_ / 4.0 + 256.0 * L,                     # site in, hint planes + sign planes, d2 sign flips
+        "sweep_x": 4.0 * C_ + 8.0 * C_ + 256.0 * L,                   # u32 in, site u32 + signed d2 u32 out, sign planes
+        "signs": 0.0,                                                 # fused into sweep_x
     }[stage]
 
 

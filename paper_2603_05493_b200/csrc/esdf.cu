@@ -3,8 +3,7 @@
 // behind the C ABI in include/ks_b200.h.  See DESIGN.md for layouts and byte counts.
 //
 // Device layout of the finished field (per cell, 8 bytes):
-//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites; bit 31 is scratch
-//                  between the x sweep and the sign pass)
+//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites)
 //   d2s  : uint32  bit31 = negative, bits0-30 = squared integer site offset
 //                  (0x7FFFFFFF: no sites).  distance = sqrt((double)d2) * voxel_size
 //                  is formed on the fly, so queries see exactly the reference's doubles.
@@ -423,57 +422,84 @@ __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
 //   only this axis != 0   : normalize() gives exactly +-1 (sqrt(d*d) == |d|)  -> table rows kVoxPe / kVoxMe
 //   otherwise             : fp32 estimate of the offset, accepted only when it is farther from a voxel
 //                           face than its error bound; else the reference's own fp64 sequence.
-// so the voxel index is always the one the reference computes.  With kHints (planes left by the brick
-// gather of the same build) two tests come first and skip work without changing the result: a site with
-// no stamped block within reach cannot resolve a geometry probe (gbits), and a cell in a brick without a
-// live block in reach has no allocated block under its own centre (fallback lookup).
-template <bool kHints>
-__device__ __forceinline__ bool cell_negative(const EsdfView& E, const TsdfView& T, int x, int y, int z, int sx, int sy, int sz) {
-  const int total = E.nx + E.ny + E.nz;
-  const int iy = E.nx + y, iz = E.nx + E.ny + z;
-  const int dx = x - sx, dy = y - sy, dz = z - sz;
-  bool probe = (dx | dy | dz) != 0;  // delta.squaredNorm() > 0 (distinct cells have distinct centres)
-  if (kHints && probe) probe = ((__ldg(E.gbits + ((sz * E.ny + sy) * E.wpr + (sx >> 5))) >> (sx & 31)) & 1u) != 0;
-  if (probe) {
-    const int jx = sx, jy = E.nx + sy, jz = E.nx + E.ny + sz;
-    int vx, vy, vz;
-    if ((dx != 0) + (dy != 0) + (dz != 0) == 1) {
-      vx = E.vox[(dx == 0 ? kVoxC : (dx > 0 ? kVoxPe : kVoxMe)) * total + jx];
-      vy = E.vox[(dy == 0 ? kVoxC : (dy > 0 ? kVoxPe : kVoxMe)) * total + jy];
-      vz = E.vox[(dz == 0 ? kVoxC : (dz > 0 ? kVoxPe : kVoxMe)) * total + jz];
-    } else {
-      const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
-      const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
-      const float ox = E.qsf[jx] + fx * rinv, oy = E.qsf[jy] + fy * rinv, oz = E.qsf[jz] + fz * rinv;
-      const float tol = 4e-6f * (1.0f + E.ratio);
-      const bool sure = (dx == 0 || fabsf(ox - rintf(ox)) > tol) && (dy == 0 || fabsf(oy - rintf(oy)) > tol) &&
-                        (dz == 0 || fabsf(oz - rintf(oz)) > tol);
-      if (sure) {
-        vx = E.vox[jx] + (dx == 0 ? 0 : __float2int_rd(ox));
-        vy = E.vox[jy] + (dy == 0 ? 0 : __float2int_rd(oy));
-        vz = E.vox[jz] + (dz == 0 ? 0 : __float2int_rd(oz));
-      } else {  // the reference's arithmetic, operation by operation
-        const double px = E.ctr[jx], py = E.ctr[jy], pz = E.ctr[jz];
-        const double ex = E.ctr[x] - px, ey = E.ctr[iy] - py, ez = E.ctr[iz] - pz;
-        const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
-        vx = voxel_index(px + E.ve * (ex / n), T.voxel) - 8 * E.dlo[0];
-        vy = voxel_index(py + E.ve * (ey / n), T.voxel) - 8 * E.dlo[1];
-        vz = voxel_index(pz + E.ve * (ez / n), T.voxel) - 8 * E.dlo[2];
-      }
-    }
-    const int pool = dir_lookup(E, vx, vy, vz);
-    if (pool >= 0) {
-      const uint32_t g = pair_bits(T, pool, kDigestGeom, local_index(vx, vy, vz));
-      if (g & 1u) return (g & 2u) != 0;  // query_tsdf_geom has a value: its sign decides
+// so the voxel index is always the one the reference computes.  Two hints skip work without changing the
+// result: a site with no stamped block within reach cannot resolve a geometry probe (gbits), and a cell
+// in an inactive brick has no allocated block under its own centre (fallback lookup).
+struct SignProbe {
+  const EsdfView& E;
+  const TsdfView& T;
+  int total;
+  int y, z, iy, iz;
+  int own_vy, own_vz;   // the cell's own voxel (fallback lookup)
+  int brick_row;
+  // current site
+  int sx, sy, sz, jx, jy, jz;
+  int v0x, v0y, v0z;
+  float qx, qy, qz;
+  bool geom_near;
+
+  __device__ __forceinline__ SignProbe(const EsdfView& E_, const TsdfView& T_, int y_, int z_) : E(E_), T(T_) {
+    total = E.nx + E.ny + E.nz;
+    y = y_, z = z_;
+    iy = E.nx + y, iz = E.nx + E.ny + z;
+    own_vy = E.vox[iy], own_vz = E.vox[iz];
+    brick_row = E.bnx * ((y >> 3) + E.bny * (z >> 3));
+    sx = sy = sz = -1;
+    geom_near = true;
+  }
+  template <bool kHints>
+  __device__ __forceinline__ void set_site(int sx_, int sy_, int sz_) {
+    sx = sx_, sy = sy_, sz = sz_;
+    jx = sx, jy = E.nx + sy, jz = E.nx + E.ny + sz;
+    geom_near = !kHints || ((__ldg(E.gbits + ((sz * E.ny + sy) * E.wpr + (sx >> 5))) >> (sx & 31)) & 1u) != 0;
+    if (geom_near) {
+      v0x = E.vox[jx], v0y = E.vox[jy], v0z = E.vox[jz];
+      qx = E.qsf[jx], qy = E.qsf[jy], qz = E.qsf[jz];
     }
   }
-  // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
-  if (kHints && !(E.brick[(x >> 3) + E.bnx * ((y >> 3) + E.bny * (z >> 3))] & 1)) return false;
-  const int vx = E.vox[x], vy = E.vox[iy], vz = E.vox[iz];
-  const int pool = dir_lookup(E, vx, vy, vz);
-  if (pool < 0) return false;
-  return pair_bits(T, pool, kDigestComb, local_index(vx, vy, vz)) == 3u;
-}
+  template <bool kHints>
+  __device__ __forceinline__ bool negative(int x) const {
+    const int dx = x - sx, dy = y - sy, dz = z - sz;
+    if (geom_near && (dx | dy | dz) != 0) {  // delta.squaredNorm() > 0 (distinct cells have distinct centres)
+      int vx, vy, vz;
+      if ((dx != 0) + (dy != 0) + (dz != 0) == 1) {
+        vx = dx == 0 ? v0x : E.vox[(dx > 0 ? kVoxPe : kVoxMe) * total + jx];
+        vy = dy == 0 ? v0y : E.vox[(dy > 0 ? kVoxPe : kVoxMe) * total + jy];
+        vz = dz == 0 ? v0z : E.vox[(dz > 0 ? kVoxPe : kVoxMe) * total + jz];
+      } else {
+        const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+        const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
+        const float ox = qx + fx * rinv, oy = qy + fy * rinv, oz = qz + fz * rinv;
+        const float tol = 4e-6f * (1.0f + E.ratio);
+        const bool sure = (dx == 0 || fabsf(ox - rintf(ox)) > tol) && (dy == 0 || fabsf(oy - rintf(oy)) > tol) &&
+                          (dz == 0 || fabsf(oz - rintf(oz)) > tol);
+        if (sure) {
+          vx = v0x + (dx == 0 ? 0 : __float2int_rd(ox));
+          vy = v0y + (dy == 0 ? 0 : __float2int_rd(oy));
+          vz = v0z + (dz == 0 ? 0 : __float2int_rd(oz));
+        } else {  // the reference's arithmetic, operation by operation
+          const double px = E.ctr[jx], py = E.ctr[jy], pz = E.ctr[jz];
+          const double ex = E.ctr[x] - px, ey = E.ctr[iy] - py, ez = E.ctr[iz] - pz;
+          const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
+          vx = voxel_index(px + E.ve * (ex / n), T.voxel) - 8 * E.dlo[0];
+          vy = voxel_index(py + E.ve * (ey / n), T.voxel) - 8 * E.dlo[1];
+          vz = voxel_index(pz + E.ve * (ez / n), T.voxel) - 8 * E.dlo[2];
+        }
+      }
+      const int pool = dir_lookup(E, vx, vy, vz);
+      if (pool >= 0) {
+        const uint32_t g = pair_bits(T, pool, kDigestGeom, local_index(vx, vy, vz));
+        if (g & 1u) return (g & 2u) != 0;  // query_tsdf_geom has a value: its sign decides
+      }
+    }
+    // unresolved: combined sdf at the query cell's own centre (esdf.hpp:309-312)
+    if (kHints && !(E.brick[brick_row + (x >> 3)] & 1)) return false;
+    const int vx = E.vox[x];
+    const int pool = dir_lookup(E, vx, own_vy, own_vz);
+    if (pool < 0) return false;
+    return pair_bits(T, pool, kDigestComb, local_index(vx, own_vy, own_vz)) == 3u;
+  }
+};
 
 // ---- phases 2 and 3: banded lower-envelope sweeps (esdf.hpp:236-280), see edt_core.cuh ----
 __device__ __forceinline__ edt::RowTile carve_tile(unsigned char* base, int n, int band, int bands, size_t in_bytes) {
@@ -553,14 +579,10 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // grid = (ceil(ny/32), nz); block = 32 * bands.  lane <-> y, positions = x.
 // The x-fastest input tile is loaded coalesced and turned into the [x][lane] layout with a
 // bank rotation (write at bank (row + x) & 31, then rotate each 32-word group in place).
-// Writes the unsigned field; recover_signs is a separate full-occupancy pass (its dependent global
-// lookups would stall warps that are pinned here by the tile's shared memory).  With kMark the store
-// also classifies the cell for that pass using the hint planes of this build: a cell needs sign work
-// only if its site has stamped geometry in reach (and is not the cell itself) or a live block may lie
-// under its own centre; such cells get bit 31 of `site` set ("sign pending"), all others are exterior.
-constexpr uint32_t kSignPending = 0x80000000u;
-template <bool kMark>
-__global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int bands) {
+// kSigns: 0 = unsigned field (propagate), 1 = recover_signs fused into the store of the finished cell,
+// 2 = the same using the hint planes left by the bit-packed gather of this build.
+template <int kSigns>
+__global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * 32, z = blockIdx.y;
@@ -584,14 +606,11 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int b
   sweep_stages(T, src, warp, lane);
   const int y = y0 + lane;
   if (warp < bands && y < ny) {
+    SignProbe probe(E, Tw, kSigns ? y : 0, kSigns ? z : 0);
     const int obase = y + ny * nx * z;
     uint16_t last = edt::kNone;
     uint32_t site = kSiteNone;
     int r2w = 0, sx = 0;
-    bool near = false;        // site has stamped geometry in reach
-    int brick_x = -1;         // brick column of the cached flag below
-    bool brick_live = false;  // a live block may lie under this cell's own centre
-    const uint8_t* brick_row = E.brick + E.bnx * ((y >> 3) + E.bny * (z >> 3));
     edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
       const int o = obase + ny * x;
       if (win == edt::kNone) {
@@ -606,56 +625,28 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_x(EsdfView E, int band, int b
         sx = win;
         r2w = (y - sy) * (y - sy) + (z - sz) * (z - sz);
         site = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-        if (kMark) near = ((__ldg(E.gbits + ((sz * ny + sy) * E.wpr + (sx >> 5))) >> (sx & 31)) & 1u) != 0;
+        if (kSigns) probe.template set_site<kSigns == 2>(sx, sy, sz);
       }
-      const uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
-      uint32_t word = site;
-      if (kMark) {
-        if ((x >> 3) != brick_x) {
-          brick_x = x >> 3;
-          brick_live = (brick_row[brick_x] & 1) != 0;
-        }
-        if ((near && d2 != 0) || brick_live) word |= kSignPending;
-      }
-      E.site[o] = word;
+      uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
+      if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
+      E.site[o] = site;
       E.d2s[o] = d2;
     });
   }
 }
 
-// ---- recover_signs (esdf.hpp:288-320): one thread per cell of the y-fastest field ----
-// kPending: only cells the x sweep marked are looked at (everything else is exterior); cells that
-// resolve to "exterior" never touch d2s, the others flip its sign bit.  The cell index is decoded with
-// multiply-shift divisions: for d <= 1024 and v <= 2^30, v / d == (v * ceil(2^s / d)) >> s with
-// s = 31 + ceil(log2 d) (the multiplier stays below 2^33, the product below 2^63).
-struct DivMagic {
-  unsigned long long mul;
-  int shift;
-};
-static DivMagic make_div_magic(int d) {
-  int log2d = 1;
-  while ((1 << log2d) < d) ++log2d;
-  const int shift = 31 + log2d;
-  return DivMagic{((1ull << shift) + d - 1) / d, shift};
-}
-__device__ __forceinline__ int div_magic(int v, DivMagic m) {
-  return static_cast<int>((static_cast<unsigned long long>(static_cast<unsigned>(v)) * m.mul) >> m.shift);
-}
-template <bool kPending>
-__global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T, DivMagic magic_ny, DivMagic magic_nx) {
+// ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
+__global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
   const uint32_t site = E.site[o];
   if (site == kSiteNone) return;
-  if (kPending) {
-    if (!(site & kSignPending)) return;
-    E.site[o] = site & ~kSignPending;
-  }
-  const int q = div_magic(o, magic_ny);
-  const int y = o - q * E.ny;
-  const int z = div_magic(q, magic_nx);
-  const int x = q - z * E.nx;
-  if (cell_negative<kPending>(E, T, x, y, z, site & 1023, (site >> 10) & 1023, (site >> 20) & 1023)) E.d2s[o] ^= 0x80000000u;
+  const int y = o % E.ny;
+  const int x = (o / E.ny) % E.nx;
+  const int z = o / (E.ny * E.nx);
+  SignProbe probe(E, T, y, z);
+  probe.template set_site<false>(site & 1023, (site >> 10) & 1023, site >> 20);
+  if (probe.template negative<false>(x)) E.d2s[o] ^= 0x80000000u;
 }
 
 // ---- query (esdf.hpp:337-387) ----
@@ -860,7 +851,7 @@ __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ si
   if (site_xyz) {
     site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
     site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
-    site_xyz[3 * idx + 2] = s == kSiteNone ? -1 : static_cast<int>((s >> 20) & 1023);
+    site_xyz[3 * idx + 2] = s == kSiteNone ? -1 : static_cast<int>(s >> 20);
   }
   if (distance) {
     double d = CUDART_INF;
@@ -895,9 +886,11 @@ struct ks_esdf {
 namespace ksb {
 
 static void pick_bands(int n, int& band, int& bands) {
-  int target = 24, max_warps = 16;  // positions per band / warps per tile (KS_BAND_TARGET, KS_MAX_WARPS: tuning only)
+  // 24 positions per band and at most 16 warps per tile measured best on B200 (tools/tune_bands.sh);
+  // KS_BAND_TARGET / KS_MAX_WARPS override them for tuning runs only.
+  int target = 24, max_warps = 16;
   if (const char* v = std::getenv("KS_BAND_TARGET")) target = std::max(2, std::atoi(v));
-  if (const char* v = std::getenv("KS_MAX_WARPS")) max_warps = std::min(32, std::max(1, std::atoi(v)));
+  if (const char* v = std::getenv("KS_MAX_WARPS")) max_warps = std::min(16, std::max(1, std::atoi(v)));
   int warps = std::min(max_warps, std::max(1, (n + target - 1) / target));
   band = (n + warps - 1) / warps;
   bands = (n + band - 1) / band;
@@ -991,25 +984,21 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
-  const bool mark = t && bits;  // hint planes are fresh only when this build gathered into the bit planes
-  if (mark) KS_LAUNCH(k_sweep_x<true>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
-  else KS_LAUNCH(k_sweep_x<false>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, e->band_x, e->bands_x);
-  if (t) {
-    if (e->profile_stages) cudaEventRecord(e->ev[5], e->stream);
-    const unsigned sgrid = static_cast<unsigned>((E.cells + 255) / 256);
-    const DivMagic mny = make_div_magic(E.ny), mnx = make_div_magic(E.nx);
-    if (mark) KS_LAUNCH(k_recover_signs<true>, sgrid, 256, 0, e->stream, E, tsdf_view(t), mny, mnx);
-    else KS_LAUNCH(k_recover_signs<false>, sgrid, 256, 0, e->stream, E, tsdf_view(t), mny, mnx);
-    KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
+  if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
+    KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
+  } else if (t) {
+    KS_LAUNCH(k_sweep_x<1>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
+  } else {
+    KS_LAUNCH(k_sweep_x<0>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
   }
+  if (t) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
 
 static int signs_async(ks_esdf* e, const ks_tsdf* t) {
   EsdfView& E = e->view;
-  KS_LAUNCH(k_recover_signs<false>, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t),
-            make_div_magic(E.ny), make_div_magic(E.nx));
+  KS_LAUNCH(k_recover_signs, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, tsdf_view(t));
   KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -1047,8 +1036,9 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
@@ -1122,9 +1112,8 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   const bool bits = e->cfg.seeding == 1;
   if ((rc = seed_async(e, t, e->cfg.seeding, bits)) != KS_OK) return rc;
   if (prof) cudaEventRecord(e->ev[2], e->stream);
-  static const bool no_signs = std::getenv("KS_EXPERIMENT_NO_SIGNS") != nullptr;  // profiling aid only
-  rc = propagate_async(e, bits, no_signs ? nullptr : t);  // records ev[5] before the sign pass
-  if (prof && no_signs) cudaEventRecord(e->ev[5], e->stream);
+  rc = propagate_async(e, bits, t);  // sign recovery rides in the x sweep
+  if (prof) cudaEventRecord(e->ev[5], e->stream);
   if (prof) cudaEventRecord(e->ev[6], e->stream);
   e->profile_stages = false;
   return rc;
