@@ -10,6 +10,12 @@
 //   * SparseTsdf::pool / table and DenseEsdf::site / distance are not public vectors: call
 //     .site() / .distance() (downloaded on demand) or the ks_tsdf_export_* functions.
 //   * query_batch() is new: callers that looped over query() should hand the whole batch over.
+//   * scene_collision_static / scene_collision (collision.hpp:130-239) are here too, as one batched
+//     kernel each; the cost is a fixed-shape tree sum on the GPU (1e-12 relative to the reference's
+//     left-to-right sum), everything else is identical.
+//   * save/load_depth_frame and save/load_esdf read and write the reference's KSDEPTH1 / KSESDF1 files;
+//     the JSON header is emitted with sorted keys like the reference's nlohmann dump, numbers in shortest
+//     round-trip form (values, not bytes, are what both sides agree on).
 // Vec3 / Mat3 / Pose / ValidationError are taken from the reference's own core.hpp when
 // KS_B200_USE_REFERENCE_CORE is defined (mixing with the planner headers), else declared here.
 #ifndef KS_B200_KS_HPP
@@ -17,9 +23,17 @@
 
 #include <Eigen/Dense>
 
+#include <algorithm>
 #include <array>
+#include <charconv>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
 #include <limits>
+#include <span>
+#include <sstream>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -125,6 +139,7 @@ struct DepthFrame {  // sdf_world.hpp:191-204
     if (width <= 0 || height <= 0 || fx <= 0.0 || fy <= 0.0) throw ValidationError("depth frame: invalid intrinsics");
     if (static_cast<int>(depth.size()) != width * height) throw ValidationError("depth frame: depth buffer size mismatch");
   }
+  bool depth_valid(float d) const { return std::isfinite(d) && d > 0.0f; }  // sdf_world.hpp:203
   ks_camera camera() const {
     ks_camera cam{};
     cam.width = width, cam.height = height;
@@ -344,6 +359,243 @@ inline void query_batch(const DenseEsdf& esdf, const std::vector<double>& points
   gradient_xyz.resize(3 * n);
   inside.resize(n);
   b200_detail::check(ks_esdf_query(esdf.get(), points_xyz.data(), n, distance.data(), gradient_xyz.data(), inside.data()));
+}
+
+// ---- collision.hpp, scene part (collision.hpp:30-52, :130-239) ---------------------------------------
+inline double hinge_cost(double clearance, double margin) {  // collision.hpp:30-37
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) {
+    const double gap = margin - clearance;
+    return gap * gap / (2.0 * margin);
+  }
+  return 0.5 * margin - clearance;
+}
+inline double hinge_slope(double clearance, double margin) {  // collision.hpp:40-44
+  if (clearance >= margin) return 0.0;
+  if (clearance >= 0.0) return -(margin - clearance) / margin;
+  return -1.0;
+}
+
+struct CollisionReport {  // collision.hpp:46-52
+  double max_penetration = -kInf;
+  int worst_first = -1;
+  int worst_second = -1;
+  double cost = 0.0;
+  std::vector<Vec3> gradient;
+};
+
+/// One batched kernel instead of the reference's per-sphere query loop.
+inline CollisionReport scene_collision_static(const DenseEsdf& esdf, std::span<const Vec3> centers,
+                                              std::span<const double> radii, double activation_margin = 0.025) {
+  if (centers.size() != radii.size()) throw ValidationError("scene_collision: center/radius count mismatch");
+  std::vector<double> xyz(3 * centers.size()), grad(3 * centers.size());
+  for (std::size_t s = 0; s < centers.size(); ++s)
+    for (int a = 0; a < 3; ++a) xyz[3 * s + a] = centers[s][a];
+  ks_collision_report rep{};
+  b200_detail::check(ks_esdf_scene_collision_static(esdf.get(), xyz.data(), radii.data(), static_cast<std::int64_t>(radii.size()),
+                                                    activation_margin, &rep, grad.data()));
+  CollisionReport out;
+  out.max_penetration = rep.max_penetration;
+  out.worst_first = rep.worst_sphere;
+  out.cost = rep.cost;
+  out.gradient.resize(centers.size());
+  for (std::size_t s = 0; s < centers.size(); ++s) out.gradient[s] = Vec3(grad[3 * s], grad[3 * s + 1], grad[3 * s + 2]);
+  return out;
+}
+
+struct SceneCollisionConfig {  // collision.hpp:154-158
+  double activation_margin = 0.025;
+  double dt = 1.0;
+  int max_checks = 10000;
+};
+struct SceneTimestepReport {  // collision.hpp:161-168
+  double max_penetration = -kInf;
+  int worst_sphere = -1;
+  double cost = 0.0;
+  std::vector<Vec3> center_gradient, next_center_gradient, velocity_gradient;
+};
+
+inline std::vector<SceneTimestepReport> scene_collision(const DenseEsdf& esdf, const std::vector<std::vector<Vec3>>& centers,
+                                                        std::span<const double> radii,
+                                                        const std::vector<std::vector<Vec3>>& velocities,
+                                                        const SceneCollisionConfig& config = {}) {  // collision.hpp:177-239
+  if (!esdf.signs_recovered) throw ValidationError("scene_collision: esdf signs not recovered");
+  if (centers.size() != velocities.size()) throw ValidationError("scene_collision: centers/velocities timestep mismatch");
+  const std::size_t steps = centers.size(), spheres = radii.size();
+  std::vector<double> c(3 * steps * spheres), v(3 * steps * spheres);
+  for (std::size_t t = 0; t < steps; ++t) {
+    if (centers[t].size() != spheres || velocities[t].size() != spheres)
+      throw ValidationError("scene_collision: sphere count mismatch at timestep");
+    for (std::size_t s = 0; s < spheres; ++s)
+      for (int a = 0; a < 3; ++a) {
+        c[3 * (t * spheres + s) + a] = centers[t][s][a];
+        v[3 * (t * spheres + s) + a] = velocities[t][s][a];
+      }
+  }
+  std::vector<ks_collision_report> reps(steps);
+  std::vector<double> g0(c.size()), g1(c.size()), g2(c.size());
+  if (steps > 0 && spheres > 0)
+    b200_detail::check(ks_esdf_scene_collision_swept(esdf.get(), c.data(), radii.data(), v.data(), static_cast<std::int32_t>(steps),
+                                                     static_cast<std::int32_t>(spheres), config.activation_margin, config.dt,
+                                                     config.max_checks, reps.data(), g0.data(), g1.data(), g2.data()));
+  std::vector<SceneTimestepReport> out(steps);
+  for (std::size_t t = 0; t < steps; ++t) {
+    out[t].max_penetration = spheres ? reps[t].max_penetration : 0.0;
+    out[t].worst_sphere = spheres ? reps[t].worst_sphere : -1;
+    out[t].cost = spheres ? reps[t].cost : 0.0;
+    out[t].center_gradient.resize(spheres);
+    out[t].velocity_gradient.resize(spheres);
+    if (t + 1 < steps) out[t].next_center_gradient.resize(spheres);
+    for (std::size_t s = 0; s < spheres; ++s) {
+      const std::size_t at = 3 * (t * spheres + s);
+      out[t].center_gradient[s] = Vec3(g0[at], g0[at + 1], g0[at + 2]);
+      out[t].velocity_gradient[s] = Vec3(g2[at], g2[at + 1], g2[at + 2]);
+      if (t + 1 < steps) out[t].next_center_gradient[s] = Vec3(g1[at], g1[at + 1], g1[at + 2]);
+    }
+  }
+  return out;
+}
+
+// ---- file formats (sdf_world.hpp:511-579, esdf.hpp:389-443) ---------------------------------------------
+// KSDEPTH1: "KSDEPTH1" + u32 header length + JSON {width,height,fx,fy,cx,cy,pose:{xyz,rpy}} + f32 depths.
+// KSESDF1 : "KSESDF1\0" + u32 header length + JSON {origin,dims,voxel_size} + f32 distances (x fastest).
+// Host-only code; the JSON headers are flat enough to be written and read without a JSON library.
+namespace b200_detail {
+inline std::string num(double v) {  // shortest text that reads back to the same double
+  char buf[40];
+  const auto res = std::to_chars(buf, buf + sizeof buf, v);
+  return std::string(buf, res.ptr);
+}
+/// value text following "key": in a flat JSON object (numbers or [..] arrays of numbers)
+inline std::vector<double> json_numbers(const std::string& text, const std::string& key, const std::string& path) {
+  const std::size_t k = text.find("\"" + key + "\"");
+  if (k == std::string::npos) throw ParseError("'" + path + "': bad header: missing key " + key);
+  std::size_t i = text.find(':', k);
+  if (i == std::string::npos) throw ParseError("'" + path + "': bad header");
+  ++i;
+  while (i < text.size() && std::isspace(static_cast<unsigned char>(text[i]))) ++i;
+  std::vector<double> out;
+  const bool array = i < text.size() && text[i] == '[';
+  if (array) ++i;
+  while (i < text.size()) {
+    while (i < text.size() && (std::isspace(static_cast<unsigned char>(text[i])) || text[i] == ',')) ++i;
+    if (i >= text.size() || text[i] == ']' || text[i] == '}') break;
+    char* end = nullptr;
+    const double v = std::strtod(text.c_str() + i, &end);
+    if (end == text.c_str() + i) throw ParseError("'" + path + "': bad header: bad number for " + key);
+    out.push_back(v);
+    i = static_cast<std::size_t>(end - text.c_str());
+    if (!array) break;
+  }
+  return out;
+}
+inline Mat3 rpy_to_matrix(double roll, double pitch, double yaw) {  // core.hpp:85-89: Rz(yaw) Ry(pitch) Rx(roll)
+  const double cr = std::cos(roll), sr = std::sin(roll), cp = std::cos(pitch), sp = std::sin(pitch), cy = std::cos(yaw),
+               sy = std::sin(yaw);
+  Mat3 m;
+  m(0, 0) = cy * cp, m(0, 1) = cy * sp * sr - sy * cr, m(0, 2) = cy * sp * cr + sy * sr;
+  m(1, 0) = sy * cp, m(1, 1) = sy * sp * sr + cy * cr, m(1, 2) = sy * sp * cr - cy * sr;
+  m(2, 0) = -sp, m(2, 1) = cp * sr, m(2, 2) = cp * cr;
+  return m;
+}
+}  // namespace b200_detail
+
+inline void save_depth_frame(const std::string& path, const DepthFrame& frame) {  // sdf_world.hpp:518-542
+  frame.validate();
+  const Mat3& r = frame.pose.rotation;
+  const double pitch = std::asin(std::clamp(-r(2, 0), -1.0, 1.0));
+  using b200_detail::num;
+  const std::string header = "{\"cx\":" + num(frame.cx) + ",\"cy\":" + num(frame.cy) + ",\"fx\":" + num(frame.fx) + ",\"fy\":" +
+                             num(frame.fy) + ",\"height\":" + std::to_string(frame.height) + ",\"pose\":{\"rpy\":[" +
+                             num(std::atan2(r(2, 1), r(2, 2))) + "," + num(pitch) + "," + num(std::atan2(r(1, 0), r(0, 0))) +
+                             "],\"xyz\":[" + num(frame.pose.translation[0]) + "," + num(frame.pose.translation[1]) + "," +
+                             num(frame.pose.translation[2]) + "]},\"width\":" + std::to_string(frame.width) + "}";
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw ParseError("cannot open '" + path + "' for writing");
+  out.write("KSDEPTH1", 8);
+  const auto len = static_cast<std::uint32_t>(header.size());
+  out.write(reinterpret_cast<const char*>(&len), 4);
+  out.write(header.data(), static_cast<std::streamsize>(header.size()));
+  out.write(reinterpret_cast<const char*>(frame.depth.data()), static_cast<std::streamsize>(frame.depth.size() * sizeof(float)));
+}
+
+inline DepthFrame load_depth_frame(const std::string& path) {  // sdf_world.hpp:544-579
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError("cannot open depth frame '" + path + "'");
+  char magic[8];
+  in.read(magic, 8);
+  if (!in || std::memcmp(magic, "KSDEPTH1", 8) != 0) throw ParseError("'" + path + "' is not a KSDEPTH1 file");
+  std::uint32_t len = 0;
+  in.read(reinterpret_cast<char*>(&len), 4);
+  std::string header(len, '\0');
+  in.read(header.data(), len);
+  if (!in) throw ParseError("'" + path + "': truncated header");
+  using b200_detail::json_numbers;
+  DepthFrame frame;
+  frame.width = static_cast<int>(json_numbers(header, "width", path).at(0));
+  frame.height = static_cast<int>(json_numbers(header, "height", path).at(0));
+  frame.fx = json_numbers(header, "fx", path).at(0);
+  frame.fy = json_numbers(header, "fy", path).at(0);
+  frame.cx = json_numbers(header, "cx", path).at(0);
+  frame.cy = json_numbers(header, "cy", path).at(0);
+  const std::vector<double> xyz = json_numbers(header, "xyz", path), rpy = json_numbers(header, "rpy", path);
+  if (xyz.size() != 3 || rpy.size() != 3) throw ParseError("'" + path + "': bad header: pose");
+  frame.pose.translation = Vec3(xyz[0], xyz[1], xyz[2]);
+  frame.pose.rotation = b200_detail::rpy_to_matrix(rpy[0], rpy[1], rpy[2]);
+  if (frame.width <= 0 || frame.height <= 0) throw ValidationError("depth frame: invalid intrinsics");
+  frame.depth.resize(static_cast<std::size_t>(frame.width) * frame.height);
+  in.read(reinterpret_cast<char*>(frame.depth.data()), static_cast<std::streamsize>(frame.depth.size() * sizeof(float)));
+  if (!in) throw ParseError("'" + path + "': truncated depth data");
+  frame.validate();
+  return frame;
+}
+
+inline void save_esdf(const std::string& path, const DenseEsdf& esdf) {  // esdf.hpp:395-411
+  using b200_detail::num;
+  const EsdfConfig& c = esdf.config;
+  const std::string header = "{\"dims\":[" + std::to_string(c.nx) + "," + std::to_string(c.ny) + "," + std::to_string(c.nz) +
+                             "],\"origin\":[" + num(c.origin[0]) + "," + num(c.origin[1]) + "," + num(c.origin[2]) +
+                             "],\"voxel_size\":" + num(c.voxel_size) + "}";
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw ParseError("cannot open '" + path + "' for writing");
+  out.write("KSESDF1\0", 8);
+  const auto len = static_cast<std::uint32_t>(header.size());
+  out.write(reinterpret_cast<const char*>(&len), 4);
+  out.write(header.data(), static_cast<std::streamsize>(header.size()));
+  const std::vector<double> distance = esdf.distance();
+  std::vector<float> narrow(distance.size());
+  for (std::size_t i = 0; i < distance.size(); ++i) narrow[i] = static_cast<float>(distance[i]);
+  out.write(reinterpret_cast<const char*>(narrow.data()), static_cast<std::streamsize>(narrow.size() * sizeof(float)));
+}
+
+struct EsdfExport {  // esdf.hpp:413-418
+  Vec3 origin;
+  int nx, ny, nz;
+  double voxel_size;
+  std::vector<float> distance;
+};
+
+inline EsdfExport load_esdf(const std::string& path) {  // esdf.hpp:420-443
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError("cannot open esdf '" + path + "'");
+  char magic[8];
+  in.read(magic, 8);
+  if (!in || std::memcmp(magic, "KSESDF1\0", 8) != 0) throw ParseError("'" + path + "' is not a KSESDF1 file");
+  std::uint32_t len = 0;
+  in.read(reinterpret_cast<char*>(&len), 4);
+  std::string header(len, '\0');
+  in.read(header.data(), len);
+  using b200_detail::json_numbers;
+  const std::vector<double> origin = json_numbers(header, "origin", path), dims = json_numbers(header, "dims", path);
+  if (origin.size() != 3 || dims.size() != 3) throw ParseError("'" + path + "': bad header");
+  EsdfExport out;
+  out.origin = Vec3(origin[0], origin[1], origin[2]);
+  out.nx = static_cast<int>(dims[0]), out.ny = static_cast<int>(dims[1]), out.nz = static_cast<int>(dims[2]);
+  out.voxel_size = json_numbers(header, "voxel_size", path).at(0);
+  out.distance.resize(static_cast<std::size_t>(out.nx) * out.ny * out.nz);
+  in.read(reinterpret_cast<char*>(out.distance.data()), static_cast<std::streamsize>(out.distance.size() * sizeof(float)));
+  if (!in) throw ParseError("'" + path + "': truncated distance data");
+  return out;
 }
 
 }  // namespace ks

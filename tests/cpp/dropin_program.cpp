@@ -4,7 +4,9 @@
 // The only source difference between the two builds is how DenseEsdf's arrays are reached.
 #include <cstdio>
 #include <cmath>
+#include <vector>
 #ifdef USE_REFERENCE
+#include "ks/collision.hpp"
 #include "ks/esdf.hpp"
 #include "ks/sdf_world.hpp"
 #define DISTANCES(e) (e).distance
@@ -13,7 +15,8 @@
 #define DISTANCES(e) (e).distance()
 #endif
 
-int main() {
+int main(int argc, char** argv) {
+  const std::string scratch = argc > 1 ? argv[1] : "/tmp";
   ks::TsdfConfig config = ks::make_tsdf_config(0.02);
   config.capacity = 4096;
   ks::SparseTsdf world = ks::make_tsdf(config);
@@ -59,6 +62,21 @@ int main() {
     const ks::EsdfSample s = ks::query(esdf, ks::Vec3(x, 0.37, 0.29));
     std::printf("query %.17g %.17g %.17g %.17g %d\n", s.distance, s.gradient.x(), s.gradient.y(), s.gradient.z(), s.inside);
   }
+  // scene collision over a few spheres, and the KSESDF1 export round trip
+  std::vector<ks::Vec3> centers;
+  std::vector<double> radii;
+  for (int i = 0; i < 12; ++i) {
+    centers.emplace_back(0.08 * i + 0.05, 0.31 + 0.01 * i, 0.2 + 0.015 * i);
+    radii.push_back(0.03 + 0.004 * i);
+  }
+  const ks::CollisionReport hit = ks::scene_collision_static(esdf, centers, radii, 0.03);
+  std::printf("collision %.17g %d %.12g %.17g %.17g\n", hit.max_penetration, hit.worst_first, hit.cost, hit.gradient[3].x(),
+              hit.gradient[7].z());
+  ks::save_esdf(scratch + "/dropin_field.ksesdf", esdf);
+  const ks::EsdfExport back = ks::load_esdf(scratch + "/dropin_field.ksesdf");
+  double fsum = 0.0;
+  for (float d : back.distance) fsum += d;
+  std::printf("export %d %d %d %.17g %.17g\n", back.nx, back.ny, back.nz, back.voxel_size, fsum);
   try {
     ks::TsdfConfig tiny = ks::make_tsdf_config(0.02);
     tiny.capacity = 4;

@@ -30,9 +30,9 @@ def test_golden_output_is_what_the_reference_prints(tmp_path):
         pytest.skip("reference tree not mounted")
     json_inc = Path(sysconfig.get_paths()["purelib"]) / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
     exe = tmp_path / "dropin_ref"
-    subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-DUSE_REFERENCE", "-I/root/reference/proj/include",
-                    f"-I{STANDIN}", f"-I{json_inc}", str(SRC), "-o", str(exe)], check=True)
-    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-DUSE_REFERENCE", f"-I{ROOT / 'oracle' / 'ref_stubs'}",
+                    "-I/root/reference/proj/include", f"-I{STANDIN}", f"-I{json_inc}", str(SRC), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), str(tmp_path)], check=True, capture_output=True, text=True).stdout
     assert out == GOLD.read_text()
 
 
@@ -40,5 +40,49 @@ def test_golden_output_is_what_the_reference_prints(tmp_path):
 def test_program_prints_the_reference_output_on_the_gpu(tmp_path):
     exe = tmp_path / "dropin_b200"
     build_b200_variant(exe)
-    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    out = subprocess.run([str(exe), str(tmp_path)], check=True, capture_output=True, text=True).stdout
     assert out == GOLD.read_text()
+
+
+# ---- KSDEPTH1 / KSESDF1 files: host-only, so checked on the CPU too -------------------------------------
+FILEIO = ROOT / "tests" / "cpp" / "fileio_program.cpp"
+G = ROOT / "tests" / "golden"
+
+
+def _build_fileio(out: Path, reference: bool):
+    if reference:
+        json_inc = Path(sysconfig.get_paths()["purelib"]) / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
+        cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-DUSE_REFERENCE", "-I/root/reference/proj/include",
+               f"-I{STANDIN}", f"-I{json_inc}", str(FILEIO), "-o", str(out)]
+    else:
+        from paper_2603_05493_b200 import build
+        build.build()
+        lib_dir = ROOT / "paper_2603_05493_b200"
+        cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{STANDIN}", str(FILEIO), "-o", str(out), f"-L{lib_dir}",
+               "-lks_b200", f"-Wl,-rpath,{lib_dir}"]
+    subprocess.run(cmd, check=True)
+
+
+def test_reads_files_written_by_the_reference(tmp_path):
+    exe = tmp_path / "fileio_b200"
+    _build_fileio(exe, reference=False)
+    out = subprocess.run([str(exe), "read", str(G / "frame_reference.ksdepth"), str(G / "field_reference.ksesdf"),
+                          str(tmp_path / "resaved.ksdepth")], check=True, capture_output=True, text=True).stdout
+    assert out == (G / "fileio_expected.txt").read_text()
+    # what we write reads back to the same values
+    again = subprocess.run([str(exe), "read", str(tmp_path / "resaved.ksdepth"), str(G / "field_reference.ksesdf"),
+                            str(tmp_path / "again.ksdepth")], check=True, capture_output=True, text=True).stdout
+    assert again == out
+
+
+def test_reference_reads_files_written_by_us(tmp_path):
+    if not os.path.isdir("/root/reference/proj/include"):
+        pytest.skip("reference tree not mounted")
+    ours, ref = tmp_path / "fileio_b200", tmp_path / "fileio_ref"
+    _build_fileio(ours, reference=False)
+    _build_fileio(ref, reference=True)
+    subprocess.run([str(ours), "read", str(G / "frame_reference.ksdepth"), str(G / "field_reference.ksesdf"),
+                    str(tmp_path / "ours.ksdepth")], check=True, capture_output=True)
+    out = subprocess.run([str(ref), "read", str(tmp_path / "ours.ksdepth"), str(G / "field_reference.ksesdf"),
+                          str(tmp_path / "x.ksdepth")], check=True, capture_output=True, text=True).stdout
+    assert out == (G / "fileio_expected.txt").read_text()
