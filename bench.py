@@ -215,9 +215,25 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the perception path has no CPU implementation")
+    # KS_BENCH_SHARE_GPU=1 (tests only): every rank uses device 0 and the collective runs on gloo, so the
+    # N > 1 control flow can be exercised on a one-GPU box.  The real multi-GPU run is NCCL, one rank per GPU.
+    share_gpu = os.environ.get("KS_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def all_reduce_max(t):
+        if share_gpu:
+            c = t.cpu()
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
     scene = make_scene(args.workload, env=rank)
     nx, ny, nz = scene.esdf_dims
@@ -258,7 +274,12 @@ def run_ours(args):
         summary_in[1] = probe_d.min()
         summary_in[2] = (probe_d < 0.02).sum()
         if world > 1:
-            dist.all_gather_into_tensor(summary_all, summary_in)
+            if share_gpu:
+                host_all = torch.empty(4 * world, dtype=torch.float64)
+                dist.all_gather_into_tensor(host_all, summary_in.cpu())
+                summary_all.copy_(host_all)
+            else:
+                dist.all_gather_into_tensor(summary_all, summary_in)
 
     with torch.cuda.stream(stream):
         # ---- eager warm-up (allocates blocks, binds the directory), then stage timings ---------------
@@ -315,7 +336,7 @@ def run_ours(args):
         per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+            all_reduce_max(total_ms)
         total_ms = float(total_ms.item())
         rep = tsdf.sync()
         erep = esdf.report()
@@ -343,7 +364,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+            all_reduce_max(e2e_s)
         e2e_s = float(e2e_s.item())
 
         # ---- e2e through the graph API (stage + upload + replay + report), informational ----------------
