@@ -209,10 +209,18 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2603_05493_b200 import api, build
-    build.build()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # the library normally travels prebuilt; if it is missing exactly one rank per node compiles it
+    if not build.LIB.exists():
+        if local == 0:
+            build.build(force=True)
+        else:
+            deadline = time.time() + 300
+            while not build.LIB.exists() and time.time() < deadline:
+                time.sleep(1.0)
+            time.sleep(2.0)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the perception path has no CPU implementation")
     # KS_BENCH_SHARE_GPU=1 (tests only): every rank uses device 0 and the collective runs on gloo, so the
