@@ -49,6 +49,8 @@ def make_scene(workload: str, env: int = 0):
         sc = scenes.config2()
     elif workload == "cfg3":
         sc = scenes.config3()
+    elif workload == "cfg4":
+        sc = scenes.config4()[0]
     elif workload == "cfg5env":
         sc = scenes.config5_env(env)
     else:
@@ -63,7 +65,8 @@ WORKLOAD_DESC = {
     "cfg1": "configs[0]: 640x480 depth frame into 1 m^3 at 1 cm (100^3 cells)",
     "cfg2": "configs[1]: 2 m^3 (2x1x1 m) workspace at 5 mm, 400x200x200 cells, one 640x480 depth camera + 3 cuboids, full ESDF every frame",
     "cfg3": "configs[2]: 1 m^3 at 2 mm, 500^3 cells, 4 depth cameras + 2 cuboids",
-    "cfg5env": "configs[4]: one 1.5x1x1 m environment at 5 mm (300x200x200 cells) per rank",
+    "cfg4": "configs[3]: configs[1] scene + sphere, 1 M batched distance+gradient queries per update",
+    "cfg5env": "configs[4]: independent 1.5x1x1 m environments at 5 mm (300x200x200 cells), --envs-per-gpu per rank",
 }
 
 
@@ -243,65 +246,124 @@ def run_ours(args):
         else:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
-    scene = make_scene(args.workload, env=rank)
-    nx, ny, nz = scene.esdf_dims
-    cells = nx * ny * nz
-    frames = [api.DepthFrame(f.width, f.height, *f.intr, f.R, f.t, f.depth) for f in scene.frames]
-    prims = [api.Cuboid(c.R, c.t, c.half_extents) for c in scene.cuboids] + \
-            [api.SphereShape(s.center, s.radius) for s in scene.spheres]
-    pixels = sum(f.width * f.height for f in frames)
+    from paper_2603_05493_b200 import multi_env
 
     stream = torch.cuda.Stream()
-    cfg = api.make_tsdf_config(scene.tsdf_voxel)
-    cfg.capacity = scene.capacity
-    tsdf = api.make_tsdf(cfg, stream.cuda_stream)
-    ecfg = api.EsdfConfig(tuple(scene.esdf_origin), nx, ny, nz, scene.esdf_voxel, "gather")
-    esdf = api.DenseEsdf(ecfg, stream.cuda_stream)
+    E_local = max(1, args.envs_per_gpu)
+    n_envs = world * E_local
+    env_lo, env_hi = multi_env.partition_envs(n_envs, world, rank)
+
+    class Environment:
+        """One independent scene: its own TSDF + ESDF handles, all on this rank's stream."""
+
+        def __init__(self, env_id):
+            self.env_id = env_id
+            queries = None
+            if args.workload == "cfg4":
+                from paper_2603_05493_b200 import scenes as _scenes
+                self.scene, queries = _scenes.config4()
+            else:
+                self.scene = make_scene(args.workload, env=env_id)
+            sc = self.scene
+            self.dims = sc.esdf_dims
+            self.frames = [api.DepthFrame(f.width, f.height, *f.intr, f.R, f.t, f.depth) for f in sc.frames]
+            self.prims = [api.Cuboid(c.R, c.t, c.half_extents) for c in sc.cuboids] + \
+                         [api.SphereShape(s.center, s.radius) for s in sc.spheres]
+            cfg = api.make_tsdf_config(sc.tsdf_voxel)
+            cfg.capacity = sc.capacity
+            self.tsdf = api.make_tsdf(cfg, stream.cuda_stream)
+            self.ecfg = api.EsdfConfig(tuple(sc.esdf_origin), *sc.esdf_dims, sc.esdf_voxel, "gather")
+            self.esdf = api.DenseEsdf(self.ecfg, stream.cuda_stream)
+            ext = np.array(sc.esdf_dims) * sc.esdf_voxel
+            probes = sc.esdf_origin + np.random.RandomState(3 + env_id).random_sample((4096, 3)) * ext
+            self.probes = torch.from_numpy(np.ascontiguousarray(probes)).cuda()
+            self.probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
+            self.queries = None
+            if queries is not None:  # configs[3]: 1 M batched distance + gradient queries per update
+                self.queries_host = queries
+                self.queries = torch.from_numpy(queries).cuda()
+                self.q_dist = torch.empty(len(queries), dtype=torch.float64, device="cuda")
+                self.q_grad = torch.empty((len(queries), 3), dtype=torch.float64, device="cuda")
+                self.q_inside = torch.empty(len(queries), dtype=torch.uint8, device="cuda")
+
+        def stage(self):
+            for slot, f in enumerate(self.frames):
+                self.tsdf.stage_frame(f, slot)
+
+        def enqueue_update(self, upload):
+            for slot in range(len(self.frames)):  # one staging slot per camera
+                if upload:
+                    self.tsdf.upload_frame_async(slot)
+                self.tsdf.integrate_async(slot)
+            for p in self.prims:
+                self.tsdf.stamp_async(p)
+            self.esdf.build_async(self.tsdf)
+            if self.queries is not None:
+                api._check(self.esdf.lib.ks_esdf_query_device_async(
+                    self.esdf.h, C.c_void_p(self.queries.data_ptr()), self.queries.shape[0], C.c_void_p(self.q_dist.data_ptr()),
+                    C.c_void_p(self.q_grad.data_ptr()), C.c_void_p(self.q_inside.data_ptr())))
+
+        def blocking_update(self):
+            k = 0
+            for f in self.frames:
+                k = api.integrate_depth(self.tsdf, f)          # pinned staging + H2D + 4 phases + D2H report
+            for p in self.prims:
+                api.stamp_primitive(self.tsdf, p)
+            api.build_esdf(self.tsdf, self.ecfg, self.esdf)
+            r = self.esdf.report()                              # D2H: has_sites / seed count
+            if self.queries is not None:
+                api.query(self.esdf, self.queries_host)         # H2D points, D2H distance + gradient + inside
+            return k, r.seed_count
+
+        def summary_into(self, row):
+            """collision summary of this environment: probe-sphere minimum distance and near-contact count"""
+            api._check(self.esdf.lib.ks_esdf_query_device_async(self.esdf.h, C.c_void_p(self.probes.data_ptr()), 4096,
+                                                               C.c_void_p(self.probe_d.data_ptr()), None, None))
+            row[0] = self.env_id
+            row[1] = self.probe_d.min()
+            row[2] = (self.probe_d < 0.02).sum()
+
+    envs = [Environment(e) for e in range(env_lo, env_hi)]
+    scene = envs[0].scene
+    nx, ny, nz = scene.esdf_dims
+    cells = nx * ny * nz
+    frames, prims = envs[0].frames, envs[0].prims
+    tsdf, esdf, ecfg = envs[0].tsdf, envs[0].esdf, envs[0].ecfg
+    pixels = sum(f.width * f.height for f in frames)
+    n_queries = 0 if envs[0].queries is None else int(envs[0].queries.shape[0])
+    exchange = world > 1 or E_local > 1
 
     def enqueue_update(upload: bool):
-        for slot in range(len(frames)):  # one staging slot per camera
-            if upload:
-                tsdf.upload_frame_async(slot)
-            tsdf.integrate_async(slot)
-        for p in prims:
-            tsdf.stamp_async(p)
-        esdf.build_async(tsdf)
+        for env in envs:
+            env.enqueue_update(upload)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    summary_in = torch.zeros(4, dtype=torch.float64, device="cuda")
-    summary_all = torch.zeros(4 * world, dtype=torch.float64, device="cuda")
-    probes = torch.from_numpy(np.ascontiguousarray(
-        scene.esdf_origin + np.random.RandomState(3).random_sample((4096, 3)) * np.array([nx, ny, nz]) * scene.esdf_voxel)).cuda()
-    probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
+    summary_local, summary_all, _valid_rows = multi_env.summary_buffers(n_envs, world, rank, "cuda")
 
     def gather_summaries():
-        """per-environment collision summary, all-gathered over NCCL (the only collective on this path)."""
-        api._check(esdf.lib.ks_esdf_query_device_async(esdf.h, C.c_void_p(probes.data_ptr()), 4096,
-                                                      C.c_void_p(probe_d.data_ptr()), None, None))
-        summary_in[0] = rank
-        summary_in[1] = probe_d.min()
-        summary_in[2] = (probe_d < 0.02).sum()
-        if world > 1:
-            if share_gpu:
-                host_all = torch.empty(4 * world, dtype=torch.float64)
-                dist.all_gather_into_tensor(host_all, summary_in.cpu())
-                summary_all.copy_(host_all)
-            else:
-                dist.all_gather_into_tensor(summary_all, summary_in)
+        """per-environment collision summaries, all-gathered over NCCL (the only collective on this path)."""
+        for i, env in enumerate(envs):
+            env.summary_into(summary_local[i])
+        if world > 1 and share_gpu:
+            host_all = torch.empty(summary_all.shape, dtype=torch.float64)
+            dist.all_gather_into_tensor(host_all, summary_local.cpu())
+            summary_all.copy_(host_all)
+        else:
+            multi_env.gather_summaries(summary_local, summary_all, world)
 
     with torch.cuda.stream(stream):
         # ---- eager warm-up (allocates blocks, binds the directory), then stage timings ---------------
-        for slot, f in enumerate(frames):
-            tsdf.stage_frame(f, slot)
+        for env in envs:
+            env.stage()
         enqueue_update(upload=True)
         rep = tsdf.sync()
         touched_last, live = rep.blocks_touched, rep.live_blocks
         tsdf.profile(True)
         esdf.profile(True)
         stage_acc = {}
-        for i in range(args.warmup + args.steps):
+        for i in range(args.warmup + min(args.steps, 20)):
             flush.zero_()
-            enqueue_update(upload=False)
+            envs[0].enqueue_update(False)
             st = {**tsdf.stage_ms(), **esdf.stage_ms()}
             if i >= args.warmup:
                 for k, v in st.items():
@@ -320,7 +382,7 @@ def run_ours(args):
         for _ in range(max(args.warmup, 50)):  # also gives the clock sampler a loaded GPU to look at
             flush.zero_()
             graph.launch()
-            if world > 1:
+            if exchange:
                 gather_summaries()
         stream.synchronize()
         if world > 1:
@@ -333,7 +395,7 @@ def run_ours(args):
             flush.zero_()  # L2 flush between timed iterations (outside the event pair)
             starts[i].record(stream)
             graph.launch()
-            if world > 1:
+            if exchange:
                 gather_summaries()
             ends[i].record(stream)
         torch.cuda.synchronize()
@@ -352,14 +414,8 @@ def run_ours(args):
 
         # ---- e2e: blocking drop-in calls with host buffers ------------------------------------------------
         def blocking_update():
-            k = 0
-            for f in frames:
-                k = api.integrate_depth(tsdf, f)          # pinned staging + H2D + 4 phases + D2H report
-            for p in prims:
-                api.stamp_primitive(tsdf, p)
-            api.build_esdf(tsdf, ecfg, esdf)
-            r = esdf.report()                              # D2H: has_sites / seed count
-            return k, r.seed_count
+            for env in envs:
+                env.blocking_update()
 
         for _ in range(args.warmup):
             blocking_update()
@@ -378,12 +434,14 @@ def run_ours(args):
         # ---- e2e through the graph API (stage + upload + replay + report), informational ----------------
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            for slot, f in enumerate(frames):
-                tsdf.stage_frame(f, slot)
-                tsdf.upload_frame_async(slot)
+            for env in envs:
+                env.stage()
+                for slot in range(len(env.frames)):
+                    env.tsdf.upload_frame_async(slot)
             graph.launch()
-            tsdf.sync()
-            esdf.report()
+            for env in envs:
+                env.tsdf.sync()
+                env.esdf.report()
         e2e_graph_s = time.perf_counter() - t0
 
     if rank != 0:
@@ -409,7 +467,7 @@ def run_ours(args):
         traffic = json.loads(traffic_path.read_text()).get(args.workload, {}).get(dominant)
     update_bytes = sum(stage_bytes[s] * (len(frames) if s in ("discover", "allocate", "integrate") else 1) for s in kernel_stages)
     ms_per_step = total_ms / args.steps
-    value = world * cells * args.steps / (total_ms * 1e-3)
+    value = n_envs * cells * args.steps / (total_ms * 1e-3)
 
     cpu_base = None
     if world == 1 and not args.no_cpu_baseline:
@@ -424,20 +482,22 @@ def run_ours(args):
                               f"{ {k: round(v, 3) for k, v in runs[0][1].items()} }; host {host_cpu_model()}",
                     "seconds_per_update": secs}
 
-    h2d = sum(f.width * f.height * 4 + 248 for f in frames)
+    h2d = E_local * (sum(f.width * f.height * 4 + 248 for f in frames) + 24 * n_queries)
+    d2h = E_local * (48 * (len(frames) + len(prims)) + 16 + 33 * n_queries)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.workload], "cells": cells, "tsdf_voxel_m": scene.tsdf_voxel,
                    "esdf_voxel_m": scene.esdf_voxel, "blocks_touched": touched_last, "live_blocks": live,
-                   "seeds": int(erep.seed_count), "environments": world, "execution": "cuda-graph replay",
+                   "seeds": int(erep.seed_count), "environments": n_envs, "environments_per_gpu": E_local,
+                   "queries_per_update": n_queries, "execution": "cuda-graph replay",
                    "l2": "flushed between timed steps (256 MiB memset outside the event pairs); per-step working set ~22 B/cell > 126 MB L2",
-                   "collective": "none" if world == 1 else "ncclAllGather of 32-byte per-environment summaries each step"},
+                   "collective": "none" if not exchange else "ncclAllGather of 32-byte per-environment summaries each step"},
         "clocks": clocks,
-        "e2e": {"value": world * cells * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 48 * (len(frames) + len(prims)) + 16,
+        "e2e": {"value": n_envs * cells * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": 1e3 * e2e_s / args.steps, "path": "blocking ks:: calls: integrate_depth(host frame) + stamp_primitive x%d + build_esdf + report" % len(prims)},
-        "e2e_graph": {"value": cells * args.steps / e2e_graph_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_graph_s / args.steps,
+        "e2e_graph": {"value": E_local * cells * args.steps / e2e_graph_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_graph_s / args.steps,
                       "path": "stage_frame + upload_frame_async + graph replay + sync/report"},
         "gpu_launches": int(kernel_nodes * args.steps),
         "graph": {"kernel_nodes": int(kernel_nodes), "all_nodes": int(all_nodes)},
@@ -460,6 +520,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--envs-per-gpu", type=int, default=1, help="independent environments per rank (cfg5: 128 / N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

@@ -194,6 +194,12 @@ def test_config2_full_size_against_oracle(oracle_lib):
     assert int(e.report().seed_count) == int(mask0.sum())
     assert np.array_equal(site, site0) and np.array_equal(dist, dist0)
     assert np.array_equal(np.signbit(dist), np.signbit(dist0))
+    # BASELINE configs[3]: one million batched distance + gradient queries on that field
+    rng = np.random.RandomState(7)
+    pts = scene.esdf_origin + rng.random_sample((1_000_000, 3)) * np.array(scene.esdf_dims) * scene.esdf_voxel
+    s = api.query(e, pts)
+    d0, g0, i0 = oracle_lib.query_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel, has0, dist0, pts)
+    assert same_bits(s.distance, d0) and same_bits(s.gradient, g0) and np.array_equal(s.inside, i0)
 
 
 # ---- error behaviour, lifecycle, graph replay -------------------------------------------------------------
