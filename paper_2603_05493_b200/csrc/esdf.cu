@@ -958,8 +958,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
     if (bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
-      KS_CUDA(cudaMemsetAsync(E.mbits, 0, plane_bytes, e->stream));
-      KS_CUDA(cudaMemsetAsync(E.gbits, 0, plane_bytes, e->stream));
+      KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * plane_bytes, e->stream));  // seed plane + geometry-near plane (contiguous)
       KS_LAUNCH(k_seed_gather_bricks, 6 * kSmCount, kGatherWarps * 32, 0, e->stream, E, tsdf_view(t));
     } else KS_LAUNCH(k_seed_gather<false>, grid, 256, 0, e->stream, E, tsdf_view(t));
   } else {
@@ -1051,8 +1050,8 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.brick, static_cast<size_t>(E.bnx) * E.bny * E.bnz));
   KS_CUDA(cudaMalloc(&E.active, static_cast<size_t>(E.bnx) * E.bny * E.bnz * sizeof(int)));
   E.wpr = (E.nx + 31) / 32;
-  KS_CUDA(cudaMalloc(&E.mbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
-  KS_CUDA(cudaMalloc(&E.gbits, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.mbits, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));  // both bit planes
+  E.gbits = E.mbits + static_cast<size_t>(E.wpr) * E.ny * E.nz;
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
@@ -1061,8 +1060,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.mbits, 0, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.gbits, 0, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
   KS_CUDA(cudaMemsetAsync(E.site, 0xFF, E.cells * sizeof(uint32_t), e->stream));  // no sites yet
   KS_CUDA(cudaMemsetAsync(E.d2s, 0xFF, E.cells * sizeof(uint32_t), e->stream));
   KS_CUDA(cudaStreamSynchronize(e->stream));
@@ -1074,7 +1072,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.gbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
