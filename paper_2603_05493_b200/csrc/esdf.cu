@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "edt_core.cuh"
+#include "edt_dc.cuh"
 
 namespace ksb {
 
@@ -635,6 +636,169 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
   }
 }
 
+// ---- phases 2 and 3 by monotone divide and conquer (edt_dc.cuh); used whenever the keys fit 32 bits ----
+// One CTA per tile of 32 rows, 2^warps_log2 warps.  G = packed candidates [position][32 rows].
+// Top levels (visits at the multiples of kTopStep): fewer visits than warps, so the windows are cut into
+// slices whose minima meet in Kt through atomicMin, one barrier per level.  Below them every warp
+// resolves whole stretches of kTopStep positions on its own (edt_dc::subtree), no barrier.
+using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
+using KeysX = edt_dc::Keys<0>;
+constexpr int kTopShift = 5, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+
+template <int kPay>
+__device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, int n, int warp, int lane, int warps_log2) {
+  const edt_dc::Plan plan = edt_dc::make_plan(n);
+  for (int level = 0; level < plan.levels; ++level) {
+    const int s = edt_dc::level_step(plan, level);
+    if (s < kTopStep) break;
+    const int parts_log2 = warps_log2 > level ? warps_log2 - level : 0;
+    const int items = edt_dc::level_visits(plan, level) << parts_log2;
+    for (int item = warp; item < items; item += 1 << warps_log2) {
+      const int tp = s * (2 * (item >> parts_log2) + 1);
+      int lo, len;
+      edt_dc::top_window<kPay>(Kt, n, kTopShift, tp, s, item & ((1 << parts_log2) - 1), parts_log2, lane, lo, len);
+      const int longest = __reduce_max_sync(0xFFFFFFFFu, len);
+      if (longest <= 0) continue;
+      const uint32_t key = edt_dc::scan<kPay>(G, edt_dc::clamp_start(lo, longest, n), longest, tp - 1, lane);
+      if (parts_log2 != 0) atomicMin(Kt + edt_dc::at(tp >> kTopShift, lane), key);
+      else Kt[edt_dc::at(tp >> kTopShift, lane)] = key;
+    }
+    __syncthreads();
+  }
+}
+
+// stretch j = positions t' in (j*kTopStep, (j+1)*kTopStep]; emit(t, key) sees each of them once
+template <int kPay, class Emit>
+__device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt, int n, int j, int lane, Emit&& emit) {
+  const int a = j << kTopShift;
+  const bool closed = a + kTopStep <= n;
+  const uint32_t right = closed ? Kt[edt_dc::at(j + 1, lane)] : 0u;
+  const int lo_w = a > 0 ? edt_dc::Keys<kPay>::winner(Kt[edt_dc::at(j, lane)]) : 0;
+  const int hi_w = closed ? edt_dc::Keys<kPay>::winner(right) : n - 1;
+  edt_dc::subtree<kPay, kSubStep>(G, n, a + kSubStep, lo_w, hi_w, lane,
+                                  [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); }, emit);
+  if (closed) emit(a + kTopStep - 1, right);
+}
+
+static size_t dc_top_bytes(int n) { return static_cast<size_t>((n >> kTopShift) + 1) * 32 * sizeof(uint32_t); }
+static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n); }
+static size_t dc_smem_bytes_x(int n) { return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n); }
+
+// root of a perfect square below 2^24 (one MUFU; its error of a few ulp cannot reach the next integer)
+__device__ __forceinline__ int exact_root(int sq) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(sq)));
+  return __float2int_rn(r);
+}
+
+// grid = (ceil(nx/32), nz); lane <-> x, positions = y.  Output = the winning key itself
+// (in-plane d2 << 11 | site_y << 1 | seed above z), which is what phase 3 consumes.
+constexpr int kLoadBatch = 8;
+__global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
+  const int x = blockIdx.x * 32 + lane, z = blockIdx.y;
+  const int ny = E.ny, nx = E.nx;
+  uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
+  uint32_t* Kt = G + ny * 32;
+  const int zoff = nx * ny * z + min(x, nx - 1);
+  const bool live = x < nx;
+  for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
+    uint16_t v[kLoadBatch];
+#pragma unroll
+    for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(E.near_z + zoff + nx * min(yb + i, ny - 1));
+#pragma unroll
+    for (int i = 0; i < kLoadBatch; ++i) {
+      const int y = yb + i;
+      const int dz = static_cast<int>(v[i]) - z;
+      const uint32_t g = (v[i] == edt::kNone || !live) ? KeysY::pack(none_y, y, 0)
+                                                        : KeysY::pack(static_cast<uint32_t>(dz * dz), y, dz > 0 ? 1u : 0u);
+      if (y < ny) G[edt_dc::at(y, lane)] = g;
+    }
+  }
+  for (int i = warp; i <= ny >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
+  __syncthreads();
+  dc_top_levels<1>(G, Kt, ny, warp, lane, warps_log2);
+  uint32_t* out = E.yz + nx * ny * z + x;
+  for (int j = warp; (j << kTopShift) < ny; j += nwarps)
+    dc_stretch<1>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
+      if (live) out[nx * y] = k;
+    });
+}
+
+// grid = (ceil(ny/32), nz); lane <-> y, positions = x.  The x-fastest input rows (phase 2's keys) are
+// loaded coalesced into K with a bank rotation and packed into G in the [x][lane] layout.  kSigns as in
+// k_sweep_x.  A warp colours each stretch right after resolving it, walking x upwards so that what
+// depends only on the site is reused while the winner stays the same.
+template <int kSigns>
+__global__ void __launch_bounds__(512) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
+  const int y0 = blockIdx.x * 32, z = blockIdx.y;
+  const int nx = E.nx, ny = E.ny;
+  uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
+  uint32_t* K = G + nx * 32;
+  uint32_t* Kt = K + nx * 32;
+  const int zoff = nx * ny * z;
+  for (int r = warp; r < 32; r += nwarps) {
+    const uint32_t* row = E.yz + zoff + nx * min(y0 + r, ny - 1);
+    const uint32_t dead = y0 + r < ny ? 0u : 0xFFFFFFFFu;
+    for (int xb = lane; xb < nx; xb += 32 * kLoadBatch) {
+      uint32_t v[kLoadBatch];
+#pragma unroll
+      for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(row + min(xb + 32 * i, nx - 1));
+#pragma unroll
+      for (int i = 0; i < kLoadBatch; ++i) {
+        const int x = xb + 32 * i;
+        if (x < nx) K[x * 32 + ((r + x) & 31)] = v[i] | dead;
+      }
+    }
+  }
+  for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
+  __syncthreads();
+  const int y = y0 + lane;
+  for (int x = warp; x < nx; x += nwarps) {
+    const uint32_t r2 = KeysY::cost(K[x * 32 + ((lane + x) & 31)]);  // in-plane d2 of the candidate at x
+    G[edt_dc::at(x, lane)] = KeysX::pack(r2 >= none_y ? none_x : r2, x, 0);
+  }
+  __syncthreads();
+  dc_top_levels<0>(G, Kt, nx, warp, lane, warps_log2);
+  SignProbe probe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
+  const uint32_t* yzrow = E.yz + zoff + nx * min(y, ny - 1);
+  const int obase = y + ny * nx * z;
+  for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
+    dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
+    if (y >= ny) continue;
+    const int end = min((j + 1) << kTopShift, nx);
+    int last = -1;
+    uint32_t site = kSiteNone;
+    for (int x = j << kTopShift; x < end; ++x) {
+      const uint32_t k = K[edt_dc::at(x, lane)];
+      const int o = obase + ny * x;
+      if (KeysX::cost(k) >= none_x) {  // the row holds no candidate at all
+        E.site[o] = kSiteNone;
+        E.d2s[o] = kD2None;
+        continue;
+      }
+      const int u = KeysX::winner(k);
+      if (u != last) {
+        last = u;
+        const uint32_t v = __ldg(yzrow + u);  // phase 2's key at the winning x
+        const int sy = KeysY::winner(v);
+        const int dy = y - sy;
+        const int dz = exact_root(static_cast<int>(KeysY::cost(v)) - dy * dy);
+        const int sz = KeysY::payload(v) ? z + dz : z - dz;
+        site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+        if (kSigns) probe.template set_site<kSigns == 2>(u, sy, sz);
+      }
+      uint32_t d2 = KeysX::cost(k);
+      if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
+      E.site[o] = site;
+      E.d2s[o] = d2;
+    }
+  }
+}
+
 // ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -878,6 +1042,9 @@ struct ks_esdf {
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
+  bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
+  int dc_wl_y, dc_wl_x;    // log2(warps per tile)
+  uint32_t none_y, none_x; // offsets of positions without candidate
   int sticky_err;
   bool profile, profile_stages;
   cudaEvent_t ev[7];
@@ -980,10 +1147,16 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
-  KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
+  if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + 31) / 32, E.nz), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
+  else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
-  if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
+  if (e->dc) {
+    const unsigned threads = 32u << e->dc_wl_x;
+    if (t && bits) KS_LAUNCH(k_sweep_x_dc<2>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
+    else if (t) KS_LAUNCH(k_sweep_x_dc<1>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
+    else KS_LAUNCH(k_sweep_x_dc<0>, xgrid, threads, e->smem_x, e->stream, E, TsdfView{}, e->dc_wl_x, e->none_y, e->none_x);
+  } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
     KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
   } else if (t) {
     KS_LAUNCH(k_sweep_x<1>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
@@ -1030,6 +1203,18 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   pick_bands(E.nx, e->band_x, e->bands_x);
   e->smem_y = sweep_smem_bytes(E.ny, e->bands_y, 2);
   e->smem_x = sweep_smem_bytes(E.nx, e->bands_x, 4);
+  {  // divide-and-conquer sweeps whenever their 32-bit keys hold every reachable cost (all dims <= ~830, or a long x axis)
+    const uint32_t gmax_y = static_cast<uint32_t>((E.nz - 1) * (E.nz - 1));
+    const uint32_t gmax_x = gmax_y + static_cast<uint32_t>((E.ny - 1) * (E.ny - 1));
+    e->dc = KeysY::fits(E.ny, gmax_y) && KeysX::fits(E.nx, gmax_x) && dc_smem_bytes_x(E.nx) <= 227 * 1024 && dc_smem_bytes_y(E.ny) <= 227 * 1024;
+    if (const char* v = std::getenv("KS_SWEEP")) e->dc = e->dc && std::strcmp(v, "stack") != 0;
+    e->none_y = KeysY::none_offset(E.ny, gmax_y);
+    e->none_x = KeysX::none_offset(E.nx, gmax_x);
+    e->dc_wl_y = 3, e->dc_wl_x = 4;
+    if (const char* v = std::getenv("KS_DC_WARPS_Y")) e->dc_wl_y = std::min(4, std::max(0, std::atoi(v)));
+    if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(4, std::max(0, std::atoi(v)));
+    if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx);
+  }
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
     delete e;
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
@@ -1038,6 +1223,10 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
