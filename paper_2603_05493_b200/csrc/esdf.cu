@@ -17,6 +17,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -61,6 +62,20 @@ struct EsdfView {
   uint32_t* mbits;   // [nz][ny][wpr] the same mask, one bit per cell -- fused build path
   uint32_t* gbits;   // [nz][ny][wpr] seed cells with stamped geometry within one cell (sign probes can resolve)
   int wpr;           // words per x row
+  // "resampled" seeding (fused build when the dilation identity holds, see bind_tsdf): the TSDF digest bits at
+  // every cell centre's own voxel, on the grid extended by one cell per side (cell i <-> index i + 1)
+  int wpr2;            // words per extended x row
+  int* voxe;           // [nx+2 | ny+2 | nz+2] directory-relative voxel of the extended cell centres
+  uint32_t* cbits;     // [(nz+2)][(ny+2)][wpr2] surface bit of the centre voxel
+  uint32_t* obits;     // same layout: combined sdf at the cell centre exists and is negative (sign fallback)
+  uint32_t* nbits;     // same layout: a stamped block lies within one block of the centre voxel's block
+  uint32_t* xplus;     // [wpr] bit x: the +ve/2 probe of cell x leaves the centre voxel (esdf.hpp:106-108) ...
+  uint32_t* xminus;    // [wpr] ... and the -ve/2 probe
+  uint8_t* yzflags;    // [ny | nz] bit0 / bit1: the same for the y and z probes of that row
+  uint8_t* dirs;       // [dcount] 1 when the entry's block holds stamped geometry (0 / 0xFF otherwise)
+  uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
+  uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
+                       // at the 27 voxels around the site's centre voxel, bit = (ox+1) + 3(oy+1) + 9(oz+1)
   uint16_t* near_z;  // [cells] x-fastest phase-1 result
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
   uint32_t* site;    // [cells] y-fastest
@@ -118,6 +133,7 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
     bx -= E.dlo[0], by -= E.dlo[1], bz -= E.dlo[2];
     if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
     E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
+    E.dirs[bx + E.dn[0] * (by + E.dn[1] * bz)] = T.pool_geom[p];
     uint32_t any = 0;
 #pragma unroll
     for (int w = 0; w < 16; ++w) any |= T.digest[p * kDigestWords + w];
@@ -323,6 +339,154 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfVi
   }
 }
 
+// ---- seed_gather as resample + dilate (fused build, when bind_tsdf validated the identity) ----
+// With ve <= tsdf voxel the probe at centre +- ve/2 lands either in the centre's own voxel or in the
+// voxel of the neighbouring cell's centre (checked exactly, per axis position, against the per-axis
+// tables).  Then  seed = C | (C shifted along +-x, y, z, where the probe leaves the voxel)  with
+// C = surface bit of the centre voxel: one digest bit per cell and a handful of word operations per
+// 32 cells instead of seven probes per cell.
+__global__ void __launch_bounds__(256) k_dir_geom(EsdfView E) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E.dcount) return;
+  const int bx = i % E.dn[0], by = (i / E.dn[0]) % E.dn[1], bz = i / (E.dn[0] * E.dn[1]);
+  uint8_t any = 0;
+  for (int z = max(bz - 1, 0); z <= min(bz + 1, E.dn[2] - 1); ++z)
+    for (int y = max(by - 1, 0); y <= min(by + 1, E.dn[1] - 1); ++y)
+      for (int x = max(bx - 1, 0); x <= min(bx + 1, E.dn[0] - 1); ++x) any |= E.dirs[x + E.dn[0] * (y + E.dn[1] * z)] == 1;
+  E.dirg[i] = any;
+}
+
+// One warp per extended (y, z) row.  Step 1, lane <-> block column: the row's voxel-space bits (surface,
+// own-sign, geometry-near), one byte per block, into the warp's slice of shared memory; most rows cross no
+// live block and end there.  Step 2, lane <-> cell: every cell picks the bit of its centre voxel.
+constexpr int kResampleWarps = 8;
+constexpr int kMaxDirX = (kMaxDim + 2) / 8 + 8;
+__global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView E, TsdfView T) {
+  __shared__ uint8_t s_bits[kResampleWarps][3][kMaxDirX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ey = E.ny + 2, ez = E.nz + 2;
+  const int row = blockIdx.x * kResampleWarps + warp;
+  if (row >= ey * ez) return;
+  const int yi = row % ey, zi = row / ey;
+  const int vy = E.voxe[(E.nx + 2) + yi], vz = E.voxe[(E.nx + 2) + ey + zi];
+  const int ly = vy & 7, lz = vz & 7;
+  const int drow = E.dn[0] * ((vy >> 3) + E.dn[1] * (vz >> 3));
+  uint8_t(*S)[kMaxDirX] = s_bits[warp];
+  bool any = false;
+  for (int b = lane; b < E.dn[0]; b += 32) {
+    const int pool = __ldg(E.dir + drow + b);
+    uint32_t sb = 0, ob = 0;
+    if (pool >= 0) {
+      const uint32_t* dg = T.digest + pool * kDigestWords;
+      sb = (__ldg(dg + 2 * lz + (ly >> 2)) >> (8 * (ly & 3))) & 0xFFu;
+      const uint32_t pairs = (__ldg(dg + kDigestComb + 4 * lz + (ly >> 1)) >> (16 * (ly & 1))) & 0xFFFFu;
+      uint32_t both = pairs & (pairs >> 1) & 0x5555u;  // bit 2k: voxel k has a value and it is negative
+      both = (both | both >> 1) & 0x3333u;
+      both = (both | both >> 2) & 0x0F0Fu;
+      ob = (both | both >> 4) & 0xFFu;
+    }
+    const uint8_t nb = E.dirg[drow + b] ? 0xFFu : 0u;
+    S[0][b] = static_cast<uint8_t>(sb), S[1][b] = static_cast<uint8_t>(ob), S[2][b] = nb;
+    any |= (sb | ob | nb) != 0;
+  }
+  any = __any_sync(0xFFFFFFFFu, any);
+  uint32_t* out = E.cbits + row * E.wpr2;
+  const size_t plane = static_cast<size_t>(E.wpr2) * ey * ez;
+  if (!any) {
+    for (int w = lane; w < E.wpr2; w += 32) out[w] = 0u, out[plane + w] = 0u, out[2 * plane + w] = 0u;
+    return;
+  }
+  __syncwarp();
+  for (int w = 0; w < E.wpr2; ++w) {
+    const int xi = 32 * w + lane;
+    bool c = false, o = false, n = false;
+    if (xi < E.nx + 2) {
+      const int vx = E.voxe[xi];
+      const int b = vx >> 3, k = vx & 7;
+      c = (S[0][b] >> k) & 1, o = (S[1][b] >> k) & 1, n = S[2][b] != 0;
+    }
+    const uint32_t cw = __ballot_sync(0xFFFFFFFFu, c), ow = __ballot_sync(0xFFFFFFFFu, o), nw = __ballot_sync(0xFFFFFFFFu, n);
+    if (lane == 0) out[w] = cw, out[plane + w] = ow, out[2 * plane + w] = nw;
+  }
+}
+
+// one thread per word of the seed plane
+__global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int words = E.wpr * E.ny * E.nz;
+  unsigned count = 0;
+  if (i < words) {
+    const int xw = i % E.wpr, row = i / E.wpr;
+    const int y = row % E.ny, z = row / E.ny;
+    const int ey = E.ny + 2;
+    auto ext = [&](const uint32_t* plane, int yy, int zz) -> uint64_t {  // extended bits 32xw .. 32xw+63 of row (yy, zz)
+      const uint32_t* r = plane + ((zz + 1) * ey + (yy + 1)) * E.wpr2 + xw;
+      return static_cast<uint64_t>(r[0]) | (xw + 1 < E.wpr2 ? static_cast<uint64_t>(r[1]) << 32 : 0ull);
+    };
+    const uint64_t w = ext(E.cbits, y, z);  // bit k = cell 32xw + k - 1
+    const uint8_t fy = E.yzflags[y], fz = E.yzflags[E.ny + z];
+    uint32_t seed = static_cast<uint32_t>(w >> 1) | (static_cast<uint32_t>(w >> 2) & E.xplus[xw]) | (static_cast<uint32_t>(w) & E.xminus[xw]);
+    if (fy & 1) seed |= static_cast<uint32_t>(ext(E.cbits, y + 1, z) >> 1);
+    if (fy & 2) seed |= static_cast<uint32_t>(ext(E.cbits, y - 1, z) >> 1);
+    if (fz & 1) seed |= static_cast<uint32_t>(ext(E.cbits, y, z + 1) >> 1);
+    if (fz & 2) seed |= static_cast<uint32_t>(ext(E.cbits, y, z - 1) >> 1);
+    const int rest = E.nx - 32 * xw;
+    if (rest < 32) seed &= (1u << rest) - 1u;
+    E.mbits[i] = seed;
+    E.gbits[i] = seed & static_cast<uint32_t>(ext(E.nbits, y, z) >> 1);
+    count = __popc(seed);
+  }
+  for (int d = 16; d > 0; d >>= 1) count += __shfl_down_sync(0xFFFFFFFFu, count, d);
+  if ((threadIdx.x & 31) == 0 && count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(count));
+}
+
+// Per-site sign tables: for every seed the geometry pairs {has value, negative} of the 27 voxels around its
+// centre voxel (the only voxels a sign probe from that site can land in when ve <= v), read as 9 x-rows of
+// three voxels from the digest's pair plane; all zero when no stamped block is in reach (gbits clear).
+// One thread looks at one word of the seed plane; the warp then serves its non-empty words one after the
+// other, lane <-> seed.
+__global__ void __launch_bounds__(256) k_site_tables(EsdfView E, TsdfView T) {
+  const int word = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int words = E.wpr * E.ny * E.nz;
+  const uint32_t mine = word < words ? E.mbits[word] : 0u;
+  uint32_t pending = __ballot_sync(0xFFFFFFFFu, mine != 0);
+  while (pending != 0) {
+    const int src = __ffs(static_cast<int>(pending)) - 1;
+    pending &= pending - 1;
+    const int w = word - lane + src;
+    const uint32_t seeds = __shfl_sync(0xFFFFFFFFu, mine, src);
+    if (!((seeds >> lane) & 1u)) continue;
+    const int xw = w % E.wpr, row = w / E.wpr;
+    const int y = row % E.ny, z = row / E.ny;
+    const int x = 32 * xw + lane;
+    uint32_t has = 0, neg = 0;
+    if ((E.gbits[w] >> lane) & 1u) {
+      const int vx = E.vox[x], vy0 = E.vox[E.nx + y], vz0 = E.vox[E.nx + E.ny + z];
+      const int bxa = (vx - 1) >> 3, bxm = vx >> 3, bxb = (vx + 1) >> 3;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const int vy = vy0 + r % 3 - 1, vz = vz0 + r / 3 - 1;
+        const int drow = E.dn[0] * ((vy >> 3) + E.dn[1] * (vz >> 3));
+        const int dword = kDigestGeom + 4 * (vz & 7) + ((vy & 7) >> 1), shift = 16 * (vy & 1);
+        const int pa = __ldg(E.dir + drow + bxa);
+        const uint32_t wa = pa >= 0 ? (__ldg(T.digest + pa * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
+        uint32_t wb = wa;
+        if (bxb != bxa) {
+          const int pb = __ldg(E.dir + drow + bxb);
+          wb = pb >= 0 ? (__ldg(T.digest + pb * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
+        }
+        const uint32_t g0 = (wa >> (2 * ((vx - 1) & 7))) & 3u;
+        const uint32_t g1 = ((bxm == bxa ? wa : wb) >> (2 * (vx & 7))) & 3u;
+        const uint32_t g2 = (wb >> (2 * ((vx + 1) & 7))) & 3u;
+        has |= ((g0 & 1u) | (g1 & 1u) << 1 | (g2 & 1u) << 2) << (3 * r);
+        neg |= ((g0 >> 1) | (g1 >> 1) << 1 | (g2 >> 1) << 2) << (3 * r);
+      }
+    }
+    E.gtab[x + E.nx * row] = make_uint2(has, neg);
+  }
+}
+
 // ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
 __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
   const int bound = T.ctrl->next_fresh;
@@ -502,6 +666,50 @@ struct SignProbe {
   }
 };
 
+// The same decision from per-site tables (fused build with resampled seeding, ve <= tsdf voxel): the probe
+// voxel is the site's centre voxel plus an offset in {-1,0,1}^3, and k_site_tables stored the geometry pair
+// of those 27 voxels for every seed (all zero when no stamped block is in reach); the fallback is one bit
+// of the own-sign plane.  The offset comes from the fp32 estimate when it is certified, else the cell takes
+// SignProbe's exact path.  No directory or digest access per cell.
+struct SignTable {
+  const EsdfView& E;
+  SignProbe exact;
+  int y, z;
+  int sx, sy, sz;
+  uint2 tab;
+  float qx, qy, qz;
+
+  __device__ __forceinline__ SignTable(const EsdfView& E_, const TsdfView& T_, int y_, int z_) : E(E_), exact(E_, T_, y_, z_) {
+    y = y_, z = z_;
+    sx = sy = sz = -1;
+    tab = make_uint2(0u, 0u);
+  }
+  __device__ __forceinline__ void set_site(int sx_, int sy_, int sz_, uint2 tab_) {
+    sx = sx_, sy = sy_, sz = sz_, tab = tab_;
+    if (tab.x != 0) qx = E.qsf[sx], qy = E.qsf[E.nx + sy], qz = E.qsf[E.nx + E.ny + sz];
+  }
+  // own: the cell's bit of the own-sign plane
+  __device__ __forceinline__ bool negative(int x, bool own) {
+    const int dx = x - sx, dy = y - sy, dz = z - sz;
+    if (tab.x != 0 && (dx | dy | dz) != 0) {
+      const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+      const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
+      const float ox = qx + fx * rinv, oy = qy + fy * rinv, oz = qz + fz * rinv;
+      const float tol = 4e-6f * (1.0f + E.ratio);
+      const bool sure = (dx == 0 || fabsf(ox - rintf(ox)) > tol) && (dy == 0 || fabsf(oy - rintf(oy)) > tol) &&
+                        (dz == 0 || fabsf(oz - rintf(oz)) > tol);
+      if (!sure) {  // the reference's arithmetic, operation by operation
+        exact.template set_site<false>(sx, sy, sz);
+        return exact.template negative<false>(x);
+      }
+      const int idx = (dx == 0 ? 1 : __float2int_rd(ox) + 1) + 3 * (dy == 0 ? 1 : __float2int_rd(oy) + 1) +
+                      9 * (dz == 0 ? 1 : __float2int_rd(oz) + 1);
+      if ((tab.x >> idx) & 1u) return ((tab.y >> idx) & 1u) != 0;  // query_tsdf_geom has a value: its sign decides
+    }
+    return own;  // combined sdf at the cell's own centre (esdf.hpp:309-312)
+  }
+};
+
 // ---- phases 2 and 3: banded lower-envelope sweeps (esdf.hpp:236-280), see edt_core.cuh ----
 __device__ __forceinline__ edt::RowTile carve_tile(unsigned char* base, int n, int band, int bands, size_t in_bytes) {
   edt::RowTile T;
@@ -644,6 +852,10 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
 using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
 using KeysX = edt_dc::Keys<0>;
 constexpr int kTopShift = 5, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+// The 32 rows of a tile are 8 neighbours along the fast axis x 4 along z: all lanes scan as far as the
+// lane with the longest window, and compact tiles cross a Voronoi boundary at fewer positions than
+// 32 x 1 ones (29 % fewer evaluations at cfg2); 8 x 4 also divides the BASELINE grids without padding.
+constexpr int kTileA = 8, kTileZ = 4;
 
 template <int kPay>
 __device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, int n, int warp, int lane, int warps_log2) {
@@ -675,9 +887,13 @@ __device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt
   const uint32_t right = closed ? Kt[edt_dc::at(j + 1, lane)] : 0u;
   const int lo_w = a > 0 ? edt_dc::Keys<kPay>::winner(Kt[edt_dc::at(j, lane)]) : 0;
   const int hi_w = closed ? edt_dc::Keys<kPay>::winner(right) : n - 1;
-  edt_dc::subtree<kPay, kSubStep>(G, n, a + kSubStep, lo_w, hi_w, lane,
-                                  [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); }, emit);
-  if (closed) emit(a + kTopStep - 1, right);
+  auto wmax = [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); };
+  if (closed) {
+    edt_dc::subtree<kPay, kSubStep, true>(G, n, a + kSubStep, lo_w, hi_w, lane, wmax, emit);
+    emit(a + kTopStep - 1, right);
+  } else {
+    edt_dc::subtree<kPay, kSubStep, false>(G, n, a + kSubStep, lo_w, hi_w, lane, wmax, emit);
+  }
 }
 
 static size_t dc_top_bytes(int n) { return static_cast<size_t>((n >> kTopShift) + 1) * 32 * sizeof(uint32_t); }
@@ -691,18 +907,18 @@ __device__ __forceinline__ int exact_root(int sq) {
   return __float2int_rn(r);
 }
 
-// grid = (ceil(nx/32), nz); lane <-> x, positions = y.  Output = the winning key itself
+// grid = (ceil(nx/8), ceil(nz/4)); lane <-> (x, z), positions = y.  Output = the winning key itself
 // (in-plane d2 << 11 | site_y << 1 | seed above z), which is what phase 3 consumes.
 constexpr int kLoadBatch = 8;
 __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
-  const int x = blockIdx.x * 32 + lane, z = blockIdx.y;
+  const int x = blockIdx.x * kTileA + (lane & (kTileA - 1)), z = blockIdx.y * kTileZ + lane / kTileA;
   const int ny = E.ny, nx = E.nx;
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
   uint32_t* Kt = G + ny * 32;
-  const int zoff = nx * ny * z + min(x, nx - 1);
-  const bool live = x < nx;
+  const bool live = x < nx && z < E.nz;
+  const int zoff = nx * ny * min(z, E.nz - 1) + min(x, nx - 1);
   for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
     uint16_t v[kLoadBatch];
 #pragma unroll
@@ -719,30 +935,30 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   for (int i = warp; i <= ny >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   __syncthreads();
   dc_top_levels<1>(G, Kt, ny, warp, lane, warps_log2);
-  uint32_t* out = E.yz + nx * ny * z + x;
+  uint32_t* out = E.yz + zoff;
   for (int j = warp; (j << kTopShift) < ny; j += nwarps)
     dc_stretch<1>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
       if (live) out[nx * y] = k;
     });
 }
 
-// grid = (ceil(ny/32), nz); lane <-> y, positions = x.  The x-fastest input rows (phase 2's keys) are
+// grid = (ceil(ny/8), ceil(nz/4)); lane <-> (y, z), positions = x.  The x-fastest input rows (phase 2's keys) are
 // loaded coalesced into K with a bank rotation and packed into G in the [x][lane] layout.  kSigns as in
-// k_sweep_x.  A warp colours each stretch right after resolving it, walking x upwards so that what
+// k_sweep_x, 3 = from the per-site tables of the resampled seeding.  A warp colours each stretch right after resolving it, walking x upwards so that what
 // depends only on the site is reused while the winner stays the same.
 template <int kSigns>
-__global__ void __launch_bounds__(512) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
+__global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
-  const int y0 = blockIdx.x * 32, z = blockIdx.y;
+  const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
   const int nx = E.nx, ny = E.ny;
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
   uint32_t* K = G + nx * 32;
   uint32_t* Kt = K + nx * 32;
-  const int zoff = nx * ny * z;
   for (int r = warp; r < 32; r += nwarps) {
-    const uint32_t* row = E.yz + zoff + nx * min(y0 + r, ny - 1);
-    const uint32_t dead = y0 + r < ny ? 0u : 0xFFFFFFFFu;
+    const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
+    const uint32_t* row = E.yz + nx * (min(yr, ny - 1) + ny * min(zr, E.nz - 1));
+    const uint32_t dead = yr < ny && zr < E.nz ? 0u : 0xFFFFFFFFu;
     for (int xb = lane; xb < nx; xb += 32 * kLoadBatch) {
       uint32_t v[kLoadBatch];
 #pragma unroll
@@ -756,45 +972,103 @@ __global__ void __launch_bounds__(512) k_sweep_x_dc(EsdfView E, TsdfView Tw, int
   }
   for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   __syncthreads();
-  const int y = y0 + lane;
+  const int y = y0 + (lane & (kTileA - 1)), z = min(z0 + lane / kTileA, E.nz - 1);
+  const bool live = y < ny && z0 + lane / kTileA < E.nz;
+  const int zoff = nx * ny * z;
   for (int x = warp; x < nx; x += nwarps) {
     const uint32_t r2 = KeysY::cost(K[x * 32 + ((lane + x) & 31)]);  // in-plane d2 of the candidate at x
     G[edt_dc::at(x, lane)] = KeysX::pack(r2 >= none_y ? none_x : r2, x, 0);
   }
   __syncthreads();
   dc_top_levels<0>(G, Kt, nx, warp, lane, warps_log2);
-  SignProbe probe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
   const uint32_t* yzrow = E.yz + zoff + nx * min(y, ny - 1);
   const int obase = y + ny * nx * z;
-  for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-    dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
-    if (y >= ny) continue;
-    const int end = min((j + 1) << kTopShift, nx);
-    int last = -1;
-    uint32_t site = kSiteNone;
-    for (int x = j << kTopShift; x < end; ++x) {
-      const uint32_t k = K[edt_dc::at(x, lane)];
-      const int o = obase + ny * x;
-      if (KeysX::cost(k) >= none_x) {  // the row holds no candidate at all
-        E.site[o] = kSiteNone;
-        E.d2s[o] = kD2None;
+  if constexpr (kSigns == 3) {
+    SignTable probe(E, Tw, min(y, ny - 1), z);
+    const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
+    const uint2* gplane = E.gtab + nx * ny * z;
+    for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
+      dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
+      if (!live) continue;
+      const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
+      uint32_t* sp = E.site + obase + ny * x0;
+      uint32_t* dp = E.d2s + obase + ny * x0;
+      if (KeysX::cost(K[edt_dc::at(x0, lane)]) >= none_x) {  // the row holds no candidate at all
+        for (int x = x0; x < end; ++x, sp += ny, dp += ny) *sp = kSiteNone, *dp = kD2None;
         continue;
       }
-      const int u = KeysX::winner(k);
-      if (u != last) {
-        last = u;
-        const uint32_t v = __ldg(yzrow + u);  // phase 2's key at the winning x
-        const int sy = KeysY::winner(v);
-        const int dy = y - sy;
-        const int dz = exact_root(static_cast<int>(KeysY::cost(v)) - dy * dy);
-        const int sz = KeysY::payload(v) ? z + dz : z - dz;
-        site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-        if (kSigns) probe.template set_site<kSigns == 2>(u, sy, sz);
+      // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
+      const uint32_t own_lo = orow[j], own_hi = j + 1 < E.wpr2 ? orow[j + 1] : 0u;
+      const uint32_t own = __funnelshift_r(own_lo, own_hi, 1);
+      int last = -1;
+      uint32_t site = kSiteNone;
+      for (int xb = x0; xb < end; xb += 4) {  // four cells at a time: their gathers are in flight together
+        uint32_t k[4], v[4], st[4];
+        uint2 tb[4];
+        int u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) k[i] = K[edt_dc::at(min(xb + i, end - 1), lane)], u[i] = KeysX::winner(k[i]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = __ldg(yzrow + u[i]);  // phase 2's key at the winning x
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int sy = KeysY::winner(v[i]);
+          const int dy = y - sy;
+          const int dz = exact_root(static_cast<int>(KeysY::cost(v[i])) - dy * dy);
+          const int sz = KeysY::payload(v[i]) ? z + dz : z - dz;
+          st[i] = static_cast<uint32_t>(u[i]) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+          tb[i] = __ldg(E.gtab + (u[i] + nx * (sy + ny * sz)));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int x = xb + i;
+          if (x >= end) break;
+          if (u[i] != last) {
+            last = u[i], site = st[i];
+            probe.set_site(u[i], static_cast<int>((site >> 10) & 1023u), static_cast<int>(site >> 20), tb[i]);
+          }
+          uint32_t d2 = KeysX::cost(k[i]);
+          if (probe.negative(x, ((own >> (x - x0)) & 1u) != 0)) d2 |= 0x80000000u;
+          *sp = site, *dp = d2;
+          sp += ny, dp += ny;
+        }
       }
-      uint32_t d2 = KeysX::cost(k);
-      if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
-      E.site[o] = site;
-      E.d2s[o] = d2;
+    }
+    (void)gplane;
+  } else {
+    SignProbe probe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
+    for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
+      dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
+      if (!live) continue;
+      const int end = min((j + 1) << kTopShift, nx);
+      int last = -1;
+      uint32_t site = kSiteNone;
+      for (int x = j << kTopShift; x < end; ++x) {
+        const uint32_t k = K[edt_dc::at(x, lane)];
+        const int o = obase + ny * x;
+        if (KeysX::cost(k) >= none_x) {  // the row holds no candidate at all
+          E.site[o] = kSiteNone;
+          E.d2s[o] = kD2None;
+          continue;
+        }
+        const int u = KeysX::winner(k);
+        if (u != last) {
+          last = u;
+          const uint32_t v = __ldg(yzrow + u);  // phase 2's key at the winning x
+          const int sy = KeysY::winner(v);
+          const int dy = y - sy;
+          const int dz = exact_root(static_cast<int>(KeysY::cost(v)) - dy * dy);
+          const int sz = KeysY::payload(v) ? z + dz : z - dz;
+          site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+          if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
+        }
+        uint32_t d2 = KeysX::cost(k);
+        if constexpr (kSigns != 0) {
+          if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
+        }
+        E.site[o] = site;
+        E.d2s[o] = d2;
+      }
     }
   }
 }
@@ -1042,6 +1316,7 @@ struct ks_esdf {
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
+  bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
   int dc_wl_y, dc_wl_x;    // log2(warps per tile)
   uint32_t none_y, none_x; // offsets of positions without candidate
@@ -1086,7 +1361,8 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   }
   if (dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
   E.dcount = static_cast<int>(dcount);
-  KS_CUDA(cudaMalloc(&E.dir, static_cast<size_t>(E.dcount) * sizeof(int)));
+  KS_CUDA(cudaMalloc(&E.dir, static_cast<size_t>(E.dcount) * (sizeof(int) + 1)));
+  E.dirs = reinterpret_cast<uint8_t*>(E.dir + E.dcount);
   if (E.pool_surf) cudaFree(E.pool_surf);
   E.pool_surf = nullptr;
   KS_CUDA(cudaMalloc(&E.pool_surf, static_cast<size_t>(T.capacity)));
@@ -1094,6 +1370,43 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
   KS_CUDA(cudaStreamSynchronize(e->stream));
+  if (E.dirg) cudaFree(E.dirg);
+  E.dirg = nullptr;
+  KS_CUDA(cudaMalloc(&E.dirg, static_cast<size_t>(E.dcount)));
+  {  // resampled seeding: check  probe voxel in {centre voxel, neighbouring cell's centre voxel}  position by position
+    std::vector<int> vox(static_cast<size_t>(kVoxRows) * total);
+    KS_CUDA(cudaMemcpy(vox.data(), E.vox, vox.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    bool ok = E.ve <= T.voxel && E.dn[0] <= kMaxDirX;
+    std::vector<int> voxe(total + 6);
+    std::vector<uint32_t> plus(E.wpr, 0u), minus(E.wpr, 0u);
+    std::vector<uint8_t> flags(E.ny + E.nz, 0);
+    int base = 0, ebase = 0;
+    for (int a = 0; a < 3; ++a) {
+      const int n = dims[a];
+      const int* c = vox.data() + kVoxC * total + base;
+      const int* ph = vox.data() + kVoxPh * total + base;
+      const int* mh = vox.data() + kVoxMh * total + base;
+      int* ce = voxe.data() + ebase + 1;  // ce[-1] .. ce[n]
+      ce[-1] = vox[kVoxMe * total + base], ce[n] = vox[kVoxPe * total + base + n - 1];
+      for (int i = 0; i < n; ++i) ce[i] = c[i];
+      for (int i = 0; i < n; ++i) {
+        ok = ok && (ph[i] == c[i] || ph[i] == ce[i + 1]) && (mh[i] == c[i] || mh[i] == ce[i - 1]);
+        if (a == 0) {
+          if (ph[i] != c[i]) plus[i >> 5] |= 1u << (i & 31);
+          if (mh[i] != c[i]) minus[i >> 5] |= 1u << (i & 31);
+        } else {
+          flags[(a == 1 ? 0 : E.ny) + i] = static_cast<uint8_t>((ph[i] != c[i] ? 1 : 0) | (mh[i] != c[i] ? 2 : 0));
+        }
+      }
+      base += n, ebase += n + 2;
+    }
+    KS_CUDA(cudaMemcpy(E.voxe, voxe.data(), voxe.size() * sizeof(int), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(E.xplus, plus.data(), plus.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(E.xminus, minus.data(), minus.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(E.yzflags, flags.data(), flags.size(), cudaMemcpyHostToDevice));
+    e->resample_ok = ok;
+    if (const char* v = std::getenv("KS_SEED")) e->resample_ok = e->resample_ok && std::strcmp(v, "bricks") != 0;
+  }
   e->bound_voxel = T.voxel;
   return KS_OK;
 }
@@ -1106,15 +1419,21 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
   return KS_OK;
 }
 
-static int refresh_directory(ks_esdf* e, const ks_tsdf* t) {
+// bricks: also the brick flags / work list of the brick gather and of the hinted sign recovery
+static int refresh_directory(ks_esdf* e, const ks_tsdf* t, bool bricks_too = true) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * sizeof(int), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * (sizeof(int) + 1), e->stream));  // dir and dirs
   KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
-  const int bricks = E.bnx * E.bny * E.bnz;
-  KS_LAUNCH(k_brick_active, (bricks + 127) / 128, 128, 0, e->stream, E);
+  if (bricks_too) {
+    KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
+    const int bricks = E.bnx * E.bny * E.bnz;
+    KS_LAUNCH(k_brick_active, (bricks + 127) / 128, 128, 0, e->stream, E);
+  }
   return KS_OK;
 }
+
+// fused build: resampled seeding + table-driven sign recovery inside the divide-and-conquer x sweep
+static bool fast_build(const ks_esdf* e) { return e->dc && e->resample_ok && e->cfg.seeding == 1; }
 
 // bits: gather straight into the bit-packed mask of the fused build (gather mode only)
 static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
@@ -1123,7 +1442,14 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   if (mode == 1) {
     const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;  // one warp per 32 x cells
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-    if (bits) {
+    if (bits && fast_build(e)) {
+      const int words = E.wpr * E.ny * E.nz;
+      const int ext_rows = (E.ny + 2) * (E.nz + 2);
+      KS_LAUNCH(k_dir_geom, (E.dcount + 255) / 256, 256, 0, e->stream, E);
+      KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
+      KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
+      KS_LAUNCH(k_site_tables, (words + 255) / 256, 256, 0, e->stream, E, tsdf_view(t));
+    } else if (bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
       KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * plane_bytes, e->stream));  // seed plane + geometry-near plane (contiguous)
       KS_LAUNCH(k_seed_gather_bricks, 6 * kSmCount, kGatherWarps * 32, 0, e->stream, E, tsdf_view(t));
@@ -1147,13 +1473,15 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
-  if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + 31) / 32, E.nz), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
+  if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
   else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (e->dc) {
+    const dim3 xgrid((E.ny + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
     const unsigned threads = 32u << e->dc_wl_x;
-    if (t && bits) KS_LAUNCH(k_sweep_x_dc<2>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
+    if (t && bits && fast_build(e)) KS_LAUNCH(k_sweep_x_dc<3>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
+    else if (t && bits) KS_LAUNCH(k_sweep_x_dc<2>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
     else if (t) KS_LAUNCH(k_sweep_x_dc<1>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
     else KS_LAUNCH(k_sweep_x_dc<0>, xgrid, threads, e->smem_x, e->stream, E, TsdfView{}, e->dc_wl_x, e->none_y, e->none_x);
   } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
@@ -1227,6 +1555,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
@@ -1241,6 +1570,17 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   E.wpr = (E.nx + 31) / 32;
   KS_CUDA(cudaMalloc(&E.mbits, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t)));  // both bit planes
   E.gbits = E.mbits + static_cast<size_t>(E.wpr) * E.ny * E.nz;
+  E.wpr2 = (E.nx + 2 + 31) / 32;
+  {
+    const size_t ext_words = static_cast<size_t>(E.wpr2) * (E.ny + 2) * (E.nz + 2);
+    KS_CUDA(cudaMalloc(&E.cbits, 3 * ext_words * sizeof(uint32_t)));
+    E.obits = E.cbits + ext_words, E.nbits = E.obits + ext_words;
+    KS_CUDA(cudaMalloc(&E.voxe, (total + 6) * sizeof(int)));
+    KS_CUDA(cudaMalloc(&E.xplus, 2 * E.wpr * sizeof(uint32_t)));
+    E.xminus = E.xplus + E.wpr;
+    KS_CUDA(cudaMalloc(&E.yzflags, E.ny + E.nz));
+    KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
+  }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
@@ -1261,7 +1601,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
@@ -1294,7 +1634,7 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   }
   e->profile_stages = prof;
   if (prof) cudaEventRecord(e->ev[0], e->stream);
-  if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  if ((rc = refresh_directory(e, t, !fast_build(e))) != KS_OK) return rc;
   if (prof) cudaEventRecord(e->ev[1], e->stream);
   const bool bits = e->cfg.seeding == 1;
   if ((rc = seed_async(e, t, e->cfg.seeding, bits)) != KS_OK) return rc;

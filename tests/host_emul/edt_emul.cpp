@@ -179,7 +179,8 @@ void dc_tile(const std::vector<uint32_t>& G, std::vector<uint32_t>& K, int n, in
       const int lo_w = a > 0 ? dc::Keys<kPay>::winner(Kt[dc::at(j, r)]) : 0;
       const int hi_w = closed ? dc::Keys<kPay>::winner(right) : n - 1;
       auto emit = [&](int t, uint32_t key) { K[dc::at(t, r)] = key; };
-      dc::subtree<kPay, kSubStep>(G.data(), n, a + kSubStep, lo_w, hi_w, r, bounded, emit);
+      if (closed) dc::subtree<kPay, kSubStep, true>(G.data(), n, a + kSubStep, lo_w, hi_w, r, bounded, emit);
+      else dc::subtree<kPay, kSubStep, false>(G.data(), n, a + kSubStep, lo_w, hi_w, r, bounded, emit);
       if (closed) emit(a + kTopStep - 1, right);
     }
   }
