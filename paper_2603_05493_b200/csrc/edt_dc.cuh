@@ -156,20 +156,22 @@ KS_DC_HD uint32_t scan(const uint32_t* G, int lo, int scan_len, int t, int row) 
 // a stretch of positions (a, a + 2*kS) resolves everything inside on its own, keeping the winners
 // it still needs in registers (the recursion is unrolled at compile time; every test on tp / n is
 // warp-uniform).  wmax(v) returns the largest v among the warp's lanes; emit(t, key) receives every
-// position visited.  Centre tp = a + kS; lo_w / hi_w = winners at a and a + 2*kS (row ends outside).
+// position visited, in ascending order of t.  Centre tp = a + kS; lo_w / hi_w = winners at a and a + 2*kS (row ends outside).
 // kInside: the whole stretch lies inside the row (a + 2*kS <= n), so no position needs a bounds test.
 template <int kPay, int kS, bool kInside, class WarpMax, class Emit>
 KS_DC_HD void subtree(const uint32_t* G, int n, int tp, int lo_w, int hi_w, int row, WarpMax&& wmax, Emit&& emit) {
   if (!kInside && tp - kS >= n) return;  // the whole stretch lies right of the row
+  const bool here = kInside || tp <= n;
   int mid = hi_w;
-  if (kInside || tp <= n) {
+  uint32_t key = 0;
+  if (here) {
     const int longest = wmax(hi_w - lo_w + 1);
-    const uint32_t key = scan<kPay>(G, clamp_start(lo_w, longest, n), longest, tp - 1, row);
-    emit(tp - 1, key);
+    key = scan<kPay>(G, clamp_start(lo_w, longest, n), longest, tp - 1, row);
     mid = Keys<kPay>::winner(key);
   }
+  if constexpr (kS > 1) subtree<kPay, kS / 2, kInside>(G, n, tp - kS / 2, lo_w, mid, row, wmax, emit);
+  if (here) emit(tp - 1, key);  // positions reach emit() in ascending order
   if constexpr (kS > 1) {
-    subtree<kPay, kS / 2, kInside>(G, n, tp - kS / 2, lo_w, mid, row, wmax, emit);
     if (kInside || tp < n) subtree<kPay, kS / 2, kInside>(G, n, tp + kS / 2, mid, hi_w, row, wmax, emit);
   }
 }

@@ -673,23 +673,25 @@ struct SignProbe {
 // SignProbe's exact path.  No directory or digest access per cell.
 struct SignTable {
   const EsdfView& E;
-  SignProbe exact;
+  const TsdfView& T;
+  const float* qsf;  // E.qsf, staged in shared memory by the caller
   int y, z;
   int sx, sy, sz;
   uint2 tab;
   float qx, qy, qz;
 
-  __device__ __forceinline__ SignTable(const EsdfView& E_, const TsdfView& T_, int y_, int z_) : E(E_), exact(E_, T_, y_, z_) {
+  __device__ __forceinline__ SignTable(const EsdfView& E_, const TsdfView& T_, const float* qsf_, int y_, int z_)
+      : E(E_), T(T_), qsf(qsf_) {
     y = y_, z = z_;
     sx = sy = sz = -1;
     tab = make_uint2(0u, 0u);
   }
   __device__ __forceinline__ void set_site(int sx_, int sy_, int sz_, uint2 tab_) {
     sx = sx_, sy = sy_, sz = sz_, tab = tab_;
-    if (tab.x != 0) qx = E.qsf[sx], qy = E.qsf[E.nx + sy], qz = E.qsf[E.nx + E.ny + sz];
+    if (tab.x != 0) qx = qsf[sx], qy = qsf[E.nx + sy], qz = qsf[E.nx + E.ny + sz];
   }
   // own: the cell's bit of the own-sign plane
-  __device__ __forceinline__ bool negative(int x, bool own) {
+  __device__ __forceinline__ bool negative(int x, bool own) const {
     const int dx = x - sx, dy = y - sy, dz = z - sz;
     if (tab.x != 0 && (dx | dy | dz) != 0) {
       const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
@@ -698,15 +700,28 @@ struct SignTable {
       const float tol = 4e-6f * (1.0f + E.ratio);
       const bool sure = (dx == 0 || fabsf(ox - rintf(ox)) > tol) && (dy == 0 || fabsf(oy - rintf(oy)) > tol) &&
                         (dz == 0 || fabsf(oz - rintf(oz)) > tol);
-      if (!sure) {  // the reference's arithmetic, operation by operation
-        exact.template set_site<false>(sx, sy, sz);
-        return exact.template negative<false>(x);
-      }
+      if (!sure) return exact_negative(x, own);
       const int idx = (dx == 0 ? 1 : __float2int_rd(ox) + 1) + 3 * (dy == 0 ? 1 : __float2int_rd(oy) + 1) +
                       9 * (dz == 0 ? 1 : __float2int_rd(oz) + 1);
       if ((tab.x >> idx) & 1u) return ((tab.y >> idx) & 1u) != 0;  // query_tsdf_geom has a value: its sign decides
     }
     return own;  // combined sdf at the cell's own centre (esdf.hpp:309-312)
+  }
+  // rare: the fp32 estimate sits too close to a voxel face -- the reference's arithmetic, operation by operation
+  // (esdf.hpp:297-308), straight from the directory and the digest
+  __device__ __forceinline__ bool exact_negative(int x, bool own) const {
+    const double px = E.ctr[sx], py = E.ctr[E.nx + sy], pz = E.ctr[E.nx + E.ny + sz];
+    const double ex = E.ctr[x] - px, ey = E.ctr[E.nx + y] - py, ez = E.ctr[E.nx + E.ny + z] - pz;
+    const double n = sqrt(sum3(ex * ex, ey * ey, ez * ez));
+    const int vx = voxel_index(px + E.ve * (ex / n), T.voxel) - 8 * E.dlo[0];
+    const int vy = voxel_index(py + E.ve * (ey / n), T.voxel) - 8 * E.dlo[1];
+    const int vz = voxel_index(pz + E.ve * (ez / n), T.voxel) - 8 * E.dlo[2];
+    const int pool = dir_lookup(E, vx, vy, vz);
+    if (pool >= 0) {
+      const uint32_t g = pair_bits(T, pool, kDigestGeom, local_index(vx, vy, vz));
+      if (g & 1u) return (g & 2u) != 0;
+    }
+    return own;
   }
 };
 
@@ -898,7 +913,9 @@ __device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt
 
 static size_t dc_top_bytes(int n) { return static_cast<size_t>((n >> kTopShift) + 1) * 32 * sizeof(uint32_t); }
 static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n); }
-static size_t dc_smem_bytes_x(int n) { return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n); }
+static size_t dc_smem_bytes_x(int n, int total) {  // G, K, Kt and the per-axis fraction table of the sign tables
+  return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n) + static_cast<size_t>(total) * sizeof(float);
+}
 
 // root of a perfect square below 2^24 (one MUFU; its error of a few ulp cannot reach the next integer)
 __device__ __forceinline__ int exact_root(int sq) {
@@ -971,104 +988,70 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, 
     }
   }
   for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
+  float* s_qsf = reinterpret_cast<float*>(Kt + ((nx >> kTopShift) + 1) * 32);
+  if constexpr (kSigns == 3)
+    for (int i = threadIdx.x; i < nx + ny + E.nz; i += blockDim.x) s_qsf[i] = E.qsf[i];
   __syncthreads();
   const int y = y0 + (lane & (kTileA - 1)), z = min(z0 + lane / kTileA, E.nz - 1);
   const bool live = y < ny && z0 + lane / kTileA < E.nz;
-  const int zoff = nx * ny * z;
+  // The slot of (this lane's row, position x) in the rotated layout.  After the conversion below its low
+  // half keeps what phase 3 still needs of the candidate at x (site_y << 1 | seed above z; its in-plane d2
+  // is in G) and its high half receives the winner of position x -- so the tile needs no third array.
+  auto slot = [&](int x) { return x * 32 + ((lane + x) & 31); };
+  uint16_t* K16 = reinterpret_cast<uint16_t*>(K);
   for (int x = warp; x < nx; x += nwarps) {
-    const uint32_t r2 = KeysY::cost(K[x * 32 + ((lane + x) & 31)]);  // in-plane d2 of the candidate at x
+    const uint32_t v = K[slot(x)];
+    const uint32_t r2 = KeysY::cost(v);  // in-plane d2 of the candidate at x
     G[edt_dc::at(x, lane)] = KeysX::pack(r2 >= none_y ? none_x : r2, x, 0);
+    K[slot(x)] = v & KeysY::kLowMask;
   }
   __syncthreads();
   dc_top_levels<0>(G, Kt, nx, warp, lane, warps_log2);
-  const uint32_t* yzrow = E.yz + zoff + nx * min(y, ny - 1);
   const int obase = y + ny * nx * z;
-  if constexpr (kSigns == 3) {
-    SignTable probe(E, Tw, min(y, ny - 1), z);
-    const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
-    const uint2* gplane = E.gtab + nx * ny * z;
-    for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-      dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
-      if (!live) continue;
-      const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
-      uint32_t* sp = E.site + obase + ny * x0;
-      uint32_t* dp = E.d2s + obase + ny * x0;
-      if (KeysX::cost(K[edt_dc::at(x0, lane)]) >= none_x) {  // the row holds no candidate at all
-        for (int x = x0; x < end; ++x, sp += ny, dp += ny) *sp = kSiteNone, *dp = kD2None;
+  auto make_probe = [&]() {
+    if constexpr (kSigns == 3) return SignTable(E, Tw, s_qsf, min(y, ny - 1), z);
+    else return SignProbe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
+  };
+  auto probe = make_probe();
+  const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
+  for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
+    dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
+    if (!live) continue;
+    // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
+    const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
+    uint32_t own = 0;  // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
+    if constexpr (kSigns == 3) own = __funnelshift_r(orow[j], j + 1 < E.wpr2 ? orow[j + 1] : 0u, 1);
+    uint32_t* sp = E.site + obase + ny * x0;
+    uint32_t* dp = E.d2s + obase + ny * x0;
+    int last = -1, r2 = 0;
+    uint32_t site = kSiteNone;
+    for (int x = x0; x < end; ++x, sp += ny, dp += ny) {
+      const int u = K16[2 * slot(x) + 1];
+      if (u != last) {
+        last = u;
+        r2 = static_cast<int>(KeysX::cost(G[edt_dc::at(u, lane)]));
+        if (r2 < static_cast<int>(none_x)) {
+          const uint32_t h = K16[2 * slot(u)];
+          const int sy = static_cast<int>(h >> 1);
+          const int dy = y - sy;
+          const int dz = exact_root(r2 - dy * dy);
+          const int sz = (h & 1u) ? z + dz : z - dz;
+          site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+          if constexpr (kSigns == 3) probe.set_site(u, sy, sz, __ldg(E.gtab + (u + nx * (sy + ny * sz))));
+          else if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
+        }
+      }
+      if (r2 >= static_cast<int>(none_x)) {  // the row holds no candidate at all
+        *sp = kSiteNone, *dp = kD2None;
         continue;
       }
-      // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
-      const uint32_t own_lo = orow[j], own_hi = j + 1 < E.wpr2 ? orow[j + 1] : 0u;
-      const uint32_t own = __funnelshift_r(own_lo, own_hi, 1);
-      int last = -1;
-      uint32_t site = kSiteNone;
-      for (int xb = x0; xb < end; xb += 4) {  // four cells at a time: their gathers are in flight together
-        uint32_t k[4], v[4], st[4];
-        uint2 tb[4];
-        int u[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) k[i] = K[edt_dc::at(min(xb + i, end - 1), lane)], u[i] = KeysX::winner(k[i]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = __ldg(yzrow + u[i]);  // phase 2's key at the winning x
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int sy = KeysY::winner(v[i]);
-          const int dy = y - sy;
-          const int dz = exact_root(static_cast<int>(KeysY::cost(v[i])) - dy * dy);
-          const int sz = KeysY::payload(v[i]) ? z + dz : z - dz;
-          st[i] = static_cast<uint32_t>(u[i]) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-          tb[i] = __ldg(E.gtab + (u[i] + nx * (sy + ny * sz)));
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int x = xb + i;
-          if (x >= end) break;
-          if (u[i] != last) {
-            last = u[i], site = st[i];
-            probe.set_site(u[i], static_cast<int>((site >> 10) & 1023u), static_cast<int>(site >> 20), tb[i]);
-          }
-          uint32_t d2 = KeysX::cost(k[i]);
-          if (probe.negative(x, ((own >> (x - x0)) & 1u) != 0)) d2 |= 0x80000000u;
-          *sp = site, *dp = d2;
-          sp += ny, dp += ny;
-        }
+      uint32_t d2 = static_cast<uint32_t>((x - u) * (x - u) + r2);
+      if constexpr (kSigns == 3) {
+        if (probe.negative(x, ((own >> (x - x0)) & 1u) != 0)) d2 |= 0x80000000u;
+      } else if constexpr (kSigns != 0) {
+        if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
       }
-    }
-    (void)gplane;
-  } else {
-    SignProbe probe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
-    for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-      dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K[edt_dc::at(x, lane)] = k; });
-      if (!live) continue;
-      const int end = min((j + 1) << kTopShift, nx);
-      int last = -1;
-      uint32_t site = kSiteNone;
-      for (int x = j << kTopShift; x < end; ++x) {
-        const uint32_t k = K[edt_dc::at(x, lane)];
-        const int o = obase + ny * x;
-        if (KeysX::cost(k) >= none_x) {  // the row holds no candidate at all
-          E.site[o] = kSiteNone;
-          E.d2s[o] = kD2None;
-          continue;
-        }
-        const int u = KeysX::winner(k);
-        if (u != last) {
-          last = u;
-          const uint32_t v = __ldg(yzrow + u);  // phase 2's key at the winning x
-          const int sy = KeysY::winner(v);
-          const int dy = y - sy;
-          const int dz = exact_root(static_cast<int>(KeysY::cost(v)) - dy * dy);
-          const int sz = KeysY::payload(v) ? z + dz : z - dz;
-          site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-          if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
-        }
-        uint32_t d2 = KeysX::cost(k);
-        if constexpr (kSigns != 0) {
-          if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
-        }
-        E.site[o] = site;
-        E.d2s[o] = d2;
-      }
+      *sp = site, *dp = d2;
     }
   }
 }
@@ -1534,14 +1517,14 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   {  // divide-and-conquer sweeps whenever their 32-bit keys hold every reachable cost (all dims <= ~830, or a long x axis)
     const uint32_t gmax_y = static_cast<uint32_t>((E.nz - 1) * (E.nz - 1));
     const uint32_t gmax_x = gmax_y + static_cast<uint32_t>((E.ny - 1) * (E.ny - 1));
-    e->dc = KeysY::fits(E.ny, gmax_y) && KeysX::fits(E.nx, gmax_x) && dc_smem_bytes_x(E.nx) <= 227 * 1024 && dc_smem_bytes_y(E.ny) <= 227 * 1024;
+    e->dc = KeysY::fits(E.ny, gmax_y) && KeysX::fits(E.nx, gmax_x) && dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) <= 227 * 1024 && dc_smem_bytes_y(E.ny) <= 227 * 1024;
     if (const char* v = std::getenv("KS_SWEEP")) e->dc = e->dc && std::strcmp(v, "stack") != 0;
     e->none_y = KeysY::none_offset(E.ny, gmax_y);
     e->none_x = KeysX::none_offset(E.nx, gmax_x);
     e->dc_wl_y = 3, e->dc_wl_x = 4;
     if (const char* v = std::getenv("KS_DC_WARPS_Y")) e->dc_wl_y = std::min(4, std::max(0, std::atoi(v)));
     if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(4, std::max(0, std::atoi(v)));
-    if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx);
+    if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz);
   }
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
     delete e;
