@@ -34,6 +34,7 @@ constexpr int kMaxDim = 1024;  // 10-bit site packing, uint16 stacks
 struct EsdfCtrl {
   unsigned long long seed_count;
   int signs_recovered;
+  int seed_words;     // entries of EsdfView::seedw (resampled seeding)
   int active_bricks;  // entries of EsdfView::active, rebuilt with the directory
 };
 
@@ -72,6 +73,8 @@ struct EsdfView {
   uint32_t* xplus;     // [wpr] bit x: the +ve/2 probe of cell x leaves the centre voxel (esdf.hpp:106-108) ...
   uint32_t* xminus;    // [wpr] ... and the -ve/2 probe
   uint8_t* yzflags;    // [ny | nz] bit0 / bit1: the same for the y and z probes of that row
+  int xshift;          // voxe[i] == i + xshift along x (cell and voxel grids in step), else -1
+  int* seedw;          // compacted indices of the seed-plane words that hold seeds (count in ctrl->seed_words)
   uint8_t* dirs;       // [dcount] 1 when the entry's block holds stamped geometry (0 / 0xFF otherwise)
   uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
   uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
@@ -397,6 +400,26 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView 
     return;
   }
   __syncwarp();
+  if (E.xshift >= 0) {  // grids in step: a cell word is 32 consecutive bits of the voxel-space row
+    for (int w = lane; w < E.wpr2; w += 32) {
+      const int o = 32 * w + E.xshift;
+      uint32_t word[3];
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl) {
+        uint64_t bits = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int b = (o >> 3) + k;
+          bits |= static_cast<uint64_t>(b < E.dn[0] ? S[pl][b] : 0) << (8 * k);
+        }
+        word[pl] = static_cast<uint32_t>(bits >> (o & 7));
+      }
+      const int rest = E.nx + 2 - 32 * w;
+      const uint32_t keep = rest < 32 ? (1u << rest) - 1u : 0xFFFFFFFFu;
+      out[w] = word[0] & keep, out[plane + w] = word[1] & keep, out[2 * plane + w] = word[2] & keep;
+    }
+    return;
+  }
   for (int w = 0; w < E.wpr2; ++w) {
     const int xi = 32 * w + lane;
     bool c = false, o = false, n = false;
@@ -436,6 +459,16 @@ __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
     E.gbits[i] = seed & static_cast<uint32_t>(ext(E.nbits, y, z) >> 1);
     count = __popc(seed);
   }
+  {  // compact list of the words that hold seeds (one atomic per warp)
+    const uint32_t holders = __ballot_sync(0xFFFFFFFFu, count != 0);
+    if (holders != 0) {
+      const int lane = threadIdx.x & 31;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&E.ctrl->seed_words, __popc(holders));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (count != 0) E.seedw[base + __popc(holders & ((1u << lane) - 1u))] = i;
+    }
+  }
   for (int d = 16; d > 0; d >>= 1) count += __shfl_down_sync(0xFFFFFFFFu, count, d);
   if ((threadIdx.x & 31) == 0 && count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(count));
 }
@@ -443,20 +476,14 @@ __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
 // Per-site sign tables: for every seed the geometry pairs {has value, negative} of the 27 voxels around its
 // centre voxel (the only voxels a sign probe from that site can land in when ve <= v), read as 9 x-rows of
 // three voxels from the digest's pair plane; all zero when no stamped block is in reach (gbits clear).
-// One thread looks at one word of the seed plane; the warp then serves its non-empty words one after the
-// other, lane <-> seed.
+// Persistent grid over the compacted list of seed words, one warp per word, lane <-> seed.
 __global__ void __launch_bounds__(256) k_site_tables(EsdfView E, TsdfView T) {
-  const int word = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const int words = E.wpr * E.ny * E.nz;
-  const uint32_t mine = word < words ? E.mbits[word] : 0u;
-  uint32_t pending = __ballot_sync(0xFFFFFFFFu, mine != 0);
-  while (pending != 0) {
-    const int src = __ffs(static_cast<int>(pending)) - 1;
-    pending &= pending - 1;
-    const int w = word - lane + src;
-    const uint32_t seeds = __shfl_sync(0xFFFFFFFFu, mine, src);
-    if (!((seeds >> lane) & 1u)) continue;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int count = E.ctrl->seed_words;
+  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < count; item += nwarps) {
+    const int w = E.seedw[item];
+    if (!((E.mbits[w] >> lane) & 1u)) continue;
     const int xw = w % E.wpr, row = w / E.wpr;
     const int y = row % E.ny, z = row / E.ny;
     const int x = 32 * xw + lane;
@@ -577,6 +604,63 @@ __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
     else if (above < 0) pick = below;
     else pick = (above - z) < (z - below) ? above : below;
     out[plane * z] = static_cast<uint16_t>(pick);
+  }
+}
+
+// The fused build's phase 1: one CTA per 32 consecutive x columns of one y, one warp per 32 z.  Warp w
+// transposes its 32(z) x 32(x) bit tile of the x-packed mask into word w of every column's bit string
+// (shared memory, [word][lane]); after the barrier it walks its own 32 z upwards, so a column's work is
+// spread over nz/32 warps instead of one.
+__global__ void __launch_bounds__(1024) k_flood_z_chunks(EsdfView E) {
+  extern __shared__ uint32_t s_words[];  // [nwords][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nwords = (E.nz + 31) >> 5;
+  const int xw = blockIdx.x % E.wpr, y = blockIdx.x / E.wpr;
+  const int x = xw * 32 + lane;
+  {
+    const int z = 32 * w + lane;
+    const uint32_t mine = z < E.nz ? __ldg(E.mbits + (z * E.ny + y) * E.wpr + xw) : 0u;  // 32 x-bits of row (y, z)
+    uint32_t bits = 0;
+#pragma unroll
+    for (int xb = 0; xb < 32; ++xb) {
+      const uint32_t col = __ballot_sync(0xFFFFFFFFu, (mine >> xb) & 1u);  // column xb: bit z
+      if (lane == xb) bits = col;
+    }
+    s_words[w * 32 + lane] = bits;
+  }
+  __syncthreads();
+  if (x >= E.nx) return;
+  const uint32_t* words = s_words + lane;  // words[k * 32]
+  const int z0 = 32 * w, z1 = min(z0 + 32, E.nz);
+  // nearest seed strictly below z0, and at or above z0
+  int below = -1;
+  for (int k = w - 1; k >= 0; --k) {
+    const uint32_t m = words[k * 32];
+    if (m != 0) {
+      below = 32 * k + 31 - __clz(static_cast<int>(m));
+      break;
+    }
+  }
+  auto next_set = [&](int from) -> int {  // first set bit at position >= from, or -1
+    if (from >= E.nz) return -1;
+    int k = from >> 5;
+    uint32_t m = words[k * 32] & (0xFFFFFFFFu << (from & 31));
+    while (m == 0 && ++k < nwords) m = words[k * 32];
+    return m != 0 ? 32 * k + __ffs(static_cast<int>(m)) - 1 : -1;
+  };
+  int above = next_set(z0);
+  uint16_t* out = E.near_z + (z0 * E.ny + y) * E.nx + x;
+  const int plane = E.nx * E.ny;
+  for (int z = z0; z < z1; ++z, out += plane) {
+    if (z == above) {
+      below = z;
+      above = next_set(z + 1);
+    }
+    int pick;
+    if (below < 0) pick = above < 0 ? static_cast<int>(edt::kNone) : above;
+    else if (above < 0) pick = below;
+    else pick = (above - z) < (z - below) ? above : below;  // ties keep the lower z (strict '<', esdf.hpp:229)
+    *out = static_cast<uint16_t>(pick);
   }
 }
 
@@ -1387,6 +1471,9 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
     KS_CUDA(cudaMemcpy(E.xplus, plus.data(), plus.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(E.xminus, minus.data(), minus.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(E.yzflags, flags.data(), flags.size(), cudaMemcpyHostToDevice));
+    bool in_step = voxe[0] >= 0;
+    for (int i = 0; i < E.nx + 2; ++i) in_step = in_step && voxe[i] == i + voxe[0];
+    E.xshift = in_step ? voxe[0] : -1;
     e->resample_ok = ok;
     if (const char* v = std::getenv("KS_SEED")) e->resample_ok = e->resample_ok && std::strcmp(v, "bricks") != 0;
   }
@@ -1431,7 +1518,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
       KS_LAUNCH(k_dir_geom, (E.dcount + 255) / 256, 256, 0, e->stream, E);
       KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
-      KS_LAUNCH(k_site_tables, (words + 255) / 256, 256, 0, e->stream, E, tsdf_view(t));
+      KS_LAUNCH(k_site_tables, 8 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
     } else if (bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
       KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * plane_bytes, e->stream));  // seed plane + geometry-near plane (contiguous)
@@ -1453,7 +1540,7 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   const unsigned fgrid = static_cast<unsigned>((E.wpr * E.ny + kFloodWarps - 1) / kFloodWarps);
   const size_t fsmem = static_cast<size_t>(nwords) * 32 * kFloodWarps * sizeof(uint32_t);
   (void)plane;
-  if (bits) KS_LAUNCH(k_flood_z<true>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
+  if (bits) KS_LAUNCH(k_flood_z_chunks, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
@@ -1563,6 +1650,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     E.xminus = E.xplus + E.wpr;
     KS_CUDA(cudaMalloc(&E.yzflags, E.ny + E.nz));
     KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
+    KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(int)));
   }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
@@ -1584,7 +1672,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
