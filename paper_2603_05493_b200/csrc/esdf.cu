@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
 // resolves whole stretches of kTopStep positions on its own (edt_dc::subtree), no barrier.
 using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
 using KeysX = edt_dc::Keys<0>;
-constexpr int kTopShift = 5, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+constexpr int kTopShift = 4, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
 // The 32 rows of a tile are 8 neighbours along the fast axis x 4 along z: all lanes scan as far as the
 // lane with the longest window, and compact tiles cross a Voronoi boundary at fewer positions than
 // 32 x 1 ones (29 % fewer evaluations at cfg2); 8 x 4 also divides the BASELINE grids without padding.
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, 
     // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
     const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
     uint32_t own = 0;  // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
-    if constexpr (kSigns == 3) own = __funnelshift_r(orow[j], j + 1 < E.wpr2 ? orow[j + 1] : 0u, 1);
+    if constexpr (kSigns == 3) own = __funnelshift_rc(orow[x0 >> 5], (x0 >> 5) + 1 < E.wpr2 ? orow[(x0 >> 5) + 1] : 0u, (x0 & 31) + 1);
     uint32_t* sp = E.site + obase + ny * x0;
     uint32_t* dp = E.d2s + obase + ny * x0;
     int last = -1, r2 = 0;

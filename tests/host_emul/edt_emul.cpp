@@ -132,7 +132,7 @@ namespace dc = ksb::edt_dc;
 // as atomicMin does), then one subtree per stretch.  Rows are independent except for the warp-wide scan
 // length; `fuzz` stands in for it by lengthening every scan pseudo-randomly, which must not change any
 // winner.  scans += scan lengths, visits += visits (of row 0, as a proxy for the warp).
-constexpr int kTopShift = 5, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+constexpr int kTopShift = 4, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
 
 struct Fuzz {
   uint32_t state;
