@@ -34,7 +34,7 @@ constexpr int kMaxDim = 1024;  // 10-bit site packing, uint16 stacks
 struct EsdfCtrl {
   unsigned long long seed_count;
   int signs_recovered;
-  int seed_words;     // entries of EsdfView::seedw (resampled seeding)
+  int seed_words;     // entries of EsdfView::seedw (resampled seeding): seeds with a stamped block in reach
   int active_bricks;  // entries of EsdfView::active, rebuilt with the directory
 };
 
@@ -74,7 +74,7 @@ struct EsdfView {
   uint32_t* xminus;    // [wpr] ... and the -ve/2 probe
   uint8_t* yzflags;    // [ny | nz] bit0 / bit1: the same for the y and z probes of that row
   int xshift;          // voxe[i] == i + xshift along x (cell and voxel grids in step), else -1
-  int* seedw;          // compacted indices of the seed-plane words that hold seeds (count in ctrl->seed_words)
+  int* seedw;          // compacted cell indices of the seeds whose sign table is not all zero (count in ctrl->seed_words)
   uint8_t* dirs;       // [dcount] 1 when the entry's block holds stamped geometry (0 / 0xFF otherwise)
   uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
   uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
@@ -436,81 +436,87 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView 
 // one thread per word of the seed plane
 __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int words = E.wpr * E.ny * E.nz;
-  unsigned count = 0;
+  uint32_t seed = 0, near = 0;
+  int row = 0, xw = 0;
   if (i < words) {
-    const int xw = i % E.wpr, row = i / E.wpr;
+    xw = i % E.wpr, row = i / E.wpr;
     const int y = row % E.ny, z = row / E.ny;
     const int ey = E.ny + 2;
     auto ext = [&](const uint32_t* plane, int yy, int zz) -> uint64_t {  // extended bits 32xw .. 32xw+63 of row (yy, zz)
       const uint32_t* r = plane + ((zz + 1) * ey + (yy + 1)) * E.wpr2 + xw;
       return static_cast<uint64_t>(r[0]) | (xw + 1 < E.wpr2 ? static_cast<uint64_t>(r[1]) << 32 : 0ull);
     };
+    // every load up front (one round trip): the row itself, its four neighbours, the geometry-near row
     const uint64_t w = ext(E.cbits, y, z);  // bit k = cell 32xw + k - 1
+    const uint64_t wyp = ext(E.cbits, y + 1, z), wym = ext(E.cbits, y - 1, z), wzp = ext(E.cbits, y, z + 1), wzm = ext(E.cbits, y, z - 1);
+    const uint64_t wn = ext(E.nbits, y, z);
     const uint8_t fy = E.yzflags[y], fz = E.yzflags[E.ny + z];
-    uint32_t seed = static_cast<uint32_t>(w >> 1) | (static_cast<uint32_t>(w >> 2) & E.xplus[xw]) | (static_cast<uint32_t>(w) & E.xminus[xw]);
-    if (fy & 1) seed |= static_cast<uint32_t>(ext(E.cbits, y + 1, z) >> 1);
-    if (fy & 2) seed |= static_cast<uint32_t>(ext(E.cbits, y - 1, z) >> 1);
-    if (fz & 1) seed |= static_cast<uint32_t>(ext(E.cbits, y, z + 1) >> 1);
-    if (fz & 2) seed |= static_cast<uint32_t>(ext(E.cbits, y, z - 1) >> 1);
+    seed = static_cast<uint32_t>(w >> 1) | (static_cast<uint32_t>(w >> 2) & E.xplus[xw]) | (static_cast<uint32_t>(w) & E.xminus[xw]);
+    if (fy & 1) seed |= static_cast<uint32_t>(wyp >> 1);
+    if (fy & 2) seed |= static_cast<uint32_t>(wym >> 1);
+    if (fz & 1) seed |= static_cast<uint32_t>(wzp >> 1);
+    if (fz & 2) seed |= static_cast<uint32_t>(wzm >> 1);
     const int rest = E.nx - 32 * xw;
     if (rest < 32) seed &= (1u << rest) - 1u;
+    near = seed & static_cast<uint32_t>(wn >> 1);
     E.mbits[i] = seed;
-    E.gbits[i] = seed & static_cast<uint32_t>(ext(E.nbits, y, z) >> 1);
-    count = __popc(seed);
+    E.gbits[i] = near;
   }
-  {  // compact list of the words that hold seeds (one atomic per warp)
-    const uint32_t holders = __ballot_sync(0xFFFFFFFFu, count != 0);
-    if (holders != 0) {
-      const int lane = threadIdx.x & 31;
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&E.ctrl->seed_words, __popc(holders));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      if (count != 0) E.seedw[base + __popc(holders & ((1u << lane) - 1u))] = i;
-    }
+  // seeds with no stamped block in reach resolve no sign probe: their table is all zero
+  for (uint32_t m = seed & ~near; m != 0; m &= m - 1) E.gtab[32 * xw + __ffs(static_cast<int>(m)) - 1 + E.nx * row] = make_uint2(0u, 0u);
+  // the others go on the work list of k_site_tables (one atomic per warp)
+  const int mine = __popc(near);
+  int before = mine;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int up = __shfl_up_sync(0xFFFFFFFFu, before, d);
+    if (lane >= d) before += up;
   }
+  const int total = __shfl_sync(0xFFFFFFFFu, before, 31);
+  if (total != 0) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&E.ctrl->seed_words, total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0) + before - mine;
+    for (uint32_t m = near; m != 0; m &= m - 1) E.seedw[base++] = 32 * xw + __ffs(static_cast<int>(m)) - 1 + E.nx * row;
+  }
+  unsigned count = __popc(seed);
   for (int d = 16; d > 0; d >>= 1) count += __shfl_down_sync(0xFFFFFFFFu, count, d);
-  if ((threadIdx.x & 31) == 0 && count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(count));
+  if (lane == 0 && count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(count));
 }
 
-// Per-site sign tables: for every seed the geometry pairs {has value, negative} of the 27 voxels around its
-// centre voxel (the only voxels a sign probe from that site can land in when ve <= v), read as 9 x-rows of
-// three voxels from the digest's pair plane; all zero when no stamped block is in reach (gbits clear).
-// Persistent grid over the compacted list of seed words, one warp per word, lane <-> seed.
+// Per-site sign tables: for every seed with a stamped block in reach, the geometry pairs {has value, negative}
+// of the 27 voxels around its centre voxel (the only voxels a sign probe from that site can land in when
+// ve <= v), read as 9 x-rows of three voxels from the digest's pair plane.  Persistent grid over the
+// compacted list of those seeds, one thread per seed.
 __global__ void __launch_bounds__(256) k_site_tables(EsdfView E, TsdfView T) {
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int count = E.ctrl->seed_words;
-  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < count; item += nwarps) {
-    const int w = E.seedw[item];
-    if (!((E.mbits[w] >> lane) & 1u)) continue;
-    const int xw = w % E.wpr, row = w / E.wpr;
+  for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < count; item += gridDim.x * blockDim.x) {
+    const int cell = E.seedw[item];
+    const int x = cell % E.nx, row = cell / E.nx;
     const int y = row % E.ny, z = row / E.ny;
-    const int x = 32 * xw + lane;
+    const int vx = E.vox[x], vy0 = E.vox[E.nx + y], vz0 = E.vox[E.nx + E.ny + z];
+    const int bxa = (vx - 1) >> 3, bxm = vx >> 3, bxb = (vx + 1) >> 3;
     uint32_t has = 0, neg = 0;
-    if ((E.gbits[w] >> lane) & 1u) {
-      const int vx = E.vox[x], vy0 = E.vox[E.nx + y], vz0 = E.vox[E.nx + E.ny + z];
-      const int bxa = (vx - 1) >> 3, bxm = vx >> 3, bxb = (vx + 1) >> 3;
 #pragma unroll
-      for (int r = 0; r < 9; ++r) {
-        const int vy = vy0 + r % 3 - 1, vz = vz0 + r / 3 - 1;
-        const int drow = E.dn[0] * ((vy >> 3) + E.dn[1] * (vz >> 3));
-        const int dword = kDigestGeom + 4 * (vz & 7) + ((vy & 7) >> 1), shift = 16 * (vy & 1);
-        const int pa = __ldg(E.dir + drow + bxa);
-        const uint32_t wa = pa >= 0 ? (__ldg(T.digest + pa * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
-        uint32_t wb = wa;
-        if (bxb != bxa) {
-          const int pb = __ldg(E.dir + drow + bxb);
-          wb = pb >= 0 ? (__ldg(T.digest + pb * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
-        }
-        const uint32_t g0 = (wa >> (2 * ((vx - 1) & 7))) & 3u;
-        const uint32_t g1 = ((bxm == bxa ? wa : wb) >> (2 * (vx & 7))) & 3u;
-        const uint32_t g2 = (wb >> (2 * ((vx + 1) & 7))) & 3u;
-        has |= ((g0 & 1u) | (g1 & 1u) << 1 | (g2 & 1u) << 2) << (3 * r);
-        neg |= ((g0 >> 1) | (g1 >> 1) << 1 | (g2 >> 1) << 2) << (3 * r);
+    for (int r = 0; r < 9; ++r) {
+      const int vy = vy0 + r % 3 - 1, vz = vz0 + r / 3 - 1;
+      const int drow = E.dn[0] * ((vy >> 3) + E.dn[1] * (vz >> 3));
+      const int dword = kDigestGeom + 4 * (vz & 7) + ((vy & 7) >> 1), shift = 16 * (vy & 1);
+      const int pa = __ldg(E.dir + drow + bxa);
+      const uint32_t wa = pa >= 0 ? (__ldg(T.digest + pa * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
+      uint32_t wb = wa;
+      if (bxb != bxa) {
+        const int pb = __ldg(E.dir + drow + bxb);
+        wb = pb >= 0 ? (__ldg(T.digest + pb * kDigestWords + dword) >> shift) & 0xFFFFu : 0u;
       }
+      const uint32_t g0 = (wa >> (2 * ((vx - 1) & 7))) & 3u;
+      const uint32_t g1 = ((bxm == bxa ? wa : wb) >> (2 * (vx & 7))) & 3u;
+      const uint32_t g2 = (wb >> (2 * ((vx + 1) & 7))) & 3u;
+      has |= ((g0 & 1u) | (g1 & 1u) << 1 | (g2 & 1u) << 2) << (3 * r);
+      neg |= ((g0 >> 1) | (g1 >> 1) << 1 | (g2 >> 1) << 2) << (3 * r);
     }
-    E.gtab[x + E.nx * row] = make_uint2(has, neg);
+    E.gtab[cell] = make_uint2(has, neg);
   }
 }
 
@@ -1518,7 +1524,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
       KS_LAUNCH(k_dir_geom, (E.dcount + 255) / 256, 256, 0, e->stream, E);
       KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
-      KS_LAUNCH(k_site_tables, 8 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+      KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
     } else if (bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
       KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * plane_bytes, e->stream));  // seed plane + geometry-near plane (contiguous)
@@ -1650,7 +1656,7 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     E.xminus = E.xplus + E.wpr;
     KS_CUDA(cudaMalloc(&E.yzflags, E.ny + E.nz));
     KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
-    KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(int)));
+    KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.cells) * sizeof(int)));
   }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));

@@ -154,6 +154,32 @@ def test_scene_scatter_mode_against_oracle(oracle_lib):
     _compare_scene(oracle_lib, scenes.small_scene(41, ratio=2.0, dims=(24, 20, 18)), seeding="scatter")
 
 
+@pytest.mark.parametrize("env", [{"KS_SWEEP": "stack"}, {"KS_SEED": "bricks"}, {"KS_SWEEP": "stack", "KS_SEED": "bricks"}],
+                         ids=["stack-sweeps", "brick-gather", "round-1-path"])
+@pytest.mark.parametrize("name", ["small1", "ratio0.5-offset"])
+def test_fallback_kernels_against_oracle(oracle_lib, monkeypatch, env, name):
+    """The library picks the divide-and-conquer sweeps / resampled seeding whenever they apply; the banded-stack
+    sweeps (grids whose keys do not fit 32 bits) and the brick gather (ESDF coarser than the TSDF) are the
+    fallbacks.  The knobs are read when the ESDF is created / bound, so this forces them for one scene."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _compare_scene(oracle_lib, SCENES[name]())
+
+
+@pytest.mark.parametrize("dims,density", [((500, 33, 20), 0.001), ((37, 500, 9), 0.01), ((16, 24, 500), 0.0005), ((130, 130, 7), 0.3)])
+def test_propagate_long_axes_against_oracle(oracle_lib, dims, density):
+    """Row lengths up to BASELINE configs[2]'s 500 on each axis in turn (top levels, partial last stretch)."""
+    rng = np.random.RandomState(dims[0] + dims[1])
+    cells = dims[0] * dims[1] * dims[2]
+    mask = (rng.random_sample(cells) < density).astype(np.uint8)
+    mask[rng.randint(cells)] = 1
+    e = api.propagate(mask, api.EsdfConfig(nx=dims[0], ny=dims[1], nz=dims[2], voxel_size=0.01))
+    site, dist, d2 = e.download()
+    _, site0, dist0 = oracle_lib.propagate(mask, dims, 0.01)
+    assert np.array_equal(site, site0) and np.array_equal(dist, dist0)
+    assert np.array_equal(d2, d2_from_site(site0, dims))
+
+
 @pytest.mark.parametrize("seed", sorted(SCENE_CASES))
 def test_scene_pipeline_matches_reference_vectors(seed):
     gold = np.load(GOLD / f"scene{seed}_reference.npz")
