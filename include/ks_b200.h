@@ -130,6 +130,13 @@ KS_API int ks_tsdf_integrate_async(ks_tsdf* t);
  * update (repeated integrate_depth) is a single replayable graph; slot 0 is the one used above */
 #define KS_MAX_FRAME_SLOTS 8
 KS_API int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host);
+/* Zero-copy staging.  ks_tsdf_frame_buffer returns the pinned staging area of a slot (width*height floats,
+ * owned by the handle, stable until a larger frame is requested): a producer that writes its pixels there and
+ * passes the same pointer to ks_tsdf_stage_frame_slot skips the staging copy.  ks_tsdf_integrate_depth does
+ * the same for ANY page-locked depth_host (e.g. from ks_host_alloc): it is uploaded in place. */
+KS_API int ks_tsdf_frame_buffer(ks_tsdf* t, int32_t slot, int32_t width, int32_t height, float** out);
+KS_API int ks_host_alloc(size_t bytes, void** out);  /* page-locked host memory (cudaMallocHost) */
+KS_API void ks_host_free(void* p);
 KS_API int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot);
 KS_API int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot);
 

@@ -72,7 +72,7 @@ ABI_SYMBOLS = [
     "ks_stream_destroy", "ks_stream_sync", "ks_graph_begin_capture", "ks_graph_end_capture", "ks_graph_launch",
     "ks_graph_node_count", "ks_graph_destroy", "ks_tsdf_config_init", "ks_tsdf_create", "ks_tsdf_destroy",
     "ks_tsdf_set_stream", "ks_tsdf_get_stream", "ks_tsdf_integrate_depth", "ks_tsdf_stage_frame",
-    "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stage_frame_slot",
+    "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stage_frame_slot", "ks_tsdf_frame_buffer", "ks_host_alloc", "ks_host_free",
     "ks_tsdf_upload_frame_slot_async", "ks_tsdf_integrate_slot_async", "ks_tsdf_stamp_cuboid", "ks_tsdf_stamp_sphere",
     "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_tsdf_decay_weights",
     "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
@@ -117,6 +117,9 @@ def load_library() -> C.CDLL:
         "ks_tsdf_stage_frame": (C.c_int, [VP, P(CameraC), VP]),
         "ks_tsdf_upload_frame_async": (C.c_int, [VP]),
         "ks_tsdf_stage_frame_slot": (C.c_int, [VP, I32, P(CameraC), VP]),
+        "ks_tsdf_frame_buffer": (C.c_int, [VP, I32, I32, I32, P(VP)]),
+        "ks_host_alloc": (C.c_int, [C.c_size_t, P(VP)]),
+        "ks_host_free": (None, [VP]),
         "ks_tsdf_upload_frame_slot_async": (C.c_int, [VP, I32]),
         "ks_tsdf_integrate_slot_async": (C.c_int, [VP, I32]),
         "ks_tsdf_integrate_async": (C.c_int, [VP]),
@@ -286,6 +289,14 @@ class SparseTsdf:
         except Exception:
             pass
 
+    def frame_buffer(self, width: int, height: int, slot: int = 0) -> np.ndarray:
+        """The slot's page-locked staging area as a (height, width) float32 array: pixels written here and staged
+        with this very array skip the staging copy."""
+        out = C.c_void_p()
+        _check(self.lib.ks_tsdf_frame_buffer(self.h, slot, width, height, C.byref(out)))
+        buf = (C.c_float * (width * height)).from_address(out.value)
+        return np.frombuffer(buf, dtype=np.float32).reshape(height, width)
+
     # capturable pieces
     def stage_frame(self, frame: DepthFrame, slot: int = 0):
         depth = np.ascontiguousarray(frame.depth, np.float32).reshape(-1)
@@ -421,6 +432,29 @@ class DenseEsdf:
 
 
 # ---- the reference's free functions ------------------------------------------------------------------
+
+class PinnedArray:
+    """A page-locked float32 host array (ks_host_alloc): integrate_depth uploads such a frame in place."""
+
+    def __init__(self, shape):
+        self.lib = load_library()
+        n = int(np.prod(shape))
+        self.ptr = C.c_void_p()
+        _check(self.lib.ks_host_alloc(n * 4, C.byref(self.ptr)))
+        self.array = np.frombuffer((C.c_float * n).from_address(self.ptr.value), dtype=np.float32).reshape(shape)
+
+    def close(self):
+        if self.ptr:
+            self.array = None
+            self.lib.ks_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 def make_tsdf(config: TsdfConfig, stream: Optional[int] = None) -> SparseTsdf:  # sdf_world.hpp:327-334
     return SparseTsdf(config, stream)

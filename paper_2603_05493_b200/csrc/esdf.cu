@@ -126,7 +126,8 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
   E.qsf[i] = static_cast<float>(q - floor(q));
 }
 
-__global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
+// surf_too: also the per-block "holds surface voxels" flag the brick gather's work list is built from
+__global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T, bool surf_too) {
   const int bound = T.ctrl->next_fresh;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < bound; p += gridDim.x * blockDim.x) {
     const uint64_t key = T.pool_key[p];
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T) {
     if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
     E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
     E.dirs[bx + E.dn[0] * (by + E.dn[1] * bz)] = T.pool_geom[p];
+    if (!surf_too) continue;
     uint32_t any = 0;
 #pragma unroll
     for (int w = 0; w < 16; ++w) any |= T.digest[p * kDigestWords + w];
@@ -1499,7 +1501,7 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
 static int refresh_directory(ks_esdf* e, const ks_tsdf* t, bool bricks_too = true) {
   EsdfView& E = e->view;
   KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * (sizeof(int) + 1), e->stream));  // dir and dirs
-  KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+  KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t), bricks_too);
   if (bricks_too) {
     KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
     const int bricks = E.bnx * E.bny * E.bnz;

@@ -836,7 +836,8 @@ int ks_tsdf_set_stream(ks_tsdf* t, ks_stream s) {
 
 ks_stream ks_tsdf_get_stream(const ks_tsdf* t) { return t ? static_cast<ks_stream>(t->stream) : nullptr; }
 
-int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host) {
+// copy_pixels = false: the caller uploads the pixels from where they are (page-locked source)
+static int stage_frame_impl(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host, bool copy_pixels) {
   if (!t || !cam) return fail(KS_ERR_INVALID, "null argument");
   if (slot < 0 || slot >= KS_MAX_FRAME_SLOTS) return fail(KS_ERR_INVALID, "tsdf: camera slot out of range");
   // DepthFrame::validate (sdf_world.hpp:197-202)
@@ -858,9 +859,32 @@ int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, con
   F.w2c = rigid_inverse(F.c2w);
   F.half_samples = hs;
   F.step = step;
-  std::memcpy(S.h_depth, depth_host, pixels * sizeof(float));
+  if (copy_pixels && depth_host != S.h_depth) std::memcpy(S.h_depth, depth_host, pixels * sizeof(float));  // else written in place
   S.staged = true;
   return KS_OK;
+}
+
+int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host) {
+  return stage_frame_impl(t, slot, cam, depth_host, true);
+}
+
+int ks_tsdf_frame_buffer(ks_tsdf* t, int32_t slot, int32_t width, int32_t height, float** out) {
+  if (!t || !out) return fail(KS_ERR_INVALID, "null argument");
+  if (slot < 0 || slot >= KS_MAX_FRAME_SLOTS) return fail(KS_ERR_INVALID, "tsdf: camera slot out of range");
+  if (width <= 0 || height <= 0) return fail(KS_ERR_INVALID, "depth frame: invalid intrinsics");
+  const int rc = ensure_slot(t, slot, static_cast<size_t>(width) * height);
+  if (rc != KS_OK) return rc;
+  *out = t->slots[slot].h_depth;
+  return KS_OK;
+}
+
+int ks_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(KS_ERR_INVALID, "null argument");
+  KS_CUDA(cudaMallocHost(out, bytes));
+  return KS_OK;
+}
+void ks_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot) {
@@ -915,9 +939,22 @@ int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
 }
 
 int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float* depth_host, int32_t* blocks_touched) {
-  int rc = ks_tsdf_stage_frame(t, cam, depth_host);
+  if (!t) return fail(KS_ERR_INVALID, "null argument");
+  // a page-locked source is uploaded in place: only the camera parameters go through the staging slot
+  bool in_place = false;
+  if (depth_host && depth_host != t->slots[0].h_depth) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, depth_host) == cudaSuccess) in_place = attr.type == cudaMemoryTypeHost;
+    else cudaGetLastError();
+  }
+  int rc = stage_frame_impl(t, 0, cam, depth_host, !in_place);
   if (rc != KS_OK) return rc;
-  if ((rc = ks_tsdf_upload_frame_async(t)) != KS_OK) return rc;
+  if (in_place) {
+    ks_tsdf::FrameSlot& S = t->slots[0];
+    const size_t pixels = static_cast<size_t>(cam->width) * cam->height;
+    KS_CUDA(cudaMemcpyAsync(S.d_frame, S.h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
+    KS_CUDA(cudaMemcpyAsync(S.d_depth, depth_host, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
+  } else if ((rc = ks_tsdf_upload_frame_async(t)) != KS_OK) return rc;
   if ((rc = ks_tsdf_integrate_async(t)) != KS_OK) return rc;
   ks_tsdf_report rep;
   rc = ks_tsdf_sync(t, &rep);

@@ -457,3 +457,37 @@ def test_scene_collision_against_oracle(oracle_lib, seed):
     unsigned = api.propagate(np.ones(8, np.uint8), api.EsdfConfig(nx=2, ny=2, nz=2))
     with pytest.raises(api.ValidationError, match="scene_collision: esdf signs not recovered"):
         api.scene_collision(unsigned, centers[:, :1], radii[:1], vel[:, :1])
+
+
+def test_page_locked_frames_are_uploaded_in_place(oracle_lib):
+    """integrate_depth from ks_host_alloc memory and stage_frame from the slot's own staging area (zero-copy
+    staging) give the same world as the pageable path."""
+    scene = scenes.small_scene(1)
+    ref, touched0 = gpu_world(scene)
+    f = scene.frames[0]
+    cfg = api.make_tsdf_config(scene.tsdf_voxel)
+    cfg.capacity = scene.capacity
+    pin = api.PinnedArray((f.height, f.width))
+    pin.array[...] = np.asarray(f.depth, np.float32).reshape(f.height, f.width)
+    a = api.make_tsdf(cfg)
+    assert api.integrate_depth(a, api.DepthFrame(f.width, f.height, *f.intr, f.R, f.t, pin.array)) == touched0[0]
+    b = api.make_tsdf(cfg)
+    buf = b.frame_buffer(f.width, f.height, 0)
+    buf[...] = pin.array
+    b.stage_frame(api.DepthFrame(f.width, f.height, *f.intr, f.R, f.t, buf), 0)
+    b.upload_frame_async(0)
+    b.integrate_async(0)
+    assert b.sync().blocks_touched == touched0[0]
+    for c in scene.cuboids:
+        for t in (a, b):
+            api.stamp_primitive(t, api.Cuboid(c.R, c.t, c.half_extents))
+    for s in scene.spheres:
+        for t in (a, b):
+            api.stamp_primitive(t, api.SphereShape(s.center, s.radius))
+    rk, rp = ref.export_blocks()
+    for t in (a, b):
+        k, p = t.export_blocks()
+        assert np.array_equal(k, rk) and np.array_equal(p, rp)
+        for x, y in zip(t.download_blocks(p[:8]), ref.download_blocks(rp[:8])):
+            assert same_bits(x, y)
+    pin.close()

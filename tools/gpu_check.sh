@@ -2,7 +2,7 @@
 # Run on the GPU box via gpurun: GPU tests, bench (both arms), ncu launch list and one full capture.
 # Usage: tools/gpu_check.sh [tag] [kernel-regex-for-full-capture]
 TAG=${1:-r1}
-KREGEX=${2:-k_sweep_x}
+KREGEX=${2:-k_sweep_x_dc}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
