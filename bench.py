@@ -321,7 +321,7 @@ def run_ours(args):
             for p in self.prims:
                 api.stamp_primitive(self.tsdf, p)
             api.build_esdf(self.tsdf, self.ecfg, self.esdf)
-            r = self.esdf.report()                              # D2H: has_sites / seed count
+            r = self.esdf.last_report()                         # has_sites / seed count, read back by build_esdf (D2H)
             if self.queries is not None:
                 api.query(self.esdf, self.queries_host)         # H2D points, D2H distance + gradient + inside
             return k, r.seed_count

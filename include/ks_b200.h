@@ -195,6 +195,8 @@ KS_API int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_
 /* recover_signs (esdf.hpp:288-320) on the field left by ks_esdf_propagate */
 KS_API int ks_esdf_recover_signs(ks_esdf* e, const ks_tsdf* t);
 KS_API int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report);
+/* what the last ks_esdf_sync / blocking call saw (DenseEsdf::has_sites, ::signs_recovered as plain members); no wait */
+KS_API int ks_esdf_last_report(const ks_esdf* e, ks_esdf_report* report);
 /* measurement hook: device ms of {directory, seeding, z flood, y sweep, x sweep, sign recovery}
  * of the last non-captured ks_esdf_build_async */
 KS_API int ks_esdf_profile(ks_esdf* e, int32_t enable);

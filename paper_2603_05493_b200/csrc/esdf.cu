@@ -1757,6 +1757,15 @@ int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {
   return KS_OK;
 }
 
+int ks_esdf_last_report(const ks_esdf* e, ks_esdf_report* report) {
+  if (!e || !report) return fail(KS_ERR_INVALID, "null argument");
+  report->status = KS_OK;
+  report->has_sites = e->h_ctrl->seed_count > 0;
+  report->signs_recovered = e->h_ctrl->signs_recovered != 0;
+  report->seed_count = static_cast<int64_t>(e->h_ctrl->seed_count);
+  return KS_OK;
+}
+
 int ks_esdf_build(ks_esdf* e, const ks_tsdf* t) {
   int rc = ks_esdf_build_async(e, t);
   return rc != KS_OK ? rc : ks_esdf_sync(e, nullptr);

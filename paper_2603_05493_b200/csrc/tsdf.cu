@@ -60,6 +60,12 @@ struct ks_tsdf {
   cudaStream_t stream;
   bool own_stream;
   TsdfCtrl* h_ctrl;  // pinned
+  // Lower bounds, as of the last synchronisation minus what was enqueued since, on the free pool entries and
+  // the free hash slots.  A blocking stamp whose candidate blocks fit both cannot fail on the device
+  // (exhaustion / table full / range are the only device-side errors), so it returns without waiting.
+  bool bounds_valid;
+  long long known_avail, known_room;
+  bool last_stamp_safe;  // the stamp enqueued last fits those bounds (and its block range is legal)
   // frame staging: one slot per camera, so a multi-camera update is one graph
   struct FrameSlot {
     FrameParams* h_frame;  // pinned
@@ -709,6 +715,14 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
     if (B.n[a] < 1) B.n[a] = 0;
     B.count *= B.n[a];
   }
+  {  // at most B.count blocks are new: can this stamp fail on the device at all?
+    bool safe = t->bounds_valid && B.count <= t->known_avail && B.count <= t->known_room;
+    for (int a = 0; a < 3; ++a)
+      if (B.lo[a] <= -kKeyBias || B.lo[a] + B.n[a] >= kKeyBias) safe = false;
+    if (safe) t->known_avail -= B.count, t->known_room -= B.count;
+    else t->bounds_valid = false;  // unknown until the next synchronisation
+    t->last_stamp_safe = safe;
+  }
   const double reach = trunc + 0.5 * kBlockEdge * v * std::sqrt(3.0);  // sdf_world.hpp:288-290, :425
   if (B.count > 0) {
     const int grid = static_cast<int>(std::min<long long>((B.count + 255) / 256, 8 * kSmCount));
@@ -901,6 +915,7 @@ int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) {
   ks_tsdf::FrameSlot& S = t->slots[slot];
   const int pixels = S.h_frame->width * S.h_frame->height;
   const bool prof = profiling(t);
+  t->bounds_valid = false;  // a frame allocates a number of blocks only the device knows
   KS_MARK(t, 0);
   KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_MARK(t, 1);
@@ -925,6 +940,9 @@ int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
     KS_CUDA(cudaMemsetAsync(&t->view.ctrl->err, 0, sizeof(int), t->stream));
     KS_CUDA(cudaStreamSynchronize(t->stream));
   }
+  t->bounds_valid = c.err == 0;
+  t->known_avail = static_cast<long long>(t->view.capacity) - c.next_fresh + c.free_count;  // BlockHashTable::available
+  t->known_room = static_cast<long long>(t->view.nslots) - c.live;
   if (report) {
     report->status = c.err;
     report->blocks_touched = c.last_touched;
@@ -1004,14 +1022,24 @@ int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double radius
   return stamp_async(t, P, lo, hi);
 }
 
+// stamp_primitive throws on exhaustion (sdf_world.hpp:436-439).  When the candidate blocks of the stamp just
+// enqueued fit the known free pool entries and hash slots, that cannot happen and the call returns at once;
+// otherwise it waits for the device's verdict.
+static int finish_stamp(ks_tsdf* t) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(t->stream, &cap);
+  if (cap == cudaStreamCaptureStatusNone && t->last_stamp_safe) return KS_OK;
+  return ks_tsdf_sync(t, nullptr);
+}
+
 int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t[3], const double he[3]) {
   int rc = ks_tsdf_stamp_cuboid_async(t, pose_R, pose_t, he);
-  return rc != KS_OK ? rc : ks_tsdf_sync(t, nullptr);
+  return rc != KS_OK ? rc : finish_stamp(t);
 }
 
 int ks_tsdf_stamp_sphere(ks_tsdf* t, const double center[3], double radius) {
   int rc = ks_tsdf_stamp_sphere_async(t, center, radius);
-  return rc != KS_OK ? rc : ks_tsdf_sync(t, nullptr);
+  return rc != KS_OK ? rc : finish_stamp(t);
 }
 
 int ks_tsdf_decay_weights_async(ks_tsdf* t, const ks_camera* cam) {

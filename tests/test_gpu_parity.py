@@ -491,3 +491,24 @@ def test_page_locked_frames_are_uploaded_in_place(oracle_lib):
         for x, y in zip(t.download_blocks(p[:8]), ref.download_blocks(rp[:8])):
             assert same_bits(x, y)
     pin.close()
+
+
+def test_stamp_reports_exhaustion_at_the_call(oracle_lib):
+    """stamp_primitive returns without waiting only when its candidate blocks provably fit the free pool; a
+    stamp that does not fit must still raise at the call, with the reference's text, and leave the world as is."""
+    big = api.Cuboid(np.eye(3), np.array([0.4, 0.4, 0.4]), np.array([0.3, 0.3, 0.3]))
+    small = api.SphereShape(np.array([0.1, 0.1, 0.1]), 0.03)
+    cfg = api.make_tsdf_config(0.02)
+    cfg.capacity = 64
+    tsdf = api.make_tsdf(cfg)
+    cpu = oracle_lib.make_tsdf(0.02, capacity=64)
+    api.stamp_primitive(tsdf, small)       # fits: the fast return
+    cpu.stamp_sphere(small.center, small.radius)
+    with pytest.raises(Exception) as ref:
+        cpu.stamp_cuboid(big.pose_R, big.pose_t, big.half_extents)
+    with pytest.raises(api.ValidationError) as got:
+        api.stamp_primitive(tsdf, big)     # does not fit: waits for the device's verdict
+    assert str(got.value) == str(ref.value).split(": ", 1)[-1] or str(got.value) in str(ref.value)
+    assert api.allocated_block_count(tsdf) == cpu.allocated_block_count()
+    api.stamp_primitive(tsdf, small)       # and the handle keeps working
+    assert_world_parity(tsdf, cpu)
