@@ -79,7 +79,11 @@ struct EsdfView {
   uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
   uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
                        // at the 27 voxels around the site's centre voxel, bit = (ox+1) + 3(oy+1) + 9(oz+1)
-  uint16_t* near_z;  // [cells] x-fastest phase-1 result
+  uint16_t* near_z;  // [cells] x-fastest phase-1 result (banded-stack fallback only)
+  // phase 1 of the divide-and-conquer path (aliases near_z): every column's seeds as a bit string along z
+  uint32_t* zbits;   // [ny][nzw][nx] word w of column (x, y): bit b = cell z = 32w + b is a seed
+  uint32_t* zinfo;   // same layout: nearest seed z in the words below w | the words above w << 16 (0xFFFF: none)
+  int nzw;           // words per column
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
   uint32_t* site;    // [cells] y-fastest
   uint32_t* d2s;     // [cells] y-fastest
@@ -615,6 +619,60 @@ __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
   }
 }
 
+// byte mask (the reference's SeedMask) -> x-packed bit plane, one warp per word
+__global__ void __launch_bounds__(256) k_pack_mask(EsdfView E) {
+  const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp_id >= E.wpr * E.ny * E.nz) return;
+  const int xw = warp_id % E.wpr, row = warp_id / E.wpr;
+  const int x = 32 * xw + lane;
+  const uint32_t bits = __ballot_sync(0xFFFFFFFFu, x < E.nx && E.mask[x + E.nx * row] != 0);
+  if (lane == 0) E.mbits[warp_id] = bits;
+}
+
+// Phase 1 of the divide-and-conquer path (esdf.hpp:213-233), as data for phase 2 rather than a field: one CTA
+// per 32 consecutive x columns of one y, one warp per 32 z.  Warp w transposes its 32(z) x 32(x) bit tile of
+// the x-packed mask into word w of every column's bit string and adds, per word, the nearest seed in the
+// words below and above.  Phase 2 resolves "nearest seed along z" from one word + one info word per
+// candidate, so the 2-byte-per-cell nearest-z field is never written or read.
+__global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
+  extern __shared__ uint32_t s_words[];  // [nzw][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int xw = blockIdx.x % E.wpr, y = blockIdx.x / E.wpr;
+  const int x = xw * 32 + lane;
+  {
+    const int z = 32 * w + lane;
+    const uint32_t mine = z < E.nz ? __ldg(E.mbits + (z * E.ny + y) * E.wpr + xw) : 0u;  // 32 x-bits of row (y, z)
+    uint32_t bits = 0;
+#pragma unroll
+    for (int xb = 0; xb < 32; ++xb) {
+      const uint32_t col = __ballot_sync(0xFFFFFFFFu, (mine >> xb) & 1u);  // column xb: bit z
+      if (lane == xb) bits = col;
+    }
+    s_words[w * 32 + lane] = bits;
+  }
+  __syncthreads();
+  if (x >= E.nx) return;
+  uint32_t below = 0xFFFFu, above = 0xFFFFu;
+  for (int k = w - 1; k >= 0; --k) {
+    const uint32_t m = s_words[k * 32 + lane];
+    if (m != 0) {
+      below = 32 * k + 31 - __clz(static_cast<int>(m));
+      break;
+    }
+  }
+  for (int k = w + 1; k < E.nzw; ++k) {
+    const uint32_t m = s_words[k * 32 + lane];
+    if (m != 0) {
+      above = 32 * k + __ffs(static_cast<int>(m)) - 1;
+      break;
+    }
+  }
+  const int o = (y * E.nzw + w) * E.nx + x;
+  E.zbits[o] = s_words[w * 32 + lane];
+  E.zinfo[o] = below | above << 16;
+}
+
 // The fused build's phase 1: one CTA per 32 consecutive x columns of one y, one warp per 32 z.  Warp w
 // transposes its 32(z) x 32(x) bit tile of the x-packed mask into word w of every column's bit string
 // (shared memory, [word][lane]); after the barrier it walks its own 32 z upwards, so a column's work is
@@ -1028,17 +1086,32 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   uint32_t* Kt = G + ny * 32;
   const bool live = x < nx && z < E.nz;
   const int zoff = nx * ny * min(z, E.nz - 1) + min(x, nx - 1);
-  for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
-    uint16_t v[kLoadBatch];
+  {  // candidates: the nearest seed along z of every column (esdf.hpp:213-233; ties keep the lower z, strict '<' :229)
+    const int zc = min(z, E.nz - 1);
+    const int col = (zc >> 5) * nx + min(x, nx - 1), stride = E.nzw * nx;
+    const int zbase = zc & ~31, zb = zc & 31;
+    const uint32_t le = 0xFFFFFFFFu >> (31 - zb), ge = 0xFFFFFFFFu << zb;
+    for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
+      uint32_t wd[kLoadBatch], inf[kLoadBatch];
 #pragma unroll
-    for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(E.near_z + zoff + nx * min(yb + i, ny - 1));
+      for (int i = 0; i < kLoadBatch; ++i) {
+        const int o = col + stride * min(yb + i, ny - 1);
+        wd[i] = __ldg(E.zbits + o), inf[i] = __ldg(E.zinfo + o);
+      }
 #pragma unroll
-    for (int i = 0; i < kLoadBatch; ++i) {
-      const int y = yb + i;
-      const int dz = static_cast<int>(v[i]) - z;
-      const uint32_t g = (v[i] == edt::kNone || !live) ? KeysY::pack(none_y, y, 0)
-                                                        : KeysY::pack(static_cast<uint32_t>(dz * dz), y, dz > 0 ? 1u : 0u);
-      if (y < ny) G[edt_dc::at(y, lane)] = g;
+      for (int i = 0; i < kLoadBatch; ++i) {
+        const int y = yb + i;
+        const uint32_t lo_m = wd[i] & le, hi_m = wd[i] & ge;
+        const int below = lo_m ? zbase + 31 - __clz(static_cast<int>(lo_m)) : static_cast<int>(inf[i] & 0xFFFFu);
+        const int above = hi_m ? zbase + __ffs(static_cast<int>(hi_m)) - 1 : static_cast<int>(inf[i] >> 16);
+        const bool has_b = below != 0xFFFF, has_a = above != 0xFFFF;
+        const int db = zc - below, da = above - zc;
+        const bool up = has_a && (!has_b || da < db);
+        const int dz = up ? da : db;
+        const uint32_t g = (!(has_a || has_b) || !live) ? KeysY::pack(none_y, y, 0)
+                                                         : KeysY::pack(static_cast<uint32_t>(dz * dz), y, up && dz > 0 ? 1u : 0u);
+        if (y < ny) G[edt_dc::at(y, lane)] = g;
+      }
     }
   }
   for (int i = warp; i <= ny >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
@@ -1548,7 +1621,10 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   const unsigned fgrid = static_cast<unsigned>((E.wpr * E.ny + kFloodWarps - 1) / kFloodWarps);
   const size_t fsmem = static_cast<size_t>(nwords) * 32 * kFloodWarps * sizeof(uint32_t);
   (void)plane;
-  if (bits) KS_LAUNCH(k_flood_z_chunks, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
+  if (e->dc) {
+    if (!bits) KS_LAUNCH(k_pack_mask, (E.wpr * E.ny * E.nz + 7) / 8, 256, 0, e->stream, E);  // the reference's byte mask -> bit plane
+    KS_LAUNCH(k_flood_cols, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
+  } else if (bits) KS_LAUNCH(k_flood_z_chunks, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
@@ -1661,7 +1737,12 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.cells) * sizeof(int)));
   }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
-  KS_CUDA(cudaMalloc(&E.near_z, E.cells * sizeof(uint16_t)));
+  E.nzw = (E.nz + 31) / 32;
+  {
+    const size_t col_words = static_cast<size_t>(E.nzw) * E.ny * E.nx;
+    KS_CUDA(cudaMalloc(&E.near_z, std::max(static_cast<size_t>(E.cells) * sizeof(uint16_t), 2 * col_words * sizeof(uint32_t))));
+    E.zbits = reinterpret_cast<uint32_t*>(E.near_z), E.zinfo = E.zbits + col_words;
+  }
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.site, E.cells * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.d2s, E.cells * sizeof(uint32_t)));
