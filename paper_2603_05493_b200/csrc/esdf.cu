@@ -1124,11 +1124,22 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
     });
 }
 
-// grid = (ceil(ny/8), ceil(nz/4)); lane <-> (y, z), positions = x.  The x-fastest input rows (phase 2's keys) are
-// loaded coalesced into K with a bank rotation and packed into G in the [x][lane] layout.  kSigns as in
-// k_sweep_x, 3 = from the per-site tables of the resampled seeding.  A warp colours each stretch right after resolving it, walking x upwards so that what
-// depends only on the site is reused while the winner stays the same.
-template <int kSigns>
+// grid = (ceil(ny/8), ceil(nz/4)); lane <-> (y, z), positions = x.  kSigns as in k_sweep_x, 3 = from the per-site
+// tables of the resampled seeding.  A warp colours each stretch right after resolving it, walking x upwards so
+// that what depends only on the site is reused while the winner stays the same.
+//
+// Tile fill.  The input rows (phase 2's keys) are x-fastest, the tile wants [x][row].  kChunks (nx % 4 == 0):
+// every thread sends 16-byte chunks of the rows straight to shared memory with cp.async -- the whole 51 KB tile
+// is in flight at once, no register staging -- to a chunk-rotated place: chunk c of row r at 16-byte slot
+// c*32 + ((r + c) & 31).  A lane then reads ITS row's chunk c with one conflict-free LDS.128, packs four
+// candidates into G and writes the four slots back in place.  Otherwise: 4-byte loads through registers into a
+// word-rotated layout.  Either way the slot of (row, x) later holds {winner of x : 16 | candidate's site_y, side : 16}.
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gmem_src));
+}
+
+template <int kSigns, bool kChunks>
 __global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
@@ -1137,18 +1148,30 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, 
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
   uint32_t* K = G + nx * 32;
   uint32_t* Kt = K + nx * 32;
-  for (int r = warp; r < 32; r += nwarps) {
-    const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
-    const uint32_t* row = E.yz + nx * (min(yr, ny - 1) + ny * min(zr, E.nz - 1));
-    const uint32_t dead = yr < ny && zr < E.nz ? 0u : 0xFFFFFFFFu;
-    for (int xb = lane; xb < nx; xb += 32 * kLoadBatch) {
-      uint32_t v[kLoadBatch];
+  if constexpr (kChunks) {
+    const int chunks = nx >> 2;
+    for (int i = threadIdx.x; i < 32 * chunks; i += blockDim.x) {
+      const int r = i / chunks, c = i - r * chunks;  // consecutive threads: consecutive chunks of one row
+      const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
+      uint32_t* dst = K + 4 * (c * 32 + ((r + c) & 31));
+      if (yr < ny && zr < E.nz) cp_async_16(dst, E.yz + nx * (yr + ny * zr) + 4 * c);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);  // padding row: no candidate
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    for (int r = warp; r < 32; r += nwarps) {
+      const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
+      const uint32_t* row = E.yz + nx * (min(yr, ny - 1) + ny * min(zr, E.nz - 1));
+      const uint32_t dead = yr < ny && zr < E.nz ? 0u : 0xFFFFFFFFu;
+      for (int xb = lane; xb < nx; xb += 32 * kLoadBatch) {
+        uint32_t v[kLoadBatch];
 #pragma unroll
-      for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(row + min(xb + 32 * i, nx - 1));
+        for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(row + min(xb + 32 * i, nx - 1));
 #pragma unroll
-      for (int i = 0; i < kLoadBatch; ++i) {
-        const int x = xb + 32 * i;
-        if (x < nx) K[x * 32 + ((r + x) & 31)] = v[i] | dead;
+        for (int i = 0; i < kLoadBatch; ++i) {
+          const int x = xb + 32 * i;
+          if (x < nx) K[x * 32 + ((r + x) & 31)] = v[i] | dead;
+        }
       }
     }
   }
@@ -1156,19 +1179,30 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, 
   float* s_qsf = reinterpret_cast<float*>(Kt + ((nx >> kTopShift) + 1) * 32);
   if constexpr (kSigns == 3)
     for (int i = threadIdx.x; i < nx + ny + E.nz; i += blockDim.x) s_qsf[i] = E.qsf[i];
+  if constexpr (kChunks) asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int y = y0 + (lane & (kTileA - 1)), z = min(z0 + lane / kTileA, E.nz - 1);
   const bool live = y < ny && z0 + lane / kTileA < E.nz;
-  // The slot of (this lane's row, position x) in the rotated layout.  After the conversion below its low
-  // half keeps what phase 3 still needs of the candidate at x (site_y << 1 | seed above z; its in-plane d2
-  // is in G) and its high half receives the winner of position x -- so the tile needs no third array.
-  auto slot = [&](int x) { return x * 32 + ((lane + x) & 31); };
+  // the slot of (this lane's row, position x)
+  auto slot = [&](int x) {
+    if constexpr (kChunks) return 4 * ((x >> 2) * 32 + ((lane + (x >> 2)) & 31)) + (x & 3);
+    else return x * 32 + ((lane + x) & 31);
+  };
   uint16_t* K16 = reinterpret_cast<uint16_t*>(K);
-  for (int x = warp; x < nx; x += nwarps) {
-    const uint32_t v = K[slot(x)];
-    const uint32_t r2 = KeysY::cost(v);  // in-plane d2 of the candidate at x
+  auto convert = [&](int x, uint32_t v) {  // candidate at x: in-plane d2 into G, what phase 3 still needs of it stays in the slot
+    const uint32_t r2 = KeysY::cost(v);
     G[edt_dc::at(x, lane)] = KeysX::pack(r2 >= none_y ? none_x : r2, x, 0);
-    K[slot(x)] = v & KeysY::kLowMask;
+    return v & KeysY::kLowMask;
+  };
+  if constexpr (kChunks) {
+    for (int c = warp; c < (nx >> 2); c += nwarps) {
+      uint4* q = reinterpret_cast<uint4*>(K + 4 * (c * 32 + ((lane + c) & 31)));
+      uint4 v = *q;
+      v.x = convert(4 * c, v.x), v.y = convert(4 * c + 1, v.y), v.z = convert(4 * c + 2, v.z), v.w = convert(4 * c + 3, v.w);
+      *q = v;
+    }
+  } else {
+    for (int x = warp; x < nx; x += nwarps) K[slot(x)] = convert(x, K[slot(x)]);
   }
   __syncthreads();
   dc_top_levels<0>(G, Kt, nx, warp, lane, warps_log2);
@@ -1634,10 +1668,21 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (e->dc) {
     const dim3 xgrid((E.ny + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
     const unsigned threads = 32u << e->dc_wl_x;
-    if (t && bits && fast_build(e)) KS_LAUNCH(k_sweep_x_dc<3>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
-    else if (t && bits) KS_LAUNCH(k_sweep_x_dc<2>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
-    else if (t) KS_LAUNCH(k_sweep_x_dc<1>, xgrid, threads, e->smem_x, e->stream, E, tsdf_view(t), e->dc_wl_x, e->none_y, e->none_x);
-    else KS_LAUNCH(k_sweep_x_dc<0>, xgrid, threads, e->smem_x, e->stream, E, TsdfView{}, e->dc_wl_x, e->none_y, e->none_x);
+    const int mode = t && bits && fast_build(e) ? 3 : (t && bits ? 2 : (t ? 1 : 0));
+    const TsdfView tv = t ? tsdf_view(t) : TsdfView{};
+#define KS_X_DC(M, C) KS_LAUNCH((k_sweep_x_dc<M, C>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_y, e->none_x)
+    if (E.nx % 4 == 0) {  // rows start 16-byte aligned: tile filled by cp.async
+      if (mode == 3) KS_X_DC(3, true);
+      else if (mode == 2) KS_X_DC(2, true);
+      else if (mode == 1) KS_X_DC(1, true);
+      else KS_X_DC(0, true);
+    } else {
+      if (mode == 3) KS_X_DC(3, false);
+      else if (mode == 2) KS_X_DC(2, false);
+      else if (mode == 1) KS_X_DC(1, false);
+      else KS_X_DC(0, false);
+    }
+#undef KS_X_DC
   } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
     KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
   } else if (t) {
@@ -1706,10 +1751,10 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
+#define KS_X_ATTR(M, C) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)))
+  KS_X_ATTR(0, true); KS_X_ATTR(1, true); KS_X_ATTR(2, true); KS_X_ATTR(3, true);
+  KS_X_ATTR(0, false); KS_X_ATTR(1, false); KS_X_ATTR(2, false); KS_X_ATTR(3, false);
+#undef KS_X_ATTR
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
