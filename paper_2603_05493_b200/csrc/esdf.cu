@@ -1139,8 +1139,9 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src
                "l"(gmem_src));
 }
 
-template <int kSigns, bool kChunks>
-__global__ void __launch_bounds__(512, 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
+// kBig: rows so long that only one tile fits an SM -- then the tile gets 32 warps instead of 16
+template <int kSigns, bool kChunks, bool kBig>
+__global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
@@ -1670,18 +1671,19 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
     const unsigned threads = 32u << e->dc_wl_x;
     const int mode = t && bits && fast_build(e) ? 3 : (t && bits ? 2 : (t ? 1 : 0));
     const TsdfView tv = t ? tsdf_view(t) : TsdfView{};
-#define KS_X_DC(M, C) KS_LAUNCH((k_sweep_x_dc<M, C>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_y, e->none_x)
+#define KS_X_DC(M, C, B) KS_LAUNCH((k_sweep_x_dc<M, C, B>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_y, e->none_x)
+#define KS_X_DC_MODE(C, B)        \
+  if (mode == 3) KS_X_DC(3, C, B);      \
+  else if (mode == 2) KS_X_DC(2, C, B); \
+  else if (mode == 1) KS_X_DC(1, C, B); \
+  else KS_X_DC(0, C, B)
+    const bool big = e->dc_wl_x == 5;
     if (E.nx % 4 == 0) {  // rows start 16-byte aligned: tile filled by cp.async
-      if (mode == 3) KS_X_DC(3, true);
-      else if (mode == 2) KS_X_DC(2, true);
-      else if (mode == 1) KS_X_DC(1, true);
-      else KS_X_DC(0, true);
+      if (big) { KS_X_DC_MODE(true, true); } else { KS_X_DC_MODE(true, false); }
     } else {
-      if (mode == 3) KS_X_DC(3, false);
-      else if (mode == 2) KS_X_DC(2, false);
-      else if (mode == 1) KS_X_DC(1, false);
-      else KS_X_DC(0, false);
+      if (big) { KS_X_DC_MODE(false, true); } else { KS_X_DC_MODE(false, false); }
     }
+#undef KS_X_DC_MODE
 #undef KS_X_DC
   } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
     KS_LAUNCH(k_sweep_x<2>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, tsdf_view(t), e->band_x, e->bands_x);
@@ -1737,9 +1739,12 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     if (const char* v = std::getenv("KS_SWEEP")) e->dc = e->dc && std::strcmp(v, "stack") != 0;
     e->none_y = KeysY::none_offset(E.ny, gmax_y);
     e->none_x = KeysX::none_offset(E.nx, gmax_x);
-    e->dc_wl_y = 3, e->dc_wl_x = 4;
+    // warps per tile: 8 (y) and 16 (x) measured best while several tiles share an SM (tools/ab_sweeps.sh); long rows
+    // leave room for fewer tiles, which then get more warps each
+    e->dc_wl_y = dc_smem_bytes_y(E.ny) > 56 * 1024 ? 4 : 3;
+    e->dc_wl_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) > 113 * 1024 ? 5 : 4;
     if (const char* v = std::getenv("KS_DC_WARPS_Y")) e->dc_wl_y = std::min(4, std::max(0, std::atoi(v)));
-    if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(4, std::max(0, std::atoi(v)));
+    if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(5, std::max(0, std::atoi(v)));
     if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz);
   }
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
@@ -1751,9 +1756,10 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-#define KS_X_ATTR(M, C) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)))
-  KS_X_ATTR(0, true); KS_X_ATTR(1, true); KS_X_ATTR(2, true); KS_X_ATTR(3, true);
-  KS_X_ATTR(0, false); KS_X_ATTR(1, false); KS_X_ATTR(2, false); KS_X_ATTR(3, false);
+#define KS_X_ATTR(M, C, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)))
+#define KS_X_ATTR4(C, B) KS_X_ATTR(0, C, B); KS_X_ATTR(1, C, B); KS_X_ATTR(2, C, B); KS_X_ATTR(3, C, B)
+  KS_X_ATTR4(true, false); KS_X_ATTR4(false, false); KS_X_ATTR4(true, true); KS_X_ATTR4(false, true);
+#undef KS_X_ATTR4
 #undef KS_X_ATTR
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
