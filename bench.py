@@ -200,8 +200,8 @@ def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcou
         "stamp_blocks": Kp * (512 * (8 + 8 + 16) + 320),
         "directory": 4.0 * dcount + 8.0 * L,
         "seed": 3.0 * C_ / 8.0 + 6.0 * C_ / 8.0 + 2.0 * C_ / 8.0 + 128.0 * L + 5.0 * dcount,  # 3 resampled planes out; 5 rows + near row in, seed + near planes out; digest rows + directory in
-        "flood_z": C_ / 8.0 + 2.0 * C_,                               # bit mask in, nearest-z (u16) out
-        "sweep_y": 2.0 * C_ + 4.0 * C_,                               # u16 in, winning key u32 out
+        "flood_z": C_ / 8.0 + 2.0 * C_ / 8.0,                         # bit mask in; column bit strings + per-word info out
+        "sweep_y": 2.0 * C_ / 8.0 + 4.0 * C_,                         # column words + info in, winning key u32 out
         "sweep_x": 4.0 * C_ + 8.0 * C_ + C_ / 8.0,                    # u32 in, site u32 + signed d2 u32 out, own-sign plane
         "signs": 0.0,                                                 # fused into sweep_x
     }[stage]
