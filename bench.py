@@ -327,12 +327,10 @@ def run_ours(args):
             return k, r.seed_count
 
         def summary_into(self, row):
-            """collision summary of this environment: probe-sphere minimum distance and near-contact count"""
-            api._check(self.esdf.lib.ks_esdf_query_device_async(self.esdf.h, C.c_void_p(self.probes.data_ptr()), 4096,
-                                                               C.c_void_p(self.probe_d.data_ptr()), None, None))
-            row[0] = self.env_id
-            row[1] = self.probe_d.min()
-            row[2] = (self.probe_d < 0.02).sum()
+            """collision summary of this environment (env id, probe-sphere minimum distance, near-contact count, seeds):
+            one kernel, written straight into this environment's row of the exchange buffer"""
+            api._check(self.esdf.lib.ks_esdf_probe_summary_device_async(
+                self.esdf.h, C.c_void_p(self.probes.data_ptr()), 4096, 0.02, float(self.env_id), C.c_void_p(row.data_ptr())))
 
     envs = [Environment(e) for e in range(env_lo, env_hi)]
     scene = envs[0].scene
@@ -344,17 +342,18 @@ def run_ours(args):
     n_queries = 0 if envs[0].queries is None else int(envs[0].queries.shape[0])
     exchange = world > 1 or E_local > 1
 
-    def enqueue_update(upload: bool):
-        for env in envs:
-            env.enqueue_update(upload)
-
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     summary_local, summary_all, _valid_rows = multi_env.summary_buffers(n_envs, world, rank, "cuda")
 
-    def gather_summaries():
-        """per-environment collision summaries, all-gathered over NCCL (the only collective on this path)."""
+    def enqueue_update(upload: bool):
         for i, env in enumerate(envs):
-            env.summary_into(summary_local[i])
+            env.enqueue_update(upload)
+            if exchange:  # the environment's collision summary is one more kernel of the same (captured) update
+                env.summary_into(summary_local[i])
+
+    def gather_summaries():
+        """per-environment collision summaries (written by the update itself), all-gathered over NCCL -- the only
+        collective on this path."""
         if world > 1 and share_gpu:
             host_all = torch.empty(summary_all.shape, dtype=torch.float64)
             dist.all_gather_into_tensor(host_all, summary_local.cpu())

@@ -212,6 +212,10 @@ KS_API int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, doubl
 /* the same with device-resident buffers, enqueued on the handle's stream */
 KS_API int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, double* distance_dev,
                                       double* gradient_dev, uint8_t* inside_dev);
+/* one launch, capturable: {tag, min distance over the n probe points, probes closer than near_distance, seed count}
+ * as four doubles at summary_dev -- the fixed-size per-environment summary that multi-GPU runs all-gather */
+KS_API int ks_esdf_probe_summary_device_async(ks_esdf* e, const double* points_dev, int64_t n, double near_distance,
+                                              double tag, double* summary_dev);
 
 /* ---- scene collision (SURVEY 8f "next": the consumer of query) ---------------- */
 /* CollisionReport / SceneTimestepReport scalars (collision.hpp:46-52, :161-168) */

@@ -78,7 +78,7 @@ ABI_SYMBOLS = [
     "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
     "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
     "ks_tsdf_free_list", "ks_tsdf_profile", "ks_tsdf_stage_ms", "ks_esdf_profile", "ks_esdf_stage_ms", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
-    "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync", "ks_esdf_last_report",
+    "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync", "ks_esdf_last_report", "ks_esdf_probe_summary_device_async",
     "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async", "ks_esdf_scene_collision_static",
     "ks_esdf_scene_collision_swept",
 ]
@@ -151,6 +151,7 @@ def load_library() -> C.CDLL:
         "ks_esdf_recover_signs": (C.c_int, [VP, VP]),
         "ks_esdf_sync": (C.c_int, [VP, P(EsdfReportC)]),
         "ks_esdf_last_report": (C.c_int, [VP, P(EsdfReportC)]),
+        "ks_esdf_probe_summary_device_async": (C.c_int, [VP, VP, C.c_int64, C.c_double, C.c_double, VP]),
         "ks_esdf_download": (C.c_int, [VP, VP, VP, VP]),
         "ks_esdf_query": (C.c_int, [VP, VP, I64, VP, VP, VP]),
         "ks_esdf_query_device_async": (C.c_int, [VP, VP, I64, VP, VP, VP]),

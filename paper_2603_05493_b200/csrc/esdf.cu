@@ -1332,6 +1332,56 @@ __global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restr
   if (grad) grad[3 * i] = g[0], grad[3 * i + 1] = g[1], grad[3 * i + 2] = g[2];
 }
 
+// Per-environment summary for the multi-environment exchange: {tag, minimum distance over the
+// probe points, number of probes closer than `near`, seed count} as four doubles, in one capturable launch.
+// One probe per thread; the last CTA to finish folds the per-CTA partials (fixed order: deterministic).
+constexpr int kSummaryCtas = 64;
+struct SummaryScratch {
+  double part_min[kSummaryCtas];
+  int part_cnt[kSummaryCtas];
+  unsigned arrivals;
+};
+__global__ void __launch_bounds__(128) k_probe_summary(EsdfView E, const double* __restrict__ pts, int n, double near, double tag,
+                                                       SummaryScratch* scratch, double* __restrict__ out) {
+  __shared__ double s_min[4];
+  __shared__ int s_cnt[4];
+  __shared__ bool s_last;
+  double best = CUDART_INF;
+  int count = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    double d, g[3];
+    bool in;
+    query_point(E, p, d, g, in);
+    best = d < best ? d : best;
+    count += d < near;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double other = __shfl_down_sync(0xFFFFFFFFu, best, o);
+    best = other < best ? other : best;
+    count += __shfl_down_sync(0xFFFFFFFFu, count, o);
+  }
+  if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = best, s_cnt[threadIdx.x >> 5] = count;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 4; ++w) best = s_min[w] < best ? s_min[w] : best, count += s_cnt[w];
+    scratch->part_min[blockIdx.x] = best, scratch->part_cnt[blockIdx.x] = count;
+    __threadfence();
+    s_last = atomicAdd(&scratch->arrivals, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    best = CUDART_INF, count = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      const double m = scratch->part_min[b];
+      best = m < best ? m : best, count += scratch->part_cnt[b];
+    }
+    out[0] = tag, out[1] = best, out[2] = static_cast<double>(count), out[3] = static_cast<double>(E.ctrl->seed_count);
+    scratch->arrivals = 0;  // ready for the next launch
+  }
+}
+
 // ---- scene collision (collision.hpp:30-44, :130-239) ----
 __device__ __forceinline__ double hinge_cost(double clearance, double margin) {  // collision.hpp:30-37
   if (clearance >= margin) return 0.0;
@@ -1499,6 +1549,7 @@ struct ks_esdf {
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
+  SummaryScratch* summary_scratch;  // partials of k_probe_summary
   bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
   int dc_wl_y, dc_wl_x;    // log2(warps per tile)
@@ -1798,6 +1849,8 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMalloc(&E.site, E.cells * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.d2s, E.cells * sizeof(uint32_t)));
   KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
+  KS_CUDA(cudaMalloc(&e->summary_scratch, sizeof(SummaryScratch)));
+  KS_CUDA(cudaMemsetAsync(e->summary_scratch, 0, sizeof(SummaryScratch), e->stream));
   KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
   KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
@@ -1812,7 +1865,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
@@ -1963,6 +2016,17 @@ int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, 
   if (n <= 0) return KS_OK;
   KS_LAUNCH(k_query, static_cast<unsigned>((n + 255) / 256), 256, 0, e->stream, e->view, points_dev, static_cast<long long>(n),
             distance_dev, gradient_dev, inside_dev);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+int ks_esdf_probe_summary_device_async(ks_esdf* e, const double* points_dev, int64_t n, double near_distance, double tag,
+                                       double* summary_dev) {
+  if (!e || !points_dev || !summary_dev) return fail(KS_ERR_INVALID, "null argument");
+  if (n < 0 || n > (1 << 30)) return fail(KS_ERR_INVALID, "esdf: bad probe count");
+  const int ctas = static_cast<int>(std::min<int64_t>(kSummaryCtas, std::max<int64_t>(1, (n + 127) / 128)));
+  KS_LAUNCH(k_probe_summary, ctas, 128, 0, e->stream, e->view, points_dev, static_cast<int>(n), near_distance, tag, e->summary_scratch,
+            summary_dev);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
