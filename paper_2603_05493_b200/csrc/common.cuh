@@ -146,5 +146,6 @@ __host__ __device__ __forceinline__ int voxel_index(double p, double v) { return
 
 const TsdfView& tsdf_view(const ks_tsdf* t);
 cudaStream_t tsdf_stream(const ks_tsdf* t);
+uint64_t tsdf_uid(const ks_tsdf* t);  // unique per created handle (a recycled address is not the same world)
 
 }  // namespace ksb

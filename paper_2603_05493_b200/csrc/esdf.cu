@@ -1550,6 +1550,12 @@ struct ks_esdf {
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
   SummaryScratch* summary_scratch;  // partials of k_probe_summary
+  // private graph of the fused build (ks_esdf_build_async outside a caller's capture)
+  bool own_graphs;
+  cudaGraphExec_t build_exec;
+  uint64_t build_tsdf;  // tsdf_uid of the world the graph was recorded for
+  double build_voxel;
+  int64_t build_nodes;
   bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
   int dc_wl_y, dc_wl_x;    // log2(warps per tile)
@@ -1814,6 +1820,8 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
 #undef KS_X_ATTR
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
+  e->own_graphs = true;
+  if (const char* v = std::getenv("KS_OWN_GRAPHS")) e->own_graphs = std::atoi(v) != 0;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
   for (cudaEvent_t& ev : e->ev) KS_CUDA(cudaEventCreate(&ev));
   const int total = E.nx + E.ny + E.nz;
@@ -1870,6 +1878,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
   cudaFreeHost(e->h_ctrl);
+  if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
   cudaEventDestroy(e->dep);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   if (e->own_stream) cudaStreamDestroy(e->stream);
@@ -1882,20 +1891,13 @@ int ks_esdf_set_stream(ks_esdf* e, ks_stream s) {
   if (e->own_stream) cudaStreamDestroy(e->stream);
   e->own_stream = false;
   e->stream = static_cast<cudaStream_t>(s);
+  if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
+  e->build_exec = nullptr;
   return KS_OK;
 }
 
-int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
-  if (!e || !t) return fail(KS_ERR_INVALID, "null argument");
+static int enqueue_build(ks_esdf* e, const ks_tsdf* t, bool prof) {
   int rc;
-  if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
-  if ((rc = order_after(e, t)) != KS_OK) return rc;
-  bool prof = e->profile;
-  if (prof) {
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(e->stream, &cap);
-    prof = cap == cudaStreamCaptureStatusNone;
-  }
   e->profile_stages = prof;
   if (prof) cudaEventRecord(e->ev[0], e->stream);
   if ((rc = refresh_directory(e, t, !fast_build(e))) != KS_OK) return rc;
@@ -1908,6 +1910,50 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   if (prof) cudaEventRecord(e->ev[6], e->stream);
   e->profile_stages = false;
   return rc;
+}
+
+// The build is a fixed sequence of launches whose arguments only depend on the two handles, so outside a
+// caller's own capture (and when no stage timing is asked for) it is recorded once per TSDF into a private
+// CUDA graph and replayed: one launch call and graph-internal dependencies instead of ~15 stream launches.
+int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
+  if (!e || !t) return fail(KS_ERR_INVALID, "null argument");
+  int rc;
+  if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
+  if ((rc = order_after(e, t)) != KS_OK) return rc;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(e->stream, &cap);
+  const bool outer_capture = cap != cudaStreamCaptureStatusNone;
+  const bool prof = e->profile && !outer_capture;
+  if (outer_capture || prof || !e->own_graphs) return enqueue_build(e, t, prof);
+  if (!e->build_exec || e->build_tsdf != tsdf_uid(t) || e->build_voxel != e->bound_voxel) {
+    if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
+    e->build_exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    KS_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_build(e, t, false);
+    const cudaError_t end = cudaStreamEndCapture(e->stream, &graph);
+    if (rc != KS_OK || end != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      e->own_graphs = false;  // this context cannot capture: plain launches from now on
+      return rc != KS_OK ? rc : enqueue_build(e, t, false);
+    }
+    size_t nodes = 0;
+    cudaGraphGetNodes(graph, nullptr, &nodes);
+    e->build_nodes = static_cast<int64_t>(nodes);
+    const cudaError_t inst = cudaGraphInstantiate(&e->build_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (inst != cudaSuccess) {
+      cudaGetLastError();
+      e->build_exec = nullptr, e->own_graphs = false;
+      return enqueue_build(e, t, false);
+    }
+    e->build_tsdf = tsdf_uid(t), e->build_voxel = e->bound_voxel;
+  } else {
+    g_kernel_launches.fetch_add(e->build_nodes, std::memory_order_relaxed);  // the capture counted its own launches once
+  }
+  KS_CUDA(cudaGraphLaunch(e->build_exec, e->stream));
+  return KS_OK;
 }
 
 int ks_esdf_profile(ks_esdf* e, int32_t enable) {

@@ -60,6 +60,7 @@ struct ks_tsdf {
   cudaStream_t stream;
   bool own_stream;
   TsdfCtrl* h_ctrl;  // pinned
+  uint64_t uid;
   // Lower bounds, as of the last synchronisation minus what was enqueued since, on the free pool entries and
   // the free hash slots.  A blocking stamp whose candidate blocks fit both cannot fail on the device
   // (exhaustion / table full / range are the only device-side errors), so it returns without waiting.
@@ -84,6 +85,7 @@ struct ks_tsdf {
 namespace ksb {
 const TsdfView& tsdf_view(const ks_tsdf* t) { return t->view; }
 cudaStream_t tsdf_stream(const ks_tsdf* t) { return t->stream; }
+uint64_t tsdf_uid(const ks_tsdf* t) { return t->uid; }
 
 // ---- device helpers ---------------------------------------------------------------
 
@@ -762,6 +764,8 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   ks_tsdf* t = new ks_tsdf();
   std::memset(static_cast<void*>(t), 0, sizeof(*t));
   t->cfg = *cfg;
+  static std::atomic<uint64_t> next_uid{1};
+  t->uid = next_uid.fetch_add(1);
   TsdfView& V = t->view;
   V.capacity = cfg->capacity;
   V.nslots = cfg->slot_count > 0 ? cfg->slot_count : 2 * cfg->capacity;  // BlockHashTable::init (sdf_world.hpp:115-120)
