@@ -1647,6 +1647,10 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
     bool in_step = voxe[0] >= 0;
     for (int i = 0; i < E.nx + 2; ++i) in_step = in_step && voxe[i] == i + voxe[0];
     E.xshift = in_step ? voxe[0] : -1;
+    if (ok && e->dc && !E.gtab) {  // the site tables (8 B per cell, touched at the seeds only) exist once the fast path is known to apply
+      KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
+      KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.cells) * sizeof(int)));
+    }
     e->resample_ok = ok;
     if (const char* v = std::getenv("KS_SEED")) e->resample_ok = e->resample_ok && std::strcmp(v, "bricks") != 0;
   }
@@ -1843,8 +1847,6 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     KS_CUDA(cudaMalloc(&E.xplus, 2 * E.wpr * sizeof(uint32_t)));
     E.xminus = E.xplus + E.wpr;
     KS_CUDA(cudaMalloc(&E.yzflags, E.ny + E.nz));
-    KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
-    KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.cells) * sizeof(int)));
   }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   E.nzw = (E.nz + 31) / 32;

@@ -184,7 +184,7 @@ __device__ __forceinline__ void note_block(const TsdfView& T, const OpLists& L, 
 }
 
 // ---- phase 1+2: block discovery along rays + dedup (sdf_world.hpp:346-361, :308-311) ----
-__global__ void __launch_bounds__(256) k_discover(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
+__global__ void __launch_bounds__(256, 6) k_discover(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
                                                   const float* __restrict__ depth) {
   const FrameParams& F = *Fp;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
