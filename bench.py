@@ -515,7 +515,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": stage_bytes[dominant],
-                     "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
+                     "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
+                     "note": "HBM is the nominal roof of every stage (no contraction on this path), but the sweeps are "
+                             "instruction-issue bound: see profiles/README.md and profiles/r1/j_ncu_k_sweep_x_dc.txt"},
         "cpu_baseline": cpu_base,
     }
     print(json.dumps(line))
