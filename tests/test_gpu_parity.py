@@ -512,3 +512,29 @@ def test_stamp_reports_exhaustion_at_the_call(oracle_lib):
     assert api.allocated_block_count(tsdf) == cpu.allocated_block_count()
     api.stamp_primitive(tsdf, small)       # and the handle keeps working
     assert_world_parity(tsdf, cpu)
+
+
+def test_probe_summary_matches_the_batched_query():
+    """ks_esdf_probe_summary_device_async (the per-environment collision summary of the multi-GPU exchange) against
+    the same numbers formed from ks_esdf_query; ks_esdf_last_report against ks_esdf_sync."""
+    import ctypes as C
+
+    import torch
+
+    scene = scenes.small_scene(9)
+    tsdf, _ = gpu_world(scene)
+    e = api.build_esdf(tsdf, esdf_config(scene))
+    last, fresh = e.last_report(), e.report()
+    assert (last.has_sites, last.signs_recovered, last.seed_count) == (fresh.has_sites, fresh.signs_recovered, fresh.seed_count)
+    rng = np.random.RandomState(3)
+    ext = np.array(scene.esdf_dims) * scene.esdf_voxel
+    for n in (1, 100, 4096, 10000):
+        pts = scene.esdf_origin + rng.random_sample((n, 3)) * ext
+        want = api.query(e, pts).distance
+        d_pts = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+        out = torch.full((4,), float("nan"), dtype=torch.float64, device="cuda")
+        near = 0.03
+        api._check(e.lib.ks_esdf_probe_summary_device_async(e.h, C.c_void_p(d_pts.data_ptr()), n, near, 7.0, C.c_void_p(out.data_ptr())))
+        e.report()  # waits for the handle's stream
+        got = out.cpu().numpy()
+        assert got[0] == 7.0 and got[1] == want.min() and got[2] == float((want < near).sum()) and got[3] == float(fresh.seed_count)
