@@ -1545,6 +1545,10 @@ struct ks_esdf {
   cudaStream_t stream;
   bool own_stream;
   cudaEvent_t dep;
+  // the site tables are only read by the last sweep: they are built on a side stream while phase 1 and 2 run
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+  bool side_pending;
   EsdfCtrl* h_ctrl;  // pinned
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
@@ -1695,7 +1699,15 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
       KS_LAUNCH(k_dir_geom, (E.dcount + 255) / 256, 256, 0, e->stream, E);
       KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
-      KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+      if (e->profile_stages) {  // stage timing: everything in line
+        KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
+      } else {
+        KS_CUDA(cudaEventRecord(e->fork, e->stream));
+        KS_CUDA(cudaStreamWaitEvent(e->side, e->fork, 0));
+        KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->side, E, tsdf_view(t));
+        KS_CUDA(cudaEventRecord(e->join, e->side));
+        e->side_pending = true;
+      }
     } else if (bits) {
       const size_t plane_bytes = static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t);
       KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * plane_bytes, e->stream));  // seed plane + geometry-near plane (contiguous)
@@ -1726,6 +1738,10 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
   else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
+  if (e->side_pending) {  // the site tables must be complete before the sweep that reads them
+    KS_CUDA(cudaStreamWaitEvent(e->stream, e->join, 0));
+    e->side_pending = false;
+  }
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (e->dc) {
     const dim3 xgrid((E.ny + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
@@ -1827,6 +1843,9 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   e->own_graphs = true;
   if (const char* v = std::getenv("KS_OWN_GRAPHS")) e->own_graphs = std::atoi(v) != 0;
   KS_CUDA(cudaEventCreateWithFlags(&e->dep, cudaEventDisableTiming));
+  KS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  KS_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+  KS_CUDA(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
   for (cudaEvent_t& ev : e->ev) KS_CUDA(cudaEventCreate(&ev));
   const int total = E.nx + E.ny + E.nz;
   KS_CUDA(cudaMalloc(&E.vox, kVoxRows * total * sizeof(int)));
@@ -1881,6 +1900,9 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (E.pool_surf) cudaFree(E.pool_surf);
   cudaFreeHost(e->h_ctrl);
   if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
+  cudaStreamSynchronize(e->side);
+  cudaStreamDestroy(e->side);
+  cudaEventDestroy(e->fork), cudaEventDestroy(e->join);
   cudaEventDestroy(e->dep);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   if (e->own_stream) cudaStreamDestroy(e->stream);
