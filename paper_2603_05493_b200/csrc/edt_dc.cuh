@@ -11,7 +11,7 @@
 // window of candidates.  Per level the windows of one row add up to <= n + (number of visits), so a
 // row costs n*(log2 n + 1) evaluations of 4-5 instructions each, in straight-line code: no stack,
 // no division, no data-dependent branch.  Only the first few levels (fewer visits than warps) need
-// the warps of a tile to cooperate; below them each warp owns a stretch of positions (subtree()).
+// the warps of a tile to cooperate; below them each warp owns a stretch of positions (stretch()).
 //
 // Keys.  A candidate u with offset g = r2(u) is stored once as  G[u] = g << S | low(u),  where
 // low(u) holds u (and for the y sweep one payload bit below it); its cost at t is then
@@ -152,27 +152,70 @@ KS_DC_HD uint32_t scan(const uint32_t* G, int lo, int scan_len, int t, int row) 
   return best;
 }
 
-// The levels below the top ones need no cooperation: a warp that knows the winners at both ends of
-// a stretch of positions (a, a + 2*kS) resolves everything inside on its own, keeping the winners
-// it still needs in registers (the recursion is unrolled at compile time; every test on tp / n is
-// warp-uniform).  wmax(v) returns the largest v among the warp's lanes; emit(t, key) receives every
-// position visited, in ascending order of t.  Centre tp = a + kS; lo_w / hi_w = winners at a and a + 2*kS (row ends outside).
-// kInside: the whole stretch lies inside the row (a + 2*kS <= n), so no position needs a bounds test.
-template <int kPay, int kS, bool kInside, class WarpMax, class Emit>
-KS_DC_HD void subtree(const uint32_t* G, int n, int tp, int lo_w, int hi_w, int row, WarpMax&& wmax, Emit&& emit) {
-  if (!kInside && tp - kS >= n) return;  // the whole stretch lies right of the row
-  const bool here = kInside || tp <= n;
-  int mid = hi_w;
-  uint32_t key = 0;
-  if (here) {
+// Below the top levels no cooperation is needed, and no tree either: a warp that knows the winners at both
+// ends of a stretch of positions resolves ALL kM positions inside in one pass over the candidates between
+// those two winners, keeping kM running minima in registers.  A candidate costs one load and, per position,
+// one multiply-add and one add-min -- (d0 + j)^2 = d0^2 + 2 j d0 + j^2 with j a compile-time constant --
+// instead of a visit of its own per position (window, warp-wide maximum, loop set-up: ~50 instructions each,
+// which is what the unrolled binary recursion spent most of its time on).
+// Positions: t = a .. a + kM - 1 (those < n); lo_w / hi_w = winners at t = a - 1 and t = a + kM (row ends when
+// those lie outside).  wmax(v) returns the largest v among the warp's lanes; emit(t, key) receives every position.
+// kM > kFatMax: the centre position is resolved first by a plain scan of the window, which halves the windows of
+// the two halves (a pass over W candidates costs about 4 + 2*kM instructions each, so wide stretches pay twice:
+// more positions per candidate AND more candidates).
+constexpr int kFatMax = 7;
+template <int kPay, int kM, class WarpMax, class Emit>
+KS_DC_HD void stretch(const uint32_t* G, int n, int a, int lo_w, int hi_w, int row, WarpMax&& wmax, Emit&& emit) {
+  constexpr int S = Keys<kPay>::kShift;
+  if constexpr (kM > kFatMax) {
+    constexpr int kHalf = (kM - 1) / 2;
+    static_assert(2 * kHalf + 1 == kM, "stretch lengths are 2^k - 1");
+    const int t = a + kHalf;
+    int mid = hi_w;
+    if (t < n) {
+      const int longest = wmax(hi_w - lo_w + 1);
+      const uint32_t key = scan<kPay>(G, clamp_start(lo_w, longest, n), longest, t, row);
+      emit(t, key);
+      mid = Keys<kPay>::winner(key);
+    }
+    stretch<kPay, kHalf>(G, n, a, lo_w, mid, row, wmax, emit);
+    if (t + 1 < n) stretch<kPay, kHalf>(G, n, t + 1, mid, hi_w, row, wmax, emit);
+    return;
+  } else {
     const int longest = wmax(hi_w - lo_w + 1);
-    key = scan<kPay>(G, clamp_start(lo_w, longest, n), longest, tp - 1, row);
-    mid = Keys<kPay>::winner(key);
-  }
-  if constexpr (kS > 1) subtree<kPay, kS / 2, kInside>(G, n, tp - kS / 2, lo_w, mid, row, wmax, emit);
-  if (here) emit(tp - 1, key);  // positions reach emit() in ascending order
-  if constexpr (kS > 1) {
-    if (kInside || tp < n) subtree<kPay, kS / 2, kInside>(G, n, tp + kS / 2, mid, hi_w, row, wmax, emit);
+    const int lo = clamp_start(lo_w, longest, n);
+    uint32_t best[kM];
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int j = 0; j < kM; ++j) best[j] = 0xFFFFFFFFu;
+    const uint32_t* g = G + at(lo, row);
+    int d0 = a - lo;
+#if defined(__CUDA_ARCH__)
+#pragma unroll 2
+#endif
+    for (int i = 0; i < longest; ++i) {
+      // key_j = ((d0 + j)^2 << S) + g = base + j * slope + (j*j << S): one multiply-add and one add-min per position
+      const uint32_t base = (static_cast<uint32_t>(d0 * d0) << S) + g[0];
+      uint32_t slope = static_cast<uint32_t>(2 * d0) << S;
+#if defined(__CUDA_ARCH__)
+      asm volatile("" : "+r"(slope));  // keeps the compiler from folding the keys back into (d0 + j)^2, three instructions each
+#endif
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+      for (int j = 0; j < kM; ++j) {
+        const uint32_t key = base + static_cast<uint32_t>(j) * slope + (static_cast<uint32_t>(j * j) << S);  // modular
+        best[j] = best[j] < key ? best[j] : key;
+      }
+      g += kRows;
+      --d0;
+    }
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int j = 0; j < kM; ++j)
+      if (a + j < n) emit(a + j, best[j]);
   }
 }
 

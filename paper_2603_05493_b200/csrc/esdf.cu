@@ -1013,10 +1013,10 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
 // One CTA per tile of 32 rows, 2^warps_log2 warps.  G = packed candidates [position][32 rows].
 // Top levels (visits at the multiples of kTopStep): fewer visits than warps, so the windows are cut into
 // slices whose minima meet in Kt through atomicMin, one barrier per level.  Below them every warp
-// resolves whole stretches of kTopStep positions on its own (edt_dc::subtree), no barrier.
+// resolves whole stretches of kTopStep positions on its own (edt_dc::stretch), no barrier.
 using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
 using KeysX = edt_dc::Keys<0>;
-constexpr int kTopShift = 4, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+constexpr int kTopShift = 4, kTopStep = 1 << kTopShift;
 // The 32 rows of a tile are 8 neighbours along the fast axis x 4 along z: all lanes scan as far as the
 // lane with the longest window, and compact tiles cross a Voronoi boundary at fewer positions than
 // 32 x 1 ones (29 % fewer evaluations at cfg2); 8 x 4 also divides the BASELINE grids without padding.
@@ -1052,13 +1052,8 @@ __device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt
   const uint32_t right = closed ? Kt[edt_dc::at(j + 1, lane)] : 0u;
   const int lo_w = a > 0 ? edt_dc::Keys<kPay>::winner(Kt[edt_dc::at(j, lane)]) : 0;
   const int hi_w = closed ? edt_dc::Keys<kPay>::winner(right) : n - 1;
-  auto wmax = [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); };
-  if (closed) {
-    edt_dc::subtree<kPay, kSubStep, true>(G, n, a + kSubStep, lo_w, hi_w, lane, wmax, emit);
-    emit(a + kTopStep - 1, right);
-  } else {
-    edt_dc::subtree<kPay, kSubStep, false>(G, n, a + kSubStep, lo_w, hi_w, lane, wmax, emit);
-  }
+  edt_dc::stretch<kPay, kTopStep - 1>(G, n, a, lo_w, hi_w, lane, [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); }, emit);
+  if (closed) emit(a + kTopStep - 1, right);
 }
 
 static size_t dc_top_bytes(int n) { return static_cast<size_t>((n >> kTopShift) + 1) * 32 * sizeof(uint32_t); }
@@ -1118,6 +1113,7 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   __syncthreads();
   dc_top_levels<1>(G, Kt, ny, warp, lane, warps_log2);
   uint32_t* out = E.yz + zoff;
+  asm volatile("" : "+l"(out));  // a pointer in registers: each store is then one wide multiply-add away
   for (int j = warp; (j << kTopShift) < ny; j += nwarps)
     dc_stretch<1>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
       if (live) out[nx * y] = k;

@@ -132,7 +132,7 @@ namespace dc = ksb::edt_dc;
 // as atomicMin does), then one subtree per stretch.  Rows are independent except for the warp-wide scan
 // length; `fuzz` stands in for it by lengthening every scan pseudo-randomly, which must not change any
 // winner.  scans += scan lengths, visits += visits (of row 0, as a proxy for the warp).
-constexpr int kTopShift = 4, kTopStep = 1 << kTopShift, kSubStep = kTopStep / 2;
+constexpr int kTopShift = 4, kTopStep = 1 << kTopShift;
 
 struct Fuzz {
   uint32_t state;
@@ -179,8 +179,7 @@ void dc_tile(const std::vector<uint32_t>& G, std::vector<uint32_t>& K, int n, in
       const int lo_w = a > 0 ? dc::Keys<kPay>::winner(Kt[dc::at(j, r)]) : 0;
       const int hi_w = closed ? dc::Keys<kPay>::winner(right) : n - 1;
       auto emit = [&](int t, uint32_t key) { K[dc::at(t, r)] = key; };
-      if (closed) dc::subtree<kPay, kSubStep, true>(G.data(), n, a + kSubStep, lo_w, hi_w, r, bounded, emit);
-      else dc::subtree<kPay, kSubStep, false>(G.data(), n, a + kSubStep, lo_w, hi_w, r, bounded, emit);
+      dc::stretch<kPay, kTopStep - 1>(G.data(), n, a, lo_w, hi_w, r, bounded, emit);
       if (closed) emit(a + kTopStep - 1, right);
     }
   }
