@@ -1011,19 +1011,21 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
 
 // ---- phases 2 and 3 by monotone divide and conquer (edt_dc.cuh); used whenever the keys fit 32 bits ----
 // One CTA per tile of 32 rows, 2^warps_log2 warps.  G = packed candidates [position][32 rows].
-// Top levels (visits at the multiples of kTopStep): fewer visits than warps, so the windows are cut into
+// Top levels (visits at the multiples of the stretch length 2^kTopShift): fewer visits than warps, so the windows are cut into
 // slices whose minima meet in Kt through atomicMin, one barrier per level.  Below them every warp
-// resolves whole stretches of kTopStep positions on its own (edt_dc::stretch), no barrier.
+// resolves whole stretches of that many positions on its own (edt_dc::stretch), no barrier.
 using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
 using KeysX = edt_dc::Keys<0>;
-constexpr int kTopShift = 4, kTopStep = 1 << kTopShift;
+// stretch length per sweep (measured, cfg2): 16 positions along y, 8 along x
+constexpr int kTopShiftY = 4, kTopShiftX = 3;
 // The 32 rows of a tile are 8 neighbours along the fast axis x 4 along z: all lanes scan as far as the
 // lane with the longest window, and compact tiles cross a Voronoi boundary at fewer positions than
 // 32 x 1 ones (29 % fewer evaluations at cfg2); 8 x 4 also divides the BASELINE grids without padding.
 constexpr int kTileA = 8, kTileZ = 4;
 
-template <int kPay>
+template <int kPay, int kTopShift>
 __device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, int n, int warp, int lane, int warps_log2) {
+  constexpr int kTopStep = 1 << kTopShift;
   const edt_dc::Plan plan = edt_dc::make_plan(n);
   for (int level = 0; level < plan.levels; ++level) {
     const int s = edt_dc::level_step(plan, level);
@@ -1044,9 +1046,10 @@ __device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, i
   }
 }
 
-// stretch j = positions t' in (j*kTopStep, (j+1)*kTopStep]; emit(t, key) sees each of them once
-template <int kPay, class Emit>
+// stretch j = positions t' in (j << kTopShift, (j+1) << kTopShift]; emit(t, key) sees each of them once
+template <int kPay, int kTopShift, class Emit>
 __device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt, int n, int j, int lane, Emit&& emit) {
+  constexpr int kTopStep = 1 << kTopShift;
   const int a = j << kTopShift;
   const bool closed = a + kTopStep <= n;
   const uint32_t right = closed ? Kt[edt_dc::at(j + 1, lane)] : 0u;
@@ -1056,10 +1059,10 @@ __device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt
   if (closed) emit(a + kTopStep - 1, right);
 }
 
-static size_t dc_top_bytes(int n) { return static_cast<size_t>((n >> kTopShift) + 1) * 32 * sizeof(uint32_t); }
-static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n); }
+static size_t dc_top_bytes(int n, int top_shift) { return static_cast<size_t>((n >> top_shift) + 1) * 32 * sizeof(uint32_t); }
+static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n, kTopShiftY); }
 static size_t dc_smem_bytes_x(int n, int total) {  // G, K, Kt and the per-axis fraction table of the sign tables
-  return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n) + static_cast<size_t>(total) * sizeof(float);
+  return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n, kTopShiftX) + static_cast<size_t>(total) * sizeof(float);
 }
 
 // root of a perfect square below 2^24 (one MUFU; its error of a few ulp cannot reach the next integer)
@@ -1109,13 +1112,13 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
       }
     }
   }
-  for (int i = warp; i <= ny >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
+  for (int i = warp; i <= ny >> kTopShiftY; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   __syncthreads();
-  dc_top_levels<1>(G, Kt, ny, warp, lane, warps_log2);
+  dc_top_levels<1, kTopShiftY>(G, Kt, ny, warp, lane, warps_log2);
   uint32_t* out = E.yz + zoff;
   asm volatile("" : "+l"(out));  // a pointer in registers: each store is then one wide multiply-add away
-  for (int j = warp; (j << kTopShift) < ny; j += nwarps)
-    dc_stretch<1>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
+  for (int j = warp; (j << kTopShiftY) < ny; j += nwarps)
+    dc_stretch<1, kTopShiftY>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
       if (live) out[nx * y] = k;
     });
 }
@@ -1172,6 +1175,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
       }
     }
   }
+  constexpr int kTopShift = kTopShiftX, kTopStep = 1 << kTopShift;
   for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   float* s_qsf = reinterpret_cast<float*>(Kt + ((nx >> kTopShift) + 1) * 32);
   if constexpr (kSigns == 3)
@@ -1202,7 +1206,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
     for (int x = warp; x < nx; x += nwarps) K[slot(x)] = convert(x, K[slot(x)]);
   }
   __syncthreads();
-  dc_top_levels<0>(G, Kt, nx, warp, lane, warps_log2);
+  dc_top_levels<0, kTopShift>(G, Kt, nx, warp, lane, warps_log2);
   const int obase = y + ny * nx * z;
   auto make_probe = [&]() {
     if constexpr (kSigns == 3) return SignTable(E, Tw, s_qsf, min(y, ny - 1), z);
@@ -1211,7 +1215,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   auto probe = make_probe();
   const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
   for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-    dc_stretch<0>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
+    dc_stretch<0, kTopShift>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
     if (!live) continue;
     // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
     const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
