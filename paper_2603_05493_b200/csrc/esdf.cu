@@ -85,8 +85,7 @@ struct EsdfView {
   uint32_t* zinfo;   // same layout: nearest seed z in the words below w | the words above w << 16 (0xFFFF: none)
   int nzw;           // words per column
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
-  uint32_t* site;    // [cells] y-fastest
-  uint32_t* d2s;     // [cells] y-fastest
+  uint2* field;      // [cells] y-fastest: {site (x | y << 10 | z << 20), squared distance | sign << 31}, one 8-byte store per cell
   EsdfCtrl* ctrl;
 };
 
@@ -988,8 +987,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
     edt::colour_band(T, warp, lane, [&](int x, uint16_t win) {
       const int o = obase + ny * x;
       if (win == edt::kNone) {
-        E.site[o] = kSiteNone;
-        E.d2s[o] = kD2None;
+        E.field[o] = make_uint2(kSiteNone, kD2None);
         return;
       }
       if (win != last) {  // everything that only depends on the winning site
@@ -1003,8 +1001,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
       }
       uint32_t d2 = static_cast<uint32_t>((x - sx) * (x - sx) + r2w);
       if (kSigns && probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
-      E.site[o] = site;
-      E.d2s[o] = d2;
+      E.field[o] = make_uint2(site, d2);
     });
   }
 }
@@ -1221,11 +1218,10 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
     const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
     uint32_t own = 0;  // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
     if constexpr (kSigns == 3) own = __funnelshift_rc(orow[x0 >> 5], (x0 >> 5) + 1 < E.wpr2 ? orow[(x0 >> 5) + 1] : 0u, (x0 & 31) + 1);
-    uint32_t* sp = E.site + obase + ny * x0;
-    uint32_t* dp = E.d2s + obase + ny * x0;
+    uint2* fp = E.field + obase + ny * x0;
     int last = -1, r2 = 0;
     uint32_t site = kSiteNone;
-    for (int x = x0; x < end; ++x, sp += ny, dp += ny) {
+    for (int x = x0; x < end; ++x, fp += ny) {
       const int u = K16[2 * slot(x) + 1];
       if (u != last) {
         last = u;
@@ -1242,7 +1238,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
         }
       }
       if (r2 >= static_cast<int>(none_x)) {  // the row holds no candidate at all
-        *sp = kSiteNone, *dp = kD2None;
+        *fp = make_uint2(kSiteNone, kD2None);
         continue;
       }
       uint32_t d2 = static_cast<uint32_t>((x - u) * (x - u) + r2);
@@ -1251,7 +1247,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
       } else if constexpr (kSigns != 0) {
         if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
       }
-      *sp = site, *dp = d2;
+      *fp = make_uint2(site, d2);
     }
   }
 }
@@ -1260,19 +1256,19 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
-  const uint32_t site = E.site[o];
+  const uint32_t site = E.field[o].x;
   if (site == kSiteNone) return;
   const int y = o % E.ny;
   const int x = (o / E.ny) % E.nx;
   const int z = o / (E.ny * E.nx);
   SignProbe probe(E, T, y, z);
   probe.template set_site<false>(site & 1023, (site >> 10) & 1023, site >> 20);
-  if (probe.template negative<false>(x)) E.d2s[o] ^= 0x80000000u;
+  if (probe.template negative<false>(x)) E.field[o].y ^= 0x80000000u;
 }
 
 // ---- query (esdf.hpp:337-387) ----
 __device__ __forceinline__ double cell_distance(const EsdfView& E, int x, int y, int z) {
-  const uint32_t v = E.d2s[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)];
+  const uint32_t v = E.field[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)].y;
   const double d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;  // esdf.hpp:276-277
   return (v & 0x80000000u) ? -d : d;
 }
@@ -1518,7 +1514,8 @@ __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ si
   const int y = static_cast<int>((idx / E.nx) % E.ny);
   const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
   const long long o = y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z);
-  const uint32_t s = E.site[o], v = E.d2s[o];
+  const uint2 cell = E.field[o];
+  const uint32_t s = cell.x, v = cell.y;
   if (site_xyz) {
     site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
     site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
@@ -1875,16 +1872,14 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     E.zbits = reinterpret_cast<uint32_t*>(E.near_z), E.zinfo = E.zbits + col_words;
   }
   KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
-  KS_CUDA(cudaMalloc(&E.site, E.cells * sizeof(uint32_t)));
-  KS_CUDA(cudaMalloc(&E.d2s, E.cells * sizeof(uint32_t)));
+  KS_CUDA(cudaMalloc(&E.field, static_cast<size_t>(E.cells) * sizeof(uint2)));
   KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMalloc(&e->summary_scratch, sizeof(SummaryScratch)));
   KS_CUDA(cudaMemsetAsync(e->summary_scratch, 0, sizeof(SummaryScratch), e->stream));
   KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
   KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.site, 0xFF, E.cells * sizeof(uint32_t), e->stream));  // no sites yet
-  KS_CUDA(cudaMemsetAsync(E.d2s, 0xFF, E.cells * sizeof(uint32_t), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.field, 0xFF, static_cast<size_t>(E.cells) * sizeof(uint2), e->stream));  // no sites yet
   KS_CUDA(cudaStreamSynchronize(e->stream));
   *out = e;
   return KS_OK;
@@ -1894,7 +1889,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.site), cudaFree(E.d2s);
+  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
