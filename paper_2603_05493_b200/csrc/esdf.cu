@@ -75,7 +75,6 @@ struct EsdfView {
   uint8_t* yzflags;    // [ny | nz] bit0 / bit1: the same for the y and z probes of that row
   int xshift;          // voxe[i] == i + xshift along x (cell and voxel grids in step), else -1
   int* seedw;          // compacted cell indices of the seeds whose sign table is not all zero (count in ctrl->seed_words)
-  uint8_t* dirs;       // [dcount] 1 when the entry's block holds stamped geometry (0 / 0xFF otherwise)
   uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
   uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
                        // at the 27 voxels around the site's centre voxel, bit = (ox+1) + 3(oy+1) + 9(oz+1)
@@ -129,23 +128,30 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
   E.qsf[i] = static_cast<float>(q - floor(q));
 }
 
-// surf_too: also the per-block "holds surface voxels" flag the brick gather's work list is built from
+// One warp per live pool entry: its directory slot; for a stamped block, the "stamped geometry within one block"
+// flag of the 3x3x3 directory entries around it (lanes 0..26; cleared with the directory); surf_too: also the
+// per-block "holds surface voxels" flag the brick gather's work list is built from.
 __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T, bool surf_too) {
   const int bound = T.ctrl->next_fresh;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < bound; p += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < bound; p += nwarps) {
     const uint64_t key = T.pool_key[p];
     if (key == kKeyEmpty) continue;
     int bx, by, bz;
     unpack_key(key, bx, by, bz);
     bx -= E.dlo[0], by -= E.dlo[1], bz -= E.dlo[2];
     if (bx < 0 || bx >= E.dn[0] || by < 0 || by >= E.dn[1] || bz < 0 || bz >= E.dn[2]) continue;
-    E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
-    E.dirs[bx + E.dn[0] * (by + E.dn[1] * bz)] = T.pool_geom[p];
-    if (!surf_too) continue;
-    uint32_t any = 0;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) any |= T.digest[p * kDigestWords + w];
-    E.pool_surf[p] = any != 0;
+    if (lane == 0) E.dir[bx + E.dn[0] * (by + E.dn[1] * bz)] = p;
+    if (lane < 27 && T.pool_geom[p]) {
+      const int x = bx + lane % 3 - 1, y = by + (lane / 3) % 3 - 1, z = bz + lane / 9 - 1;
+      if (x >= 0 && x < E.dn[0] && y >= 0 && y < E.dn[1] && z >= 0 && z < E.dn[2]) E.dirg[x + E.dn[0] * (y + E.dn[1] * z)] = 1;
+    }
+    if (surf_too) {
+      const uint32_t word = lane < 16 ? T.digest[p * kDigestWords + lane] : 0u;
+      const bool any = __any_sync(0xFFFFFFFFu, word != 0);
+      if (lane == 0) E.pool_surf[p] = any;
+    }
   }
 }
 
@@ -353,17 +359,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfVi
 // tables).  Then  seed = C | (C shifted along +-x, y, z, where the probe leaves the voxel)  with
 // C = surface bit of the centre voxel: one digest bit per cell and a handful of word operations per
 // 32 cells instead of seven probes per cell.
-__global__ void __launch_bounds__(256) k_dir_geom(EsdfView E) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= E.dcount) return;
-  const int bx = i % E.dn[0], by = (i / E.dn[0]) % E.dn[1], bz = i / (E.dn[0] * E.dn[1]);
-  uint8_t any = 0;
-  for (int z = max(bz - 1, 0); z <= min(bz + 1, E.dn[2] - 1); ++z)
-    for (int y = max(by - 1, 0); y <= min(by + 1, E.dn[1] - 1); ++y)
-      for (int x = max(bx - 1, 0); x <= min(bx + 1, E.dn[0] - 1); ++x) any |= E.dirs[x + E.dn[0] * (y + E.dn[1] * z)] == 1;
-  E.dirg[i] = any;
-}
-
 // One warp per extended (y, z) row.  Step 1, lane <-> block column: the row's voxel-space bits (surface,
 // own-sign, geometry-near), one byte per block, into the warp's slice of shared memory; most rows cross no
 // live block and end there.  Step 2, lane <-> cell: every cell picks the bit of its centre voxel.
@@ -1603,7 +1598,7 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   if (dcount > (1ll << 30)) return fail(KS_ERR_UNSUPPORTED, "esdf: TSDF blocks per workspace exceed the directory limit");
   E.dcount = static_cast<int>(dcount);
   KS_CUDA(cudaMalloc(&E.dir, static_cast<size_t>(E.dcount) * (sizeof(int) + 1)));
-  E.dirs = reinterpret_cast<uint8_t*>(E.dir + E.dcount);
+  E.dirg = reinterpret_cast<uint8_t*>(E.dir + E.dcount);
   if (E.pool_surf) cudaFree(E.pool_surf);
   E.pool_surf = nullptr;
   KS_CUDA(cudaMalloc(&E.pool_surf, static_cast<size_t>(T.capacity)));
@@ -1611,9 +1606,6 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
   KS_CUDA(cudaStreamSynchronize(e->stream));
-  if (E.dirg) cudaFree(E.dirg);
-  E.dirg = nullptr;
-  KS_CUDA(cudaMalloc(&E.dirg, static_cast<size_t>(E.dcount)));
   {  // resampled seeding: check  probe voxel in {centre voxel, neighbouring cell's centre voxel}  position by position
     std::vector<int> vox(static_cast<size_t>(kVoxRows) * total);
     KS_CUDA(cudaMemcpy(vox.data(), E.vox, vox.size() * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1670,8 +1662,9 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
 // bricks: also the brick flags / work list of the brick gather and of the hinted sign recovery
 static int refresh_directory(ks_esdf* e, const ks_tsdf* t, bool bricks_too = true) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * (sizeof(int) + 1), e->stream));  // dir and dirs
-  KS_LAUNCH(k_dir_fill, 2 * kSmCount, 256, 0, e->stream, E, tsdf_view(t), bricks_too);
+  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * sizeof(int), e->stream));
+  KS_CUDA(cudaMemsetAsync(E.dirg, 0, static_cast<size_t>(E.dcount), e->stream));
+  KS_LAUNCH(k_dir_fill, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t), bricks_too);
   if (bricks_too) {
     KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
     const int bricks = E.bnx * E.bny * E.bnz;
@@ -1693,7 +1686,6 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
     if (bits && fast_build(e)) {
       const int words = E.wpr * E.ny * E.nz;
       const int ext_rows = (E.ny + 2) * (E.nz + 2);
-      KS_LAUNCH(k_dir_geom, (E.dcount + 255) / 256, 256, 0, e->stream, E);
       KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
       if (e->profile_stages) {  // stage timing: everything in line
@@ -1889,7 +1881,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.dirg), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
+  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
