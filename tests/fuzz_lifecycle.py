@@ -2,7 +2,7 @@
 (exhaustion included), CUDA path vs oracle after every step: return values, exception texts, key -> pool
 assignment, hash slot order, free list, channels.
 
-    python tools/fuzz_lifecycle.py [--seconds 300] [--seed 1]
+    python tests/fuzz_lifecycle.py [--seconds 300] [--seed 1]
 """
 import argparse
 import sys

@@ -1,6 +1,6 @@
 """Randomised parity run on the GPU box (not a pytest: minutes, not seconds).
 
-    python tools/fuzz_parity.py [--seconds 300] [--seed 1]
+    python tests/fuzz_parity.py [--seconds 300] [--seed 1]
 
 Draws small mixed scenes with random grid shapes, ESDF/TSDF voxel ratios, off-grid origins and primitive counts,
 runs the CUDA path and the CPU oracle on each, and compares block tables, seed masks, sites, signed distances and
