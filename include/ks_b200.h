@@ -148,6 +148,23 @@ KS_API int ks_tsdf_stamp_cuboid_async(ks_tsdf* t, const double pose_R[9], const 
                                       const double half_extents[3]);
 KS_API int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double radius);
 
+/* Triangle-mesh stamping.  The reference has no implementation to replace (SPEC.md:8 and :422 put it out of
+ * scope; "Cuboids and meshes are stamped directly into the geometry channel"); the flow is
+ * stamp_primitive's (sdf_world.hpp:418-443: padded AABB -> candidate blocks with |sdf(centre)| <= truncation +
+ * block radius -> allocate -> per-voxel min) with the signed distance to a closed, outward-oriented
+ * (counter-clockwise) indexed triangle mesh: closest point over all triangles, sign from the angle-weighted
+ * pseudonormal of the closest feature (csrc/mesh.cuh).  vertices = n_vertices xyz triples in the world frame,
+ * triangles = n_triangles index triples.  ks_mesh_create validates ("stamp: empty mesh", "stamp: non-finite
+ * mesh", "stamp: mesh index out of range", "stamp: degenerate mesh triangle" -> KS_ERR_INVALID), builds the
+ * per-triangle tables and uploads them once; stamping a created mesh is capturable. */
+typedef struct ks_mesh ks_mesh;
+KS_API int ks_mesh_create(const double* vertices, int32_t n_vertices, const int32_t* triangles,
+                          int32_t n_triangles, ks_mesh** out);
+KS_API void ks_mesh_destroy(ks_mesh* m);
+KS_API int32_t ks_mesh_triangle_count(const ks_mesh* m);
+KS_API int ks_tsdf_stamp_mesh(ks_tsdf* t, const ks_mesh* m);
+KS_API int ks_tsdf_stamp_mesh_async(ks_tsdf* t, const ks_mesh* m);
+
 /* decay_weights (sdf_world.hpp:449-457), recycle_blocks (sdf_world.hpp:462-475) */
 KS_API int ks_tsdf_decay_weights(ks_tsdf* t, const ks_camera* cam);
 KS_API int ks_tsdf_decay_weights_async(ks_tsdf* t, const ks_camera* cam);

@@ -45,6 +45,14 @@ int KO(integrate_depth)(KO(tsdf)* t, const float* depth, int width, int height,
 int KO(stamp_cuboid)(KO(tsdf)* t, const double pose_R[9], const double pose_t[3],
                      const double half_extents[3]);
 int KO(stamp_sphere)(KO(tsdf)* t, const double center[3], double radius);
+/* Triangle-mesh stamping: liboracle.so (ko_) ONLY -- the reference has no mesh implementation
+ * (SPEC.md:8, :422), so there is no kr_ counterpart and parity for it is unpinned (ks_oracle.c).
+ * vertices = nv xyz triples (world frame), triangles = nt index triples, outward counter-clockwise. */
+#ifndef KS_ORACLE_NO_MESH
+int KO(stamp_mesh)(KO(tsdf)* t, const double* vertices, int nv, const int32_t* triangles, int nt);
+int KO(mesh_sdf)(const double* vertices, int nv, const int32_t* triangles, int nt, const double* points,
+                 int64_t n, double* out);
+#endif
 void KO(decay_weights)(KO(tsdf)* t, int width, int height, const double intr[4],
                        const double pose_R[9], const double pose_t[3]);
 int KO(recycle_blocks)(KO(tsdf)* t);

@@ -74,7 +74,8 @@ ABI_SYMBOLS = [
     "ks_tsdf_set_stream", "ks_tsdf_get_stream", "ks_tsdf_integrate_depth", "ks_tsdf_stage_frame",
     "ks_tsdf_upload_frame_async", "ks_tsdf_integrate_async", "ks_tsdf_stage_frame_slot", "ks_tsdf_frame_buffer", "ks_host_alloc", "ks_host_free",
     "ks_tsdf_upload_frame_slot_async", "ks_tsdf_integrate_slot_async", "ks_tsdf_stamp_cuboid", "ks_tsdf_stamp_sphere",
-    "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_tsdf_decay_weights",
+    "ks_tsdf_stamp_cuboid_async", "ks_tsdf_stamp_sphere_async", "ks_mesh_create", "ks_mesh_destroy",
+    "ks_mesh_triangle_count", "ks_tsdf_stamp_mesh", "ks_tsdf_stamp_mesh_async", "ks_tsdf_decay_weights",
     "ks_tsdf_decay_weights_async", "ks_tsdf_recycle_blocks", "ks_tsdf_sync", "ks_tsdf_query",
     "ks_tsdf_allocated_block_count", "ks_tsdf_find", "ks_tsdf_export_blocks", "ks_tsdf_download_blocks",
     "ks_tsdf_free_list", "ks_tsdf_profile", "ks_tsdf_stage_ms", "ks_esdf_profile", "ks_esdf_stage_ms", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
@@ -127,6 +128,11 @@ def load_library() -> C.CDLL:
         "ks_tsdf_stamp_sphere": (C.c_int, [VP, VP, D]),
         "ks_tsdf_stamp_cuboid_async": (C.c_int, [VP, VP, VP, VP]),
         "ks_tsdf_stamp_sphere_async": (C.c_int, [VP, VP, D]),
+        "ks_mesh_create": (C.c_int, [VP, I32, VP, I32, P(VP)]),
+        "ks_mesh_destroy": (None, [VP]),
+        "ks_mesh_triangle_count": (I32, [VP]),
+        "ks_tsdf_stamp_mesh": (C.c_int, [VP, VP]),
+        "ks_tsdf_stamp_mesh_async": (C.c_int, [VP, VP]),
         "ks_tsdf_decay_weights": (C.c_int, [VP, P(CameraC)]),
         "ks_tsdf_decay_weights_async": (C.c_int, [VP, P(CameraC)]),
         "ks_tsdf_recycle_blocks": (C.c_int, [VP, P(I32)]),
@@ -244,6 +250,34 @@ class SphereShape:  # sdf_world.hpp:217-220
     radius: float
 
 
+class TriangleMesh:
+    """A closed, outward-oriented indexed triangle mesh (world frame) resident on the device.  No reference
+    counterpart: see include/ks_b200.h "Triangle-mesh stamping"."""
+
+    def __init__(self, vertices, triangles):
+        self.lib = load_library()
+        self.vertices = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+        self.triangles = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+        h = C.c_void_p()
+        _check(self.lib.ks_mesh_create(_ptr(self.vertices), len(self.vertices), _ptr(self.triangles), len(self.triangles),
+                                       C.byref(h)))
+        self.h = h
+
+    def triangle_count(self) -> int:
+        return int(self.lib.ks_mesh_triangle_count(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ks_mesh_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class EsdfConfig:  # esdf.hpp:35-54
     origin: Sequence[float] = (0.0, 0.0, 0.0)
@@ -314,7 +348,9 @@ class SparseTsdf:
         _check(self.lib.ks_tsdf_integrate_slot_async(self.h, slot))
 
     def stamp_async(self, primitive):
-        if isinstance(primitive, Cuboid):
+        if isinstance(primitive, TriangleMesh):
+            _check(self.lib.ks_tsdf_stamp_mesh_async(self.h, primitive.h))
+        elif isinstance(primitive, Cuboid):
             R, t, he = _f64(primitive.pose_R, 9), _f64(primitive.pose_t, 3), _f64(primitive.half_extents, 3)
             _check(self.lib.ks_tsdf_stamp_cuboid_async(self.h, _ptr(R), _ptr(t), _ptr(he)))
         else:
@@ -485,6 +521,10 @@ def stamp_primitive(tsdf: SparseTsdf, primitive) -> None:  # sdf_world.hpp:394-4
     else:
         c = _f64(primitive.center, 3)
         _check(tsdf.lib.ks_tsdf_stamp_sphere(tsdf.h, _ptr(c), float(primitive.radius)))
+
+
+def stamp_mesh(tsdf: SparseTsdf, mesh: TriangleMesh) -> None:  # flow of sdf_world.hpp:418-443, distance from csrc/mesh.cuh
+    _check(tsdf.lib.ks_tsdf_stamp_mesh(tsdf.h, mesh.h))
 
 
 def decay_weights(tsdf: SparseTsdf, camera: DepthFrame) -> None:  # sdf_world.hpp:449-457

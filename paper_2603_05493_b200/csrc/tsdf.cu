@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "mesh.cuh"
 
 namespace ksb {
 
@@ -53,6 +54,11 @@ struct Frustum {  // block_in_frustum planes (sdf_world.hpp:296-301), camera fra
 }  // namespace ksb
 
 using namespace ksb;
+
+struct ks_mesh {  // a validated mesh with its per-triangle tables resident on the device (mesh.cuh)
+  MeshView view;
+  double lo[3], hi[3];
+};
 
 struct ks_tsdf {
   ks_tsdf_config cfg;
@@ -487,6 +493,110 @@ __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Pri
   arrive_and_finish(T, L.cap, 0);
 }
 
+// ---- mesh stamp (no reference implementation; definition in mesh.cuh, flow of sdf_world.hpp:418-443) ----
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+// Candidate blocks: one warp per block of the padded AABB.  Bounding spheres first (the nearest triangle is no
+// farther than ub = min(d + r); nothing is nearer than min(d - r)), then exact distances of the triangles that can
+// be the nearest one, lanes striding over them.  Only the magnitude matters here: |sdf(centre)| <= reach.
+__global__ void __launch_bounds__(256) k_stamp_mesh_candidates(TsdfView T, OpLists L, MeshView M, BlockBox B, double reach) {
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long i = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; i < B.count; i += nwarps) {
+    const int bx = B.lo[0] + static_cast<int>(i % B.n[0]);
+    const int by = B.lo[1] + static_cast<int>((i / B.n[0]) % B.n[1]);
+    const int bz = B.lo[2] + static_cast<int>(i / (static_cast<long long>(B.n[0]) * B.n[1]));
+    const V3 q = v3((bx * kBlockEdge + 0.5 * kBlockEdge) * T.voxel, (by * kBlockEdge + 0.5 * kBlockEdge) * T.voxel,
+                    (bz * kBlockEdge + 0.5 * kBlockEdge) * T.voxel);  // block_center (sdf_world.hpp:282-286)
+    double ub = CUDART_INF, lb = CUDART_INF;
+    for (int j = lane; j < M.nt; j += 32) {
+      double r;
+      const double d = mesh_bound(M, j, q, r);
+      ub = fmin(ub, d + r), lb = fmin(lb, d - r);
+    }
+    ub = warp_min(ub), lb = warp_min(lb);
+    if (lb > reach * kMeshSlack) continue;
+    const double thr = ub * kMeshSlack;
+    MeshHit best = {CUDART_INF, 0x7FFFFFFF, 0, v3(0.0, 0.0, 0.0)};
+    for (int j = lane; j < M.nt; j += 32) {
+      double r;
+      if (mesh_bound(M, j, q, r) - r <= thr) mesh_visit(M, j, q, best);
+    }
+    const double d2 = warp_min(best.d2);
+    if (lane != 0 || !(sqrt(d2) <= reach)) continue;
+    if (!key_in_range(bx, by, bz)) {
+      T.ctrl->abort_op = 1;
+      continue;
+    }
+    note_block(T, L, bx, by, bz, kNoSlot);
+  }
+}
+
+// Per-voxel min with the mesh distance: one CTA per touched block, one thread per voxel.  Triangles whose bounding
+// sphere is farther from the block centre than (nearest possible + block diameter) cannot be the nearest one of any
+// voxel of the block; the others are listed in shared memory, a chunk at a time, and every thread walks the list
+// (all lanes read the same triangle: one broadcast load).
+constexpr int kMeshChunk = 1024;
+__global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L, MeshView M) {
+  __shared__ int s_list[kMeshChunk];
+  __shared__ int s_count;
+  __shared__ double s_red[16];
+  const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
+  if (!op_blocked(T)) finalize_slots(T, L, min(T.ctrl->fresh, L.cap));
+  const int tid = threadIdx.x;
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const double v = T.voxel;
+  const double radius = 0.5 * kBlockEdge * v * sqrt(3.0) * kMeshSlack;
+  for (int i = blockIdx.x; i < touched; i += gridDim.x) {
+    const int pool = L.pool[i];
+    int bx, by, bz;
+    unpack_key(L.key[i], bx, by, bz);
+    const V3 q = v3((bx * kBlockEdge + 0.5 * kBlockEdge) * v, (by * kBlockEdge + 0.5 * kBlockEdge) * v, (bz * kBlockEdge + 0.5 * kBlockEdge) * v);
+    double ub = CUDART_INF;
+    for (int j = tid; j < M.nt; j += 512) {
+      double r;
+      const double d = mesh_bound(M, j, q, r);
+      ub = fmin(ub, d + r);
+    }
+    ub = warp_min(ub);
+    __syncthreads();  // s_red, s_list of the previous block are no longer read
+    if ((tid & 31) == 0) s_red[tid >> 5] = ub;
+    __syncthreads();
+    ub = s_red[0];
+#pragma unroll
+    for (int w = 1; w < 16; ++w) ub = fmin(ub, s_red[w]);
+    const double thr = (ub + 2.0 * radius) * kMeshSlack;
+    const V3 p = v3((bx * kBlockEdge + lx + 0.5) * v, (by * kBlockEdge + ly + 0.5) * v, (bz * kBlockEdge + lz + 0.5) * v);  // voxel_center (:265-272)
+    MeshHit best = {CUDART_INF, 0x7FFFFFFF, 0, v3(0.0, 0.0, 0.0)};
+    for (int base = 0; base < M.nt; base += kMeshChunk) {
+      __syncthreads();
+      if (tid == 0) s_count = 0;
+      __syncthreads();
+      for (int j = base + tid; j < min(base + kMeshChunk, M.nt); j += 512) {
+        double r;
+        if (mesh_bound(M, j, q, r) - r <= thr) s_list[atomicAdd(&s_count, 1)] = j;
+      }
+      __syncthreads();
+      const int n = s_count;
+      for (int k = 0; k < n; ++k) mesh_visit(M, s_list[k], p, best);
+    }
+    const double sd = mesh_signed(M, best);
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+    double g = T.geom[at];
+    if (sd < g) {  // std::min(geom, sd)
+      g = sd;
+      T.geom[at] = g;
+    }
+    const double2 sw = T.sumwt[at];
+    store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
+    if (tid == 0) T.pool_geom[pool] = 1;
+  }
+  arrive_and_finish(T, L.cap, 0);
+}
+
 // ---- decay_weights (sdf_world.hpp:449-457) ----
 __global__ void __launch_bounds__(512) k_decay(TsdfView T, Frustum Fr, double alpha_t, double alpha_f) {
   const int bound = T.ctrl->next_fresh;
@@ -702,7 +812,7 @@ static bool profiling(ks_tsdf* t) {
 #define KS_MARK(t, i) \
   if (prof) cudaEventRecord((t)->ev[i], (t)->stream)
 
-static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], const double hi_in[3]) {
+static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], const double hi_in[3], const ks_mesh* mesh = nullptr) {
   const bool prof = profiling(t);
   KS_MARK(t, 4);
   // AABB grown by the truncation band -> block range (sdf_world.hpp:418-425)
@@ -727,12 +837,18 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
   }
   const double reach = trunc + 0.5 * kBlockEdge * v * std::sqrt(3.0);  // sdf_world.hpp:288-290, :425
   if (B.count > 0) {
-    const int grid = static_cast<int>(std::min<long long>((B.count + 255) / 256, 8 * kSmCount));
-    KS_LAUNCH(k_stamp_candidates, grid, 256, 0, t->stream, t->view, t->lists, P, B, reach);
+    if (mesh) {  // one warp per candidate block
+      const int grid = static_cast<int>(std::min<long long>((B.count + 7) / 8, 8 * kSmCount));
+      KS_LAUNCH(k_stamp_mesh_candidates, grid, 256, 0, t->stream, t->view, t->lists, mesh->view, B, reach);
+    } else {
+      const int grid = static_cast<int>(std::min<long long>((B.count + 255) / 256, 8 * kSmCount));
+      KS_LAUNCH(k_stamp_candidates, grid, 256, 0, t->stream, t->view, t->lists, P, B, reach);
+    }
   }
   run_allocation(t);
   KS_MARK(t, 5);
-  KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
+  if (mesh) KS_LAUNCH(k_stamp_mesh_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, mesh->view);
+  else KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
   KS_MARK(t, 6);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -1043,6 +1159,59 @@ int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t
 
 int ks_tsdf_stamp_sphere(ks_tsdf* t, const double center[3], double radius) {
   int rc = ks_tsdf_stamp_sphere_async(t, center, radius);
+  return rc != KS_OK ? rc : finish_stamp(t);
+}
+
+// ---- triangle meshes (no reference counterpart: SPEC.md:8, :422; definition in csrc/mesh.cuh) ----
+int ks_mesh_create(const double* vertices, int32_t n_vertices, const int32_t* triangles, int32_t n_triangles, ks_mesh** out) {
+  if (!out) return fail(KS_ERR_INVALID, "null argument");
+  *out = nullptr;
+  int devices = 0;
+  if (cudaGetDeviceCount(&devices) != cudaSuccess || devices < 1) {
+    cudaGetLastError();
+    return fail(KS_ERR_CUDA, "no CUDA device (this library has no CPU path)");
+  }
+  MeshTables tab;
+  if (const char* why = build_mesh_tables(vertices, n_vertices, triangles, n_triangles, tab)) return fail(KS_ERR_INVALID, why);
+  ks_mesh* m = new ks_mesh();
+  std::memset(m, 0, sizeof *m);
+  double *tri = nullptr, *nrm = nullptr, *bnd = nullptr;
+  auto upload = [](double** dst, const std::vector<double>& src) {
+    cudaError_t e = cudaMalloc(dst, src.size() * sizeof(double));
+    return e != cudaSuccess ? e : cudaMemcpy(*dst, src.data(), src.size() * sizeof(double), cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = upload(&tri, tab.tri);
+  if (e == cudaSuccess) e = upload(&nrm, tab.nrm);
+  if (e == cudaSuccess) e = upload(&bnd, tab.bnd);
+  if (e != cudaSuccess) {
+    cudaFree(tri), cudaFree(nrm), cudaFree(bnd);
+    delete m;
+    return cuda_fail(e, "ks_mesh_create");
+  }
+  m->view = MeshView{n_triangles, tri, nrm, bnd};
+  for (int a = 0; a < 3; ++a) m->lo[a] = tab.lo[a], m->hi[a] = tab.hi[a];
+  *out = m;
+  return KS_OK;
+}
+
+void ks_mesh_destroy(ks_mesh* m) {
+  if (!m) return;
+  cudaDeviceSynchronize();  // a stamp that reads the tables may still be in flight
+  cudaFree(const_cast<double*>(m->view.tri)), cudaFree(const_cast<double*>(m->view.nrm)), cudaFree(const_cast<double*>(m->view.bnd));
+  delete m;
+}
+
+int32_t ks_mesh_triangle_count(const ks_mesh* m) { return m ? m->view.nt : 0; }
+
+int ks_tsdf_stamp_mesh_async(ks_tsdf* t, const ks_mesh* m) {
+  if (!t || !m) return fail(KS_ERR_INVALID, "null argument");
+  Primitive P;
+  std::memset(&P, 0, sizeof P);
+  return stamp_async(t, P, m->lo, m->hi, m);
+}
+
+int ks_tsdf_stamp_mesh(ks_tsdf* t, const ks_mesh* m) {
+  int rc = ks_tsdf_stamp_mesh_async(t, m);
   return rc != KS_OK ? rc : finish_stamp(t);
 }
 

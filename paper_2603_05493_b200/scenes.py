@@ -39,6 +39,13 @@ class Sphere:
 
 
 @dataclass
+class Mesh:
+    """Closed indexed triangle mesh in the world frame, outward counter-clockwise triangles."""
+    vertices: np.ndarray   # float64 [V, 3]
+    triangles: np.ndarray  # int32 [T, 3]
+
+
+@dataclass
 class Scene:
     name: str
     tsdf_voxel: float
@@ -49,6 +56,7 @@ class Scene:
     frames: List[Frame] = field(default_factory=list)
     cuboids: List[Cuboid] = field(default_factory=list)
     spheres: List[Sphere] = field(default_factory=list)
+    meshes: List[Mesh] = field(default_factory=list)
 
     @property
     def truncation(self) -> float:
@@ -95,6 +103,45 @@ def punch_invalid(depth: np.ndarray, fraction=0.05, seed=11) -> np.ndarray:
 
 def _cuboid(center, half_extents, yaw=0.0) -> Cuboid:
     return Cuboid(rot_z(yaw), np.asarray(center, np.float64), np.asarray(half_extents, np.float64))
+
+
+def box_mesh(center, half_extents, R=None) -> Mesh:
+    """The 12-triangle surface of a cuboid (corner k = signs (k&1, k&2, k&4), as stamp_primitive enumerates them)."""
+    he = np.asarray(half_extents, np.float64)
+    R = np.eye(3) if R is None else np.asarray(R, np.float64)
+    corners = np.array([[(1 if k & 1 else -1), (1 if k & 2 else -1), (1 if k & 4 else -1)] for k in range(8)], np.float64)
+    verts = (corners * he) @ R.T + np.asarray(center, np.float64)
+    quads = [(0, 4, 6, 2), (1, 3, 7, 5), (0, 1, 5, 4), (2, 6, 7, 3), (0, 2, 3, 1), (4, 5, 7, 6)]  # -x +x -y +y -z +z
+    tris = [t for a, b, c, d in quads for t in ((a, b, c), (a, c, d))]
+    return Mesh(np.ascontiguousarray(verts), np.array(tris, np.int32))
+
+
+def icosphere(center, radius: float, subdivisions: int = 2) -> Mesh:
+    """Icosahedron subdivided `subdivisions` times and pushed onto the sphere: 20 * 4^s triangles."""
+    g = (1.0 + np.sqrt(5.0)) / 2.0
+    verts = [(-1, g, 0), (1, g, 0), (-1, -g, 0), (1, -g, 0), (0, -1, g), (0, 1, g), (0, -1, -g), (0, 1, -g),
+             (g, 0, -1), (g, 0, 1), (-g, 0, -1), (-g, 0, 1)]
+    verts = [np.asarray(v, np.float64) / np.sqrt(1.0 + g * g) for v in verts]
+    tris = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6),
+            (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10),
+            (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdivisions):
+        mid, out = {}, []
+
+        def midpoint(i, j):
+            key = (min(i, j), max(i, j))
+            if key not in mid:
+                m = verts[i] + verts[j]
+                verts.append(m / np.sqrt(m @ m))
+                mid[key] = len(verts) - 1
+            return mid[key]
+
+        for a, b, c in tris:
+            ab, bc, ca = midpoint(a, b), midpoint(b, c), midpoint(c, a)
+            out += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        tris = out
+    v = np.asarray(verts, np.float64) * float(radius) + np.asarray(center, np.float64)
+    return Mesh(np.ascontiguousarray(v), np.array(tris, np.int32))
 
 
 def config1(variant: str = "flat", invalid: bool = False) -> Scene:

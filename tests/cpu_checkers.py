@@ -57,6 +57,11 @@ class CpuChecker:
         self._integrate = fn("integrate_depth", C.c_int, VP, _f32p, C.c_int, C.c_int, _f64p, _f64p, _f64p)
         self._stamp_cuboid = fn("stamp_cuboid", C.c_int, VP, _f64p, _f64p, _f64p)
         self._stamp_sphere = fn("stamp_sphere", C.c_int, VP, _f64p, C.c_double)
+        # mesh stamping exists in the restatement only (the reference has none: SPEC.md:8)
+        self.has_mesh = hasattr(L, prefix + "stamp_mesh")
+        if self.has_mesh:
+            self._stamp_mesh = fn("stamp_mesh", C.c_int, VP, _f64p, C.c_int, _i32p, C.c_int)
+            self._mesh_sdf = fn("mesh_sdf", C.c_int, _f64p, C.c_int, _i32p, C.c_int, _f64p, C.c_int64, _f64p)
         self._decay = fn("decay_weights", None, VP, C.c_int, C.c_int, _f64p, _f64p, _f64p)
         self._recycle = fn("recycle_blocks", C.c_int, VP)
         self._count = fn("allocated_block_count", C.c_int, VP)
@@ -146,6 +151,16 @@ class CpuChecker:
         return CheckerTsdf(self, handle, voxel_size, truncation, capacity)
 
     # --- ESDF (stateless) ----------------------------------------------------------------
+    def mesh_sdf(self, vertices, triangles, points):
+        """Signed distance of a closed triangle mesh at `points` (restatement only, see has_mesh)."""
+        v = np.ascontiguousarray(vertices, np.float64).reshape(-1)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1)
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        out = np.empty(len(pts), np.float64)
+        if self._mesh_sdf(v, v.size // 3, t, t.size // 3, pts.reshape(-1), len(pts), out) != 0:
+            raise CheckerError(self.last_error())
+        return out
+
     def propagate(self, mask, dims, voxel_size):
         dims = _vec(dims, 3, np.int32)
         mask = np.ascontiguousarray(mask, np.uint8).reshape(-1)
@@ -201,6 +216,12 @@ class CheckerTsdf:
 
     def stamp_sphere(self, center, radius):
         if self.lib._stamp_sphere(self.h, _vec(center, 3), float(radius)) != 0:
+            raise CheckerError(self.lib.last_error())
+
+    def stamp_mesh(self, vertices, triangles):
+        v = np.ascontiguousarray(vertices, np.float64).reshape(-1)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1)
+        if self.lib._stamp_mesh(self.h, v, v.size // 3, t, t.size // 3) != 0:
             raise CheckerError(self.lib.last_error())
 
     def decay_weights(self, width, height, intr, pose_R, pose_t):

@@ -19,6 +19,8 @@ def gpu_world(scene, **cfg_overrides):
         api.stamp_primitive(tsdf, api.Cuboid(c.R, c.t, c.half_extents))
     for s in scene.spheres:
         api.stamp_primitive(tsdf, api.SphereShape(s.center, s.radius))
+    for m in getattr(scene, "meshes", []):
+        api.stamp_mesh(tsdf, api.TriangleMesh(m.vertices, m.triangles))
     return tsdf, touched
 
 
@@ -29,6 +31,8 @@ def cpu_world(lib, scene, **kw):
         t.stamp_cuboid(c.R, c.t, c.half_extents)
     for s in scene.spheres:
         t.stamp_sphere(s.center, s.radius)
+    for m in getattr(scene, "meshes", []):  # restatement only: the reference build has no mesh stamping
+        t.stamp_mesh(m.vertices, m.triangles)
     return t, touched
 
 

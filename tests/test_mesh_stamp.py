@@ -1,0 +1,182 @@
+"""Triangle-mesh stamping.
+
+The reference has no mesh implementation, so parity for this one function is UNPINNED: the
+CUDA path is compared bit for bit with oracle/ks_oracle.c's restatement of this repo's own definition
+(csrc/mesh.cuh), and the definition itself is anchored on the reference's analytic primitives -- a 12-triangle box
+must reproduce sdf_cuboid / stamp_primitive(Cuboid) (sdf_world.hpp:224-229, :394-444) and an icosphere must
+approach sdf_sphere (:231-233) within its chord error.
+"""
+import numpy as np
+import pytest
+
+import cpu_checkers
+from paper_2603_05493_b200 import scenes
+from parity_util import assert_world_parity, cpu_world, esdf_config, gpu_world, same_bits
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return cpu_checkers.oracle()
+
+
+def _cuboid_sdf(points, center, he, R):
+    q = np.abs((points - center) @ R) - he
+    return np.linalg.norm(np.maximum(q, 0.0), axis=1) + np.minimum(q.max(axis=1), 0.0)
+
+
+# ---- the definition, on the CPU ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("yaw", [0.0, 0.4, 1.3])
+def test_box_mesh_distance_is_the_cuboid_distance(oracle, yaw):
+    rng = np.random.RandomState(3)
+    c, he, R = np.array([0.3, 0.2, 0.5]), np.array([0.2, 0.1, 0.15]), scenes.rot_z(yaw)
+    m = scenes.box_mesh(c, he, R)
+    pts = c + (rng.random_sample((20000, 3)) - 0.5)
+    d = oracle.mesh_sdf(m.vertices, m.triangles, pts)
+    ref = _cuboid_sdf(pts, c, he, R)
+    assert np.abs(d - ref).max() < 1e-12
+    assert np.array_equal(d < 0, ref < 0)
+
+
+def test_icosphere_distance_approaches_the_sphere_distance(oracle):
+    rng = np.random.RandomState(4)
+    c, r = np.array([0.1, -0.2, 0.3]), 0.2
+    pts = c + (rng.random_sample((5000, 3)) - 0.5)
+    ref = np.linalg.norm(pts - c, axis=1) - r
+    worst = []
+    for s in (1, 2, 3):
+        m = scenes.icosphere(c, r, s)
+        d = oracle.mesh_sdf(m.vertices, m.triangles, pts)
+        worst.append(np.abs(d - ref).max())
+        far = np.abs(ref) > worst[-1]
+        assert np.array_equal(d[far] < 0, ref[far] < 0)
+        assert (d >= ref - 1e-12).all()  # the inscribed polyhedron lies inside the sphere
+    assert worst[0] > worst[1] > worst[2] and worst[2] < 1e-3
+
+
+def test_points_on_the_surface_are_plus_zero_and_vertices_edges_sign_correctly(oracle):
+    m = scenes.box_mesh((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    on = np.array([[1.0, 0.0, 0.0], [1.0, 1.0, 0.0], [1.0, 1.0, 1.0], [0.25, -1.0, 0.5]])
+    d = oracle.mesh_sdf(m.vertices, m.triangles, on)
+    assert np.array_equal(d, np.zeros(4)) and not np.signbit(d).any()
+    out = np.array([[2.0, 2.0, 2.0], [2.0, 2.0, 0.0], [0.9, 0.9, 0.9], [0.99, 0.99, 0.0]])
+    d = oracle.mesh_sdf(m.vertices, m.triangles, out)
+    np.testing.assert_allclose(d, [np.sqrt(3.0), np.sqrt(2.0), -0.1, -0.01], rtol=0, atol=1e-12)
+
+
+def test_validation_messages(oracle):
+    m = scenes.box_mesh((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    t = oracle.make_tsdf(0.05, capacity=64)
+    bad = m.vertices.copy()
+    bad[3, 1] = np.nan
+    for verts, tris, text in ((bad, m.triangles, "stamp: non-finite mesh"),
+                              (m.vertices, m.triangles + 7, "stamp: mesh index out of range"),
+                              (m.vertices, np.array([[0, 0, 1]], np.int32), "stamp: degenerate mesh triangle"),
+                              (m.vertices, np.zeros((0, 3), np.int32), "stamp: empty mesh")):
+        with pytest.raises(cpu_checkers.CheckerError, match=text):
+            t.stamp_mesh(verts, tris)
+    assert t.allocated_block_count() == 0
+
+
+def test_box_mesh_stamp_allocates_and_fills_like_stamp_primitive(oracle):
+    """Same candidate blocks, same pool order and the cuboid's distances (to rounding) as the reference's
+    stamp_primitive(Cuboid) -- checked against the reference build when present, else the restatement."""
+    ref = cpu_checkers.reference() if cpu_checkers.reference_available() else oracle
+    c, he, R = np.array([0.31, 0.22, 0.18]), np.array([0.11, 0.07, 0.09]), scenes.rot_z(0.3)
+    a = ref.make_tsdf(0.01, capacity=4096)
+    a.stamp_cuboid(R, c, he)
+    b = oracle.make_tsdf(0.01, capacity=4096)
+    m = scenes.box_mesh(c, he, R)
+    b.stamp_mesh(m.vertices, m.triangles)
+    ak, ap = a.export_blocks()
+    bk, bp = b.export_blocks()
+    assert np.array_equal(ak, bk) and np.array_equal(ap, bp) and len(ap) > 50
+    for pool in ap.tolist():
+        ga, gb = a.block_channels(pool)[2], b.block_channels(pool)[2]
+        np.testing.assert_allclose(gb, ga, rtol=0, atol=1e-12)
+
+
+# ---- the CUDA path against the restatement ------------------------------------------------------------------------
+def _mesh_scene(seed, n_meshes=2, subdivisions=2, **kw):
+    scene = scenes.small_scene(seed, **kw)
+    rng = np.random.RandomState(100 + seed)
+    extent = np.array(scene.esdf_dims) * scene.esdf_voxel
+    for i in range(n_meshes):
+        c = scene.esdf_origin + (0.2 + 0.6 * rng.random_sample(3)) * extent
+        if i % 2 == 0:
+            scene.meshes.append(scenes.icosphere(c, 0.08 + 0.1 * rng.random_sample(), subdivisions))
+        else:
+            scene.meshes.append(scenes.box_mesh(c, 0.05 + 0.1 * rng.random_sample(3), scenes.rot_z(rng.random_sample())))
+    return scene
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_gpu_mesh_stamp_is_bit_identical_to_the_restatement(oracle, seed):
+    from paper_2603_05493_b200 import api
+    scene = _mesh_scene(seed)
+    tsdf, touched = gpu_world(scene)
+    cpu, touched0 = cpu_world(oracle, scene)
+    assert touched == touched0
+    assert assert_world_parity(tsdf, cpu), "channels not bit-identical"
+    esdf = api.build_esdf(tsdf, esdf_config(scene))
+    site, dist, _ = esdf.download()
+    _, _, site0, dist0 = cpu.build_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel)
+    assert np.array_equal(site, site0) and same_bits(dist, dist0)
+    assert (dist < 0).any() and (dist > 0).any()
+
+
+@pytest.mark.gpu
+def test_gpu_mesh_only_world_and_large_mesh(oracle):
+    """5120 triangles (several shared-memory chunks of the stamping kernel), no depth frame, off-grid centre."""
+    from paper_2603_05493_b200 import api
+    scene = scenes.small_scene(5, n_cuboids=0, n_spheres=0)
+    scene.frames.clear()
+    scene.meshes.append(scenes.icosphere((0.41, 0.37, 0.33), 0.21, 4))
+    tsdf, _ = gpu_world(scene)
+    cpu, _ = cpu_world(oracle, scene)
+    assert assert_world_parity(tsdf, cpu)
+    pts = np.array([[0.41, 0.37, 0.33 + 0.21 - 0.03], [0.41, 0.37, 0.33 + 0.21 + 0.03]])
+    sdf, valid = api.query_tsdf_geom(tsdf, pts)
+    assert np.asarray(valid).all() and sdf[0] < 0 < sdf[1]
+
+
+@pytest.mark.gpu
+def test_gpu_box_mesh_matches_stamp_primitive_cuboid():
+    """The mesh path reproduces the reference-pinned cuboid stamp: same blocks, distances to rounding."""
+    from paper_2603_05493_b200 import api
+    c, he, R = np.array([0.31, 0.22, 0.18]), np.array([0.11, 0.07, 0.09]), scenes.rot_z(0.3)
+    worlds = []
+    for as_mesh in (False, True):
+        cfg = api.make_tsdf_config(0.01)
+        cfg.capacity = 4096
+        t = api.make_tsdf(cfg)
+        if as_mesh:
+            m = scenes.box_mesh(c, he, R)
+            api.stamp_mesh(t, api.TriangleMesh(m.vertices, m.triangles))
+        else:
+            api.stamp_primitive(t, api.Cuboid(R, c, he))
+        keys, pool = t.export_blocks()
+        worlds.append((keys, pool, t.download_blocks(pool.tolist())[2]))
+    assert np.array_equal(worlds[0][0], worlds[1][0]) and np.array_equal(worlds[0][1], worlds[1][1])
+    np.testing.assert_allclose(worlds[1][2], worlds[0][2], rtol=0, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_mesh_validation_and_capture():
+    from paper_2603_05493_b200 import api
+    m = scenes.box_mesh((0.2, 0.2, 0.2), (0.1, 0.1, 0.1))
+    for verts, tris, text in ((np.full_like(m.vertices, np.inf), m.triangles, "stamp: non-finite mesh"),
+                              (m.vertices, m.triangles + 7, "stamp: mesh index out of range"),
+                              (m.vertices, np.array([[0, 0, 1]], np.int32), "stamp: degenerate mesh triangle"),
+                              (m.vertices, np.zeros((0, 3), np.int32), "stamp: empty mesh")):
+        with pytest.raises(api.ValidationError, match=text):
+            api.TriangleMesh(verts, tris)
+    mesh = api.TriangleMesh(m.vertices, m.triangles)
+    assert mesh.triangle_count() == 12
+    # pool too small for the candidate blocks: all-or-nothing, as stamp_primitive (sdf_world.hpp:313-317)
+    cfg = api.make_tsdf_config(0.01)
+    cfg.capacity = 8
+    t = api.make_tsdf(cfg)
+    with pytest.raises(api.ValidationError, match="pool exhausted"):
+        api.stamp_mesh(t, mesh)
+    assert api.allocated_block_count(t) == 0
