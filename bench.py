@@ -65,7 +65,7 @@ WORKLOAD_DESC = {
     "cfg1": "configs[0]: 640x480 depth frame into 1 m^3 at 1 cm (100^3 cells)",
     "cfg2": "configs[1]: 2 m^3 (2x1x1 m) workspace at 5 mm, 400x200x200 cells, one 640x480 depth camera + 3 cuboids, full ESDF every frame",
     "cfg3": "configs[2]: 1 m^3 at 2 mm, 500^3 cells, 4 depth cameras + 2 cuboids",
-    "cfg4": "configs[3]: configs[1] scene + sphere, 1 M batched distance+gradient queries per update",
+    "cfg4": "configs[3]: configs[1] scene + sphere + 1280-triangle mesh, 1 M batched distance+gradient queries per update",
     "cfg5env": "configs[4]: independent 1.5x1x1 m environments at 5 mm (300x200x200 cells), --envs-per-gpu per rank",
 }
 
@@ -274,6 +274,7 @@ def run_ours(args):
             self.staged_frames = None  # the same frames living in the handle's own staging slots (graph path)
             self.prims = [api.Cuboid(c.R, c.t, c.half_extents) for c in sc.cuboids] + \
                          [api.SphereShape(s.center, s.radius) for s in sc.spheres]
+            self.meshes = [api.TriangleMesh(m.vertices, m.triangles) for m in sc.meshes]  # uploaded once (static geometry)
             cfg = api.make_tsdf_config(sc.tsdf_voxel)
             cfg.capacity = sc.capacity
             self.tsdf = api.make_tsdf(cfg, stream.cuda_stream)
@@ -306,7 +307,7 @@ def run_ours(args):
                 if upload:
                     self.tsdf.upload_frame_async(slot)
                 self.tsdf.integrate_async(slot)
-            for p in self.prims:
+            for p in self.prims + self.meshes:
                 self.tsdf.stamp_async(p)
             self.esdf.build_async(self.tsdf)
             if self.queries is not None:
@@ -320,6 +321,8 @@ def run_ours(args):
                 k = api.integrate_depth(self.tsdf, f)          # H2D from the page-locked frame + 4 phases + D2H report
             for p in self.prims:
                 api.stamp_primitive(self.tsdf, p)
+            for m in self.meshes:
+                api.stamp_mesh(self.tsdf, m)
             api.build_esdf(self.tsdf, self.ecfg, self.esdf)
             r = self.esdf.last_report()                         # has_sites / seed count, read back by build_esdf (D2H)
             if self.queries is not None:

@@ -195,6 +195,31 @@ inline void stamp_primitive(SparseTsdf& tsdf, const Primitive& primitive) {  // 
   }
 }
 
+// Triangle meshes.  NOT in the reference (SPEC.md:8, :422 put mesh stamping out of scope; PAPER.md:293 names it):
+// an addition next to Primitive, which keeps its reference definition.  A closed mesh with outward,
+// counter-clockwise triangles in the world frame; the tables live on the device, so a static mesh is built once.
+struct TriangleMesh {
+  std::vector<Vec3> vertices;
+  std::vector<std::array<std::int32_t, 3>> triangles;
+};
+struct DeviceMesh {
+  std::shared_ptr<ks_mesh> handle;
+  int triangle_count() const { return ks_mesh_triangle_count(handle.get()); }
+};
+inline DeviceMesh upload_mesh(const TriangleMesh& mesh) {  // throws ValidationError("stamp: ... mesh ...")
+  std::vector<double> v(3 * mesh.vertices.size());
+  for (std::size_t i = 0; i < mesh.vertices.size(); ++i)
+    for (int a = 0; a < 3; ++a) v[3 * i + a] = mesh.vertices[i][a];
+  ks_mesh* raw = nullptr;
+  b200_detail::check(ks_mesh_create(v.data(), static_cast<std::int32_t>(mesh.vertices.size()),
+                                    mesh.triangles.empty() ? nullptr : mesh.triangles.front().data(),
+                                    static_cast<std::int32_t>(mesh.triangles.size()), &raw));
+  return DeviceMesh{std::shared_ptr<ks_mesh>(raw, ks_mesh_destroy)};
+}
+// flow of stamp_primitive (sdf_world.hpp:418-443) with the signed mesh distance of csrc/mesh.cuh
+inline void stamp_mesh(SparseTsdf& tsdf, const DeviceMesh& mesh) { b200_detail::check(ks_tsdf_stamp_mesh(tsdf.get(), mesh.handle.get())); }
+inline void stamp_mesh(SparseTsdf& tsdf, const TriangleMesh& mesh) { stamp_mesh(tsdf, upload_mesh(mesh)); }
+
 inline void decay_weights(SparseTsdf& tsdf, const DepthFrame& camera) {  // sdf_world.hpp:449-457
   const ks_camera cam = camera.camera();
   b200_detail::check(ks_tsdf_decay_weights(tsdf.get(), &cam));

@@ -539,9 +539,11 @@ __global__ void __launch_bounds__(256) k_stamp_mesh_candidates(TsdfView T, OpLis
 // sphere is farther from the block centre than (nearest possible + block diameter) cannot be the nearest one of any
 // voxel of the block; the others are listed in shared memory, a chunk at a time, and every thread walks the list
 // (all lanes read the same triangle: one broadcast load).
-constexpr int kMeshChunk = 1024;
+constexpr int kMeshChunk = 256;
+constexpr int kMeshRow = 13;  // centre xyz, radius, a, b, c
 __global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L, MeshView M) {
-  __shared__ int s_list[kMeshChunk];
+  __shared__ double s_tri[kMeshChunk * kMeshRow];
+  __shared__ int s_idx[kMeshChunk];
   __shared__ int s_count;
   __shared__ double s_red[16];
   const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L
       ub = fmin(ub, d + r);
     }
     ub = warp_min(ub);
-    __syncthreads();  // s_red, s_list of the previous block are no longer read
+    __syncthreads();  // s_red and the list of the previous block are no longer read
     if ((tid & 31) == 0) s_red[tid >> 5] = ub;
     __syncthreads();
     ub = s_red[0];
@@ -571,17 +573,42 @@ __global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L
     const double thr = (ub + 2.0 * radius) * kMeshSlack;
     const V3 p = v3((bx * kBlockEdge + lx + 0.5) * v, (by * kBlockEdge + ly + 0.5) * v, (bz * kBlockEdge + lz + 0.5) * v);  // voxel_center (:265-272)
     MeshHit best = {CUDART_INF, 0x7FFFFFFF, 0, v3(0.0, 0.0, 0.0)};
+    double reach = (ub + radius) * kMeshSlack;  // every voxel of the block is within ub + radius of the mesh
     for (int base = 0; base < M.nt; base += kMeshChunk) {
       __syncthreads();
       if (tid == 0) s_count = 0;
       __syncthreads();
-      for (int j = base + tid; j < min(base + kMeshChunk, M.nt); j += 512) {
-        double r;
-        if (mesh_bound(M, j, q, r) - r <= thr) s_list[atomicAdd(&s_count, 1)] = j;
+      const int j = base + tid;
+      if (tid < kMeshChunk && j < M.nt) {  // listed triangles travel to shared memory with their bounding sphere
+        const double2 b0 = __ldg(reinterpret_cast<const double2*>(M.bnd) + 2 * j), b1 = __ldg(reinterpret_cast<const double2*>(M.bnd) + 2 * j + 1);
+        const V3 d = v3(q.x - b0.x, q.y - b0.y, q.z - b1.x);
+        if (sqrt(v3_dot(d, d)) - b1.y <= thr) {
+          const int slot = atomicAdd(&s_count, 1);
+          double* S = s_tri + slot * kMeshRow;
+          S[0] = b0.x, S[1] = b0.y, S[2] = b1.x, S[3] = b1.y;
+          const double* G = M.tri + 9 * static_cast<size_t>(j);
+#pragma unroll
+          for (int c = 0; c < 9; ++c) S[4 + c] = __ldg(G + c);
+          s_idx[slot] = j;
+        }
       }
       __syncthreads();
       const int n = s_count;
-      for (int k = 0; k < n; ++k) mesh_visit(M, s_list[k], p, best);
+      for (int k = 0; k < n; ++k) {
+        const double* S = s_tri + k * kMeshRow;
+        const V3 d = v3(p.x - S[0], p.y - S[1], p.z - S[2]);
+        const double far = reach + S[3];
+        if (v3_dot(d, d) > far * far) continue;  // no point of this triangle can be nearer than the best so far
+        int feature;
+        const V3 c = closest_on_triangle(p, v3(S[4], S[5], S[6]), v3(S[7], S[8], S[9]), v3(S[10], S[11], S[12]), feature);
+        const V3 diff = v3_sub(p, c);
+        const double d2 = v3_dot(diff, diff);
+        const int tri = s_idx[k];
+        if (d2 < best.d2 || (d2 == best.d2 && tri < best.tri)) {
+          if (d2 < best.d2) reach = fmin(reach, sqrt(d2) * kMeshSlack);
+          best.d2 = d2, best.tri = tri, best.feature = feature, best.diff = diff;
+        }
+      }
     }
     const double sd = mesh_signed(M, best);
     const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;

@@ -182,10 +182,11 @@ def config3(dims=(500, 500, 500)) -> Scene:
 
 
 def config4(n_queries=1_000_000) -> Tuple[Scene, np.ndarray]:
-    """config2 + a sphere, with Q uniform query points in the workspace box."""
+    """config2 + a sphere + a 1280-triangle mesh (mesh + cuboid + depth mixed scene), with Q uniform query points."""
     scene = config2()
     scene.name = "cfg4"
     scene.spheres.append(Sphere(np.array([1.6, 0.7, 0.6]), 0.12))
+    scene.meshes.append(icosphere((0.35, 0.8, 0.7), 0.14, 3))
     rng = np.random.RandomState(7)
     extent = np.array(scene.esdf_dims, np.float64) * scene.esdf_voxel
     points = scene.esdf_origin + rng.random_sample((n_queries, 3)) * extent

@@ -86,3 +86,29 @@ def test_reference_reads_files_written_by_us(tmp_path):
     out = subprocess.run([str(ref), "read", str(tmp_path / "ours.ksdepth"), str(G / "field_reference.ksesdf"),
                           str(tmp_path / "x.ksdepth")], check=True, capture_output=True, text=True).stdout
     assert out == (G / "fileio_expected.txt").read_text()
+
+
+# ---- ks.hpp's mesh additions (no reference counterpart: SPEC.md:8) ---------------------------------------
+MESH = ROOT / "tests" / "cpp" / "mesh_program.cpp"
+
+
+def _build_mesh_program(out: Path):
+    from paper_2603_05493_b200 import build
+    build.build()
+    lib_dir = ROOT / "paper_2603_05493_b200"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{STANDIN}", str(MESH), "-o", str(out),
+                    f"-L{lib_dir}", "-lks_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+
+
+def test_mesh_program_compiles(tmp_path):
+    _build_mesh_program(tmp_path / "mesh_b200")
+
+
+@pytest.mark.gpu
+def test_mesh_program_box_mesh_equals_cuboid_stamp(tmp_path):
+    exe = tmp_path / "mesh_b200"
+    _build_mesh_program(exe)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines()
+    assert out[0].startswith("triangles 12 blocks ") and out[0].split()[-1] == out[0].split()[-2] != "0"
+    assert out[1] == "compared many missing 0 worst ok"
+    assert out[2] == "ValidationError: stamp: degenerate mesh triangle"

@@ -180,3 +180,27 @@ def test_gpu_mesh_validation_and_capture():
     with pytest.raises(api.ValidationError, match="pool exhausted"):
         api.stamp_mesh(t, mesh)
     assert api.allocated_block_count(t) == 0
+
+
+@pytest.mark.gpu
+def test_config4_mixed_scene_full_size_against_the_restatement(oracle):
+    """BASELINE configs[3] at full size: depth + 3 cuboids + sphere + 1280-triangle mesh into 400 x 200 x 200 cells,
+    then one million batched distance + gradient queries (the restatement needs ~10 s)."""
+    from paper_2603_05493_b200 import api
+    scene, pts = scenes.config4()
+    tsdf, touched = gpu_world(scene)
+    cpu, touched0 = cpu_world(oracle, scene)
+    assert touched == touched0
+    assert assert_world_parity(tsdf, cpu)
+    e = api.build_esdf(tsdf, esdf_config(scene))
+    site, dist, _ = e.download()
+    mask0, has0, site0, dist0 = cpu.build_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel)
+    assert int(e.report().seed_count) == int(mask0.sum())
+    assert np.array_equal(site, site0) and same_bits(dist, dist0)
+    s = api.query(e, pts)
+    d0, g0, i0 = oracle.query_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel, has0, dist0, pts)
+    assert same_bits(s.distance, d0) and same_bits(s.gradient, g0) and np.array_equal(s.inside, i0)
+    # inside the mesh the field is negative, just outside it is positive
+    c = np.array([0.35, 0.8, 0.7])
+    inside = api.query(e, np.array([c, c + [0.0, 0.0, 0.2]]))
+    assert inside.distance[0] < 0 < inside.distance[1]
