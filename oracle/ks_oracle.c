@@ -14,6 +14,10 @@
  * cases and on seeded random scenes; tests/golden/ holds vectors generated from
  * that reference build (tests/golden/make_golden.py) for boxes where the
  * reference tree is absent.
+ * ONE EXCEPTION -- PARITY UNPINNED: ko_stamp_mesh / ko_mesh_sdf (triangle-mesh
+ * stamping).  The reference has no mesh implementation and no test for one
+ * (SPEC.md:8, :422), so that section restates this repo's own definition; see
+ * the comment above it and tests/test_mesh_stamp.py for what anchors it.
  *
  * Third-party arithmetic: the reference's Vec3/Mat3 math is Eigen 3.x (version
  * unpinned, not vendored; core.hpp:18).  Restated here from Eigen's scalar
