@@ -539,37 +539,40 @@ __global__ void __launch_bounds__(256) k_stamp_mesh_candidates(TsdfView T, OpLis
 // sphere is farther from the block centre than (nearest possible + block diameter) cannot be the nearest one of any
 // voxel of the block; the others are listed in shared memory, a chunk at a time, and every thread walks the list
 // (all lanes read the same triangle: one broadcast load).
-constexpr int kMeshChunk = 256;
+constexpr int kMeshThreads = 256;  // half a block per CTA: three CTAs fit an SM's registers, and 2K items balance better than K
+constexpr int kMeshParts = kBlockVoxels / kMeshThreads;
+constexpr int kMeshChunk = kMeshThreads;
 constexpr int kMeshRow = 13;  // centre xyz, radius, a, b, c
-__global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L, MeshView M) {
+__global__ void __launch_bounds__(kMeshThreads, 3) k_stamp_mesh_blocks(TsdfView T, OpLists L, MeshView M) {
   __shared__ double s_tri[kMeshChunk * kMeshRow];
   __shared__ int s_idx[kMeshChunk];
   __shared__ int s_count;
-  __shared__ double s_red[16];
+  __shared__ double s_red[kMeshThreads / 32];
   const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
   if (!op_blocked(T)) finalize_slots(T, L, min(T.ctrl->fresh, L.cap));
   const int tid = threadIdx.x;
-  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
   const double v = T.voxel;
   const double radius = 0.5 * kBlockEdge * v * sqrt(3.0) * kMeshSlack;
-  for (int i = blockIdx.x; i < touched; i += gridDim.x) {
+  for (int item = blockIdx.x; item < touched * kMeshParts; item += gridDim.x) {
+    const int i = item / kMeshParts, voxel = (item % kMeshParts) * kMeshThreads + tid;
+    const int lx = voxel & 7, ly = (voxel >> 3) & 7, lz = voxel >> 6;
     const int pool = L.pool[i];
     int bx, by, bz;
     unpack_key(L.key[i], bx, by, bz);
     const V3 q = v3((bx * kBlockEdge + 0.5 * kBlockEdge) * v, (by * kBlockEdge + 0.5 * kBlockEdge) * v, (bz * kBlockEdge + 0.5 * kBlockEdge) * v);
     double ub = CUDART_INF;
-    for (int j = tid; j < M.nt; j += 512) {
+    for (int j = tid; j < M.nt; j += kMeshThreads) {
       double r;
       const double d = mesh_bound(M, j, q, r);
       ub = fmin(ub, d + r);
     }
     ub = warp_min(ub);
-    __syncthreads();  // s_red and the list of the previous block are no longer read
+    __syncthreads();  // s_red and the list of the previous item are no longer read
     if ((tid & 31) == 0) s_red[tid >> 5] = ub;
     __syncthreads();
     ub = s_red[0];
 #pragma unroll
-    for (int w = 1; w < 16; ++w) ub = fmin(ub, s_red[w]);
+    for (int w = 1; w < kMeshThreads / 32; ++w) ub = fmin(ub, s_red[w]);
     const double thr = (ub + 2.0 * radius) * kMeshSlack;
     const V3 p = v3((bx * kBlockEdge + lx + 0.5) * v, (by * kBlockEdge + ly + 0.5) * v, (bz * kBlockEdge + lz + 0.5) * v);  // voxel_center (:265-272)
     MeshHit best = {CUDART_INF, 0x7FFFFFFF, 0, v3(0.0, 0.0, 0.0)};
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L
       if (tid == 0) s_count = 0;
       __syncthreads();
       const int j = base + tid;
-      if (tid < kMeshChunk && j < M.nt) {  // listed triangles travel to shared memory with their bounding sphere
+      if (j < M.nt) {  // listed triangles travel to shared memory with their bounding sphere
         const double2 b0 = __ldg(reinterpret_cast<const double2*>(M.bnd) + 2 * j), b1 = __ldg(reinterpret_cast<const double2*>(M.bnd) + 2 * j + 1);
         const V3 d = v3(q.x - b0.x, q.y - b0.y, q.z - b1.x);
         if (sqrt(v3_dot(d, d)) - b1.y <= thr) {
@@ -611,14 +614,14 @@ __global__ void __launch_bounds__(512) k_stamp_mesh_blocks(TsdfView T, OpLists L
       }
     }
     const double sd = mesh_signed(M, best);
-    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+    const size_t at = static_cast<size_t>(pool) * kBlockVoxels + voxel;
     double g = T.geom[at];
     if (sd < g) {  // std::min(geom, sd)
       g = sd;
       T.geom[at] = g;
     }
     const double2 sw = T.sumwt[at];
-    store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
+    store_digest(T.digest, pool, voxel, voxel_bits(sw.x, sw.y, g, T.seed_thr));
     if (tid == 0) T.pool_geom[pool] = 1;
   }
   arrive_and_finish(T, L.cap, 0);
@@ -874,7 +877,7 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
   }
   run_allocation(t);
   KS_MARK(t, 5);
-  if (mesh) KS_LAUNCH(k_stamp_mesh_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, mesh->view);
+  if (mesh) KS_LAUNCH(k_stamp_mesh_blocks, 3 * kSmCount, kMeshThreads, 0, t->stream, t->view, t->lists, mesh->view);
   else KS_LAUNCH(k_stamp_blocks, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, P);
   KS_MARK(t, 6);
   KS_CUDA(cudaGetLastError());

@@ -23,7 +23,7 @@ from paper_2603_05493_b200 import api, scenes  # noqa: E402
 from parity_util import assert_world_parity, cpu_world, esdf_config, gpu_world, same_bits  # noqa: E402
 
 
-def one_case(oracle, rng, index):
+def one_case(oracle, rng, index, meshes=False):
     ratio = float(rng.choice([1.0, 1.0, 1.0, 0.5, 0.75, 1.0 / 3.0, 0.4, 0.9, 1.25, 2.0]))
     tsdf_voxel = float(rng.choice([0.02, 0.025, 0.013]))
     dims = tuple(int(v) for v in rng.randint(5, 72, 3))
@@ -34,6 +34,15 @@ def one_case(oracle, rng, index):
     params = dict(dims=dims, tsdf_voxel=tsdf_voxel, ratio=ratio, origin=tuple(float(v) for v in origin),
                   n_cuboids=int(rng.randint(0, 4)), n_spheres=int(rng.randint(0, 3)))
     scene = scenes.small_scene(int(rng.randint(1, 10**6)), **params)
+    n_meshes = int(rng.choice([0, 0, 1, 2])) if meshes else 0
+    ext = np.array(scene.esdf_dims) * scene.esdf_voxel
+    for _ in range(n_meshes):  # closed meshes: icospheres of 20..1280 triangles, rotated boxes; some poking out of the grid
+        c = scene.esdf_origin + (rng.random_sample(3) * 1.2 - 0.1) * ext
+        if rng.random_sample() < 0.5:
+            scene.meshes.append(scenes.icosphere(c, 0.03 + rng.random_sample() * 0.2 * ext.min(), int(rng.randint(0, 4))))
+        else:
+            scene.meshes.append(scenes.box_mesh(c, 0.02 + rng.random_sample(3) * 0.2 * ext.min(), scenes.rot_z(rng.random_sample() * 3.0) @ scenes.rot_y(rng.random_sample())))
+    params["n_meshes"] = n_meshes
     seeding = "gather" if rng.random_sample() < 0.85 else "scatter"
     tsdf, touched = gpu_world(scene)
     cpu, touched0 = cpu_world(oracle, scene)
@@ -46,7 +55,6 @@ def one_case(oracle, rng, index):
     assert int(e.report().seed_count) == int(mask0.sum()), ("seed count", params, seeding)
     assert np.array_equal(site, site0), ("sites", params, seeding)
     assert np.array_equal(dist, dist0) and np.array_equal(np.signbit(dist), np.signbit(dist0)), ("signed distance", params, seeding)
-    ext = np.array(scene.esdf_dims) * scene.esdf_voxel
     pts = scene.esdf_origin + (rng.random_sample((2000, 3)) * 1.2 - 0.1) * ext
     s = api.query(e, pts)
     d0, g0, i0 = oracle.query_esdf(scene.esdf_origin, scene.esdf_dims, scene.esdf_voxel, has0, dist0, pts)
@@ -58,6 +66,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--meshes", action="store_true", help="also stamp 0-2 random triangle meshes per scene")
     args = ap.parse_args()
     oracle = cpu_checkers.oracle()
     rng = np.random.RandomState(args.seed)
@@ -65,7 +74,7 @@ def main():
     n = 0
     ratios = {}
     while time.time() - t0 < args.seconds:
-        params, seeding, seeds = one_case(oracle, rng, n)
+        params, seeding, seeds = one_case(oracle, rng, n, args.meshes)
         ratios[round(params["ratio"], 3)] = ratios.get(round(params["ratio"], 3), 0) + 1
         n += 1
         if n % 25 == 0:
