@@ -6,12 +6,17 @@ CUDA path is compared bit for bit with oracle/ks_oracle.c's restatement of this 
 must reproduce sdf_cuboid / stamp_primitive(Cuboid) (sdf_world.hpp:224-229, :394-444) and an icosphere must
 approach sdf_sphere (:231-233) within its chord error.
 """
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 import cpu_checkers
 from paper_2603_05493_b200 import scenes
 from parity_util import assert_world_parity, cpu_world, esdf_config, gpu_world, same_bits
+
+
+GOLD = Path(__file__).resolve().parent / "golden" / "mesh_restatement.npz"
 
 
 @pytest.fixture(scope="module")
@@ -93,6 +98,32 @@ def test_box_mesh_stamp_allocates_and_fills_like_stamp_primitive(oracle):
     for pool in ap.tolist():
         ga, gb = a.block_channels(pool)[2], b.block_channels(pool)[2]
         np.testing.assert_allclose(gb, ga, rtol=0, atol=1e-12)
+
+
+def test_restatement_matches_its_committed_vectors(oracle):
+    """tests/golden/mesh_restatement.npz (made by make_mesh_golden.py from liboracle.so -- NOT reference output)."""
+    from golden.make_mesh_golden import cases, stamped_world
+    gold = np.load(GOLD)
+    for name, (mesh, pts) in cases().items():
+        assert same_bits(oracle.mesh_sdf(mesh.vertices, mesh.triangles, pts), gold[f"{name}_sdf"]), name
+    keys, geom = stamped_world(oracle)
+    assert np.array_equal(keys, gold["world_keys"]) and same_bits(geom, gold["world_geom"])
+
+
+@pytest.mark.gpu
+def test_gpu_matches_the_committed_vectors():
+    from golden.make_mesh_golden import cases
+    from paper_2603_05493_b200 import api
+    gold = np.load(GOLD)
+    cfg = api.make_tsdf_config(0.02)
+    cfg.capacity = 4096
+    t = api.make_tsdf(cfg)
+    for mesh, _ in cases().values():
+        api.stamp_mesh(t, api.TriangleMesh(mesh.vertices, mesh.triangles))
+    keys, pool = t.export_blocks()
+    order = np.lexsort((keys[:, 2], keys[:, 1], keys[:, 0]))
+    assert np.array_equal(keys[order], gold["world_keys"])
+    assert same_bits(t.download_blocks(pool[order].tolist())[2], gold["world_geom"])
 
 
 # ---- the CUDA path against the restatement ------------------------------------------------------------------------
