@@ -1206,25 +1206,8 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   };
   auto probe = make_probe();
   const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
-  auto resolve = [&](int j) {
-    dc_stretch<0, kTopShift>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
-  };
-  // The site table of a stretch's first winner is requested BEFORE the warp resolves its next stretch, so that the
-  // fetch (an L2 round trip on the critical path of the colouring otherwise) rides under a few hundred instructions.
-  auto first_table = [&](int j) {
-    const int u = K16[2 * slot(j << kTopShift) + 1];
-    const int c = static_cast<int>(KeysX::cost(G[edt_dc::at(u, lane)]));
-    if (c >= static_cast<int>(none_x)) return make_uint2(0u, 0u);
-    const uint32_t h = K16[2 * slot(u)];
-    const int sy = static_cast<int>(h >> 1), dz = exact_root(c - (y - sy) * (y - sy));
-    return __ldg(E.gtab + (u + nx * (sy + ny * ((h & 1u) ? z + dz : z - dz))));
-  };
-  if ((warp << kTopShift) < nx) resolve(warp);
   for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-    uint2 ahead = make_uint2(0u, 0u);
-    if constexpr (kSigns == 3)
-      if (live) ahead = first_table(j);
-    if (((j + nwarps) << kTopShift) < nx) resolve(j + nwarps);
+    dc_stretch<0, kTopShift>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
     if (!live) continue;
     // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
     const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
@@ -1245,7 +1228,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
           const int dz = exact_root(r2 - dy * dy);
           const int sz = (h & 1u) ? z + dz : z - dz;
           site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
-          if constexpr (kSigns == 3) probe.set_site(u, sy, sz, x == x0 ? ahead : __ldg(E.gtab + (u + nx * (sy + ny * sz))));
+          if constexpr (kSigns == 3) probe.set_site(u, sy, sz, __ldg(E.gtab + (u + nx * (sy + ny * sz))));
           else if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
         }
       }
