@@ -1,4 +1,5 @@
 // Library-level pieces of the C ABI: error text, streams, CUDA-graph helpers.
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -16,6 +17,14 @@ int fail(int status, const std::string& message) {
 int cuda_fail(cudaError_t err, const char* what) {
   g_error = std::string("cuda: ") + cudaGetErrorString(err) + " in " + what;
   return KS_ERR_CUDA;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* off = std::getenv("KS_B200_NO_PDL");
+    return !(off && off[0] == '1');
+  }();
+  return on;
 }
 
 }  // namespace ksb

@@ -13,6 +13,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "../../include/ks_b200.h"
 
@@ -30,11 +31,33 @@ int cuda_fail(cudaError_t err, const char* what);
   } while (0)
 
 extern std::atomic<int64_t> g_kernel_launches;
-#define KS_LAUNCH(kernel, grid, block, smem, stream, ...)           \
-  do {                                                              \
-    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
-    ::ksb::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+// Every kernel is launched with programmatic stream serialization (programmatic dependent launch): the next kernel
+// of the stream may be placed on the SMs while the previous one drains, and waits in pdl_enter() -- its first statement --
+// until that one has completed and flushed.  Stream order is unchanged; what goes away is the launch gap between the
+// ~20 short kernels of an update (captured into CUDA graphs as programmatic edges).  KS_B200_NO_PDL=1 turns it off.
+bool pdl_enabled();
+template <class... Exp, class... Act>
+inline cudaError_t launch_kernel(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr, cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+#define KS_LAUNCH(kernel, grid, block, smem, stream, ...)                          \
+  do {                                                                             \
+    ::ksb::launch_kernel(kernel, (grid), (block), (smem), (stream), __VA_ARGS__); \
+    ::ksb::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);              \
   } while (0)
+#ifdef __CUDACC__
+// First statement of every kernel: let the next kernel of the stream be scheduled, then wait for the previous one.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#endif
 
 constexpr int kSmCount = 148;  // B200
 

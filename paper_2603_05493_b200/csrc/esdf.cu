@@ -109,6 +109,7 @@ __device__ __forceinline__ uint32_t pair_bits(const TsdfView& T, int pool, int p
 
 // ---- per-axis tables: every fp64 division of the seeding stage happens here, once per axis position ----
 __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
+  pdl_enter();
   const int total = E.nx + E.ny + E.nz;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -132,6 +133,7 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
 // flag of the 3x3x3 directory entries around it (lanes 0..26; cleared with the directory); surf_too: also the
 // per-block "holds surface voxels" flag the brick gather's work list is built from.
 __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T, bool surf_too) {
+  pdl_enter();
   const int bound = T.ctrl->next_fresh;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(256) k_dir_fill(EsdfView E, TsdfView T, bool s
 // fallback's shortcut).  bit1: one of those blocks holds surface voxels; only these bricks can
 // contain seeds, so only they go on the gather's work list.
 __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
+  pdl_enter();
   const int nb = E.bnx * E.bny * E.bnz;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nb) return;
@@ -191,6 +194,7 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
 // recovery); the API path writes the reference's byte mask.
 template <bool kBits>
 __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
+  pdl_enter();
   const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   const int rows = E.ny * E.nz;
@@ -252,6 +256,7 @@ struct GatherStage {
   uint8_t geom[kStage];
 };
 __global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfView E, TsdfView T) {
+  pdl_enter();
   __shared__ GatherStage s_stage[kGatherWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   GatherStage& S = s_stage[warp];
@@ -365,6 +370,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfVi
 constexpr int kResampleWarps = 8;
 constexpr int kMaxDirX = (kMaxDim + 2) / 8 + 8;
 __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView E, TsdfView T) {
+  pdl_enter();
   __shared__ uint8_t s_bits[kResampleWarps][3][kMaxDirX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ey = E.ny + 2, ez = E.nz + 2;
@@ -435,6 +441,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView 
 
 // one thread per word of the seed plane
 __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int words = E.wpr * E.ny * E.nz;
@@ -490,6 +497,7 @@ __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
 // ve <= v), read as 9 x-rows of three voxels from the digest's pair plane.  Persistent grid over the
 // compacted list of those seeds, one thread per seed.
 __global__ void __launch_bounds__(256) k_site_tables(EsdfView E, TsdfView T) {
+  pdl_enter();
   const int count = E.ctrl->seed_words;
   for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < count; item += gridDim.x * blockDim.x) {
     const int cell = E.seedw[item];
@@ -522,6 +530,7 @@ __global__ void __launch_bounds__(256) k_site_tables(EsdfView E, TsdfView T) {
 
 // ---- seed_scatter (esdf.hpp:73-98): every surface voxel of every live block marks its cell ----
 __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
+  pdl_enter();
   const int bound = T.ctrl->next_fresh;
   const int tid = threadIdx.x;
   const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
@@ -542,6 +551,7 @@ __global__ void __launch_bounds__(512) k_seed_scatter(EsdfView E, TsdfView T) {
 }
 
 __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
+  pdl_enter();
   unsigned local = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.cells; i += gridDim.x * blockDim.x) local += E.mask[i] != 0;
   for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xFFFFFFFFu, local, d);
@@ -557,6 +567,7 @@ __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
 constexpr int kFloodWarps = 4;
 template <bool kBits>
 __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
+  pdl_enter();
   extern __shared__ uint32_t s_words[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int plane = E.nx * E.ny;
@@ -615,6 +626,7 @@ __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
 
 // byte mask (the reference's SeedMask) -> x-packed bit plane, one warp per word
 __global__ void __launch_bounds__(256) k_pack_mask(EsdfView E) {
+  pdl_enter();
   const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (warp_id >= E.wpr * E.ny * E.nz) return;
@@ -630,6 +642,7 @@ __global__ void __launch_bounds__(256) k_pack_mask(EsdfView E) {
 // words below and above.  Phase 2 resolves "nearest seed along z" from one word + one info word per
 // candidate, so the 2-byte-per-cell nearest-z field is never written or read.
 __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
+  pdl_enter();
   extern __shared__ uint32_t s_words[];  // [nzw][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int xw = blockIdx.x % E.wpr, y = blockIdx.x / E.wpr;
@@ -672,6 +685,7 @@ __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
 // (shared memory, [word][lane]); after the barrier it walks its own 32 z upwards, so a column's work is
 // spread over nz/32 warps instead of one.
 __global__ void __launch_bounds__(1024) k_flood_z_chunks(EsdfView E) {
+  pdl_enter();
   extern __shared__ uint32_t s_words[];  // [nwords][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nwords = (E.nz + 31) >> 5;
@@ -918,6 +932,7 @@ __device__ __forceinline__ void sweep_stages(const edt::RowTile& T, const Src& s
 
 // grid = (ceil(nx/32), nz); block = 32 * bands.  lane <-> x, positions = y.
 __global__ void k_sweep_y(EsdfView E, int band, int bands) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x = blockIdx.x * 32 + lane, z = blockIdx.y;
@@ -951,6 +966,7 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // 2 = the same using the hint planes left by the bit-packed gather of this build.
 template <int kSigns>
 __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * 32, z = blockIdx.y;
@@ -1068,6 +1084,7 @@ __device__ __forceinline__ int exact_root(int sq) {
 // (in-plane d2 << 11 | site_y << 1 | seed above z), which is what phase 3 consumes.
 constexpr int kLoadBatch = 8;
 __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int x = blockIdx.x * kTileA + (lane & (kTileA - 1)), z = blockIdx.y * kTileZ + lane / kTileA;
@@ -1133,6 +1150,7 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src
 // kBig: rows so long that only one tile fits an SM -- then the tile gets 32 warps instead of 16
 template <int kSigns, bool kChunks, bool kBig>
 __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
@@ -1249,6 +1267,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
 
 // ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
+  pdl_enter();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
   const uint32_t site = E.field[o].x;
@@ -1312,6 +1331,7 @@ __device__ __forceinline__ void query_point(const EsdfView& E, const double p[3]
 
 __global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restrict__ pts, long long n, double* __restrict__ dist,
                                                double* __restrict__ grad, uint8_t* __restrict__ inside) {
+  pdl_enter();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
@@ -1334,6 +1354,7 @@ struct SummaryScratch {
 };
 __global__ void __launch_bounds__(128) k_probe_summary(EsdfView E, const double* __restrict__ pts, int n, double near, double tag,
                                                        SummaryScratch* scratch, double* __restrict__ out) {
+  pdl_enter();
   __shared__ double s_min[4];
   __shared__ int s_cnt[4];
   __shared__ bool s_last;
@@ -1393,6 +1414,7 @@ __global__ void __launch_bounds__(256) k_collision_static(EsdfView E, const doub
                                                           const double* __restrict__ radii, int n, double margin,
                                                           double* __restrict__ pen, double* __restrict__ cost,
                                                           double* __restrict__ grad) {
+  pdl_enter();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const double p[3] = {centers[3 * s], centers[3 * s + 1], centers[3 * s + 2]};
@@ -1418,6 +1440,7 @@ __global__ void __launch_bounds__(128) k_collision_swept(EsdfView E, const doubl
                                                          double* __restrict__ pen, double* __restrict__ cost,
                                                          double* __restrict__ g_center, double* __restrict__ g_next,
                                                          double* __restrict__ g_vel) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= timesteps * spheres) return;
   const int t = i / spheres, s = i % spheres;
@@ -1471,6 +1494,7 @@ __global__ void __launch_bounds__(128) k_collision_swept(EsdfView E, const doubl
 // reference's left-to-right sum are covered by the 1e-12 relative tolerance stated in the tests).
 __global__ void __launch_bounds__(256) k_collision_reduce(const double* __restrict__ pen, const double* __restrict__ cost, int width,
                                                           double* __restrict__ report3) {
+  pdl_enter();
   __shared__ double s_pen[256], s_cost[256];
   __shared__ int s_idx[256];
   const int group = blockIdx.x, tid = threadIdx.x;
@@ -1503,6 +1527,7 @@ __global__ void __launch_bounds__(256) k_collision_reduce(const double* __restri
 // ---- export to the reference's DenseEsdf arrays (x-fastest; esdf.hpp:58-64) ----
 __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ site_xyz, double* __restrict__ distance,
                                                 int* __restrict__ d2) {
+  pdl_enter();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= E.cells) return;
   const int x = static_cast<int>(idx % E.nx);

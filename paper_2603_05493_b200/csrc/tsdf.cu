@@ -192,6 +192,7 @@ __device__ __forceinline__ void note_block(const TsdfView& T, const OpLists& L, 
 // ---- phase 1+2: block discovery along rays + dedup (sdf_world.hpp:346-361, :308-311) ----
 __global__ void __launch_bounds__(256, 6) k_discover(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
                                                   const float* __restrict__ depth) {
+  pdl_enter();
   const FrameParams& F = *Fp;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= F.width * F.height) return;
@@ -309,6 +310,7 @@ __device__ void finalize_slots(const TsdfView& T, const OpLists& L, int n_fresh)
 // warp-cooperative probe (32 slots per step, ballot, one atomicMin; see claim_slot) and the CTA
 // resets the block (VoxelBlock::reset :70-74). ----
 __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
+  pdl_enter();
   if (op_blocked(T)) return;
   const TsdfCtrl* c = T.ctrl;
   const int n = min(c->fresh, L.cap);
@@ -397,6 +399,7 @@ __device__ __forceinline__ void arrive_and_finish(const TsdfView& T, int list_ca
 // so there are no atomics; {sum, wt} moves as one 16-byte access per thread.
 __global__ void __launch_bounds__(512) k_integrate(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
                                                    const float* __restrict__ depth) {
+  pdl_enter();
   __shared__ FrameParams F;
   if (threadIdx.x < sizeof(FrameParams) / 4)
     reinterpret_cast<uint32_t*>(&F)[threadIdx.x] = reinterpret_cast<const uint32_t*>(Fp)[threadIdx.x];
@@ -449,6 +452,7 @@ struct BlockBox {
   long long count;
 };
 __global__ void __launch_bounds__(256) k_stamp_candidates(TsdfView T, OpLists L, Primitive P, BlockBox B, double reach) {
+  pdl_enter();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < B.count;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int bx = B.lo[0] + static_cast<int>(i % B.n[0]);
@@ -469,6 +473,7 @@ __global__ void __launch_bounds__(256) k_stamp_candidates(TsdfView T, OpLists L,
 
 // ---- stamp: per-voxel min with the analytic distance (sdf_world.hpp:437-443) ----
 __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Primitive P) {
+  pdl_enter();
   const int touched = op_blocked(T) ? 0 : min(T.ctrl->touched, L.cap);
   if (!op_blocked(T)) finalize_slots(T, L, min(T.ctrl->fresh, L.cap));
   const int tid = threadIdx.x;
@@ -503,6 +508,7 @@ __device__ __forceinline__ double warp_min(double v) {
 // farther than ub = min(d + r); nothing is nearer than min(d - r)), then exact distances of the triangles that can
 // be the nearest one, lanes striding over them.  Only the magnitude matters here: |sdf(centre)| <= reach.
 __global__ void __launch_bounds__(256) k_stamp_mesh_candidates(TsdfView T, OpLists L, MeshView M, BlockBox B, double reach) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   for (long long i = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; i < B.count; i += nwarps) {
@@ -544,6 +550,7 @@ constexpr int kMeshParts = kBlockVoxels / kMeshThreads;
 constexpr int kMeshChunk = kMeshThreads;
 constexpr int kMeshRow = 13;  // centre xyz, radius, a, b, c
 __global__ void __launch_bounds__(kMeshThreads, 3) k_stamp_mesh_blocks(TsdfView T, OpLists L, MeshView M) {
+  pdl_enter();
   __shared__ double s_tri[kMeshChunk * kMeshRow];
   __shared__ int s_idx[kMeshChunk];
   __shared__ int s_count;
@@ -629,6 +636,7 @@ __global__ void __launch_bounds__(kMeshThreads, 3) k_stamp_mesh_blocks(TsdfView 
 
 // ---- decay_weights (sdf_world.hpp:449-457) ----
 __global__ void __launch_bounds__(512) k_decay(TsdfView T, Frustum Fr, double alpha_t, double alpha_f) {
+  pdl_enter();
   const int bound = T.ctrl->next_fresh;
   const int tid = threadIdx.x;
   for (int pool = blockIdx.x; pool < bound; pool += gridDim.x) {
@@ -657,6 +665,7 @@ __global__ void __launch_bounds__(512) k_decay(TsdfView T, Frustum Fr, double al
 // weight_total() is a sequential sum (sdf_world.hpp:75-79); it is compared with a
 // threshold, so the summation order is kept: one thread walks its block in order.
 __global__ void __launch_bounds__(128) k_recycle_flag(TsdfView T, int* flags, double threshold) {
+  pdl_enter();
   const int bound = T.ctrl->next_fresh;
   for (int pool = blockIdx.x * blockDim.x + threadIdx.x; pool < bound; pool += gridDim.x * blockDim.x) {
     int flag = 0;
@@ -677,6 +686,7 @@ __global__ void __launch_bounds__(128) k_recycle_flag(TsdfView T, int* flags, do
 // Tombstone flagged blocks in SLOT order and append their pool entries to the free list
 // in that order (the reference's iteration order, sdf_world.hpp:464-472).
 __global__ void __launch_bounds__(1024) k_recycle_commit(TsdfView T, const int* flags) {
+  pdl_enter();
   __shared__ int warp_sum[32];
   __shared__ int s_base;
   TsdfCtrl* c = T.ctrl;
@@ -732,6 +742,7 @@ __global__ void __launch_bounds__(1024) k_recycle_commit(TsdfView T, const int* 
 // ---- query_tsdf / query_tsdf_geom (sdf_world.hpp:481-507) ----
 __global__ void __launch_bounds__(256) k_query_tsdf(TsdfView T, const double* __restrict__ pts, long long n, int geom_only,
                                                     double* __restrict__ out, uint8_t* __restrict__ valid) {
+  pdl_enter();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const int vx = voxel_index(pts[3 * i], T.voxel), vy = voxel_index(pts[3 * i + 1], T.voxel),
@@ -756,9 +767,11 @@ __global__ void __launch_bounds__(256) k_query_tsdf(TsdfView T, const double* __
   valid[i] = have;
 }
 
-__global__ void k_find(TsdfView T, int bx, int by, int bz, int* out) { *out = table_find(T, bx, by, bz); }
+__global__ void k_find(TsdfView T, int bx, int by, int bz, int* out) {
+  pdl_enter(); *out = table_find(T, bx, by, bz); }
 
 __global__ void k_fill_u64(uint64_t* p, size_t n, uint64_t v) {
+  pdl_enter();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x)
     p[i] = v;
 }
