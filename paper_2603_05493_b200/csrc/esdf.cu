@@ -129,6 +129,17 @@ __global__ void k_axis_tables(EsdfView E, double tsdf_voxel) {
   E.qsf[i] = static_cast<float>(q - floor(q));
 }
 
+// Directory reset as a kernel of the update (not two memset nodes: those would sit outside the programmatic launch
+// chain); in the fused build it also zeroes the per-build counters that seeding accumulates into.
+__global__ void __launch_bounds__(256) k_dir_clear(EsdfView E, bool reset_counters) {
+  pdl_enter();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.dcount; i += gridDim.x * blockDim.x) {
+    E.dir[i] = -1;
+    E.dirg[i] = 0;
+  }
+  if (reset_counters && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl->seed_count = 0ull, E.ctrl->signs_recovered = 0, E.ctrl->seed_words = 0;
+}
+
 // One warp per live pool entry: its directory slot; for a stamped block, the "stamped geometry within one block"
 // flag of the 3x3x3 directory entries around it (lanes 0..26; cleared with the directory); surf_too: also the
 // per-block "holds surface voxels" flag the brick gather's work list is built from.
@@ -1217,6 +1228,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   }
   __syncthreads();
   dc_top_levels<0, kTopShift>(G, Kt, nx, warp, lane, warps_log2);
+  if (kSigns != 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) E.ctrl->signs_recovered = 1;
   const int obase = y + ny * nx * z;
   auto make_probe = [&]() {
     if constexpr (kSigns == 3) return SignTable(E, Tw, s_qsf, min(y, ny - 1), z);
@@ -1566,6 +1578,7 @@ struct ks_esdf {
   cudaStream_t side;
   cudaEvent_t fork, join;
   bool side_pending;
+  bool counters_reset;  // k_dir_clear of the build being enqueued zeroed the seeding counters (no memset needed)
   EsdfCtrl* h_ctrl;  // pinned
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
   int band_y, bands_y, band_x, bands_x;
@@ -1684,11 +1697,13 @@ static int order_after(ks_esdf* e, const ks_tsdf* t) {
   return KS_OK;
 }
 
+static bool fast_build(const ks_esdf* e);
 // bricks: also the brick flags / work list of the brick gather and of the hinted sign recovery
 static int refresh_directory(ks_esdf* e, const ks_tsdf* t, bool bricks_too = true) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(E.dir, 0xFF, static_cast<size_t>(E.dcount) * sizeof(int), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.dirg, 0, static_cast<size_t>(E.dcount), e->stream));
+  const bool reset_counters = !bricks_too && fast_build(e);  // the fused build: seed_async finds its counters zeroed
+  KS_LAUNCH(k_dir_clear, std::min(2 * kSmCount, (E.dcount + 255) / 256), 256, 0, e->stream, E, reset_counters);
+  e->counters_reset = reset_counters;
   KS_LAUNCH(k_dir_fill, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t), bricks_too);
   if (bricks_too) {
     KS_CUDA(cudaMemsetAsync(&E.ctrl->active_bricks, 0, sizeof(int), e->stream));
@@ -1704,7 +1719,8 @@ static bool fast_build(const ks_esdf* e) { return e->dc && e->resample_ok && e->
 // bits: gather straight into the bit-packed mask of the fused build (gather mode only)
 static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
   EsdfView& E = e->view;
-  KS_CUDA(cudaMemsetAsync(E.ctrl, 0, offsetof(EsdfCtrl, active_bricks), e->stream));  // seed_count, signs_recovered
+  if (!e->counters_reset) KS_CUDA(cudaMemsetAsync(E.ctrl, 0, offsetof(EsdfCtrl, active_bricks), e->stream));  // seed_count, signs_recovered
+  e->counters_reset = false;
   if (mode == 1) {
     const long long threads = static_cast<long long>(E.ny) * E.nz * E.wpr * 32;  // one warp per 32 x cells
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
@@ -1783,7 +1799,7 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   } else {
     KS_LAUNCH(k_sweep_x<0>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
   }
-  if (t) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));
+  if (t && !e->dc) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));  // k_sweep_x_dc<signs> sets the flag itself
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
