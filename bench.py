@@ -520,7 +520,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": stage_bytes[dominant],
                      "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
                      "note": "HBM is the nominal roof of every stage (no contraction on this path), but the sweeps are "
-                             "instruction-issue bound: see profiles/README.md and profiles/r1/j_ncu_k_sweep_x_dc.txt"},
+                             "instruction-issue bound: see profiles/README.md and profiles/r1/l_ncu_k_sweep_x_dc.txt"},
         "cpu_baseline": cpu_base,
     }
     print(json.dumps(line))
