@@ -156,7 +156,9 @@ KS_API int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double
  * pseudonormal of the closest feature (csrc/mesh.cuh).  vertices = n_vertices xyz triples in the world frame,
  * triangles = n_triangles index triples.  ks_mesh_create validates ("stamp: empty mesh", "stamp: non-finite
  * mesh", "stamp: mesh index out of range", "stamp: degenerate mesh triangle" -> KS_ERR_INVALID), builds the
- * per-triangle tables and uploads them once; stamping a created mesh is capturable. */
+ * per-triangle tables and uploads them once; stamping a created mesh is capturable.  ks_mesh_destroy waits for the
+ * device (a stamp may still read the tables): call it outside stream capture and after the last replay of any
+ * graph that stamps the mesh. */
 typedef struct ks_mesh ks_mesh;
 KS_API int ks_mesh_create(const double* vertices, int32_t n_vertices, const int32_t* triangles,
                           int32_t n_triangles, ks_mesh** out);
