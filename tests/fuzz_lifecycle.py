@@ -49,7 +49,7 @@ def one_world(oracle, rng):
     steps = 0
     t = f.t.copy()
     for _ in range(int(rng.randint(4, 12))):
-        op = rng.choice(["integrate", "integrate", "sphere", "cuboid", "decay", "recycle"])
+        op = rng.choice(["integrate", "integrate", "sphere", "cuboid", "mesh", "decay", "recycle"])
         if op == "integrate":
             t = f.t + np.array([0.25 * rng.randint(0, 4), 0.1 * rng.randint(0, 3), 0.0])
             depth = f.depth + np.float32(0.05 * rng.randint(0, 5))
@@ -62,6 +62,12 @@ def one_world(oracle, rng):
             c, he = sc.esdf_origin + rng.random_sample(3) * 0.4, 0.02 + 0.12 * rng.random_sample(3)
             R = scenes.rot_z(float(rng.random_sample()))
             both(lambda: api.stamp_primitive(tsdf, api.Cuboid(R, c, he)), lambda: cpu.stamp_cuboid(R, c, he), op)
+        elif op == "mesh":  # icosphere or rotated box as triangles: allocation (and exhaustion) must behave like the primitives
+            c = sc.esdf_origin + rng.random_sample(3) * 0.4
+            m = (scenes.icosphere(c, 0.03 + 0.1 * rng.random_sample(), int(rng.randint(0, 3))) if rng.random_sample() < 0.5
+                 else scenes.box_mesh(c, 0.02 + 0.12 * rng.random_sample(3), scenes.rot_z(float(rng.random_sample()))))
+            dm = api.TriangleMesh(m.vertices, m.triangles)
+            both(lambda: api.stamp_mesh(tsdf, dm), lambda: cpu.stamp_mesh(m.vertices, m.triangles), op)
         elif op == "decay":
             fr = api.DepthFrame(f.width, f.height, *f.intr, f.R, t, f.depth)
             for _ in range(int(rng.randint(1, 4))):
