@@ -1237,12 +1237,14 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   auto probe = make_probe();
   const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
   for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
+    const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
+    uint32_t own_lo = 0, own_hi = 0;  // requested before the stretch is resolved, so that the loads ride under it
+    if constexpr (kSigns == 3) own_lo = __ldg(orow + (x0 >> 5)), own_hi = (x0 >> 5) + 1 < E.wpr2 ? __ldg(orow + (x0 >> 5) + 1) : 0u;
     dc_stretch<0, kTopShift>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
     if (!live) continue;
     // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
-    const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
     uint32_t own = 0;  // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
-    if constexpr (kSigns == 3) own = __funnelshift_rc(orow[x0 >> 5], (x0 >> 5) + 1 < E.wpr2 ? orow[(x0 >> 5) + 1] : 0u, (x0 & 31) + 1);
+    if constexpr (kSigns == 3) own = __funnelshift_rc(own_lo, own_hi, (x0 & 31) + 1);
     uint2* fp = E.field + obase + ny * x0;
     int last = -1, r2 = 0;
     uint32_t site = kSiteNone;
