@@ -57,6 +57,12 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// Wait only, no early release: for kernels whose successor is not under this library's control (the last kernel of
+// a build, the query / export / collision kernels) and for the fallback kernels.  CTAs of a dependent that become
+// resident while this kernel still has CTAs to place only sit in their wait and take the place of real work
+// (measured: a 1 M-point k_query released at the start of the x sweep cost 0.11 ms at configs[3]); inside the update
+// chain every successor is known and too large to slip into a freed slot early, so those kernels use pdl_enter().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif
 
 constexpr int kSmCount = 148;  // B200

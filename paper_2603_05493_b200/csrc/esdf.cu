@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(128) k_brick_active(EsdfView E) {
 // recovery); the API path writes the reference's byte mask.
 template <bool kBits>
 __global__ void __launch_bounds__(256) k_seed_gather(EsdfView E, TsdfView T) {
-  pdl_enter();
+  pdl_wait();
   const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   const int rows = E.ny * E.nz;
@@ -267,7 +267,7 @@ struct GatherStage {
   uint8_t geom[kStage];
 };
 __global__ void __launch_bounds__(kGatherWarps * 32) k_seed_gather_bricks(EsdfView E, TsdfView T) {
-  pdl_enter();
+  pdl_wait();
   __shared__ GatherStage s_stage[kGatherWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   GatherStage& S = s_stage[warp];
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(256) k_count_mask(EsdfView E) {
 constexpr int kFloodWarps = 4;
 template <bool kBits>
 __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
-  pdl_enter();
+  pdl_wait();
   extern __shared__ uint32_t s_words[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int plane = E.nx * E.ny;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kFloodWarps * 32) k_flood_z(EsdfView E) {
 
 // byte mask (the reference's SeedMask) -> x-packed bit plane, one warp per word
 __global__ void __launch_bounds__(256) k_pack_mask(EsdfView E) {
-  pdl_enter();
+  pdl_wait();
   const int warp_id = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (warp_id >= E.wpr * E.ny * E.nz) return;
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
 // (shared memory, [word][lane]); after the barrier it walks its own 32 z upwards, so a column's work is
 // spread over nz/32 warps instead of one.
 __global__ void __launch_bounds__(1024) k_flood_z_chunks(EsdfView E) {
-  pdl_enter();
+  pdl_wait();
   extern __shared__ uint32_t s_words[];  // [nwords][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nwords = (E.nz + 31) >> 5;
@@ -943,7 +943,7 @@ __device__ __forceinline__ void sweep_stages(const edt::RowTile& T, const Src& s
 
 // grid = (ceil(nx/32), nz); block = 32 * bands.  lane <-> x, positions = y.
 __global__ void k_sweep_y(EsdfView E, int band, int bands) {
-  pdl_enter();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x = blockIdx.x * 32 + lane, z = blockIdx.y;
@@ -977,7 +977,7 @@ __global__ void k_sweep_y(EsdfView E, int band, int bands) {
 // 2 = the same using the hint planes left by the bit-packed gather of this build.
 template <int kSigns>
 __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int band, int bands) {
-  pdl_enter();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * 32, z = blockIdx.y;
@@ -1161,7 +1161,7 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src
 // kBig: rows so long that only one tile fits an SM -- then the tile gets 32 warps instead of 16
 template <int kSigns, bool kChunks, bool kBig>
 __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
-  pdl_enter();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
@@ -1281,7 +1281,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
 
 // ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
 __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
-  pdl_enter();
+  pdl_wait();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
   const uint32_t site = E.field[o].x;
@@ -1345,7 +1345,7 @@ __device__ __forceinline__ void query_point(const EsdfView& E, const double p[3]
 
 __global__ void __launch_bounds__(256) k_query(EsdfView E, const double* __restrict__ pts, long long n, double* __restrict__ dist,
                                                double* __restrict__ grad, uint8_t* __restrict__ inside) {
-  pdl_enter();
+  pdl_wait();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
@@ -1428,7 +1428,7 @@ __global__ void __launch_bounds__(256) k_collision_static(EsdfView E, const doub
                                                           const double* __restrict__ radii, int n, double margin,
                                                           double* __restrict__ pen, double* __restrict__ cost,
                                                           double* __restrict__ grad) {
-  pdl_enter();
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const double p[3] = {centers[3 * s], centers[3 * s + 1], centers[3 * s + 2]};
@@ -1454,7 +1454,7 @@ __global__ void __launch_bounds__(128) k_collision_swept(EsdfView E, const doubl
                                                          double* __restrict__ pen, double* __restrict__ cost,
                                                          double* __restrict__ g_center, double* __restrict__ g_next,
                                                          double* __restrict__ g_vel) {
-  pdl_enter();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= timesteps * spheres) return;
   const int t = i / spheres, s = i % spheres;
@@ -1541,7 +1541,7 @@ __global__ void __launch_bounds__(256) k_collision_reduce(const double* __restri
 // ---- export to the reference's DenseEsdf arrays (x-fastest; esdf.hpp:58-64) ----
 __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ site_xyz, double* __restrict__ distance,
                                                 int* __restrict__ d2) {
-  pdl_enter();
+  pdl_wait();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= E.cells) return;
   const int x = static_cast<int>(idx % E.nx);
