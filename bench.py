@@ -288,7 +288,9 @@ def run_ours(args):
             self.probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
             self.queries = None
             if queries is not None:  # configs[3]: 1 M batched distance + gradient queries per update
-                self.queries_host = queries
+                self.query_buffers = api.QueryBuffers(len(queries))   # page-locked: the "planner" writes its points here
+                self.query_buffers.points[...] = queries
+                self.queries_host = self.query_buffers.points
                 self.queries = torch.from_numpy(queries).cuda()
                 self.q_dist = torch.empty(len(queries), dtype=torch.float64, device="cuda")
                 self.q_grad = torch.empty((len(queries), 3), dtype=torch.float64, device="cuda")
@@ -328,7 +330,7 @@ def run_ours(args):
             api.build_esdf(self.tsdf, self.ecfg, self.esdf)
             r = self.esdf.last_report()                         # has_sites / seed count, read back by build_esdf (D2H)
             if self.queries is not None:
-                api.query(self.esdf, self.queries_host)         # H2D points, D2H distance + gradient + inside
+                api.query(self.esdf, self.queries_host, self.query_buffers)  # H2D points, D2H distance + gradient + inside (page-locked)
             return k, r.seed_count
 
         def summary_into(self, row):
@@ -524,7 +526,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": stage_bytes[dominant],
                      "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
                      "note": "HBM is the nominal roof of every stage (no contraction on this path), but the sweeps are "
-                             "instruction-issue bound: see profiles/README.md and profiles/r1/l_ncu_k_sweep_x_dc.txt"},
+                             "instruction-issue bound: see profiles/README.md and profiles/r1/p_ncu_k_sweep_x_dc.txt"},
         "cpu_baseline": cpu_base,
     }
     print(json.dumps(line))

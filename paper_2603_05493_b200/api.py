@@ -594,9 +594,52 @@ def build_esdf(tsdf: SparseTsdf, config: EsdfConfig, esdf: Optional[DenseEsdf] =
     return e
 
 
-def query(esdf: DenseEsdf, points) -> EsdfSample:  # esdf.hpp:337-387, batched over points
+class QueryBuffers:
+    """Page-locked host buffers for a batch of n queries (points in, distance / gradient / inside out): with these the
+    copies of `query` run at PCIe speed and no fresh host pages are touched per call."""
+
+    def __init__(self, n: int):
+        self.lib = load_library()
+        self.n = int(n)
+        self._ptrs = []
+
+        def pinned(count, ctype, dtype, shape):
+            ptr = C.c_void_p()
+            _check(self.lib.ks_host_alloc(count * C.sizeof(ctype), C.byref(ptr)))
+            self._ptrs.append(ptr)
+            return np.frombuffer((ctype * count).from_address(ptr.value), dtype=dtype).reshape(shape)
+
+        m = max(self.n, 1)
+        self.points = pinned(3 * m, C.c_double, np.float64, (m, 3))
+        self.distance = pinned(m, C.c_double, np.float64, (m,))
+        self.gradient = pinned(3 * m, C.c_double, np.float64, (m, 3))
+        self.inside = pinned(m, C.c_uint8, np.uint8, (m,))
+
+    def close(self):
+        self.points = self.distance = self.gradient = self.inside = None
+        for ptr in self._ptrs:
+            self.lib.ks_host_free(ptr)
+        self._ptrs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def query(esdf: DenseEsdf, points, buffers: Optional[QueryBuffers] = None) -> EsdfSample:  # esdf.hpp:337-387, batched over points
+    """`buffers` (optional): results land in its page-locked arrays (views are returned, `inside` as uint8); pass
+    `buffers.points` itself as `points` to skip the host-side copy of the inputs too."""
     pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
     n = pts.shape[0]
+    if buffers is not None:
+        if n > buffers.n:
+            raise ValidationError("query: more points than the buffers hold")
+        if pts.ctypes.data != buffers.points.ctypes.data:
+            buffers.points[:n] = pts
+        _check(esdf.lib.ks_esdf_query(esdf.h, _ptr(buffers.points), n, _ptr(buffers.distance), _ptr(buffers.gradient), _ptr(buffers.inside)))
+        return EsdfSample(buffers.distance[:n], buffers.gradient[:n], buffers.inside[:n])
     d = np.empty(max(n, 1), np.float64)
     g = np.empty((max(n, 1), 3), np.float64)
     inside = np.empty(max(n, 1), np.uint8)

@@ -538,3 +538,21 @@ def test_probe_summary_matches_the_batched_query():
         e.report()  # waits for the handle's stream
         got = out.cpu().numpy()
         assert got[0] == 7.0 and got[1] == want.min() and got[2] == float((want < near).sum()) and got[3] == float(fresh.seed_count)
+
+
+def test_query_through_page_locked_buffers_is_the_same_query():
+    scene = scenes.small_scene(2)
+    tsdf, _ = gpu_world(scene)
+    e = api.build_esdf(tsdf, esdf_config(scene))
+    rng = np.random.RandomState(5)
+    pts = scene.esdf_origin + (rng.random_sample((5000, 3)) * 1.2 - 0.1) * np.array(scene.esdf_dims) * scene.esdf_voxel
+    plain = api.query(e, pts)
+    buf = api.QueryBuffers(6000)
+    a = api.query(e, pts, buf)
+    assert same_bits(a.distance, plain.distance) and same_bits(a.gradient, plain.gradient)
+    assert np.array_equal(a.inside.astype(bool), plain.inside)
+    buf.points[:100] = pts[:100]
+    b = api.query(e, buf.points[:100], buf)  # inputs already in place
+    assert same_bits(b.distance, plain.distance[:100])
+    with pytest.raises(api.ValidationError, match="more points than the buffers hold"):
+        api.query(e, np.zeros((6001, 3)), buf)
