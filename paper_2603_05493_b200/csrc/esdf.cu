@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -1580,6 +1581,9 @@ struct ks_esdf {
   cudaStream_t side;
   cudaEvent_t fork, join;
   bool side_pending;
+  void* query_scratch;   // device buffers of ks_esdf_query (host-pointer queries), grown on demand
+  int64_t query_cap;     // queries they hold
+  std::mutex query_mu;   // query() is safe to call concurrently: callers share the scratch one at a time
   bool counters_reset;  // k_dir_clear of the build being enqueued zeroed the seeding counters (no memset needed)
   EsdfCtrl* h_ctrl;  // pinned
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
@@ -1924,7 +1928,7 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
+  cudaFree(e->query_scratch), cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
@@ -2205,12 +2209,20 @@ int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host, const 
 int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, double* distance, double* gradient_xyz, uint8_t* inside) {
   if (!e) return fail(KS_ERR_INVALID, "null esdf");
   if (n <= 0) return KS_OK;
-  double *d_pts = nullptr, *d_dist = nullptr, *d_grad = nullptr;
-  uint8_t* d_in = nullptr;
-  KS_CUDA(cudaMalloc(&d_pts, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_dist, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_grad, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_in, n));
+  std::lock_guard<std::mutex> lock(e->query_mu);
+  // device scratch of the handle, grown on demand and kept: {points, gradient} 24 B, distance 8 B, inside 1 B per query
+  if (n > e->query_cap) {
+    const int64_t cap = std::max<int64_t>(n, 1024);
+    KS_CUDA(cudaStreamSynchronize(e->stream));
+    cudaFree(e->query_scratch);
+    e->query_scratch = nullptr, e->query_cap = 0;
+    KS_CUDA(cudaMalloc(&e->query_scratch, static_cast<size_t>(cap) * (7 * sizeof(double) + 1)));
+    e->query_cap = cap;
+  }
+  double* d_pts = static_cast<double*>(e->query_scratch);
+  double* d_grad = d_pts + 3 * e->query_cap;
+  double* d_dist = d_grad + 3 * e->query_cap;
+  uint8_t* d_in = reinterpret_cast<uint8_t*>(d_dist + e->query_cap);
   KS_CUDA(cudaMemcpyAsync(d_pts, points_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   int rc = ks_esdf_query_device_async(e, d_pts, n, d_dist, d_grad, d_in);
   if (rc == KS_OK) {
@@ -2219,7 +2231,6 @@ int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, double* dist
     if (inside) KS_CUDA(cudaMemcpyAsync(inside, d_in, n, cudaMemcpyDeviceToHost, e->stream));
     KS_CUDA(cudaStreamSynchronize(e->stream));
   }
-  cudaFree(d_pts), cudaFree(d_dist), cudaFree(d_grad), cudaFree(d_in);
   return rc;
 }
 
