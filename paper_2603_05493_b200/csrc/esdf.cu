@@ -1581,8 +1581,8 @@ struct ks_esdf {
   cudaStream_t side;
   cudaEvent_t fork, join;
   bool side_pending;
-  void* query_scratch;   // device buffers of ks_esdf_query (host-pointer queries), grown on demand
-  int64_t query_cap;     // queries they hold
+  void* query_scratch;   // device scratch of the host-pointer entry points (call_scratch), grown on demand
+  int64_t query_cap;     // doubles it holds
   std::mutex query_mu;   // query() is safe to call concurrently: callers share the scratch one at a time
   bool counters_reset;  // k_dir_clear of the build being enqueued zeroed the seeding counters (no memset needed)
   EsdfCtrl* h_ctrl;  // pinned
@@ -2135,19 +2135,33 @@ int ks_esdf_probe_summary_device_async(ks_esdf* e, const double* points_dev, int
   return KS_OK;
 }
 
+// Device scratch of the host-pointer entry points (query, scene collision): one buffer per handle, grown on demand
+// and kept, so that a planner calling them every iteration pays no cudaMalloc / cudaFree (each of which also
+// synchronises the device).  Callers hold e->query_mu: the reference allows concurrent queries.
+static int call_scratch(ks_esdf* e, size_t doubles, double** out) {
+  if (doubles > static_cast<size_t>(e->query_cap)) {
+    const size_t cap = std::max<size_t>(doubles + doubles / 4, 8192);
+    KS_CUDA(cudaStreamSynchronize(e->stream));
+    cudaFree(e->query_scratch);
+    e->query_scratch = nullptr, e->query_cap = 0;
+    KS_CUDA(cudaMalloc(&e->query_scratch, cap * sizeof(double)));
+    e->query_cap = static_cast<int64_t>(cap);
+  }
+  *out = static_cast<double*>(e->query_scratch);
+  return KS_OK;
+}
+
 int ks_esdf_scene_collision_static(ks_esdf* e, const double* centers_host, const double* radii_host, int64_t n,
                                    double activation_margin, ks_collision_report* report, double* gradient_xyz_host) {
   if (!e || !report) return fail(KS_ERR_INVALID, "null argument");
   report->max_penetration = 0.0, report->worst_sphere = -1, report->cost = 0.0;
   if (n <= 0) return KS_OK;
   if (n > (1 << 30)) return fail(KS_ERR_INVALID, "scene_collision: too many spheres");
-  double *d_c = nullptr, *d_r = nullptr, *d_pen = nullptr, *d_cost = nullptr, *d_grad = nullptr, *d_rep = nullptr;
-  KS_CUDA(cudaMalloc(&d_c, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_r, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_pen, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_cost, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_grad, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_rep, 3 * sizeof(double)));
+  std::lock_guard<std::mutex> lock(e->query_mu);
+  double* base = nullptr;
+  int rc = call_scratch(e, static_cast<size_t>(n) * 9 + 3, &base);
+  if (rc != KS_OK) return rc;
+  double *d_c = base, *d_grad = d_c + 3 * n, *d_r = d_grad + 3 * n, *d_pen = d_r + n, *d_cost = d_pen + n, *d_rep = d_cost + n;
   KS_CUDA(cudaMemcpyAsync(d_c, centers_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   KS_CUDA(cudaMemcpyAsync(d_r, radii_host, n * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   KS_LAUNCH(k_collision_static, static_cast<unsigned>((n + 255) / 256), 256, 0, e->stream, e->view, d_c, d_r, static_cast<int>(n),
@@ -2158,7 +2172,6 @@ int ks_esdf_scene_collision_static(ks_esdf* e, const double* centers_host, const
   if (gradient_xyz_host)
     KS_CUDA(cudaMemcpyAsync(gradient_xyz_host, d_grad, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   KS_CUDA(cudaStreamSynchronize(e->stream));
-  cudaFree(d_c), cudaFree(d_r), cudaFree(d_pen), cudaFree(d_cost), cudaFree(d_grad), cudaFree(d_rep);
   report->max_penetration = rep[0], report->worst_sphere = static_cast<int32_t>(rep[1]), report->cost = rep[2];
   return KS_OK;
 }
@@ -2174,14 +2187,10 @@ int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host, const 
   if (rc != KS_OK) return rc;
   if (!st.signs_recovered) return fail(KS_ERR_INVALID, "scene_collision: esdf signs not recovered");  // collision.hpp:181
   const size_t n = static_cast<size_t>(timesteps) * spheres;
-  double *d_c = nullptr, *d_r = nullptr, *d_v = nullptr, *d_pen = nullptr, *d_cost = nullptr, *d_g = nullptr, *d_rep = nullptr;
-  KS_CUDA(cudaMalloc(&d_c, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_v, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_r, spheres * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_pen, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_cost, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_g, 3 * n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_rep, static_cast<size_t>(timesteps) * 3 * sizeof(double)));
+  std::lock_guard<std::mutex> lock(e->query_mu);
+  double* base = nullptr;
+  if ((rc = call_scratch(e, n * 17 + spheres + static_cast<size_t>(timesteps) * 3, &base)) != KS_OK) return rc;
+  double *d_c = base, *d_v = d_c + 3 * n, *d_g = d_v + 3 * n, *d_pen = d_g + 9 * n, *d_cost = d_pen + n, *d_r = d_cost + n, *d_rep = d_r + spheres;
   KS_CUDA(cudaMemsetAsync(d_g, 0, 3 * n * 3 * sizeof(double), e->stream));
   KS_CUDA(cudaMemcpyAsync(d_c, centers_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   KS_CUDA(cudaMemcpyAsync(d_v, velocities_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
@@ -2197,7 +2206,6 @@ int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host, const 
   if (velocity_gradient)
     KS_CUDA(cudaMemcpyAsync(velocity_gradient, d_g + 2 * n * 3, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   KS_CUDA(cudaStreamSynchronize(e->stream));
-  cudaFree(d_c), cudaFree(d_v), cudaFree(d_r), cudaFree(d_pen), cudaFree(d_cost), cudaFree(d_g), cudaFree(d_rep);
   for (int t = 0; t < timesteps; ++t) {
     reports[t].max_penetration = rep[3 * t];
     reports[t].worst_sphere = static_cast<int32_t>(rep[3 * t + 1]);
@@ -2210,19 +2218,11 @@ int ks_esdf_query(ks_esdf* e, const double* points_host, int64_t n, double* dist
   if (!e) return fail(KS_ERR_INVALID, "null esdf");
   if (n <= 0) return KS_OK;
   std::lock_guard<std::mutex> lock(e->query_mu);
-  // device scratch of the handle, grown on demand and kept: {points, gradient} 24 B, distance 8 B, inside 1 B per query
-  if (n > e->query_cap) {
-    const int64_t cap = std::max<int64_t>(n, 1024);
-    KS_CUDA(cudaStreamSynchronize(e->stream));
-    cudaFree(e->query_scratch);
-    e->query_scratch = nullptr, e->query_cap = 0;
-    KS_CUDA(cudaMalloc(&e->query_scratch, static_cast<size_t>(cap) * (7 * sizeof(double) + 1)));
-    e->query_cap = cap;
-  }
-  double* d_pts = static_cast<double*>(e->query_scratch);
-  double* d_grad = d_pts + 3 * e->query_cap;
-  double* d_dist = d_grad + 3 * e->query_cap;
-  uint8_t* d_in = reinterpret_cast<uint8_t*>(d_dist + e->query_cap);
+  double* base = nullptr;  // {points, gradient} 24 B, distance 8 B, inside 1 B per query (rounded up to 8 doubles)
+  int rc0 = call_scratch(e, static_cast<size_t>(n) * 8, &base);
+  if (rc0 != KS_OK) return rc0;
+  double *d_pts = base, *d_grad = d_pts + 3 * n, *d_dist = d_grad + 3 * n;
+  uint8_t* d_in = reinterpret_cast<uint8_t*>(d_dist + n);
   KS_CUDA(cudaMemcpyAsync(d_pts, points_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   int rc = ks_esdf_query_device_async(e, d_pts, n, d_dist, d_grad, d_in);
   if (rc == KS_OK) {
