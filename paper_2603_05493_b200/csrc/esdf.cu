@@ -1834,7 +1834,6 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   if (cfg->nx > kMaxDim || cfg->ny > kMaxDim || cfg->nz > kMaxDim)
     return fail(KS_ERR_UNSUPPORTED, "esdf: dims above 1024 per axis are not supported by this build");
   ks_esdf* e = new ks_esdf();
-  std::memset(static_cast<void*>(e), 0, sizeof(*e));
   e->cfg = *cfg;
   EsdfView& E = e->view;
   E.nx = cfg->nx, E.ny = cfg->ny, E.nz = cfg->nz;

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -73,6 +74,9 @@ struct ks_tsdf {
   bool bounds_valid;
   long long known_avail, known_room;
   bool last_stamp_safe;  // the stamp enqueued last fits those bounds (and its block range is legal)
+  double* query_scratch;  // device scratch of ks_tsdf_query, grown on demand
+  int64_t query_cap;      // points it holds
+  std::mutex query_mu;
   // frame staging: one slot per camera, so a multi-camera update is one graph
   struct FrameSlot {
     FrameParams* h_frame;  // pinned
@@ -920,8 +924,7 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   if (cudaGetDeviceCount(&devices) != cudaSuccess || devices == 0)
     return fail(KS_ERR_CUDA, "ks_b200: no CUDA device (this library has no CPU path)");
 
-  ks_tsdf* t = new ks_tsdf();
-  std::memset(static_cast<void*>(t), 0, sizeof(*t));
+  ks_tsdf* t = new ks_tsdf();  // value-initialised: every member starts zeroed
   t->cfg = *cfg;
   static std::atomic<uint64_t> next_uid{1};
   t->uid = next_uid.fetch_add(1);
@@ -970,6 +973,7 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
   cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
+  cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
   for (ks_tsdf::FrameSlot& S : t->slots) {
     if (S.h_frame) cudaFreeHost(S.h_frame);
@@ -1306,18 +1310,24 @@ int ks_tsdf_recycle_blocks(ks_tsdf* t, int32_t* recycled) {
 int ks_tsdf_query(ks_tsdf* t, const double* points_host, int64_t n, int32_t geom_only, double* out_sdf, uint8_t* out_valid) {
   if (!t) return fail(KS_ERR_INVALID, "null tsdf");
   if (n <= 0) return KS_OK;
-  double *d_pts = nullptr, *d_out = nullptr;
-  uint8_t* d_valid = nullptr;
-  KS_CUDA(cudaMalloc(&d_pts, n * 3 * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_out, n * sizeof(double)));
-  KS_CUDA(cudaMalloc(&d_valid, n));
+  // device scratch kept in the handle (query_tsdf may be called concurrently, sdf_world.hpp / SPEC.md:415-416: one caller at a time here)
+  std::lock_guard<std::mutex> lock(t->query_mu);
+  if (n > t->query_cap) {
+    const int64_t cap = std::max<int64_t>(n + n / 4, 4096);
+    KS_CUDA(cudaStreamSynchronize(t->stream));
+    cudaFree(t->query_scratch);
+    t->query_scratch = nullptr, t->query_cap = 0;
+    KS_CUDA(cudaMalloc(&t->query_scratch, static_cast<size_t>(cap) * 5 * sizeof(double)));  // points 24 B, value 8 B, valid 1 B
+    t->query_cap = cap;
+  }
+  double *d_pts = t->query_scratch, *d_out = d_pts + 3 * n;
+  uint8_t* d_valid = reinterpret_cast<uint8_t*>(d_out + n);
   KS_CUDA(cudaMemcpyAsync(d_pts, points_host, n * 3 * sizeof(double), cudaMemcpyHostToDevice, t->stream));
   KS_LAUNCH(k_query_tsdf, static_cast<unsigned>((n + 255) / 256), 256, 0, t->stream, t->view, d_pts, static_cast<long long>(n),
             geom_only, d_out, d_valid);
   KS_CUDA(cudaMemcpyAsync(out_sdf, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, t->stream));
   KS_CUDA(cudaMemcpyAsync(out_valid, d_valid, n, cudaMemcpyDeviceToHost, t->stream));
   KS_CUDA(cudaStreamSynchronize(t->stream));
-  cudaFree(d_pts), cudaFree(d_out), cudaFree(d_valid);
   return KS_OK;
 }
 
