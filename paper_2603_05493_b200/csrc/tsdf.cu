@@ -74,6 +74,8 @@ struct ks_tsdf {
   bool bounds_valid;
   long long known_avail, known_room;
   bool last_stamp_safe;  // the stamp enqueued last fits those bounds (and its block range is legal)
+  TsdfCtrl* h_verdict;    // pinned: the control block as it stands once a frame's blocks are allocated (integrate_depth)
+  cudaEvent_t ev_verdict;
   double* query_scratch;  // device scratch of ks_tsdf_query, grown on demand
   int64_t query_cap;      // points it holds
   std::mutex query_mu;
@@ -952,6 +954,8 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   KS_CUDA(cudaMalloc(&t->d_flags, cap * sizeof(int)));
   for (cudaEvent_t& ev : t->ev) KS_CUDA(cudaEventCreate(&ev));
   KS_CUDA(cudaMallocHost(&t->h_ctrl, sizeof(TsdfCtrl)));
+  KS_CUDA(cudaMallocHost(&t->h_verdict, sizeof(TsdfCtrl)));
+  KS_CUDA(cudaEventCreateWithFlags(&t->ev_verdict, cudaEventDisableTiming));
   KS_CUDA(cudaMemsetAsync(V.ctrl, 0, sizeof(TsdfCtrl), t->stream));
   KS_CUDA(cudaMemsetAsync(V.slot_pool, 0xFF, V.nslots * sizeof(int), t->stream));
   KS_CUDA(cudaMemsetAsync(V.digest, 0, cap * kDigestWords * sizeof(uint32_t), t->stream));
@@ -975,6 +979,8 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
   cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
+  cudaFreeHost(t->h_verdict);
+  cudaEventDestroy(t->ev_verdict);
   for (ks_tsdf::FrameSlot& S : t->slots) {
     if (S.h_frame) cudaFreeHost(S.h_frame);
     if (S.d_frame) cudaFree(S.d_frame);
@@ -1077,7 +1083,13 @@ int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot) {
   return KS_OK;
 }
 
-int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) {
+static int integrate_enqueue(ks_tsdf* t, int32_t slot, bool verdict);
+int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) { return integrate_enqueue(t, slot, false); }
+
+// verdict: copy the control block to the host right after the allocation kernel.  Whether the frame fits (pool, table,
+// range) and how many blocks it touches is decided by then -- finish_op at the end of the voxel pass only applies
+// it -- so the blocking integrate_depth can return while k_integrate still runs.
+static int integrate_enqueue(ks_tsdf* t, int32_t slot, bool verdict) {
   if (!t || slot < 0 || slot >= KS_MAX_FRAME_SLOTS || !t->slots[slot].staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
   ks_tsdf::FrameSlot& S = t->slots[slot];
   const int pixels = S.h_frame->width * S.h_frame->height;
@@ -1088,6 +1100,10 @@ int ks_tsdf_integrate_slot_async(ks_tsdf* t, int32_t slot) {
   KS_MARK(t, 1);
   run_allocation(t);
   KS_MARK(t, 2);
+  if (verdict) {
+    KS_CUDA(cudaMemcpyAsync(t->h_verdict, t->view.ctrl, sizeof(TsdfCtrl), cudaMemcpyDeviceToHost, t->stream));
+    KS_CUDA(cudaEventRecord(t->ev_verdict, t->stream));
+  }
   KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_MARK(t, 3);
   KS_CUDA(cudaGetLastError());
@@ -1140,8 +1156,23 @@ int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float* depth
     KS_CUDA(cudaMemcpyAsync(S.d_frame, S.h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
     KS_CUDA(cudaMemcpyAsync(S.d_depth, depth_host, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
   } else if ((rc = ks_tsdf_upload_frame_async(t)) != KS_OK) return rc;
-  if ((rc = ks_tsdf_integrate_async(t)) != KS_OK) return rc;
-  ks_tsdf_report rep;
+  const bool early = !profiling(t);  // stage timing wants the whole op inside the call
+  if ((rc = integrate_enqueue(t, 0, early)) != KS_OK) return rc;
+  if (early) {
+    KS_CUDA(cudaEventSynchronize(t->ev_verdict));
+    const TsdfCtrl c = *t->h_verdict;  // what finish_op will see: the counters of the op in flight, the table before it
+    const long long avail = static_cast<long long>(t->view.capacity) - c.next_fresh + c.free_count;
+    const bool fits = c.err == 0 && c.abort_op == 0 && c.fresh <= avail && c.touched <= t->lists.cap &&
+                      static_cast<long long>(c.live) + c.fresh <= t->view.nslots;
+    if (fits) {  // integrate_depth's return value (sdf_world.hpp:388) is known; the voxel pass finishes behind the caller
+      t->bounds_valid = true;
+      t->known_avail = avail - c.fresh;
+      t->known_room = static_cast<long long>(t->view.nslots) - c.live - c.fresh;
+      if (blocks_touched) *blocks_touched = c.touched;
+      return KS_OK;
+    }
+  }
+  ks_tsdf_report rep;  // the frame does not fit (or timing is on): wait for the device's own report
   rc = ks_tsdf_sync(t, &rep);
   if (blocks_touched) *blocks_touched = rc == KS_OK ? rep.blocks_touched : 0;
   return rc;
