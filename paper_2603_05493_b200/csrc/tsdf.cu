@@ -403,7 +403,7 @@ __device__ __forceinline__ void arrive_and_finish(const TsdfView& T, int list_ca
 // ---- phase 4: voxel-centric projective integration (sdf_world.hpp:368-387) ----
 // One CTA per touched block, one thread per voxel: each thread owns its voxel,
 // so there are no atomics; {sum, wt} moves as one 16-byte access per thread.
-__global__ void __launch_bounds__(512) k_integrate(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
+__global__ void __launch_bounds__(512, 3) k_integrate(TsdfView T, OpLists L, const FrameParams* __restrict__ Fp,
                                                    const float* __restrict__ depth) {
   pdl_enter();
   __shared__ FrameParams F;
@@ -1104,7 +1104,7 @@ static int integrate_enqueue(ks_tsdf* t, int32_t slot, bool verdict) {
     KS_CUDA(cudaMemcpyAsync(t->h_verdict, t->view.ctrl, sizeof(TsdfCtrl), cudaMemcpyDeviceToHost, t->stream));
     KS_CUDA(cudaEventRecord(t->ev_verdict, t->stream));
   }
-  KS_LAUNCH(k_integrate, 4 * kSmCount, 512, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
+  KS_LAUNCH(k_integrate, 3 * kSmCount, 512, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_MARK(t, 3);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
