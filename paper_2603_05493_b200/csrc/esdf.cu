@@ -499,9 +499,15 @@ __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
     base = __shfl_sync(0xFFFFFFFFu, base, 0) + before - mine;
     for (uint32_t m = near; m != 0; m &= m - 1) E.seedw[base++] = 32 * xw + __ffs(static_cast<int>(m)) - 1 + E.nx * row;
   }
+  // seed count: one atomic per CTA (10 K same-address atomics, one per warp, were a visible part of this kernel)
+  __shared__ unsigned s_count;
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
   unsigned count = __popc(seed);
   for (int d = 16; d > 0; d >>= 1) count += __shfl_down_sync(0xFFFFFFFFu, count, d);
-  if (lane == 0 && count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(count));
+  if (lane == 0 && count != 0) atomicAdd(&s_count, count);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_count != 0) atomicAdd(&E.ctrl->seed_count, static_cast<unsigned long long>(s_count));
 }
 
 // Per-site sign tables: for every seed with a stamped block in reach, the geometry pairs {has value, negative}
