@@ -2,6 +2,7 @@
 // stamping, decay/recycle, point lookup.  Replaces the TSDF half of
 // /root/reference/proj/include/ks/sdf_world.hpp behind the C ABI in
 // include/ks_b200.h.  See DESIGN.md for the HBM layout and kernel roster.
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -15,6 +16,8 @@
 #include "mesh.cuh"
 
 namespace ksb {
+
+namespace cg = cooperative_groups;
 
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 
@@ -180,17 +183,26 @@ __device__ __forceinline__ bool op_blocked(const TsdfView& T) {
   return c->abort_op != 0 || c->fresh > c->free_count + (T.capacity - c->next_fresh) || c->live + c->fresh > T.nslots;
 }
 
+// atomicAdd(counter, 1) for every calling lane with ONE atomic per converged group of lanes: the op counters are single
+// addresses, and a warp of k_stamp_candidates appends up to 32 blocks at once.
+__device__ __forceinline__ int grouped_increment(int* counter) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  int base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(counter, static_cast<int>(g.size()));
+  return g.shfl(base, 0) + static_cast<int>(g.thread_rank());
+}
+
 // Record a block the op touches; new blocks also join the allocation list.
 __device__ __forceinline__ void note_block(const TsdfView& T, const OpLists& L, int bx, int by, int bz, uint32_t slot) {
   const int pool = table_find(T, bx, by, bz);
-  const int idx = atomicAdd(&T.ctrl->touched, 1);
+  const int idx = grouped_increment(&T.ctrl->touched);
   if (idx < L.cap) {
     L.key[idx] = pack_key(bx, by, bz);
     L.pool[idx] = pool;
     L.slot[idx] = slot;
   }
   if (pool < 0) {
-    const int j = atomicAdd(&T.ctrl->fresh, 1);
+    const int j = grouped_increment(&T.ctrl->fresh);
     if (j < L.cap) L.fresh_idx[j] = idx;
   }
 }
