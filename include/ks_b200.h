@@ -190,6 +190,13 @@ KS_API int ks_tsdf_export_blocks(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_in
 /* VoxelBlock channels of the given pool entries: n x 512 doubles each */
 KS_API int ks_tsdf_download_blocks(ks_tsdf* t, const int32_t* pool_index, int32_t n, double* depth_sum,
                                    double* depth_wt, double* geom_sdf);
+/* SparseTsdf::table.slots in slot order (sdf_world.hpp:103-110): key, pool index (-1 unless live) and state
+ * (0 empty, 1 live, 2 tombstone) of the first max_slots slots; *count = slot count.  Host mirrors (ks.hpp). */
+KS_API int ks_tsdf_export_slots(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_index, uint8_t* state, int32_t max_slots,
+                                int32_t* count);
+/* counts the mutating calls enqueued on the world so far (integrate, stamp, decay, recycle): a host copy of
+ * table / pool taken at generation g is stale once this returns something else.  No synchronisation. */
+KS_API uint64_t ks_tsdf_generation(const ks_tsdf* t);
 /* BlockHashTable::free_list, oldest first */
 KS_API int ks_tsdf_free_list(ks_tsdf* t, int32_t* out, int32_t max_out, int32_t* count);
 /* measurement hook: when enabled, non-captured ops record CUDA events between their stages;
@@ -221,6 +228,8 @@ KS_API int ks_esdf_last_report(const ks_esdf* e, ks_esdf_report* report);
 KS_API int ks_esdf_profile(ks_esdf* e, int32_t enable);
 KS_API int ks_esdf_stage_ms(ks_esdf* e, float out[6]);
 
+/* counts the calls enqueued so far that rewrite the field (build, propagate, recover_signs); see ks_tsdf_generation */
+KS_API uint64_t ks_esdf_generation(const ks_esdf* e);
 /* DenseEsdf::site / ::distance (any pointer may be NULL).  d2 = squared integer
  * site offset (exact), INT32_MAX when the grid has no sites. */
 KS_API int ks_esdf_download(ks_esdf* e, int32_t* site_xyz, double* distance, int32_t* d2);

@@ -3,23 +3,43 @@
 // Include this instead of "ks/sdf_world.hpp" and "ks/esdf.hpp"
 // (/root/reference/proj/include/ks/sdf_world.hpp, esdf.hpp) and link -lks_b200: the function
 // names, argument types, return values and exception types/texts are the reference's; the data
-// lives in HBM behind opaque handles (include/ks_b200.h).  Differences a caller can observe:
+// lives in HBM behind opaque handles (include/ks_b200.h).
+//
+// Mixing with the reference's own headers (collision.hpp, ik.hpp, ... -- the planner side, which stays the
+// reference's).  This header CLAIMS the include guards of the two headers it replaces (KS_SDF_WORLD_HPP,
+// KS_ESDF_HPP), so a later `#include "ks/esdf.hpp"` -- e.g. the one in collision.hpp:22 -- is a no-op, and it
+// takes Vec3 / Pose / ValidationError from the reference's core.hpp whenever that file is on the include path.
+// Two ways to use it, both covered by tests/cpp/mixed_program.cpp:
+//   * no source change: put include/ks_b200/overlay FIRST on the include path.  It holds forwarding headers
+//     ks/sdf_world.hpp, ks/esdf.hpp and a ks/collision.hpp that pulls the reference's own collision.hpp
+//     (#include_next) with its two scene functions renamed, so that scene_collision_static / scene_collision
+//     resolve to the batched GPU versions below while self_collision, CollisionReport, hinge_cost, ... stay the
+//     reference's.  ik.hpp:117-120 / :217-226 then run against the device field unchanged.
+//   * or include "ks_b200/ks.hpp" before any reference header; with the planner headers on the include path it
+//     pulls ks/collision.hpp itself in the same way.
+// Differences a caller can observe:
 //   * SparseTsdf / DenseEsdf hold a shared handle, so copying one aliases the same device world
 //     (the reference deep-copies its std::vectors); recover_signs(esdf, tsdf) works in place and
 //     returns the same handle.
-//   * SparseTsdf::pool / table and DenseEsdf::site / distance are not public vectors: call
-//     .site() / .distance() (downloaded on demand) or the ks_tsdf_export_* functions.
+//   * DenseEsdf::site / ::distance and SparseTsdf::table / ::pool are READ-ONLY host mirrors: they behave like
+//     the reference's const std::vector members (size, [], iteration, data) and are downloaded on first access
+//     after the device copy changed (ks_esdf_generation / ks_tsdf_generation); code that WRITES them does not
+//     compile.  A tombstoned slot mirrors as key (0,0,0) (the device table does not keep erased keys).
 //   * query_batch() is new: callers that looped over query() should hand the whole batch over.
-//   * scene_collision_static / scene_collision (collision.hpp:130-239) are here too, as one batched
-//     kernel each; the cost is a fixed-shape tree sum on the GPU (1e-12 relative to the reference's
-//     left-to-right sum), everything else is identical.
+//   * scene_collision_static / scene_collision (collision.hpp:130-239) are one batched kernel each; the cost is
+//     a fixed-shape tree sum on the GPU (1e-12 relative to the reference's left-to-right sum), everything else
+//     is identical.
 //   * save/load_depth_frame and save/load_esdf read and write the reference's KSDEPTH1 / KSESDF1 files;
 //     the JSON header is emitted with sorted keys like the reference's nlohmann dump, numbers in shortest
 //     round-trip form (values, not bytes, are what both sides agree on).
-// Vec3 / Mat3 / Pose / ValidationError are taken from the reference's own core.hpp when
-// KS_B200_USE_REFERENCE_CORE is defined (mixing with the planner headers), else declared here.
 #ifndef KS_B200_KS_HPP
 #define KS_B200_KS_HPP
+
+#if defined(KS_SDF_WORLD_HPP) || defined(KS_ESDF_HPP)
+#error "ks_b200/ks.hpp replaces ks/sdf_world.hpp and ks/esdf.hpp: include it first, or put include/ks_b200/overlay first on the include path"
+#endif
+#define KS_SDF_WORLD_HPP  // claimed: the reference's sdf_world.hpp / esdf.hpp become no-ops after this header
+#define KS_ESDF_HPP
 
 #include <Eigen/Dense>
 
@@ -31,7 +51,10 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <span>
 #include <sstream>
 #include <memory>
@@ -42,6 +65,19 @@
 #include <vector>
 
 #include "../ks_b200.h"
+
+// Reference core types whenever the reference tree is reachable (always the case when mixing with its planner headers).
+#if !defined(KS_B200_USE_REFERENCE_CORE) && defined(__has_include)
+#if __has_include("ks/core.hpp")
+#define KS_B200_USE_REFERENCE_CORE 1
+#endif
+#endif
+// Planner side present: collision.hpp's non-scene parts (self_collision, CollisionReport, ...) come from the reference.
+#if !defined(KS_B200_REFERENCE_COLLISION) && defined(KS_B200_USE_REFERENCE_CORE) && defined(__has_include)
+#if __has_include("ks/robot_model.hpp") && __has_include("ks/collision.hpp")
+#define KS_B200_REFERENCE_COLLISION 1
+#endif
+#endif
 
 #if defined(KS_B200_USE_REFERENCE_CORE)
 #include "ks/core.hpp"
@@ -95,6 +131,54 @@ inline void fill_pose(const Pose& pose, double r[9], double t[3]) {
     t[i] = pose.translation[i];
   }
 }
+
+/// Read-only host mirror of a device array: looks like a const std::vector<T> (the reference's public members,
+/// sdf_world.hpp:206-210, esdf.hpp:58-64).  The copy is fetched on the first access after the device side changed
+/// (generation counter of the handle); copies of the owning struct share it, like they share the handle.
+template <class T>
+class HostMirror {
+ public:
+  using value_type = T;
+  using const_iterator = typename std::vector<T>::const_iterator;
+  HostMirror() = default;
+  HostMirror(std::function<std::uint64_t()> generation, std::function<void(std::vector<T>&)> fetch)
+      : state_(std::make_shared<State>()) {
+    state_->generation = std::move(generation), state_->fetch = std::move(fetch);
+  }
+  const std::vector<T>& get() const {
+    static const std::vector<T> none;
+    if (!state_) return none;
+    std::lock_guard<std::mutex> lock(state_->mu);
+    const std::uint64_t now = state_->generation();
+    if (!state_->valid || now != state_->seen) {
+      state_->fetch(state_->data);
+      state_->seen = now, state_->valid = true;
+    }
+    return state_->data;
+  }
+  std::size_t size() const { return get().size(); }
+  bool empty() const { return get().empty(); }
+  const T& operator[](std::size_t i) const { return get()[i]; }
+  const T& at(std::size_t i) const { return get().at(i); }
+  const T& front() const { return get().front(); }
+  const T& back() const { return get().back(); }
+  const T* data() const { return get().data(); }
+  const_iterator begin() const { return get().begin(); }
+  const_iterator end() const { return get().end(); }
+  operator const std::vector<T>&() const { return get(); }
+  const std::vector<T>& operator()() const { return get(); }  // round-1 spelling: esdf.distance()
+
+ private:
+  struct State {
+    std::mutex mu;
+    std::vector<T> data;
+    std::uint64_t seen = 0;
+    bool valid = false;
+    std::function<std::uint64_t()> generation;
+    std::function<void(std::vector<T>&)> fetch;
+  };
+  std::shared_ptr<State> state_;
+};
 }  // namespace b200_detail
 
 // ---- sdf_world.hpp -----------------------------------------------------------------------------
@@ -149,9 +233,89 @@ struct DepthFrame {  // sdf_world.hpp:191-204
   }
 };
 
-struct SparseTsdf {  // sdf_world.hpp:206-210; the table and the pool live in HBM
+struct VoxelBlock {  // sdf_world.hpp:65-85 (host copy of one pool entry)
+  std::array<double, kBlockVoxels> depth_sum;
+  std::array<double, kBlockVoxels> depth_wt;
+  std::array<double, kBlockVoxels> geom_sdf;
+  double weight_total() const {
+    double sum = 0.0;
+    for (double w : depth_wt) sum += w;
+    return sum;
+  }
+  bool has_geometry() const {
+    for (double g : geom_sdf)
+      if (std::isfinite(g)) return true;
+    return false;
+  }
+};
+
+/// Read-only mirror of BlockHashTable (sdf_world.hpp:102-189): slots in slot order, free list, counters, find().
+struct BlockHashTableMirror {
+  enum class SlotState : std::uint8_t { kEmpty, kLive, kTombstone };
+  struct Slot {
+    BlockKey key;
+    std::int32_t pool = -1;
+    SlotState state = SlotState::kEmpty;
+  };
+  struct Counter {  // next_fresh as a live value
+    std::function<std::int32_t()> read;
+    operator std::int32_t() const { return read ? read() : 0; }
+  };
+  b200_detail::HostMirror<Slot> slots;
+  b200_detail::HostMirror<std::int32_t> free_list;
+  Counter next_fresh;
+  std::int32_t capacity = 0;
+  std::function<int(const BlockKey&)> lookup;
+  int live_count() const {
+    int count = 0;
+    for (const Slot& slot : slots.get()) count += slot.state == SlotState::kLive;
+    return count;
+  }
+  int available() const { return static_cast<int>(free_list.size()) + (capacity - next_fresh); }
+  int find(const BlockKey& key) const { return lookup ? lookup(key) : -1; }  // BlockHashTable::find, on the device table
+};
+
+/// Read-only mirror of SparseTsdf::pool: size() == capacity, pool[i] downloads entry i (cached per generation).
+class PoolMirror {
+ public:
+  PoolMirror() = default;
+  PoolMirror(std::shared_ptr<ks_tsdf> handle, std::size_t capacity) : state_(std::make_shared<State>()) {
+    state_->handle = std::move(handle), state_->capacity = capacity;
+  }
+  std::size_t size() const { return state_ ? state_->capacity : 0; }
+  const VoxelBlock& operator[](std::size_t i) const {
+    if (!state_ || i >= state_->capacity) throw ValidationError("tsdf: pool index out of range");
+    std::lock_guard<std::mutex> lock(state_->mu);
+    const std::uint64_t now = ks_tsdf_generation(state_->handle.get());
+    if (now != state_->seen) state_->blocks.clear(), state_->seen = now;
+    auto it = state_->blocks.find(i);
+    if (it == state_->blocks.end()) {
+      auto block = std::make_unique<VoxelBlock>();
+      const std::int32_t index = static_cast<std::int32_t>(i);
+      b200_detail::check(ks_tsdf_download_blocks(state_->handle.get(), &index, 1, block->depth_sum.data(), block->depth_wt.data(),
+                                                 block->geom_sdf.data()));
+      it = state_->blocks.emplace(i, std::move(block)).first;
+    }
+    return *it->second;
+  }
+  const VoxelBlock& at(std::size_t i) const { return (*this)[i]; }
+
+ private:
+  struct State {
+    std::mutex mu;
+    std::shared_ptr<ks_tsdf> handle;
+    std::size_t capacity = 0;
+    std::uint64_t seen = ~0ull;
+    std::map<std::size_t, std::unique_ptr<VoxelBlock>> blocks;
+  };
+  std::shared_ptr<State> state_;
+};
+
+struct SparseTsdf {  // sdf_world.hpp:206-210; the table and the pool live in HBM, the members below mirror them
   TsdfConfig config;
   std::shared_ptr<ks_tsdf> handle;
+  BlockHashTableMirror table;
+  PoolMirror pool;
   ks_tsdf* get() const { return handle.get(); }
 };
 
@@ -171,7 +335,44 @@ inline SparseTsdf make_tsdf(const TsdfConfig& config) {  // sdf_world.hpp:327-33
                    config.weight_threshold, config.capacity, config.slot_count};
   ks_tsdf* raw = nullptr;
   b200_detail::check(ks_tsdf_create(&c, &raw));
-  return SparseTsdf{config, std::shared_ptr<ks_tsdf>(raw, ks_tsdf_destroy)};
+  SparseTsdf tsdf;
+  tsdf.config = config;
+  tsdf.handle = std::shared_ptr<ks_tsdf>(raw, ks_tsdf_destroy);
+  const std::shared_ptr<ks_tsdf> h = tsdf.handle;
+  using Slot = BlockHashTableMirror::Slot;
+  tsdf.table.slots = b200_detail::HostMirror<Slot>([h] { return ks_tsdf_generation(h.get()); }, [h](std::vector<Slot>& out) {
+    std::int32_t n = 0;
+    b200_detail::check(ks_tsdf_export_slots(h.get(), nullptr, nullptr, nullptr, 0, &n));
+    std::vector<std::int32_t> keys(3 * static_cast<std::size_t>(n)), pools(n);
+    std::vector<std::uint8_t> state(n);
+    b200_detail::check(ks_tsdf_export_slots(h.get(), keys.data(), pools.data(), state.data(), n, &n));
+    out.resize(n);
+    for (std::int32_t i = 0; i < n; ++i) {
+      out[i].key = BlockKey{keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]};
+      out[i].pool = pools[i];
+      out[i].state = static_cast<BlockHashTableMirror::SlotState>(state[i]);
+    }
+  });
+  tsdf.table.free_list = b200_detail::HostMirror<std::int32_t>([h] { return ks_tsdf_generation(h.get()); }, [h, config](std::vector<std::int32_t>& out) {
+    out.resize(static_cast<std::size_t>(config.capacity));
+    std::int32_t n = 0;
+    b200_detail::check(ks_tsdf_free_list(h.get(), out.data(), config.capacity, &n));
+    out.resize(static_cast<std::size_t>(n));
+  });
+  tsdf.table.next_fresh.read = [h] {
+    ks_tsdf_report rep{};
+    b200_detail::check(ks_tsdf_sync(h.get(), &rep));
+    return rep.next_fresh;
+  };
+  tsdf.table.capacity = config.capacity;
+  tsdf.table.lookup = [h](const BlockKey& key) {
+    const std::int32_t k[3] = {key.x, key.y, key.z};
+    std::int32_t pool = -1;
+    b200_detail::check(ks_tsdf_find(h.get(), k, &pool));
+    return static_cast<int>(pool);
+  };
+  tsdf.pool = PoolMirror(h, static_cast<std::size_t>(config.capacity));
+  return tsdf;
 }
 
 inline int integrate_depth(SparseTsdf& tsdf, const DepthFrame& frame) {  // sdf_world.hpp:340-389
@@ -275,23 +476,15 @@ struct EsdfConfig {  // esdf.hpp:35-54
   }
 };
 
-struct DenseEsdf {  // esdf.hpp:58-64; site/distance are downloaded from HBM on demand
+struct DenseEsdf {  // esdf.hpp:58-64; the field lives in HBM, site / distance are read-only host mirrors of it
   EsdfConfig config;
-  std::shared_ptr<ks_esdf> handle;
+  b200_detail::HostMirror<std::array<std::int32_t, 3>> site;  // (-1,-1,-1) when no sites exist
+  b200_detail::HostMirror<double> distance;                   // meters; +inf sentinel without sites
   bool has_sites = false;
   bool signs_recovered = false;
+  std::shared_ptr<ks_esdf> handle;
   ks_esdf* get() const { return handle.get(); }
 
-  std::vector<std::array<std::int32_t, 3>> site() const {
-    std::vector<std::array<std::int32_t, 3>> out(config.cell_count());
-    b200_detail::check(ks_esdf_download(get(), &out[0][0], nullptr, nullptr));
-    return out;
-  }
-  std::vector<double> distance() const {
-    std::vector<double> out(config.cell_count());
-    b200_detail::check(ks_esdf_download(get(), nullptr, out.data(), nullptr));
-    return out;
-  }
   void refresh_flags() {
     ks_esdf_report rep{};
     b200_detail::check(ks_esdf_sync(get(), &rep));
@@ -316,6 +509,17 @@ inline DenseEsdf make_esdf(const EsdfConfig& config) {
   DenseEsdf esdf;
   esdf.config = config;
   esdf.handle = std::shared_ptr<ks_esdf>(raw, ks_esdf_destroy);
+  const std::shared_ptr<ks_esdf> h = esdf.handle;
+  const std::size_t cells = config.cell_count();
+  using Site = std::array<std::int32_t, 3>;
+  esdf.site = b200_detail::HostMirror<Site>([h] { return ks_esdf_generation(h.get()); }, [h, cells](std::vector<Site>& out) {
+    out.resize(cells);
+    b200_detail::check(ks_esdf_download(h.get(), &out[0][0], nullptr, nullptr));
+  });
+  esdf.distance = b200_detail::HostMirror<double>([h] { return ks_esdf_generation(h.get()); }, [h, cells](std::vector<double>& out) {
+    out.resize(cells);
+    b200_detail::check(ks_esdf_download(h.get(), nullptr, out.data(), nullptr));
+  });
   return esdf;
 }
 
@@ -387,6 +591,26 @@ inline void query_batch(const DenseEsdf& esdf, const std::vector<double>& points
 }
 
 // ---- collision.hpp, scene part (collision.hpp:30-52, :130-239) ---------------------------------------
+}  // namespace ks
+#if defined(KS_B200_REFERENCE_COLLISION)
+// The reference's own collision.hpp, with its two per-sphere query loops renamed out of the way: everything else
+// in it (hinge_cost, hinge_slope, CollisionReport, SelfCollisionConfig, self_collision, SceneCollisionConfig,
+// SceneTimestepReport) is used as is.  Its `#include "ks/esdf.hpp"` finds the guard claimed above.  With
+// include/ks_b200/overlay first on the include path this resolves to the overlay's ks/collision.hpp, which hands
+// over to the reference's file (#include_next) while KS_B200_WRAPPING_COLLISION is defined.
+#if defined(KS_COLLISION_HPP)
+#error "ks/collision.hpp was included before ks_b200/ks.hpp: include ks_b200/ks.hpp first, or put include/ks_b200/overlay first on the include path"
+#endif
+#define KS_B200_WRAPPING_COLLISION 1
+#define scene_collision_static scene_collision_static_query_loop
+#define scene_collision scene_collision_query_loop
+#include "ks/collision.hpp"
+#undef scene_collision_static
+#undef scene_collision
+#undef KS_B200_WRAPPING_COLLISION
+namespace ks {
+#else
+namespace ks {
 inline double hinge_cost(double clearance, double margin) {  // collision.hpp:30-37
   if (clearance >= margin) return 0.0;
   if (clearance >= 0.0) {
@@ -409,6 +633,8 @@ struct CollisionReport {  // collision.hpp:46-52
   std::vector<Vec3> gradient;
 };
 
+#endif
+
 /// One batched kernel instead of the reference's per-sphere query loop.
 inline CollisionReport scene_collision_static(const DenseEsdf& esdf, std::span<const Vec3> centers,
                                               std::span<const double> radii, double activation_margin = 0.025) {
@@ -428,6 +654,7 @@ inline CollisionReport scene_collision_static(const DenseEsdf& esdf, std::span<c
   return out;
 }
 
+#if !defined(KS_B200_REFERENCE_COLLISION)
 struct SceneCollisionConfig {  // collision.hpp:154-158
   double activation_margin = 0.025;
   double dt = 1.0;
@@ -439,6 +666,7 @@ struct SceneTimestepReport {  // collision.hpp:161-168
   double cost = 0.0;
   std::vector<Vec3> center_gradient, next_center_gradient, velocity_gradient;
 };
+#endif
 
 inline std::vector<SceneTimestepReport> scene_collision(const DenseEsdf& esdf, const std::vector<std::vector<Vec3>>& centers,
                                                         std::span<const double> radii,
@@ -587,7 +815,7 @@ inline void save_esdf(const std::string& path, const DenseEsdf& esdf) {  // esdf
   const auto len = static_cast<std::uint32_t>(header.size());
   out.write(reinterpret_cast<const char*>(&len), 4);
   out.write(header.data(), static_cast<std::streamsize>(header.size()));
-  const std::vector<double> distance = esdf.distance();
+  const std::vector<double>& distance = esdf.distance.get();
   std::vector<float> narrow(distance.size());
   for (std::size_t i = 0; i < distance.size(); ++i) narrow[i] = static_cast<float>(distance[i]);
   out.write(reinterpret_cast<const char*>(narrow.data()), static_cast<std::streamsize>(narrow.size() * sizeof(float)));

@@ -81,7 +81,7 @@ ABI_SYMBOLS = [
     "ks_tsdf_free_list", "ks_tsdf_profile", "ks_tsdf_stage_ms", "ks_esdf_profile", "ks_esdf_stage_ms", "ks_esdf_create", "ks_esdf_destroy", "ks_esdf_set_stream", "ks_esdf_build",
     "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync", "ks_esdf_last_report", "ks_esdf_probe_summary_device_async",
     "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async", "ks_esdf_scene_collision_static",
-    "ks_esdf_scene_collision_swept",
+    "ks_esdf_scene_collision_swept", "ks_tsdf_export_slots", "ks_tsdf_generation", "ks_esdf_generation",
 ]
 
 
@@ -163,6 +163,9 @@ def load_library() -> C.CDLL:
         "ks_esdf_query_device_async": (C.c_int, [VP, VP, I64, VP, VP, VP]),
         "ks_esdf_scene_collision_static": (C.c_int, [VP, VP, VP, I64, D, P(CollisionReportC), VP]),
         "ks_esdf_scene_collision_swept": (C.c_int, [VP, VP, VP, VP, I32, I32, D, D, I32, P(CollisionReportC), VP, VP, VP]),
+        "ks_tsdf_export_slots": (C.c_int, [VP, VP, VP, VP, I32, P(I32)]),
+        "ks_tsdf_generation": (C.c_uint64, [VP]),
+        "ks_esdf_generation": (C.c_uint64, [VP]),
     }
     assert sorted(sig) == sorted(ABI_SYMBOLS)
     for name, (res, args) in sig.items():

@@ -176,5 +176,6 @@ __host__ __device__ __forceinline__ int voxel_index(double p, double v) { return
 const TsdfView& tsdf_view(const ks_tsdf* t);
 cudaStream_t tsdf_stream(const ks_tsdf* t);
 uint64_t tsdf_uid(const ks_tsdf* t);  // unique per created handle (a recycled address is not the same world)
+void tsdf_reader_enqueued(const ks_tsdf* t, cudaStream_t reader);  // an ESDF build on another stream now reads this world
 
 }  // namespace ksb

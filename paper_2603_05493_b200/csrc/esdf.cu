@@ -1593,6 +1593,8 @@ struct ks_esdf {
   bool counters_reset;  // k_dir_clear of the build being enqueued zeroed the seeding counters (no memset needed)
   EsdfCtrl* h_ctrl;  // pinned
   double bound_voxel;  // TSDF voxel size the tables/directory were built for (0 = none)
+  int bound_capacity;  // TSDF pool capacity pool_surf was sized for
+  std::atomic<uint64_t> generation{0};  // bumped whenever a call that rewrites the field is enqueued
   int band_y, bands_y, band_x, bands_x;
   size_t smem_y, smem_x;
   SummaryScratch* summary_scratch;  // partials of k_probe_summary
@@ -1626,13 +1628,22 @@ static void pick_bands(int n, int& band, int& bands) {
 
 static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   const TsdfView& T = tsdf_view(t);
-  if (e->bound_voxel == T.voxel) return KS_OK;
+  if (e->bound_voxel == T.voxel && T.capacity <= e->bound_capacity) return KS_OK;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(e->stream, &cap);
   if (cap != cudaStreamCaptureStatusNone)
     return fail(KS_ERR_INVALID, "esdf: build once against this TSDF before capturing a graph");
   EsdfView& E = e->view;
   KS_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->bound_voxel == T.voxel) {  // same geometry, a world with a larger pool: only the per-pool-entry flags grow
+    if (E.pool_surf) cudaFree(E.pool_surf);
+    E.pool_surf = nullptr;
+    KS_CUDA(cudaMalloc(&E.pool_surf, static_cast<size_t>(T.capacity)));
+    e->bound_capacity = T.capacity;
+    if (e->build_exec) cudaGraphExecDestroy(e->build_exec);  // the private graph holds the old pointer
+    e->build_exec = nullptr;
+    return KS_OK;
+  }
   if (E.dir) cudaFree(E.dir);
   E.dir = nullptr;
   const int dims[3] = {E.nx, E.ny, E.nz};
@@ -1652,6 +1663,7 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
   if (E.pool_surf) cudaFree(E.pool_surf);
   E.pool_surf = nullptr;
   KS_CUDA(cudaMalloc(&E.pool_surf, static_cast<size_t>(T.capacity)));
+  e->bound_capacity = T.capacity;
   E.ratio = static_cast<float>(E.ve / T.voxel);
   const int total = E.nx + E.ny + E.nz;
   KS_LAUNCH(k_axis_tables, (total + 127) / 128, 128, 0, e->stream, E, T.voxel);
@@ -1828,6 +1840,8 @@ static int signs_async(ks_esdf* e, const ks_tsdf* t) {
 
 extern "C" {
 
+static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg);
+
 int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   if (!cfg || !out) return fail(KS_ERR_INVALID, "null argument");
   *out = nullptr;
@@ -1840,6 +1854,19 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   if (cfg->nx > kMaxDim || cfg->ny > kMaxDim || cfg->nz > kMaxDim)
     return fail(KS_ERR_UNSUPPORTED, "esdf: dims above 1024 per axis are not supported by this build");
   ks_esdf* e = new ks_esdf();
+  const int rc = esdf_init(e, cfg);
+  if (rc != KS_OK) {  // one cleanup path: whatever was allocated so far goes with the handle
+    const std::string message = ks_last_error();
+    ks_esdf_destroy(e);
+    cudaGetLastError();
+    set_error(message);
+    return rc;
+  }
+  *out = e;
+  return KS_OK;
+}
+
+static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
   e->cfg = *cfg;
   EsdfView& E = e->view;
   E.nx = cfg->nx, E.ny = cfg->ny, E.nz = cfg->nz;
@@ -1866,15 +1893,17 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
     if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz);
   }
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
-    delete e;
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
   }
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_y)));
-#define KS_X_ATTR(M, C, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem_x)))
+  // The attribute is per kernel and process-wide: it is set to the opt-in maximum (never to one handle's own size, which
+  // would lower it under a larger ESDF that is still alive).
+  constexpr int kSmemOptIn = 227 * 1024;
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+#define KS_X_ATTR(M, C, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
 #define KS_X_ATTR4(C, B) KS_X_ATTR(0, C, B); KS_X_ATTR(1, C, B); KS_X_ATTR(2, C, B); KS_X_ATTR(3, C, B)
   KS_X_ATTR4(true, false); KS_X_ATTR4(false, false); KS_X_ATTR4(true, true); KS_X_ATTR4(false, true);
 #undef KS_X_ATTR4
@@ -1925,13 +1954,12 @@ int ks_esdf_create(const ks_esdf_config* cfg, ks_esdf** out) {
   KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
   KS_CUDA(cudaMemsetAsync(E.field, 0xFF, static_cast<size_t>(E.cells) * sizeof(uint2), e->stream));  // no sites yet
   KS_CUDA(cudaStreamSynchronize(e->stream));
-  *out = e;
   return KS_OK;
 }
 
 void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
-  cudaStreamSynchronize(e->stream);
+  if (e->stream) cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
   cudaFree(e->query_scratch), cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
   cudaFree(E.ctrl);
@@ -1939,12 +1967,13 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (E.pool_surf) cudaFree(E.pool_surf);
   cudaFreeHost(e->h_ctrl);
   if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
-  cudaStreamSynchronize(e->side);
-  cudaStreamDestroy(e->side);
-  cudaEventDestroy(e->fork), cudaEventDestroy(e->join);
-  cudaEventDestroy(e->dep);
-  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
-  if (e->own_stream) cudaStreamDestroy(e->stream);
+  if (e->side) cudaStreamSynchronize(e->side), cudaStreamDestroy(e->side);
+  if (e->fork) cudaEventDestroy(e->fork);
+  if (e->join) cudaEventDestroy(e->join);
+  if (e->dep) cudaEventDestroy(e->dep);
+  for (cudaEvent_t ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
 
@@ -1983,11 +2012,16 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
   int rc;
   if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
   if ((rc = order_after(e, t)) != KS_OK) return rc;
+  e->generation.fetch_add(1, std::memory_order_relaxed);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(e->stream, &cap);
   const bool outer_capture = cap != cudaStreamCaptureStatusNone;
   const bool prof = e->profile && !outer_capture;
-  if (outer_capture || prof || !e->own_graphs) return enqueue_build(e, t, prof);
+  if (outer_capture || prof || !e->own_graphs) {
+    rc = enqueue_build(e, t, prof);
+    if (rc == KS_OK && !outer_capture) tsdf_reader_enqueued(t, e->stream);
+    return rc;
+  }
   if (!e->build_exec || e->build_tsdf != tsdf_uid(t) || e->build_voxel != e->bound_voxel) {
     if (e->build_exec) cudaGraphExecDestroy(e->build_exec);
     e->build_exec = nullptr;
@@ -2016,8 +2050,11 @@ int ks_esdf_build_async(ks_esdf* e, const ks_tsdf* t) {
     g_kernel_launches.fetch_add(e->build_nodes, std::memory_order_relaxed);  // the capture counted its own launches once
   }
   KS_CUDA(cudaGraphLaunch(e->build_exec, e->stream));
+  tsdf_reader_enqueued(t, e->stream);
   return KS_OK;
 }
+
+uint64_t ks_esdf_generation(const ks_esdf* e) { return e ? e->generation.load(std::memory_order_relaxed) : 0; }
 
 int ks_esdf_profile(ks_esdf* e, int32_t enable) {
   if (!e) return fail(KS_ERR_INVALID, "null esdf");
@@ -2079,6 +2116,7 @@ int ks_esdf_seed(ks_esdf* e, const ks_tsdf* t, int32_t mode, uint8_t* mask_host)
 int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_len) {
   if (!e) return fail(KS_ERR_INVALID, "null esdf");
   EsdfView& E = e->view;
+  e->generation.fetch_add(1, std::memory_order_relaxed);
   if (mask_host) {
     if (mask_len != E.cells) return fail(KS_ERR_INVALID, "esdf: seed mask size does not match grid");  // esdf.hpp:195-196
     KS_CUDA(cudaMemcpyAsync(E.mask, mask_host, E.cells, cudaMemcpyHostToDevice, e->stream));
@@ -2097,6 +2135,7 @@ int ks_esdf_recover_signs(ks_esdf* e, const ks_tsdf* t) {
   if ((rc = bind_tsdf(e, t)) != KS_OK) return rc;
   if ((rc = order_after(e, t)) != KS_OK) return rc;
   if ((rc = refresh_directory(e, t)) != KS_OK) return rc;
+  e->generation.fetch_add(1, std::memory_order_relaxed);
   if ((rc = signs_async(e, t)) != KS_OK) return rc;
   return ks_esdf_sync(e, nullptr);
 }
@@ -2107,16 +2146,20 @@ int ks_esdf_download(ks_esdf* e, int32_t* site_xyz, double* distance, int32_t* d
   int* d_site = nullptr;
   double* d_dist = nullptr;
   int* d_d2 = nullptr;
-  if (site_xyz) KS_CUDA(cudaMalloc(&d_site, E.cells * 3 * sizeof(int)));
-  if (distance) KS_CUDA(cudaMalloc(&d_dist, E.cells * sizeof(double)));
-  if (d2) KS_CUDA(cudaMalloc(&d_d2, E.cells * sizeof(int)));
-  KS_LAUNCH(k_export, static_cast<unsigned>((E.cells + 255) / 256), 256, 0, e->stream, E, d_site, d_dist, d_d2);
-  if (site_xyz) KS_CUDA(cudaMemcpyAsync(site_xyz, d_site, E.cells * 3 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
-  if (distance) KS_CUDA(cudaMemcpyAsync(distance, d_dist, E.cells * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
-  if (d2) KS_CUDA(cudaMemcpyAsync(d2, d_d2, E.cells * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
-  KS_CUDA(cudaStreamSynchronize(e->stream));
+  const size_t cells = static_cast<size_t>(E.cells);
+  const int rc = [&]() -> int {
+    if (site_xyz) KS_CUDA(cudaMalloc(&d_site, cells * 3 * sizeof(int)));
+    if (distance) KS_CUDA(cudaMalloc(&d_dist, cells * sizeof(double)));
+    if (d2) KS_CUDA(cudaMalloc(&d_d2, cells * sizeof(int)));
+    KS_LAUNCH(k_export, static_cast<unsigned>((cells + 255) / 256), 256, 0, e->stream, E, d_site, d_dist, d_d2);
+    if (site_xyz) KS_CUDA(cudaMemcpyAsync(site_xyz, d_site, cells * 3 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    if (distance) KS_CUDA(cudaMemcpyAsync(distance, d_dist, cells * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (d2) KS_CUDA(cudaMemcpyAsync(d2, d_d2, cells * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    KS_CUDA(cudaStreamSynchronize(e->stream));
+    return KS_OK;
+  }();
   cudaFree(d_site), cudaFree(d_dist), cudaFree(d_d2);
-  return KS_OK;
+  return rc;
 }
 
 int ks_esdf_query_device_async(ks_esdf* e, const double* points_dev, int64_t n, double* distance_dev, double* gradient_dev,

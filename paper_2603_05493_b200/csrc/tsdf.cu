@@ -71,6 +71,7 @@ struct ks_tsdf {
   bool own_stream;
   TsdfCtrl* h_ctrl;  // pinned
   uint64_t uid;
+  std::atomic<uint64_t> generation{0};  // bumped by every mutating call enqueued (host mirrors of ks.hpp go stale on it)
   // Lower bounds, as of the last synchronisation minus what was enqueued since, on the free pool entries and
   // the free hash slots.  A blocking stamp whose candidate blocks fit both cannot fail on the device
   // (exhaustion / table full / range are the only device-side errors), so it returns without waiting.
@@ -79,6 +80,10 @@ struct ks_tsdf {
   bool last_stamp_safe;  // the stamp enqueued last fits those bounds (and its block range is legal)
   TsdfCtrl* h_verdict;    // pinned: the control block as it stands once a frame's blocks are allocated (integrate_depth)
   cudaEvent_t ev_verdict;
+  // An ESDF build on ANOTHER stream reads this world (digest, pool keys, next_fresh); it leaves its completion here and
+  // the next mutating call waits for it, so the two handles need not share a stream.
+  cudaEvent_t ev_reader;
+  bool reader_pending;
   double* query_scratch;  // device scratch of ks_tsdf_query, grown on demand
   int64_t query_cap;      // points it holds
   std::mutex query_mu;
@@ -101,6 +106,22 @@ namespace ksb {
 const TsdfView& tsdf_view(const ks_tsdf* t) { return t->view; }
 cudaStream_t tsdf_stream(const ks_tsdf* t) { return t->stream; }
 uint64_t tsdf_uid(const ks_tsdf* t) { return t->uid; }
+// called by a reader right after it enqueued its kernels on `reader` (a stream other than the world's own)
+void tsdf_reader_enqueued(const ks_tsdf* t_const, cudaStream_t reader) {
+  ks_tsdf* t = const_cast<ks_tsdf*>(t_const);
+  if (reader == t->stream || !t->ev_reader) return;
+  if (t->reader_pending) cudaStreamWaitEvent(reader, t->ev_reader, 0);  // chain: the new record then covers the earlier reader too
+  if (cudaEventRecord(t->ev_reader, reader) == cudaSuccess) t->reader_pending = true;
+  else cudaGetLastError();
+}
+static void wait_for_readers(ks_tsdf* t) {
+  if (!t->reader_pending) return;
+  t->reader_pending = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(t->stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone) return;  // inside a capture the caller orders the two handles (one stream)
+  if (cudaStreamWaitEvent(t->stream, t->ev_reader, 0) != cudaSuccess) cudaGetLastError();
+}
 
 // ---- device helpers ---------------------------------------------------------------
 
@@ -875,6 +896,8 @@ static bool profiling(ks_tsdf* t) {
 
 static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], const double hi_in[3], const ks_mesh* mesh = nullptr) {
   const bool prof = profiling(t);
+  t->generation.fetch_add(1, std::memory_order_relaxed);
+  wait_for_readers(t);
   KS_MARK(t, 4);
   // AABB grown by the truncation band -> block range (sdf_world.hpp:418-425)
   const double v = t->cfg.voxel_size, trunc = t->cfg.truncation;
@@ -919,6 +942,8 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
 
 extern "C" {
 
+static int tsdf_init(ks_tsdf* t, const ks_tsdf_config* cfg);
+
 int ks_tsdf_config_init(double voxel_size, ks_tsdf_config* out) {
   if (!out) return fail(KS_ERR_INVALID, "null config");
   *out = ks_tsdf_config{voxel_size, 4.0 * voxel_size, 0.99, 0.5, 0.5, 8192, 0};  // sdf_world.hpp:39-45, :56-61
@@ -939,6 +964,19 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
     return fail(KS_ERR_CUDA, "ks_b200: no CUDA device (this library has no CPU path)");
 
   ks_tsdf* t = new ks_tsdf();  // value-initialised: every member starts zeroed
+  const int rc = tsdf_init(t, cfg);
+  if (rc != KS_OK) {  // one cleanup path: whatever was allocated so far goes with the handle
+    const std::string message = ks_last_error();
+    ks_tsdf_destroy(t);
+    cudaGetLastError();
+    set_error(message);
+    return rc;
+  }
+  *out = t;
+  return KS_OK;
+}
+
+static int tsdf_init(ks_tsdf* t, const ks_tsdf_config* cfg) {
   t->cfg = *cfg;
   static std::atomic<uint64_t> next_uid{1};
   t->uid = next_uid.fetch_add(1);
@@ -976,14 +1014,14 @@ int ks_tsdf_create(const ks_tsdf_config* cfg, ks_tsdf** out) {
   std::memset(t->h_ctrl, 0, sizeof(TsdfCtrl));
   int rc = ensure_lists(t, 0, 1);
   if (rc != KS_OK) return rc;
+  KS_CUDA(cudaEventCreateWithFlags(&t->ev_reader, cudaEventDisableTiming));
   KS_CUDA(cudaStreamSynchronize(t->stream));
-  *out = t;
   return KS_OK;
 }
 
 void ks_tsdf_destroy(ks_tsdf* t) {
   if (!t) return;
-  cudaStreamSynchronize(t->stream);
+  if (t->stream) cudaStreamSynchronize(t->stream);
   TsdfView& V = t->view;
   cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.slot_claim), cudaFree(V.free_list), cudaFree(V.pool_key);
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
@@ -992,15 +1030,17 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
   cudaFreeHost(t->h_verdict);
-  cudaEventDestroy(t->ev_verdict);
+  if (t->ev_verdict) cudaEventDestroy(t->ev_verdict);
+  if (t->ev_reader) cudaEventDestroy(t->ev_reader);
   for (ks_tsdf::FrameSlot& S : t->slots) {
     if (S.h_frame) cudaFreeHost(S.h_frame);
     if (S.d_frame) cudaFree(S.d_frame);
     if (S.h_depth) cudaFreeHost(S.h_depth);
     if (S.d_depth) cudaFree(S.d_depth);
   }
-  for (cudaEvent_t ev : t->ev) cudaEventDestroy(ev);
-  if (t->own_stream) cudaStreamDestroy(t->stream);
+  for (cudaEvent_t ev : t->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
   delete t;
 }
 
@@ -1107,6 +1147,8 @@ static int integrate_enqueue(ks_tsdf* t, int32_t slot, bool verdict) {
   const int pixels = S.h_frame->width * S.h_frame->height;
   const bool prof = profiling(t);
   t->bounds_valid = false;  // a frame allocates a number of blocks only the device knows
+  t->generation.fetch_add(1, std::memory_order_relaxed);
+  wait_for_readers(t);
   KS_MARK(t, 0);
   KS_LAUNCH(k_discover, (pixels + 255) / 256, 256, 0, t->stream, t->view, t->lists, S.d_frame, S.d_depth);
   KS_MARK(t, 1);
@@ -1329,6 +1371,8 @@ int ks_tsdf_decay_weights_async(ks_tsdf* t, const ks_camera* cam) {
     }
     for (int a = 0; a < 3; ++a) Fr.n[p][a] = n[a];
   }
+  t->generation.fetch_add(1, std::memory_order_relaxed);
+  wait_for_readers(t);
   KS_LAUNCH(k_decay, 4 * kSmCount, 512, 0, t->stream, t->view, Fr, t->cfg.alpha_time, t->cfg.alpha_frustum);
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -1341,6 +1385,8 @@ int ks_tsdf_decay_weights(ks_tsdf* t, const ks_camera* cam) {
 
 int ks_tsdf_recycle_blocks(ks_tsdf* t, int32_t* recycled) {
   if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  t->generation.fetch_add(1, std::memory_order_relaxed);
+  wait_for_readers(t);
   KS_LAUNCH(k_recycle_flag, 2 * kSmCount, 128, 0, t->stream, t->view, t->d_flags, t->cfg.weight_threshold);
   KS_LAUNCH(k_recycle_commit, 1, 1024, 0, t->stream, t->view, t->d_flags);
   KS_CUDA(cudaGetLastError());
@@ -1412,6 +1458,29 @@ int ks_tsdf_export_blocks(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_index, in
     ++live;
   }
   if (count) *count = live;
+  return KS_OK;
+}
+
+uint64_t ks_tsdf_generation(const ks_tsdf* t) { return t ? t->generation.load(std::memory_order_relaxed) : 0; }
+
+int ks_tsdf_export_slots(ks_tsdf* t, int32_t* keys_xyz, int32_t* pool_index, uint8_t* state, int32_t max_slots, int32_t* count) {
+  if (!t) return fail(KS_ERR_INVALID, "null tsdf");
+  const int n = t->view.nslots;
+  if (count) *count = n;
+  if (max_slots <= 0) return KS_OK;
+  std::vector<uint64_t> keys(n);
+  std::vector<int> pools(n);
+  KS_CUDA(cudaMemcpyAsync(keys.data(), t->view.slot_key, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaMemcpyAsync(pools.data(), t->view.slot_pool, n * sizeof(int), cudaMemcpyDeviceToHost, t->stream));
+  KS_CUDA(cudaStreamSynchronize(t->stream));
+  for (int s = 0; s < n && s < max_slots; ++s) {
+    const bool live = keys[s] != kKeyEmpty && keys[s] != kKeyTomb;
+    int x = 0, y = 0, z = 0;
+    if (live) unpack_key(keys[s], x, y, z);
+    if (keys_xyz) keys_xyz[3 * s] = x, keys_xyz[3 * s + 1] = y, keys_xyz[3 * s + 2] = z;
+    if (pool_index) pool_index[s] = live ? pools[s] : -1;
+    if (state) state[s] = live ? 1 : (keys[s] == kKeyTomb ? 2 : 0);
+  }
   return KS_OK;
 }
 
