@@ -202,9 +202,9 @@ def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcou
         "stamp_blocks": Kp * (512 * (8 + 8 + 16) + 320),
         "directory": 4.0 * dcount + 8.0 * L,
         "seed": 3.0 * C_ / 8.0 + 6.0 * C_ / 8.0 + 2.0 * C_ / 8.0 + 128.0 * L + 5.0 * dcount,  # 3 resampled planes out; 5 rows + near row in, seed + near planes out; digest rows + directory in
-        "flood_z": C_ / 8.0 + 2.0 * C_ / 8.0,                         # bit mask in; column bit strings + per-word info out
-        "sweep_y": 2.0 * C_ / 8.0 + 4.0 * C_,                         # column words + info in, winning key u32 out
-        "sweep_x": 4.0 * C_ + 8.0 * C_ + C_ / 8.0,                    # u32 in, site u32 + signed d2 u32 out, own-sign plane
+        "flood_z": 2.0 * C_ / 8.0 + 3.0 * C_ / 8.0,                   # seed + table bit planes in; column bit strings (seeds, tables) + per-word info out
+        "sweep_y": 3.0 * C_ / 8.0 + 6.0 * C_,                         # column words + info in; tile images out: candidate u32 + payload u16
+        "sweep_x": 6.0 * C_ + 4.0 * C_ + C_ / 8.0,                    # tile images in (u32 + u16), field word u32 out, own-sign plane
         "signs": 0.0,                                                 # fused into sweep_x
     }[stage]
 

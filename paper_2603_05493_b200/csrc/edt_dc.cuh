@@ -29,6 +29,9 @@
 #pragma once
 #include <stdint.h>
 
+#include <type_traits>
+#include <utility>
+
 #if defined(__CUDACC__)
 #define KS_DC_HD __host__ __device__ __forceinline__
 #else
@@ -164,8 +167,33 @@ KS_DC_HD uint32_t scan(const uint32_t* G, int lo, int scan_len, int t, int row) 
 // the two halves (a pass over W candidates costs about 4 + 2*kM instructions each, so wide stretches pay twice:
 // more positions per candidate AND more candidates).
 constexpr int kFatMax = 7;
-template <int kPay, int kM, class WarpMax, class Emit>
-KS_DC_HD void stretch(const uint32_t* G, int n, int a, int lo_w, int hi_w, int row, WarpMax&& wmax, Emit&& emit) {
+
+// Where the keys of a stretch go.  put<I>(t, key): I is the position's index inside the (outermost) stretch as a
+// compile-time constant, so a sink may keep the keys in a register array; t is the position itself.
+template <class F>
+struct CallSink {  // adapter for a plain callable emit(t, key)
+  F& f;
+  template <int I>
+  KS_DC_HD void put(int t, uint32_t key) {
+    f(t, key);
+  }
+};
+template <int kN>
+struct KeySink {  // keys of positions a .. a + kN - 1 in registers; positions >= n keep 0xFFFFFFFF
+  uint32_t k[kN];
+  template <int I>
+  KS_DC_HD void put(int, uint32_t key) {
+    k[I] = key;
+  }
+};
+
+template <int kBase, class Sink, int kM, int... Is>
+KS_DC_HD void put_all(Sink& sink, int a, int n, const uint32_t (&best)[kM], std::integer_sequence<int, Is...>) {
+  ((a + Is < n ? sink.template put<kBase + Is>(a + Is, best[Is]) : void()), ...);
+}
+
+template <int kPay, int kM, int kBase, class WarpMax, class Sink>
+KS_DC_HD void stretch_into(const uint32_t* G, int n, int a, int lo_w, int hi_w, int row, WarpMax&& wmax, Sink& sink) {
   constexpr int S = Keys<kPay>::kShift;
   if constexpr (kM > kFatMax) {
     constexpr int kHalf = (kM - 1) / 2;
@@ -175,11 +203,11 @@ KS_DC_HD void stretch(const uint32_t* G, int n, int a, int lo_w, int hi_w, int r
     if (t < n) {
       const int longest = wmax(hi_w - lo_w + 1);
       const uint32_t key = scan<kPay>(G, clamp_start(lo_w, longest, n), longest, t, row);
-      emit(t, key);
+      sink.template put<kBase + kHalf>(t, key);
       mid = Keys<kPay>::winner(key);
     }
-    stretch<kPay, kHalf>(G, n, a, lo_w, mid, row, wmax, emit);
-    if (t + 1 < n) stretch<kPay, kHalf>(G, n, t + 1, mid, hi_w, row, wmax, emit);
+    stretch_into<kPay, kHalf, kBase>(G, n, a, lo_w, mid, row, wmax, sink);
+    if (t + 1 < n) stretch_into<kPay, kHalf, kBase + kHalf + 1>(G, n, t + 1, mid, hi_w, row, wmax, sink);
     return;
   } else {
     const int longest = wmax(hi_w - lo_w + 1);
@@ -211,12 +239,15 @@ KS_DC_HD void stretch(const uint32_t* G, int n, int a, int lo_w, int hi_w, int r
       g += kRows;
       --d0;
     }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int j = 0; j < kM; ++j)
-      if (a + j < n) emit(a + j, best[j]);
+    put_all<kBase>(sink, a, n, best, std::make_integer_sequence<int, kM>{});
   }
+}
+
+// emit(t, key) receives every position of the stretch (any order)
+template <int kPay, int kM, class WarpMax, class Emit>
+KS_DC_HD void stretch(const uint32_t* G, int n, int a, int lo_w, int hi_w, int row, WarpMax&& wmax, Emit&& emit) {
+  CallSink<std::remove_reference_t<Emit>> sink{emit};
+  stretch_into<kPay, kM, 0>(G, n, a, lo_w, hi_w, row, wmax, sink);
 }
 
 }  // namespace edt_dc

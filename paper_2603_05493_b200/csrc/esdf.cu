@@ -2,14 +2,16 @@
 // batched trilinear queries.  Replaces /root/reference/proj/include/ks/esdf.hpp
 // behind the C ABI in include/ks_b200.h.  See DESIGN.md for layouts and byte counts.
 //
-// Device layout of the finished field (per cell, 8 bytes):
-//   site : uint32  x | y<<10 | z<<20          (0xFFFFFFFF: grid has no sites)
-//   d2s  : uint32  bit31 = negative, bits0-30 = squared integer site offset
-//                  (0x7FFFFFFF: no sites).  distance = sqrt((double)d2) * voxel_size
-//                  is formed on the fly, so queries see exactly the reference's doubles.
-// Both are stored y-fastest, index = y + ny*(x + nx*z): the x sweep runs with lane <-> y,
-// so its stores are coalesced; the download path converts back to the reference's
-// x-fastest order (esdf.hpp:48-50).
+// Device layout of the finished field.
+//   Fast path (divide-and-conquer sweeps, every squared distance below 2^21): ONE uint32 per cell, x-fastest like the
+//   reference (esdf.hpp:48-50):   negative << 31 | squared integer site offset << 10 | site_x
+//   -- which is the winning key of the x sweep itself plus the sign bit.  distance = sqrt((double)d2) * voxel_size is
+//   formed on the fly, so queries see exactly the reference's doubles.  site_y / site_z are not stored per cell: they
+//   are the payload of phase 2's winner at (site_x, y, z), which stays in HBM (gimg / himg), and only the download and
+//   the stand-alone recover_signs ask for them.  Two such buffers exist; the x sweep writes the one readers do not
+//   use and publishes it with its last CTA (readers see the old or the new field, never a mix: SPEC.md:502-503).
+//   Wide path (banded-stack fallback, grids beyond the 32-bit keys): uint2 per cell, y-fastest,
+//   {site x | y<<10 | z<<20, d2 | negative << 31}; 0xFFFFFFFF / 0x7FFFFFFF without sites.
 #include <math_constants.h>
 
 #include <algorithm>
@@ -37,6 +39,10 @@ struct EsdfCtrl {
   int signs_recovered;
   int seed_words;     // entries of EsdfView::seedw (resampled seeding): seeds with a stamped block in reach
   int active_bricks;  // entries of EsdfView::active, rebuilt with the directory
+  // what readers go by (never touched by the resets above): published by the last CTA of the last sweep
+  int front;                     // fast path: index of the field buffer readers use
+  unsigned x_done;               // CTAs of the x sweep that have finished
+  unsigned long long pub_seeds;  // seed count of the published field (0: no sites)
 };
 
 // per-axis table rows (each [nx+ny+nz]): TSDF voxel index of (cell centre + offset), stored
@@ -85,7 +91,15 @@ struct EsdfView {
   uint32_t* zinfo;   // same layout: nearest seed z in the words below w | the words above w << 16 (0xFFFF: none)
   int nzw;           // words per column
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
-  uint2* field;      // [cells] y-fastest: {site (x | y << 10 | z << 20), squared distance | sign << 31}, one 8-byte store per cell
+  uint2* field;      // wide path: [cells] y-fastest: {site (x | y << 10 | z << 20), squared distance | sign << 31}
+  // fast path
+  int fast;          // 1: the field is f32[ctrl->front], phase 2's result is gimg / himg
+  uint32_t* zgbits;  // like zbits, for gbits: bit b of word w = the seed at z = 32w + b has a sign table
+  uint32_t* gimg;    // [nzt][nyt][nx][32 rows] the x sweep's tiles as they sit in shared memory: row = (y & 7) + 8 (z & 3),
+                     //   word = in-plane d2 << 10 | x  (KeysX candidate; none_x << 10 | x without candidate)
+  uint16_t* himg;    // same layout: site_y << 2 | seed above z << 1 | the site has a sign table
+  int nyt, nzt;      // tiles along y and z
+  uint32_t* f32[2];  // [cells] x-fastest: negative << 31 | d2 << 10 | site_x
   EsdfCtrl* ctrl;
 };
 
@@ -654,47 +668,63 @@ __global__ void __launch_bounds__(256) k_pack_mask(EsdfView E) {
   if (lane == 0) E.mbits[warp_id] = bits;
 }
 
+// 32 x 32 bit transpose inside a warp: lane i enters with row i, leaves with column i (bit j = row j's bit i).
+// Five butterfly rounds (one shuffle each) instead of 32 ballots.
+__device__ __forceinline__ uint32_t transpose32(uint32_t v, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, v, s);
+    v = (lane & s) ? ((v & ~m) | ((other >> s) & m)) : ((v & m) | ((other << s) & ~m));
+  }
+  return v;
+}
+
 // Phase 1 of the divide-and-conquer path (esdf.hpp:213-233), as data for phase 2 rather than a field: one CTA
 // per 32 consecutive x columns of one y, one warp per 32 z.  Warp w transposes its 32(z) x 32(x) bit tile of
 // the x-packed mask into word w of every column's bit string and adds, per word, the nearest seed in the
 // words below and above.  Phase 2 resolves "nearest seed along z" from one word + one info word per
-// candidate, so the 2-byte-per-cell nearest-z field is never written or read.
+// candidate, so the 2-byte-per-cell nearest-z field is never written or read.  The "seed has a sign table" plane
+// (gbits) is transposed alongside: phase 2 hands that bit on, and the x sweep needs no site decode where it is 0.
+// zinfo half = z (15 bits, 0x7FFF: none) | table bit << 15.
+constexpr uint32_t kZNone = 0x7FFFu;
 __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
   pdl_enter();
-  extern __shared__ uint32_t s_words[];  // [nzw][32]
+  extern __shared__ uint32_t s_words[];  // [nzw][32] seeds, then [nzw][32] table bits
+  uint32_t* s_tab = s_words + E.nzw * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int xw = blockIdx.x % E.wpr, y = blockIdx.x / E.wpr;
   const int x = xw * 32 + lane;
   {
     const int z = 32 * w + lane;
-    const uint32_t mine = z < E.nz ? __ldg(E.mbits + (z * E.ny + y) * E.wpr + xw) : 0u;  // 32 x-bits of row (y, z)
-    uint32_t bits = 0;
-#pragma unroll
-    for (int xb = 0; xb < 32; ++xb) {
-      const uint32_t col = __ballot_sync(0xFFFFFFFFu, (mine >> xb) & 1u);  // column xb: bit z
-      if (lane == xb) bits = col;
-    }
-    s_words[w * 32 + lane] = bits;
+    const int o = (z * E.ny + y) * E.wpr + xw;
+    const uint32_t mine = z < E.nz ? __ldg(E.mbits + o) : 0u;  // 32 x-bits of row (y, z)
+    const uint32_t tab = z < E.nz ? __ldg(E.gbits + o) : 0u;
+    s_words[w * 32 + lane] = transpose32(mine, lane);
+    s_tab[w * 32 + lane] = transpose32(tab, lane) ;
   }
   __syncthreads();
   if (x >= E.nx) return;
-  uint32_t below = 0xFFFFu, above = 0xFFFFu;
+  uint32_t below = kZNone, above = kZNone;
   for (int k = w - 1; k >= 0; --k) {
     const uint32_t m = s_words[k * 32 + lane];
     if (m != 0) {
-      below = 32 * k + 31 - __clz(static_cast<int>(m));
+      const int b = 31 - __clz(static_cast<int>(m));
+      below = (32 * k + b) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
       break;
     }
   }
   for (int k = w + 1; k < E.nzw; ++k) {
     const uint32_t m = s_words[k * 32 + lane];
     if (m != 0) {
-      above = 32 * k + __ffs(static_cast<int>(m)) - 1;
+      const int b = __ffs(static_cast<int>(m)) - 1;
+      above = (32 * k + b) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
       break;
     }
   }
   const int o = (y * E.nzw + w) * E.nx + x;
   E.zbits[o] = s_words[w * 32 + lane];
+  E.zgbits[o] = s_tab[w * 32 + lane] & s_words[w * 32 + lane];
   E.zinfo[o] = below | above << 16;
 }
 
@@ -1040,7 +1070,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_x(EsdfView E, TsdfView Tw, int
 // Top levels (visits at the multiples of the stretch length 2^kTopShift): fewer visits than warps, so the windows are cut into
 // slices whose minima meet in Kt through atomicMin, one barrier per level.  Below them every warp
 // resolves whole stretches of that many positions on its own (edt_dc::stretch), no barrier.
-using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z
+using KeysY = edt_dc::Keys<1>;  // payload bit: the column's seed lies above z (k_sweep_y_dc<2> adds "site has a sign table")
 using KeysX = edt_dc::Keys<0>;
 // stretch length per sweep (measured, cfg2): 16 positions along y, 8 along x
 constexpr int kTopShiftY = 4, kTopShiftX = 3;
@@ -1072,23 +1102,24 @@ __device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, i
   }
 }
 
-// stretch j = positions t' in (j << kTopShift, (j+1) << kTopShift]; emit(t, key) sees each of them once
-template <int kPay, int kTopShift, class Emit>
-__device__ __forceinline__ void dc_stretch(const uint32_t* G, const uint32_t* Kt, int n, int j, int lane, Emit&& emit) {
+// stretch j = positions t' in (j << kTopShift, (j+1) << kTopShift]; the sink gets each of them once, with its index
+// inside the stretch as a compile-time constant (edt_dc::KeySink keeps them in registers)
+template <int kPay, int kTopShift, class Sink>
+__device__ __forceinline__ void dc_stretch_into(const uint32_t* G, const uint32_t* Kt, int n, int j, int lane, Sink& sink) {
   constexpr int kTopStep = 1 << kTopShift;
   const int a = j << kTopShift;
   const bool closed = a + kTopStep <= n;
   const uint32_t right = closed ? Kt[edt_dc::at(j + 1, lane)] : 0u;
   const int lo_w = a > 0 ? edt_dc::Keys<kPay>::winner(Kt[edt_dc::at(j, lane)]) : 0;
   const int hi_w = closed ? edt_dc::Keys<kPay>::winner(right) : n - 1;
-  edt_dc::stretch<kPay, kTopStep - 1>(G, n, a, lo_w, hi_w, lane, [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); }, emit);
-  if (closed) emit(a + kTopStep - 1, right);
+  edt_dc::stretch_into<kPay, kTopStep - 1, 0>(G, n, a, lo_w, hi_w, lane, [](int v) { return __reduce_max_sync(0xFFFFFFFFu, v); }, sink);
+  if (closed) sink.template put<kTopStep - 1>(a + kTopStep - 1, right);
 }
 
 static size_t dc_top_bytes(int n, int top_shift) { return static_cast<size_t>((n >> top_shift) + 1) * 32 * sizeof(uint32_t); }
 static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n, kTopShiftY); }
-static size_t dc_smem_bytes_x(int n, int total) {  // G, K, Kt and the per-axis fraction table of the sign tables
-  return static_cast<size_t>(n) * 32 * 2 * sizeof(uint32_t) + dc_top_bytes(n, kTopShiftX) + static_cast<size_t>(total) * sizeof(float);
+static size_t dc_smem_bytes_x(int n, int total) {  // G (u32), H (u16), Kt and the per-axis fraction table of the sign tables
+  return static_cast<size_t>(n) * 32 * (sizeof(uint32_t) + sizeof(uint16_t)) + dc_top_bytes(n, kTopShiftX) + static_cast<size_t>(total) * sizeof(float);
 }
 
 // root of a perfect square below 2^24 (one MUFU; its error of a few ulp cannot reach the next integer)
@@ -1098,11 +1129,16 @@ __device__ __forceinline__ int exact_root(int sq) {
   return __float2int_rn(r);
 }
 
-// grid = (ceil(nx/8), ceil(nz/4)); lane <-> (x, z), positions = y.  Output = the winning key itself
-// (in-plane d2 << 11 | site_y << 1 | seed above z), which is what phase 3 consumes.
+// grid = (ceil(nx/8), ceil(nz/4)); lane <-> (x, z), positions = y.  kPay = 2: key payload = {seed above z, site has a
+// sign table}; kPay = 1 (grids whose y keys have no room for the second bit): {seed above z}, every site counts as
+// having a table.  Output = phase 3's candidates ALREADY in the layout of the x sweep's shared-memory tile (gimg /
+// himg): a lane's 8 consecutive y of one x-sweep tile are 8 consecutive words, so a stretch of 16 positions leaves as
+// four 16-byte stores of candidates + two of payload, and the x sweep fills its tile with two bulk copies.
 constexpr int kLoadBatch = 8;
-__global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y) {
+template <int kPay>
+__global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y, uint32_t none_x) {
   pdl_enter();
+  using KY = edt_dc::Keys<kPay>;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int x = blockIdx.x * kTileA + (lane & (kTileA - 1)), z = blockIdx.y * kTileZ + lane / kTileA;
@@ -1110,180 +1146,255 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
   uint32_t* Kt = G + ny * 32;
   const bool live = x < nx && z < E.nz;
-  const int zoff = nx * ny * min(z, E.nz - 1) + min(x, nx - 1);
   {  // candidates: the nearest seed along z of every column (esdf.hpp:213-233; ties keep the lower z, strict '<' :229)
     const int zc = min(z, E.nz - 1);
     const int col = (zc >> 5) * nx + min(x, nx - 1), stride = E.nzw * nx;
     const int zbase = zc & ~31, zb = zc & 31;
     const uint32_t le = 0xFFFFFFFFu >> (31 - zb), ge = 0xFFFFFFFFu << zb;
     for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
-      uint32_t wd[kLoadBatch], inf[kLoadBatch];
+      uint32_t wd[kLoadBatch], inf[kLoadBatch], tb[kLoadBatch];
 #pragma unroll
       for (int i = 0; i < kLoadBatch; ++i) {
         const int o = col + stride * min(yb + i, ny - 1);
         wd[i] = __ldg(E.zbits + o), inf[i] = __ldg(E.zinfo + o);
+        if constexpr (kPay == 2) tb[i] = __ldg(E.zgbits + o);
       }
 #pragma unroll
       for (int i = 0; i < kLoadBatch; ++i) {
         const int y = yb + i;
         const uint32_t lo_m = wd[i] & le, hi_m = wd[i] & ge;
-        const int below = lo_m ? zbase + 31 - __clz(static_cast<int>(lo_m)) : static_cast<int>(inf[i] & 0xFFFFu);
-        const int above = hi_m ? zbase + __ffs(static_cast<int>(hi_m)) - 1 : static_cast<int>(inf[i] >> 16);
-        const bool has_b = below != 0xFFFF, has_a = above != 0xFFFF;
+        const int bb = 31 - __clz(static_cast<int>(lo_m)), ba = __ffs(static_cast<int>(hi_m)) - 1;
+        const uint32_t ib = inf[i] & 0xFFFFu, ia = inf[i] >> 16;
+        const int below = lo_m ? zbase + bb : static_cast<int>(ib & kZNone);
+        const int above = hi_m ? zbase + ba : static_cast<int>(ia & kZNone);
+        const bool has_b = below != static_cast<int>(kZNone), has_a = above != static_cast<int>(kZNone);
         const int db = zc - below, da = above - zc;
         const bool up = has_a && (!has_b || da < db);
         const int dz = up ? da : db;
-        const uint32_t g = (!(has_a || has_b) || !live) ? KeysY::pack(none_y, y, 0)
-                                                         : KeysY::pack(static_cast<uint32_t>(dz * dz), y, up && dz > 0 ? 1u : 0u);
+        uint32_t pay = up && dz > 0 ? 1u : 0u;
+        if constexpr (kPay == 2) {
+          const uint32_t fb = lo_m ? (tb[i] >> bb) & 1u : ib >> 15, fa = hi_m ? (tb[i] >> ba) & 1u : ia >> 15;
+          pay = pay << 1 | (up ? fa : fb);
+        }
+        const uint32_t g = (!(has_a || has_b) || !live) ? KY::pack(none_y, y, 0) : KY::pack(static_cast<uint32_t>(dz * dz), y, pay);
         if (y < ny) G[edt_dc::at(y, lane)] = g;
       }
     }
   }
   for (int i = warp; i <= ny >> kTopShiftY; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   __syncthreads();
-  dc_top_levels<1, kTopShiftY>(G, Kt, ny, warp, lane, warps_log2);
-  uint32_t* out = E.yz + zoff;
-  asm volatile("" : "+l"(out));  // a pointer in registers: each store is then one wide multiply-add away
-  for (int j = warp; (j << kTopShiftY) < ny; j += nwarps)
-    dc_stretch<1, kTopShiftY>(G, Kt, ny, j, lane, [&](int y, uint32_t k) {
-      if (live) out[nx * y] = k;
-    });
+  dc_top_levels<kPay, kTopShiftY>(G, Kt, ny, warp, lane, warps_log2);
+  // tile images: tile (yt, zt = blockIdx.y), position x, row (y & 7) + 8 (z & 3) = yy + 8 zz
+  const size_t zt_base = static_cast<size_t>(blockIdx.y) * E.nyt;
+  const int zz = lane / kTileA;
+  for (int j = warp; (j << kTopShiftY) < ny; j += nwarps) {
+    edt_dc::KeySink<16> keys;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) keys.k[i] = 0xFFFFFFFFu;
+    dc_stretch_into<kPay, kTopShiftY>(G, Kt, ny, j, lane, keys);
+    if (x >= nx) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int yt = 2 * j + h;
+      if (yt >= E.nyt) break;
+      uint32_t gw[8], hw[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t k = keys.k[8 * h + i];
+        const uint32_t c = KY::cost(k);
+        const bool none = c >= none_y;
+        gw[i] = KeysX::pack(none ? none_x : c, x, 0);
+        const uint32_t low = k & KY::kLowMask;  // site_y and the payload
+        hw[i] = none ? 0u : (kPay == 2 ? low : (low << 1 | 1u));
+      }
+      const size_t at = ((zt_base + yt) * nx + x) * 32 + 8 * zz;
+      uint4* gp = reinterpret_cast<uint4*>(E.gimg + at);
+      gp[0] = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+      gp[1] = make_uint4(gw[4], gw[5], gw[6], gw[7]);
+      *reinterpret_cast<uint4*>(E.himg + at) = make_uint4(hw[0] | hw[1] << 16, hw[2] | hw[3] << 16, hw[4] | hw[5] << 16, hw[6] | hw[7] << 16);
+    }
+  }
 }
 
-// grid = (ceil(ny/8), ceil(nz/4)); lane <-> (y, z), positions = x.  kSigns as in k_sweep_x, 3 = from the per-site
-// tables of the resampled seeding.  A warp colours each stretch right after resolving it, walking x upwards so
-// that what depends only on the site is reused while the winner stays the same.
-//
-// Tile fill.  The input rows (phase 2's keys) are x-fastest, the tile wants [x][row].  kChunks (nx % 4 == 0):
-// every thread sends 16-byte chunks of the rows straight to shared memory with cp.async -- the whole 51 KB tile
-// is in flight at once, no register staging -- to a chunk-rotated place: chunk c of row r at 16-byte slot
-// c*32 + ((r + c) & 31).  A lane then reads ITS row's chunk c with one conflict-free LDS.128, packs four
-// candidates into G and writes the four slots back in place.  Otherwise: 4-byte loads through registers into a
-// word-rotated layout.  Either way the slot of (row, x) later holds {winner of x : 16 | candidate's site_y, side : 16}.
-__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src));
+// ---- bulk asynchronous copies (cp.async.bulk, completion on an mbarrier): one thread moves a whole tile ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int arrivals) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(arrivals));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "KS_MBAR_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra KS_MBAR_DONE;\n\t"
+      "bra KS_MBAR_WAIT;\n\t"
+      "KS_MBAR_DONE:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
 }
 
+__device__ __forceinline__ uint32_t pick8(const uint32_t (&k)[8], int i) {  // k[i] for a run-time i without a local array
+  uint32_t v = k[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) v = i == j ? k[j] : v;
+  return v;
+}
+
+// site_y, site_z of the winner `u` of row (y, z) from a tile image word pair (gimg / himg or their shared-memory copies)
+__device__ __forceinline__ void decode_site(uint32_t gword, uint32_t hword, int y, int z, int& sy, int& sz) {
+  const int r2 = static_cast<int>(KeysX::cost(gword));
+  sy = static_cast<int>(hword >> 2);
+  const int dy = y - sy;
+  const int dz = exact_root(r2 - dy * dy);
+  sz = (hword & 2u) ? z + dz : z - dz;
+}
+
+// grid = (ceil(ny/8), ceil(nz/4)); lane <-> (y, z), positions = x.  kSigns: 0 = unsigned field (propagate), 1 / 2 =
+// recover_signs per cell from the directory (without / with the hint planes), 3 = from the per-site tables of the
+// resampled seeding.  The tile (candidates G, payload H) arrives by two bulk copies issued by one thread.  A warp
+// resolves a stretch of 8 positions with its 8 winning keys in registers; a key IS the field word (d2 << 10 | site_x).
+// Mode 3: a cell whose site has no sign table takes its own-sign bit and needs nothing else -- no site decode, no
+// table fetch; only cells whose site lies next to stamped geometry go through the probe.  One lane stores its 8
+// cells with two 16-byte stores (x-fastest field).
 // kBig: rows so long that only one tile fits an SM -- then the tile gets 32 warps instead of 16
-template <int kSigns, bool kChunks, bool kBig>
-__global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_y, uint32_t none_x) {
+template <int kSigns, bool kBig>
+__global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_x) {
   pdl_wait();
-  extern __shared__ __align__(16) unsigned char s_raw[];
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  __shared__ __align__(8) uint64_t s_bar;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
   const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
   const int nx = E.nx, ny = E.ny;
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
-  uint32_t* K = G + nx * 32;
-  uint32_t* Kt = K + nx * 32;
-  if constexpr (kChunks) {
-    const int chunks = nx >> 2;
-    for (int i = threadIdx.x; i < 32 * chunks; i += blockDim.x) {
-      const int r = i / chunks, c = i - r * chunks;  // consecutive threads: consecutive chunks of one row
-      const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
-      uint32_t* dst = K + 4 * (c * 32 + ((r + c) & 31));
-      if (yr < ny && zr < E.nz) cp_async_16(dst, E.yz + nx * (yr + ny * zr) + 4 * c);
-      else *reinterpret_cast<uint4*>(dst) = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);  // padding row: no candidate
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  } else {
-    for (int r = warp; r < 32; r += nwarps) {
-      const int yr = y0 + (r & (kTileA - 1)), zr = z0 + r / kTileA;
-      const uint32_t* row = E.yz + nx * (min(yr, ny - 1) + ny * min(zr, E.nz - 1));
-      const uint32_t dead = yr < ny && zr < E.nz ? 0u : 0xFFFFFFFFu;
-      for (int xb = lane; xb < nx; xb += 32 * kLoadBatch) {
-        uint32_t v[kLoadBatch];
-#pragma unroll
-        for (int i = 0; i < kLoadBatch; ++i) v[i] = __ldg(row + min(xb + 32 * i, nx - 1));
-#pragma unroll
-        for (int i = 0; i < kLoadBatch; ++i) {
-          const int x = xb + 32 * i;
-          if (x < nx) K[x * 32 + ((r + x) & 31)] = v[i] | dead;
-        }
-      }
-    }
-  }
+  uint16_t* H = reinterpret_cast<uint16_t*>(G + nx * 32);
+  uint32_t* Kt = reinterpret_cast<uint32_t*>(H + nx * 32);
   constexpr int kTopShift = kTopShiftX, kTopStep = 1 << kTopShift;
-  for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   float* s_qsf = reinterpret_cast<float*>(Kt + ((nx >> kTopShift) + 1) * 32);
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const size_t tile = static_cast<size_t>(blockIdx.y) * E.nyt + blockIdx.x;
+    const uint32_t gbytes = static_cast<uint32_t>(nx) * 32u * 4u, hbytes = static_cast<uint32_t>(nx) * 32u * 2u;
+    mbar_expect_tx(&s_bar, gbytes + hbytes);
+    bulk_g2s(G, E.gimg + tile * nx * 32, gbytes, &s_bar);
+    bulk_g2s(H, E.himg + tile * nx * 32, hbytes, &s_bar);
+  }
+  for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   if constexpr (kSigns == 3)
     for (int i = threadIdx.x; i < nx + ny + E.nz; i += blockDim.x) s_qsf[i] = E.qsf[i];
-  if constexpr (kChunks) asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  const int y = y0 + (lane & (kTileA - 1)), z = min(z0 + lane / kTileA, E.nz - 1);
-  const bool live = y < ny && z0 + lane / kTileA < E.nz;
-  // the slot of (this lane's row, position x)
-  auto slot = [&](int x) {
-    if constexpr (kChunks) return 4 * ((x >> 2) * 32 + ((lane + (x >> 2)) & 31)) + (x & 3);
-    else return x * 32 + ((lane + x) & 31);
-  };
-  uint16_t* K16 = reinterpret_cast<uint16_t*>(K);
-  auto convert = [&](int x, uint32_t v) {  // candidate at x: in-plane d2 into G, what phase 3 still needs of it stays in the slot
-    const uint32_t r2 = KeysY::cost(v);
-    G[edt_dc::at(x, lane)] = KeysX::pack(r2 >= none_y ? none_x : r2, x, 0);
-    return v & KeysY::kLowMask;
-  };
-  if constexpr (kChunks) {
-    for (int c = warp; c < (nx >> 2); c += nwarps) {
-      uint4* q = reinterpret_cast<uint4*>(K + 4 * (c * 32 + ((lane + c) & 31)));
-      uint4 v = *q;
-      v.x = convert(4 * c, v.x), v.y = convert(4 * c + 1, v.y), v.z = convert(4 * c + 2, v.z), v.w = convert(4 * c + 3, v.w);
-      *q = v;
-    }
-  } else {
-    for (int x = warp; x < nx; x += nwarps) K[slot(x)] = convert(x, K[slot(x)]);
-  }
+  const int back = 1 - E.ctrl->front;
+  mbar_wait(&s_bar, 0);
   __syncthreads();
   dc_top_levels<0, kTopShift>(G, Kt, nx, warp, lane, warps_log2);
-  if (kSigns != 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) E.ctrl->signs_recovered = 1;
-  const int obase = y + ny * nx * z;
+  const int y = min(y0 + (lane & (kTileA - 1)), ny - 1), z = min(z0 + lane / kTileA, E.nz - 1);
+  const bool live = y0 + (lane & (kTileA - 1)) < ny && z0 + lane / kTileA < E.nz;
   auto make_probe = [&]() {
-    if constexpr (kSigns == 3) return SignTable(E, Tw, s_qsf, min(y, ny - 1), z);
-    else return SignProbe(E, Tw, kSigns ? min(y, ny - 1) : 0, kSigns ? z : 0);
+    if constexpr (kSigns == 3) return SignTable(E, Tw, s_qsf, y, z);
+    else return SignProbe(E, Tw, kSigns ? y : 0, kSigns ? z : 0);
   };
   auto probe = make_probe();
-  const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (min(y, ny - 1) + 1)) * E.wpr2;
+  const uint32_t* orow = E.obits + ((z + 1) * (ny + 2) + (y + 1)) * E.wpr2;
+  uint32_t* out_row = (back ? E.f32[1] : E.f32[0]) + (static_cast<size_t>(z) * ny + y) * nx;
+  const bool vec_ok = (nx & 3) == 0;
   for (int j = warp; (j << kTopShift) < nx; j += nwarps) {
-    const int x0 = j << kTopShift, end = min(x0 + kTopStep, nx);
+    const int x0 = j << kTopShift;
     uint32_t own_lo = 0, own_hi = 0;  // requested before the stretch is resolved, so that the loads ride under it
     if constexpr (kSigns == 3) own_lo = __ldg(orow + (x0 >> 5)), own_hi = (x0 >> 5) + 1 < E.wpr2 ? __ldg(orow + (x0 >> 5) + 1) : 0u;
-    dc_stretch<0, kTopShift>(G, Kt, nx, j, lane, [&](int x, uint32_t k) { K16[2 * slot(x) + 1] = static_cast<uint16_t>(KeysX::winner(k)); });
+    edt_dc::KeySink<8> keys;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) keys.k[i] = 0xFFFFFFFFu;
+    dc_stretch_into<0, kTopShift>(G, Kt, nx, j, lane, keys);
     if (!live) continue;
-    // colour the stretch walking x upwards, so that what depends only on the site is reused while the winner stays
-    uint32_t own = 0;  // own-sign bits of cells x0 .. x0+31 (extended bits x0+1 .. x0+32)
-    if constexpr (kSigns == 3) own = __funnelshift_rc(own_lo, own_hi, (x0 & 31) + 1);
-    uint2* fp = E.field + obase + ny * x0;
-    int last = -1, r2 = 0;
-    uint32_t site = kSiteNone;
-    for (int x = x0; x < end; ++x, fp += ny) {
-      const int u = K16[2 * slot(x) + 1];
-      if (u != last) {
-        last = u;
-        r2 = static_cast<int>(KeysX::cost(G[edt_dc::at(u, lane)]));
-        if (r2 < static_cast<int>(none_x)) {
-          const uint32_t h = K16[2 * slot(u)];
-          const int sy = static_cast<int>(h >> 1);
-          const int dy = y - sy;
-          const int dz = exact_root(r2 - dy * dy);
-          const int sz = (h & 1u) ? z + dz : z - dz;
-          site = static_cast<uint32_t>(u) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+    uint32_t w[8];
+    uint32_t slow = 0;  // positions that need the site: bit i
+    if constexpr (kSigns == 3) {
+      const uint32_t own = __funnelshift_rc(own_lo, own_hi, (x0 & 31) + 1);  // own-sign bits of cells x0 .. (extended bits x0+1 ..)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t k = keys.k[i];
+        const bool none = KeysX::cost(k) >= none_x;  // the grid holds no seed at all
+        const uint32_t h = H[edt_dc::at(none ? 0 : KeysX::winner(k), lane)];  // (a position beyond the row carries key ~0)
+        w[i] = none ? 0xFFFFFFFFu : (k | ((own >> i) & 1u) << 31);
+        slow |= (none ? 0u : (h & 1u)) << i;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool none = KeysX::cost(keys.k[i]) >= none_x;
+        w[i] = none ? 0xFFFFFFFFu : keys.k[i];
+        if (kSigns != 0 && !none) slow |= 1u << i;
+      }
+    }
+    if (slow != 0) {  // cells whose site may resolve a geometry probe: the reference's decision from the site's table / the directory
+      uint32_t flip = 0;
+      int last = -1;
+      for (uint32_t m = slow; m != 0; m &= m - 1) {
+        const int i = __ffs(static_cast<int>(m)) - 1;
+        const int x = x0 + i;
+        const uint32_t k = pick8(keys.k, i);
+        const int u = KeysX::winner(k);
+        if (u != last) {
+          last = u;
+          int sy, sz;
+          decode_site(G[edt_dc::at(u, lane)], H[edt_dc::at(u, lane)], y, z, sy, sz);
           if constexpr (kSigns == 3) probe.set_site(u, sy, sz, __ldg(E.gtab + (u + nx * (sy + ny * sz))));
           else if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
         }
+        bool neg = false;
+        if constexpr (kSigns == 3) {
+          const bool own = (pick8(w, i) >> 31) != 0;
+          neg = probe.negative(x, own) != own;  // flip when the probe disagrees with the own-sign default
+        } else if constexpr (kSigns != 0) {
+          neg = probe.template negative<kSigns == 2>(x);
+        }
+        flip |= (neg ? 1u : 0u) << i;
       }
-      if (r2 >= static_cast<int>(none_x)) {  // the row holds no candidate at all
-        *fp = make_uint2(kSiteNone, kD2None);
-        continue;
-      }
-      uint32_t d2 = static_cast<uint32_t>((x - u) * (x - u) + r2);
-      if constexpr (kSigns == 3) {
-        if (probe.negative(x, ((own >> (x - x0)) & 1u) != 0)) d2 |= 0x80000000u;
-      } else if constexpr (kSigns != 0) {
-        if (probe.template negative<kSigns == 2>(x)) d2 |= 0x80000000u;
-      }
-      *fp = make_uint2(site, d2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] ^= ((flip >> i) & 1u) << 31;
+    }
+    uint32_t* out = out_row + x0;
+    if (vec_ok && x0 + 8 <= nx) {
+      reinterpret_cast<uint4*>(out)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      reinterpret_cast<uint4*>(out)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (x0 + i < nx) out[i] = w[i];
     }
   }
+  // publish: the last CTA to finish makes this buffer the one readers use
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&E.ctrl->x_done, 1u) == gridDim.x * gridDim.y - 1) {
+      E.ctrl->x_done = 0;
+      E.ctrl->pub_seeds = E.ctrl->seed_count;
+      if (kSigns != 0) E.ctrl->signs_recovered = 1;
+      __threadfence();
+      E.ctrl->front = back;
+    }
+  }
+}
+
+// ---- readers of the finished field ----
+__device__ __forceinline__ const uint32_t* front_field(const EsdfView& E) {  // fast path: the published buffer
+  return E.ctrl->front ? E.f32[1] : E.f32[0];
+}
+// fast path: site of cell (x, y, z) whose field word is w -- site_x from the word, site_y / site_z from phase 2's
+// winner at (site_x, y, z) in the tile images
+__device__ __forceinline__ void fast_site(const EsdfView& E, uint32_t w, int y, int z, int& sx, int& sy, int& sz) {
+  sx = static_cast<int>(w & 1023u);
+  const size_t at = ((static_cast<size_t>(z >> 2) * E.nyt + (y >> 3)) * E.nx + sx) * 32 + (y & 7) + 8 * (z & 3);
+  decode_site(E.gimg[at], E.himg[at], y, z, sy, sz);
 }
 
 // ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
@@ -1291,6 +1402,17 @@ __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   pdl_wait();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= E.cells) return;
+  if (E.fast) {  // o is x-fastest
+    if (E.ctrl->pub_seeds == 0) return;
+    uint32_t* f = const_cast<uint32_t*>(front_field(E));
+    const int x = o % E.nx, y = (o / E.nx) % E.ny, z = o / (E.nx * E.ny);
+    int sx, sy, sz;
+    fast_site(E, f[o], y, z, sx, sy, sz);
+    SignProbe probe(E, T, y, z);
+    probe.template set_site<false>(sx, sy, sz);
+    if (probe.template negative<false>(x)) f[o] ^= 0x80000000u;
+    return;
+  }
   const uint32_t site = E.field[o].x;
   if (site == kSiteNone) return;
   const int y = o % E.ny;
@@ -1301,11 +1423,25 @@ __global__ void __launch_bounds__(256) k_recover_signs(EsdfView E, TsdfView T) {
   if (probe.template negative<false>(x)) E.field[o].y ^= 0x80000000u;
 }
 
+// the wide path's sweeps do not publish by themselves
+__global__ void k_publish(EsdfView E) {
+  pdl_wait();
+  if (threadIdx.x == 0 && blockIdx.x == 0) E.ctrl->pub_seeds = E.ctrl->seed_count;
+}
+
 // ---- query (esdf.hpp:337-387) ----
-__device__ __forceinline__ double cell_distance(const EsdfView& E, int x, int y, int z) {
-  const uint32_t v = E.field[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)].y;
-  const double d = sqrt(static_cast<double>(v & 0x7FFFFFFFu)) * E.ve;  // esdf.hpp:276-277
-  return (v & 0x80000000u) ? -d : d;
+// f: the published fast-path buffer, or nullptr on the wide path
+__device__ __forceinline__ double cell_distance(const EsdfView& E, const uint32_t* f, int x, int y, int z) {
+  uint32_t d2, neg;
+  if (f != nullptr) {
+    const uint32_t w = f[x + static_cast<long long>(E.nx) * (y + static_cast<long long>(E.ny) * z)];
+    d2 = (w >> 10) & 0x1FFFFFu, neg = w >> 31;
+  } else {
+    const uint32_t v = E.field[y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z)].y;
+    d2 = v & 0x7FFFFFFFu, neg = v >> 31;
+  }
+  const double d = sqrt(static_cast<double>(d2)) * E.ve;  // esdf.hpp:276-277
+  return neg ? -d : d;
 }
 // One point: distance, gradient (may be null), inside flag.
 __device__ __forceinline__ void query_point(const EsdfView& E, const double p[3], double& dist, double grad[3], bool& in) {
@@ -1315,7 +1451,8 @@ __device__ __forceinline__ void query_point(const EsdfView& E, const double p[3]
   for (int a = 0; a < 3; ++a) in = in && p[a] >= E.origin[a] && p[a] <= E.origin[a] + dims[a] * E.ve;
   dist = CUDART_INF;
   grad[0] = grad[1] = grad[2] = 0.0;
-  if (E.ctrl->seed_count == 0) return;  // no sites: +inf, zero gradient (esdf.hpp:345)
+  if (E.ctrl->pub_seeds == 0) return;  // no sites: +inf, zero gradient (esdf.hpp:345)
+  const uint32_t* fld = E.fast ? front_field(E) : nullptr;
   int i0[3], i1[3];
   double f[3];
 #pragma unroll
@@ -1333,10 +1470,10 @@ __device__ __forceinline__ void query_point(const EsdfView& E, const double p[3]
     i1[a] = i0[a] + 1;
     f[a] = c - i0[a];
   }
-  const double c000 = cell_distance(E, i0[0], i0[1], i0[2]), c100 = cell_distance(E, i1[0], i0[1], i0[2]);
-  const double c010 = cell_distance(E, i0[0], i1[1], i0[2]), c110 = cell_distance(E, i1[0], i1[1], i0[2]);
-  const double c001 = cell_distance(E, i0[0], i0[1], i1[2]), c101 = cell_distance(E, i1[0], i0[1], i1[2]);
-  const double c011 = cell_distance(E, i0[0], i1[1], i1[2]), c111 = cell_distance(E, i1[0], i1[1], i1[2]);
+  const double c000 = cell_distance(E, fld, i0[0], i0[1], i0[2]), c100 = cell_distance(E, fld, i1[0], i0[1], i0[2]);
+  const double c010 = cell_distance(E, fld, i0[0], i1[1], i0[2]), c110 = cell_distance(E, fld, i1[0], i1[1], i0[2]);
+  const double c001 = cell_distance(E, fld, i0[0], i0[1], i1[2]), c101 = cell_distance(E, fld, i1[0], i0[1], i1[2]);
+  const double c011 = cell_distance(E, fld, i0[0], i1[1], i1[2]), c111 = cell_distance(E, fld, i1[0], i1[1], i1[2]);
   const double fx = f[0], fy = f[1], fz = f[2];
   const double c00 = c000 * (1 - fx) + c100 * fx, c10 = c010 * (1 - fx) + c110 * fx;
   const double c01 = c001 * (1 - fx) + c101 * fx, c11 = c011 * (1 - fx) + c111 * fx;
@@ -1410,7 +1547,7 @@ __global__ void __launch_bounds__(128) k_probe_summary(EsdfView E, const double*
       const double m = scratch->part_min[b];
       best = m < best ? m : best, count += scratch->part_cnt[b];
     }
-    out[0] = tag, out[1] = best, out[2] = static_cast<double>(count), out[3] = static_cast<double>(E.ctrl->seed_count);
+    out[0] = tag, out[1] = best, out[2] = static_cast<double>(count), out[3] = static_cast<double>(E.ctrl->pub_seeds);
     scratch->arrivals = 0;  // ready for the next launch
   }
 }
@@ -1554,9 +1691,22 @@ __global__ void __launch_bounds__(256) k_export(EsdfView E, int* __restrict__ si
   const int x = static_cast<int>(idx % E.nx);
   const int y = static_cast<int>((idx / E.nx) % E.ny);
   const int z = static_cast<int>(idx / (static_cast<long long>(E.nx) * E.ny));
-  const long long o = y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z);
-  const uint2 cell = E.field[o];
-  const uint32_t s = cell.x, v = cell.y;
+  uint32_t s, v;
+  if (E.fast) {
+    if (E.ctrl->pub_seeds == 0) {
+      s = kSiteNone, v = kD2None;
+    } else {
+      const uint32_t w = front_field(E)[idx];
+      int sx, sy, sz;
+      fast_site(E, w, y, z, sx, sy, sz);
+      s = static_cast<uint32_t>(sx) | static_cast<uint32_t>(sy) << 10 | static_cast<uint32_t>(sz) << 20;
+      v = ((w >> 10) & 0x1FFFFFu) | (w & 0x80000000u);
+    }
+  } else {
+    const long long o = y + static_cast<long long>(E.ny) * (x + static_cast<long long>(E.nx) * z);
+    const uint2 cell = E.field[o];
+    s = cell.x, v = cell.y;
+  }
   if (site_xyz) {
     site_xyz[3 * idx] = s == kSiteNone ? -1 : static_cast<int>(s & 1023);
     site_xyz[3 * idx + 1] = s == kSiteNone ? -1 : static_cast<int>((s >> 10) & 1023);
@@ -1607,6 +1757,7 @@ struct ks_esdf {
   bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
   int dc_wl_y, dc_wl_x;    // log2(warps per tile)
+  int pay_y;               // payload bits of the y keys: 2 = {seed above z, site has a sign table}, 1 = the first only
   uint32_t none_y, none_x; // offsets of positions without candidate
   int sticky_err;
   bool profile, profile_stages;
@@ -1785,12 +1936,15 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   (void)plane;
   if (e->dc) {
     if (!bits) KS_LAUNCH(k_pack_mask, (E.wpr * E.ny * E.nz + 7) / 8, 256, 0, e->stream, E);  // the reference's byte mask -> bit plane
-    KS_LAUNCH(k_flood_cols, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
+    KS_LAUNCH(k_flood_cols, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 2 * 32 * sizeof(uint32_t), e->stream, E);
   } else if (bits) KS_LAUNCH(k_flood_z_chunks, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
-  if (e->dc) KS_LAUNCH(k_sweep_y_dc, dim3((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ), 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y);
-  else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
+  if (e->dc) {
+    const dim3 ygrid((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
+    if (e->pay_y == 2) KS_LAUNCH(k_sweep_y_dc<2>, ygrid, 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y, e->none_x);
+    else KS_LAUNCH(k_sweep_y_dc<1>, ygrid, 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y, e->none_x);
+  } else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   if (e->side_pending) {  // the site tables must be complete before the sweep that reads them
     KS_CUDA(cudaStreamWaitEvent(e->stream, e->join, 0));
@@ -1798,22 +1952,17 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   }
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (e->dc) {
-    const dim3 xgrid((E.ny + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
+    const dim3 xgrid(E.nyt, E.nzt);
     const unsigned threads = 32u << e->dc_wl_x;
     const int mode = t && bits && fast_build(e) ? 3 : (t && bits ? 2 : (t ? 1 : 0));
     const TsdfView tv = t ? tsdf_view(t) : TsdfView{};
-#define KS_X_DC(M, C, B) KS_LAUNCH((k_sweep_x_dc<M, C, B>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_y, e->none_x)
-#define KS_X_DC_MODE(C, B)        \
-  if (mode == 3) KS_X_DC(3, C, B);      \
-  else if (mode == 2) KS_X_DC(2, C, B); \
-  else if (mode == 1) KS_X_DC(1, C, B); \
-  else KS_X_DC(0, C, B)
-    const bool big = e->dc_wl_x == 5;
-    if (E.nx % 4 == 0) {  // rows start 16-byte aligned: tile filled by cp.async
-      if (big) { KS_X_DC_MODE(true, true); } else { KS_X_DC_MODE(true, false); }
-    } else {
-      if (big) { KS_X_DC_MODE(false, true); } else { KS_X_DC_MODE(false, false); }
-    }
+#define KS_X_DC(M, B) KS_LAUNCH((k_sweep_x_dc<M, B>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_x)
+#define KS_X_DC_MODE(B)        \
+  if (mode == 3) KS_X_DC(3, B);      \
+  else if (mode == 2) KS_X_DC(2, B); \
+  else if (mode == 1) KS_X_DC(1, B); \
+  else KS_X_DC(0, B)
+    if (e->dc_wl_x == 5) { KS_X_DC_MODE(true); } else { KS_X_DC_MODE(false); }
 #undef KS_X_DC_MODE
 #undef KS_X_DC
   } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
@@ -1823,6 +1972,7 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   } else {
     KS_LAUNCH(k_sweep_x<0>, xgrid, 32 * e->bands_x, e->smem_x, e->stream, E, TsdfView{}, e->band_x, e->bands_x);
   }
+  if (!e->dc) KS_LAUNCH(k_publish, 1, 32, 0, e->stream, E);
   if (t && !e->dc) KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 1, 1, e->stream));  // k_sweep_x_dc<signs> sets the flag itself
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -1880,7 +2030,11 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
   {  // divide-and-conquer sweeps whenever their 32-bit keys hold every reachable cost (all dims <= ~830, or a long x axis)
     const uint32_t gmax_y = static_cast<uint32_t>((E.nz - 1) * (E.nz - 1));
     const uint32_t gmax_x = gmax_y + static_cast<uint32_t>((E.ny - 1) * (E.ny - 1));
-    e->dc = KeysY::fits(E.ny, gmax_y) && KeysX::fits(E.nx, gmax_x) && dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) <= 227 * 1024 && dc_smem_bytes_y(E.ny) <= 227 * 1024;
+    const uint64_t d2_max = static_cast<uint64_t>(gmax_x) + static_cast<uint64_t>(E.nx - 1) * (E.nx - 1);  // field word: d2 in 21 bits
+    e->dc = KeysY::fits(E.ny, gmax_y) && KeysX::fits(E.nx, gmax_x) && d2_max < (1ull << 21) &&
+            dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) <= 226 * 1024 && dc_smem_bytes_y(E.ny) <= 226 * 1024;
+    e->pay_y = edt_dc::Keys<2>::fits(E.ny, gmax_y) ? 2 : 1;
+    if (const char* v = std::getenv("KS_PAY_Y")) e->pay_y = std::atoi(v) == 1 ? 1 : e->pay_y;
     if (const char* v = std::getenv("KS_SWEEP")) e->dc = e->dc && std::strcmp(v, "stack") != 0;
     e->none_y = KeysY::none_offset(E.ny, gmax_y);
     e->none_x = KeysX::none_offset(E.nx, gmax_x);
@@ -1897,15 +2051,17 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
   }
   // The attribute is per kernel and process-wide: it is set to the opt-in maximum (never to one handle's own size, which
   // would lower it under a larger ESDF that is still alive).
-  constexpr int kSmemOptIn = 227 * 1024;
+  constexpr int kSmemOptIn = 227 * 1024 - 256;  // minus the kernels' few bytes of static shared memory
   KS_CUDA(cudaFuncSetAttribute(k_sweep_y, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
-#define KS_X_ATTR(M, C, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, C, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
-#define KS_X_ATTR4(C, B) KS_X_ATTR(0, C, B); KS_X_ATTR(1, C, B); KS_X_ATTR(2, C, B); KS_X_ATTR(3, C, B)
-  KS_X_ATTR4(true, false); KS_X_ATTR4(false, false); KS_X_ATTR4(true, true); KS_X_ATTR4(false, true);
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute(k_flood_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+#define KS_X_ATTR(M, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
+#define KS_X_ATTR4(B) KS_X_ATTR(0, B); KS_X_ATTR(1, B); KS_X_ATTR(2, B); KS_X_ATTR(3, B)
+  KS_X_ATTR4(false); KS_X_ATTR4(true);
 #undef KS_X_ATTR4
 #undef KS_X_ATTR
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
@@ -1939,20 +2095,33 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
   }
   KS_CUDA(cudaMalloc(&E.mask, E.cells));
   E.nzw = (E.nz + 31) / 32;
-  {
+  E.fast = e->dc ? 1 : 0;
+  E.nyt = (E.ny + kTileA - 1) / kTileA, E.nzt = (E.nz + kTileZ - 1) / kTileZ;
+  const size_t cells = static_cast<size_t>(E.cells);
+  if (e->dc) {  // phase 1 as per-column bit strings, phase 2 as tile images, the field as two 4-byte buffers
     const size_t col_words = static_cast<size_t>(E.nzw) * E.ny * E.nx;
-    KS_CUDA(cudaMalloc(&E.near_z, std::max(static_cast<size_t>(E.cells) * sizeof(uint16_t), 2 * col_words * sizeof(uint32_t))));
-    E.zbits = reinterpret_cast<uint32_t*>(E.near_z), E.zinfo = E.zbits + col_words;
+    KS_CUDA(cudaMalloc(&E.near_z, 3 * col_words * sizeof(uint32_t)));
+    E.zbits = reinterpret_cast<uint32_t*>(E.near_z), E.zinfo = E.zbits + col_words, E.zgbits = E.zinfo + col_words;
+    const size_t image = static_cast<size_t>(E.nzt) * E.nyt * E.nx * 32;
+    KS_CUDA(cudaMalloc(&E.gimg, image * sizeof(uint32_t)));
+    KS_CUDA(cudaMalloc(&E.himg, image * sizeof(uint16_t)));
+    bool single = false;  // KS_ESDF_SINGLE_BUFFER=1: one field buffer (readers on other streams may then see a build in progress)
+    if (const char* v = std::getenv("KS_ESDF_SINGLE_BUFFER")) single = std::atoi(v) != 0;
+    KS_CUDA(cudaMalloc(&E.f32[0], cells * sizeof(uint32_t)));
+    if (single) E.f32[1] = E.f32[0];
+    else KS_CUDA(cudaMalloc(&E.f32[1], cells * sizeof(uint32_t)));
+  } else {
+    KS_CUDA(cudaMalloc(&E.near_z, cells * sizeof(uint16_t)));
+    KS_CUDA(cudaMalloc(&E.yz, cells * sizeof(uint32_t)));
+    KS_CUDA(cudaMalloc(&E.field, cells * sizeof(uint2)));
   }
-  KS_CUDA(cudaMalloc(&E.yz, E.cells * sizeof(uint32_t)));
-  KS_CUDA(cudaMalloc(&E.field, static_cast<size_t>(E.cells) * sizeof(uint2)));
   KS_CUDA(cudaMalloc(&E.ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMalloc(&e->summary_scratch, sizeof(SummaryScratch)));
   KS_CUDA(cudaMemsetAsync(e->summary_scratch, 0, sizeof(SummaryScratch), e->stream));
   KS_CUDA(cudaMallocHost(&e->h_ctrl, sizeof(EsdfCtrl)));
   KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
   KS_CUDA(cudaMemsetAsync(E.mbits, 0, 2 * static_cast<size_t>(E.wpr) * E.ny * E.nz * sizeof(uint32_t), e->stream));
-  KS_CUDA(cudaMemsetAsync(E.field, 0xFF, static_cast<size_t>(E.cells) * sizeof(uint2), e->stream));  // no sites yet
+  if (E.field) KS_CUDA(cudaMemsetAsync(E.field, 0xFF, cells * sizeof(uint2), e->stream));  // no sites yet (fast path: pub_seeds == 0)
   KS_CUDA(cudaStreamSynchronize(e->stream));
   return KS_OK;
 }
@@ -1961,7 +2130,9 @@ void ks_esdf_destroy(ks_esdf* e) {
   if (!e) return;
   if (e->stream) cudaStreamSynchronize(e->stream);
   EsdfView& E = e->view;
-  cudaFree(e->query_scratch), cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field);
+  cudaFree(e->query_scratch), cudaFree(e->summary_scratch), cudaFree(E.cbits), cudaFree(E.voxe), cudaFree(E.xplus), cudaFree(E.yzflags), cudaFree(E.gtab), cudaFree(E.seedw), cudaFree(E.vox), cudaFree(E.ctr), cudaFree(E.qsf), cudaFree(E.brick), cudaFree(E.active), cudaFree(E.mbits), cudaFree(E.mask), cudaFree(E.near_z), cudaFree(E.yz), cudaFree(E.field), cudaFree(E.gimg), cudaFree(E.himg);
+  if (E.f32[1] != E.f32[0]) cudaFree(E.f32[1]);
+  cudaFree(E.f32[0]);
   cudaFree(E.ctrl);
   if (E.dir) cudaFree(E.dir);
   if (E.pool_surf) cudaFree(E.pool_surf);
@@ -2120,7 +2291,7 @@ int ks_esdf_propagate(ks_esdf* e, const uint8_t* mask_host, int64_t mask_len) {
   if (mask_host) {
     if (mask_len != E.cells) return fail(KS_ERR_INVALID, "esdf: seed mask size does not match grid");  // esdf.hpp:195-196
     KS_CUDA(cudaMemcpyAsync(E.mask, mask_host, E.cells, cudaMemcpyHostToDevice, e->stream));
-    KS_CUDA(cudaMemsetAsync(E.ctrl, 0, sizeof(EsdfCtrl), e->stream));
+    KS_CUDA(cudaMemsetAsync(E.ctrl, 0, offsetof(EsdfCtrl, front), e->stream));
     KS_LAUNCH(k_count_mask, 4 * kSmCount, 256, 0, e->stream, E);
   } else {
     KS_CUDA(cudaMemsetAsync(&E.ctrl->signs_recovered, 0, sizeof(int), e->stream));
