@@ -41,7 +41,7 @@ struct EsdfCtrl {
   int active_bricks;  // entries of EsdfView::active, rebuilt with the directory
   // what readers go by (never touched by the resets above): published by the last CTA of the last sweep
   int front;                     // fast path: index of the field buffer readers use
-  unsigned x_done;               // CTAs of the x sweep that have finished
+  unsigned x_done;               // CTAs of the x sweep in flight that have finished
   unsigned long long pub_seeds;  // seed count of the published field (0: no sites)
 };
 
@@ -1242,13 +1242,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t pick8(const uint32_t (&k)[8], int i) {  // k[i] for a run-time i without a local array
-  uint32_t v = k[0];
-#pragma unroll
-  for (int j = 1; j < 8; ++j) v = i == j ? k[j] : v;
-  return v;
-}
-
 // site_y, site_z of the winner `u` of row (y, z) from a tile image word pair (gimg / himg or their shared-memory copies)
 __device__ __forceinline__ void decode_site(uint32_t gword, uint32_t hword, int y, int z, int& sy, int& sz) {
   const int r2 = static_cast<int>(KeysX::cost(gword));
@@ -1316,8 +1309,9 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
     if (!live) continue;
     uint32_t w[8];
     uint32_t slow = 0;  // positions that need the site: bit i
+    uint32_t own = 0;   // own-sign bits of cells x0 .. x0 + 7 (extended bits x0 + 1 ..)
     if constexpr (kSigns == 3) {
-      const uint32_t own = __funnelshift_rc(own_lo, own_hi, (x0 & 31) + 1);  // own-sign bits of cells x0 .. (extended bits x0+1 ..)
+      own = __funnelshift_rc(own_lo, own_hi, (x0 & 31) + 1);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint32_t k = keys.k[i];
@@ -1335,13 +1329,17 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
       }
     }
     if (slow != 0) {  // cells whose site may resolve a geometry probe: the reference's decision from the site's table / the directory
+      // the eight winners, 10 bits each, in three registers (a run-time index into keys.k would put it in local memory)
+      const uint32_t p0 = (keys.k[0] & 1023u) | (keys.k[1] & 1023u) << 10 | (keys.k[2] & 1023u) << 20;
+      const uint32_t p1 = (keys.k[3] & 1023u) | (keys.k[4] & 1023u) << 10 | (keys.k[5] & 1023u) << 20;
+      const uint32_t p2 = (keys.k[6] & 1023u) | (keys.k[7] & 1023u) << 10;
       uint32_t flip = 0;
       int last = -1;
       for (uint32_t m = slow; m != 0; m &= m - 1) {
         const int i = __ffs(static_cast<int>(m)) - 1;
         const int x = x0 + i;
-        const uint32_t k = pick8(keys.k, i);
-        const int u = KeysX::winner(k);
+        const int q = (i * 11) >> 5;  // i / 3
+        const int u = static_cast<int>(((q == 0 ? p0 : (q == 1 ? p1 : p2)) >> (10 * (i - 3 * q))) & 1023u);
         if (u != last) {
           last = u;
           int sy, sz;
@@ -1351,8 +1349,8 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
         }
         bool neg = false;
         if constexpr (kSigns == 3) {
-          const bool own = (pick8(w, i) >> 31) != 0;
-          neg = probe.negative(x, own) != own;  // flip when the probe disagrees with the own-sign default
+          const bool mine = ((own >> i) & 1u) != 0;
+          neg = probe.negative(x, mine) != mine;  // flip when the probe disagrees with the own-sign default
         } else if constexpr (kSigns != 0) {
           neg = probe.template negative<kSigns == 2>(x);
         }
@@ -1952,10 +1950,10 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   }
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (e->dc) {
-    const dim3 xgrid(E.nyt, E.nzt);
     const unsigned threads = 32u << e->dc_wl_x;
     const int mode = t && bits && fast_build(e) ? 3 : (t && bits ? 2 : (t ? 1 : 0));
     const TsdfView tv = t ? tsdf_view(t) : TsdfView{};
+    const dim3 xgrid(E.nyt, E.nzt);
 #define KS_X_DC(M, B) KS_LAUNCH((k_sweep_x_dc<M, B>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_x)
 #define KS_X_DC_MODE(B)        \
   if (mode == 3) KS_X_DC(3, B);      \
