@@ -311,8 +311,10 @@ def run_ours(args):
                 if upload:
                     self.tsdf.upload_frame_async(slot)
                 self.tsdf.integrate_async(slot)
-            for p in self.prims + self.meshes:
-                self.tsdf.stamp_async(p)
+            if self.prims:  # every cuboid / sphere of the update as one batch (three launches), meshes one by one
+                self.tsdf.stamp_batch_async(self.prims)
+            for m in self.meshes:
+                self.tsdf.stamp_async(m)
             self.esdf.build_async(self.tsdf)
             if self.queries is not None:
                 api._check(self.esdf.lib.ks_esdf_query_device_async(
@@ -323,8 +325,8 @@ def run_ours(args):
             k = 0
             for f in self.frames:
                 k = api.integrate_depth(self.tsdf, f)          # H2D from the page-locked frame + 4 phases + D2H report
-            for p in self.prims:
-                api.stamp_primitive(self.tsdf, p)
+            if self.prims:
+                api.stamp_primitives(self.tsdf, self.prims)
             for m in self.meshes:
                 api.stamp_mesh(self.tsdf, m)
             api.build_esdf(self.tsdf, self.ecfg, self.esdf)

@@ -148,6 +148,18 @@ KS_API int ks_tsdf_stamp_cuboid_async(ks_tsdf* t, const double pose_R[9], const 
                                       const double half_extents[3]);
 KS_API int ks_tsdf_stamp_sphere_async(ks_tsdf* t, const double center[3], double radius);
 
+/* All primitives of an update in one call: stamp_primitive applied to prims[0 .. n-1] in order, stopping at the first
+ * one that would throw (its error is the one reported; later primitives are not applied) -- the world ends up exactly
+ * as after the sequential calls: pool indices, hash slots, free list, voxels.  Three kernel launches for the whole
+ * batch instead of three per primitive.  kind: 0 = Cuboid (pose_R, pose_t, half_extents), 1 = SphereShape (center, radius). */
+typedef struct ks_primitive {
+  int32_t kind, reserved;
+  double pose_R[9], pose_t[3], half_extents[3];
+  double center[3], radius;
+} ks_primitive;
+KS_API int ks_tsdf_stamp_batch(ks_tsdf* t, const ks_primitive* prims, int32_t n);
+KS_API int ks_tsdf_stamp_batch_async(ks_tsdf* t, const ks_primitive* prims, int32_t n);
+
 /* Triangle-mesh stamping.  The reference has no implementation to replace (SPEC.md:8 and :422 put it out of
  * scope; "Cuboids and meshes are stamped directly into the geometry channel"); the flow is
  * stamp_primitive's (sdf_world.hpp:418-443: padded AABB -> candidate blocks with |sdf(centre)| <= truncation +

@@ -396,6 +396,28 @@ inline void stamp_primitive(SparseTsdf& tsdf, const Primitive& primitive) {  // 
   }
 }
 
+/// All primitives of an update as ONE batch (addition; three kernel launches instead of three per primitive): the
+/// same as `for (p : primitives) stamp_primitive(tsdf, p);` -- pool indices, hash slots and voxels included -- and
+/// it stops at, and throws for, the first primitive the reference would throw for.
+inline void stamp_primitives(SparseTsdf& tsdf, std::span<const Primitive> primitives) {
+  std::vector<ks_primitive> batch(primitives.size());
+  for (std::size_t i = 0; i < primitives.size(); ++i) {
+    ks_primitive& out = batch[i];
+    out = ks_primitive{};
+    if (const auto* cuboid = std::get_if<Cuboid>(&primitives[i])) {
+      out.kind = 0;
+      b200_detail::fill_pose(cuboid->pose, out.pose_R, out.pose_t);
+      for (int a = 0; a < 3; ++a) out.half_extents[a] = cuboid->half_extents[a];
+    } else {
+      const auto& sphere = std::get<SphereShape>(primitives[i]);
+      out.kind = 1;
+      for (int a = 0; a < 3; ++a) out.center[a] = sphere.center[a];
+      out.radius = sphere.radius;
+    }
+  }
+  b200_detail::check(ks_tsdf_stamp_batch(tsdf.get(), batch.data(), static_cast<std::int32_t>(batch.size())));
+}
+
 // Triangle meshes.  NOT in the reference (SPEC.md:8, :422 put mesh stamping out of scope; PAPER.md:293 names it):
 // an addition next to Primitive, which keeps its reference definition.  A closed mesh with outward,
 // counter-clockwise triangles in the world frame; the tables live on the device, so a static mesh is built once.

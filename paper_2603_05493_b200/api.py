@@ -50,6 +50,11 @@ class EsdfConfigC(C.Structure):
                 ("voxel_size", C.c_double), ("seeding", C.c_int32)]
 
 
+class PrimitiveC(C.Structure):  # ks_primitive
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("pose_R", C.c_double * 9), ("pose_t", C.c_double * 3),
+                ("half_extents", C.c_double * 3), ("center", C.c_double * 3), ("radius", C.c_double)]
+
+
 class TsdfReportC(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("status", "blocks_touched", "required", "available", "live_blocks",
                                           "next_fresh", "free_count", "recycled")]
@@ -82,6 +87,7 @@ ABI_SYMBOLS = [
     "ks_esdf_build_async", "ks_esdf_seed", "ks_esdf_propagate", "ks_esdf_recover_signs", "ks_esdf_sync", "ks_esdf_last_report", "ks_esdf_probe_summary_device_async",
     "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async", "ks_esdf_scene_collision_static",
     "ks_esdf_scene_collision_swept", "ks_tsdf_export_slots", "ks_tsdf_generation", "ks_esdf_generation",
+    "ks_tsdf_stamp_batch", "ks_tsdf_stamp_batch_async",
 ]
 
 
@@ -166,6 +172,8 @@ def load_library() -> C.CDLL:
         "ks_tsdf_export_slots": (C.c_int, [VP, VP, VP, VP, I32, P(I32)]),
         "ks_tsdf_generation": (C.c_uint64, [VP]),
         "ks_esdf_generation": (C.c_uint64, [VP]),
+        "ks_tsdf_stamp_batch": (C.c_int, [VP, P(PrimitiveC), I32]),
+        "ks_tsdf_stamp_batch_async": (C.c_int, [VP, P(PrimitiveC), I32]),
     }
     assert sorted(sig) == sorted(ABI_SYMBOLS)
     for name, (res, args) in sig.items():
@@ -360,6 +368,11 @@ class SparseTsdf:
             c = _f64(primitive.center, 3)
             _check(self.lib.ks_tsdf_stamp_sphere_async(self.h, _ptr(c), float(primitive.radius)))
 
+    def stamp_batch_async(self, primitives):
+        """All cuboids / spheres of an update in three launches (ks_tsdf_stamp_batch_async): same world as the calls one by one."""
+        arr = _primitive_array(primitives)
+        _check(self.lib.ks_tsdf_stamp_batch_async(self.h, arr, len(primitives)))
+
     def sync(self) -> TsdfReportC:
         rep = TsdfReportC()
         _check(self.lib.ks_tsdf_sync(self.h, C.byref(rep)))
@@ -524,6 +537,26 @@ def stamp_primitive(tsdf: SparseTsdf, primitive) -> None:  # sdf_world.hpp:394-4
     else:
         c = _f64(primitive.center, 3)
         _check(tsdf.lib.ks_tsdf_stamp_sphere(tsdf.h, _ptr(c), float(primitive.radius)))
+
+
+def _primitive_array(primitives):
+    arr = (PrimitiveC * max(1, len(primitives)))()
+    for out, p in zip(arr, primitives):
+        if isinstance(p, Cuboid):
+            out.kind = 0
+            out.pose_R[:] = _f64(p.pose_R, 9).tolist()
+            out.pose_t[:] = _f64(p.pose_t, 3).tolist()
+            out.half_extents[:] = _f64(p.half_extents, 3).tolist()
+        else:
+            out.kind = 1
+            out.center[:] = _f64(p.center, 3).tolist()
+            out.radius = float(p.radius)
+    return arr
+
+
+def stamp_primitives(tsdf: SparseTsdf, primitives) -> None:
+    """stamp_primitive (sdf_world.hpp:394-444) over a list, in order, stopping at the first that raises -- as one batch."""
+    _check(tsdf.lib.ks_tsdf_stamp_batch(tsdf.h, _primitive_array(primitives), len(primitives)))
 
 
 def stamp_mesh(tsdf: SparseTsdf, mesh: TriangleMesh) -> None:  # flow of sdf_world.hpp:418-443, distance from csrc/mesh.cuh

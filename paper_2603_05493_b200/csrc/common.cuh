@@ -137,6 +137,10 @@ struct TsdfCtrl {  // device control block, mirrored to pinned host memory on sy
   int abort_op;         // the op in flight hit KS_ERR_RANGE
   int last_touched, last_recycled;
   int arrivals;         // CTAs of the apply kernel that are done (the last one closes the op)
+  // batched stamps
+  int abort_prim;       // lowest primitive of the batch with a block outside the key range (0x7FFFFFFF: none)
+  int batch_kstar, batch_alloc, batch_status, batch_required, batch_available;  // verdict of the batch in flight
+  int batch_stop;       // a group of the call in flight failed: its later groups do nothing
 };
 
 struct TsdfView {

@@ -39,6 +39,7 @@ struct OpLists {  // scratch of the op in flight (discover -> rank -> commit -> 
   int cap;
   uint64_t* fset;      // per-frame dedup set, open addressing
   uint32_t fset_mask;  // slots - 1
+  uint32_t* fmask;     // [slots] batched stamps: bit k = primitive k of the batch touches the block held by this set slot
 };
 
 struct Primitive {  // ks::Cuboid / ks::SphereShape (sdf_world.hpp:212-220)
@@ -537,6 +538,253 @@ __global__ void __launch_bounds__(512) k_stamp_blocks(TsdfView T, OpLists L, Pri
   arrive_and_finish(T, L.cap, 0);
 }
 
+// ---- batched stamps: every primitive of an update in three launches ----
+// stamp_primitive (sdf_world.hpp:394-444) applied to primitives 0 .. n-1 in order, stopping at the first one that
+// would throw: the result -- pool indices, hash slots, free list, every voxel, the error and its numbers -- is that of
+// the sequential calls.  A new block belongs to the FIRST primitive that touches it; new blocks are ranked by
+// (first primitive, key), which is the order in which the sequential calls would insert them (each call sorted,
+// sdf_world.hpp:308-322), so the rank-priority slot claims and the pool numbering of k_commit carry over unchanged.
+// Primitive k* fails when the new blocks of primitives 0 .. k* no longer fit (or one of its blocks is out of range);
+// primitives >= k* are then not applied and k*'s own numbers are reported, exactly as its allocate_keys would.
+constexpr int kMaxBatch = 16;
+struct BatchPrims {
+  Primitive prim[kMaxBatch];
+  BlockBox box[kMaxBatch];
+  long long offset[kMaxBatch + 1];  // candidate positions of primitive k: [offset[k], offset[k+1])
+  int n;
+};
+
+// (the batch travels as a __grid_constant__ parameter: the kernels index it at run time straight from the constant bank)
+__global__ void __launch_bounds__(256) k_batch_candidates(TsdfView T, OpLists L, const __grid_constant__ BatchPrims PB, double reach) {
+  pdl_enter();
+  if (T.ctrl->batch_stop) return;  // an earlier group of the same call failed: the reference would not get this far
+  const long long total = PB.offset[PB.n];
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int k = 0;
+    while (g >= PB.offset[k + 1]) ++k;
+    const BlockBox& B = PB.box[k];
+    const long long i = g - PB.offset[k];
+    const int bx = B.lo[0] + static_cast<int>(i % B.n[0]);
+    const int by = B.lo[1] + static_cast<int>((i / B.n[0]) % B.n[1]);
+    const int bz = B.lo[2] + static_cast<int>(i / (static_cast<long long>(B.n[0]) * B.n[1]));
+    const double sd = prim_sdf(PB.prim[k], (bx * kBlockEdge + 0.5 * kBlockEdge) * T.voxel,
+                               (by * kBlockEdge + 0.5 * kBlockEdge) * T.voxel, (bz * kBlockEdge + 0.5 * kBlockEdge) * T.voxel);
+    if (!(fabs(sd) <= reach)) continue;
+    if (!key_in_range(bx, by, bz)) {
+      atomicMin(&T.ctrl->abort_prim, k);
+      continue;
+    }
+    const uint64_t key = pack_key(bx, by, bz);
+    uint32_t slot = static_cast<uint32_t>(mix64(key)) & L.fset_mask;
+    while (true) {
+      const uint64_t cur = L.fset[slot];
+      if (cur == key) break;
+      if (cur == kKeyEmpty) {
+        const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long*>(&L.fset[slot]), kKeyEmpty, key);
+        if (old == kKeyEmpty) {
+          note_block(T, L, bx, by, bz, slot);
+          break;
+        }
+        if (old == key) break;
+      }
+      slot = (slot + 1) & L.fset_mask;
+    }
+    atomicOr(&L.fmask[slot], 1u << k);
+  }
+}
+
+// what the batch may apply: k* and the numbers behind it, from the per-primitive counts of new blocks
+struct BatchVerdict {
+  int kstar;      // primitives [0, kstar) are applied
+  int allocated;  // new blocks of those primitives
+  int status, required, available;
+};
+__device__ BatchVerdict batch_verdict(const TsdfView& T, const int* hist, int nprims, int touched, int list_cap) {
+  const TsdfCtrl* c = T.ctrl;
+  BatchVerdict v;
+  v.kstar = nprims, v.allocated = 0, v.status = 0, v.required = 0, v.available = 0;
+  int avail = c->free_count + (T.capacity - c->next_fresh), room = T.nslots - c->live;
+  if (c->batch_stop) {
+    v.kstar = 0;
+    return v;
+  }
+  if (touched > list_cap) {  // the op lists overflowed: nothing of this batch can be trusted
+    v.kstar = 0, v.status = KS_ERR_POOL_EXHAUSTED, v.required = touched, v.available = avail;
+    return v;
+  }
+  for (int k = 0; k < nprims; ++k) {
+    if (k >= c->abort_prim) {
+      v.kstar = k, v.status = KS_ERR_RANGE;
+      return v;
+    }
+    if (hist[k] > avail) {
+      v.kstar = k, v.status = KS_ERR_POOL_EXHAUSTED, v.required = hist[k], v.available = avail;
+      return v;
+    }
+    if (hist[k] > room) {
+      v.kstar = k, v.status = KS_ERR_TABLE_FULL;
+      return v;
+    }
+    avail -= hist[k], room -= hist[k], v.allocated += hist[k];
+  }
+  return v;
+}
+
+__device__ __forceinline__ int first_prim(const OpLists& L, int idx) { return __ffs(static_cast<int>(L.fmask[L.slot[idx]])) - 1; }
+
+// Allocation of a batch: k_commit with the rank taken over (first primitive, key) and the verdict above.
+__global__ void __launch_bounds__(256) k_batch_commit(TsdfView T, OpLists L, int nprims) {
+  pdl_enter();
+  const TsdfCtrl* c = T.ctrl;
+  const int n = min(c->fresh, L.cap);
+  if (n == 0 && blockIdx.x != 0) return;
+  __shared__ int s_hist[kMaxBatch];
+  __shared__ int s_count[8];
+  __shared__ BatchVerdict s_v;
+  if (threadIdx.x < kMaxBatch) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) atomicAdd(&s_hist[first_prim(L, L.fresh_idx[j])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_v = batch_verdict(T, s_hist, nprims, c->touched, L.cap);
+    if (blockIdx.x == 0) {  // for the apply kernel and its tail
+      TsdfCtrl* w = T.ctrl;
+      w->batch_kstar = s_v.kstar, w->batch_alloc = s_v.allocated, w->batch_status = s_v.status;
+      w->batch_required = s_v.required, w->batch_available = s_v.available;
+    }
+  }
+  __syncthreads();
+  const BatchVerdict v = s_v;
+  const int free_count = c->free_count, next_fresh = c->next_fresh;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int idx = L.fresh_idx[i];
+    const uint64_t key = L.key[idx];
+    const int mine = first_prim(L, idx);
+    if (mine >= v.kstar) {  // its primitive is not applied: the block is not allocated
+      if (threadIdx.x == 0) L.fresh_rank[i] = -1;
+      continue;
+    }
+    int below = 0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const int jdx = L.fresh_idx[j];
+      const int fj = first_prim(L, jdx);
+      below += fj < mine || (fj == mine && L.key[jdx] < key);
+    }
+    for (int d = 16; d > 0; d >>= 1) below += __shfl_down_sync(0xFFFFFFFFu, below, d);
+    __syncthreads();  // s_count free again
+    if ((threadIdx.x & 31) == 0) s_count[threadIdx.x >> 5] = below;
+    __syncthreads();
+    int r = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) r += s_count[w];
+    const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      if (lane == 0) {
+        L.fresh_rank[i] = r;
+        L.rank_key[r] = key;
+        L.pool[idx] = pool;
+        T.pool_key[pool] = key;
+        __threadfence();  // the key of a rank is visible before that rank can be seen in a claim
+      }
+      __syncwarp();
+      claim_slot(T, key, static_cast<uint32_t>(r), L.rank_key, lane);
+    }
+    double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
+    double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
+    for (int q = threadIdx.x; q < kBlockVoxels; q += blockDim.x) {
+      sw[q] = make_double2(0.0, 0.0);
+      g[q] = CUDART_INF;
+    }
+    if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
+    if (threadIdx.x == 0) T.pool_geom[pool] = 0;
+  }
+}
+
+__device__ void finish_batch(const TsdfView& T, int last_group) {
+  TsdfCtrl* c = T.ctrl;
+  if (c->batch_status != 0 && c->err == 0) {
+    c->err = c->batch_status;
+    c->err_required = c->batch_required, c->err_available = c->batch_available;
+  }
+  if (last_group) c->batch_stop = 0;
+  else if (c->batch_status != 0) c->batch_stop = 1;  // the remaining groups of this call do nothing
+  const int from_free = min(c->batch_alloc, c->free_count);
+  c->free_count -= from_free;
+  c->next_fresh += c->batch_alloc - from_free;
+  c->live += c->batch_alloc;
+  c->touched = 0;
+  c->fresh = 0;
+  c->abort_prim = 0x7FFFFFFF;
+}
+
+// Voxels of a batch: one CTA per touched block, the per-voxel min (sdf_world.hpp:437-443) over the applied
+// primitives that touch it, one digest refresh.
+__global__ void __launch_bounds__(512) k_batch_blocks(TsdfView T, OpLists L, const __grid_constant__ BatchPrims PB, int last_group) {
+  pdl_enter();
+  const int touched = min(T.ctrl->touched, L.cap);
+  const int kstar = T.ctrl->batch_kstar;
+  {  // settled claims -> table (finalize_slots, skipping the blocks that were not allocated)
+    const uint32_t nslots = static_cast<uint32_t>(T.nslots);
+    const int n_fresh = min(T.ctrl->fresh, L.cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_fresh; i += gridDim.x * blockDim.x) {
+      const int rank_i = L.fresh_rank[i];
+      if (rank_i < 0) continue;
+      const int idx = L.fresh_idx[i];
+      const uint64_t key = L.key[idx];
+      int bx, by, bz;
+      unpack_key(key, bx, by, bz);
+      uint32_t pos = static_cast<uint32_t>(block_hash(bx, by, bz) % nslots);
+      for (uint32_t probe = 0; probe < nslots; ++probe) {
+        if (T.slot_claim[pos] == static_cast<uint32_t>(rank_i)) {
+          T.slot_key[pos] = key;
+          T.slot_pool[pos] = L.pool[idx];
+          T.slot_claim[pos] = kNoClaim;
+          break;
+        }
+        pos = pos + 1 == nslots ? 0 : pos + 1;
+      }
+    }
+  }
+  const int tid = threadIdx.x;
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const double v = T.voxel;
+  const uint32_t applied = kstar >= 32 ? 0xFFFFFFFFu : (1u << kstar) - 1u;
+  for (int i = blockIdx.x; i < touched; i += gridDim.x) {
+    const uint32_t slot = L.slot[i];
+    const uint32_t mask = L.fmask[slot] & applied;  // the same word for the whole CTA
+    if (mask != 0) {
+      const int pool = L.pool[i];
+      int bx, by, bz;
+      unpack_key(L.key[i], bx, by, bz);
+      const size_t at = static_cast<size_t>(pool) * kBlockVoxels + tid;
+      const double g0 = T.geom[at];
+      const double2 sw = T.sumwt[at];
+      const double x = (bx * kBlockEdge + lx + 0.5) * v, y = (by * kBlockEdge + ly + 0.5) * v, z = (bz * kBlockEdge + lz + 0.5) * v;
+      double g = g0;
+      for (uint32_t m = mask; m != 0; m &= m - 1) {
+        const double sd = prim_sdf(PB.prim[__ffs(static_cast<int>(m)) - 1], x, y, z);
+        if (sd < g) g = sd;  // std::min(geom, sd)
+      }
+      if (g < g0) T.geom[at] = g;
+      store_digest(T.digest, pool, tid, voxel_bits(sw.x, sw.y, g, T.seed_thr));
+      if (tid == 0) T.pool_geom[pool] = 1;  // every voxel of a stamped block holds a finite distance
+    }
+    __syncthreads();  // every warp has read the block's mask: leave the set clean
+    if (tid == 0) L.fmask[slot] = 0u, L.fset[slot] = kKeyEmpty;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&T.ctrl->arrivals, 1) == static_cast<int>(gridDim.x) - 1) {
+      T.ctrl->arrivals = 0;
+      __threadfence();
+      finish_batch(T, last_group);
+    }
+  }
+}
+
 // ---- mesh stamp (no reference implementation; definition in mesh.cuh, flow of sdf_world.hpp:418-443) ----
 __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
@@ -830,7 +1078,7 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset), cudaFree(L.fmask);
   L.cap = static_cast<int>(want);
   KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
@@ -842,6 +1090,8 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
   while (slots < 2 * want) slots <<= 1;
   L.fset_mask = slots - 1;
   KS_CUDA(cudaMalloc(&L.fset, static_cast<size_t>(slots) * sizeof(uint64_t)));
+  KS_CUDA(cudaMalloc(&L.fmask, static_cast<size_t>(slots) * sizeof(uint32_t)));
+  KS_CUDA(cudaMemsetAsync(L.fmask, 0, static_cast<size_t>(slots) * sizeof(uint32_t), t->stream));
   KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, L.fset, static_cast<size_t>(slots), kKeyEmpty);
   KS_CUDA(cudaStreamSynchronize(t->stream));
   return KS_OK;
@@ -938,9 +1188,96 @@ static int stamp_async(ks_tsdf* t, const Primitive& P, const double lo_in[3], co
   return KS_OK;
 }
 
+static bool fill_primitive(const ks_primitive& in, Primitive& P, double lo[3], double hi[3], std::string& why) {
+  P = Primitive{};
+  if (in.kind == 1) {  // SphereShape
+    if (!std::isfinite(in.radius) || !std::isfinite(in.center[0]) || !std::isfinite(in.center[1]) || !std::isfinite(in.center[2])) {
+      why = "stamp: non-finite sphere";
+      return false;
+    }
+    P.is_sphere = 1;
+    P.radius = in.radius;
+    for (int a = 0; a < 3; ++a) P.c[a] = in.center[a], lo[a] = in.center[a] - in.radius, hi[a] = in.center[a] + in.radius;  // sdf_world.hpp:413-416
+    return true;
+  }
+  for (int a = 0; a < 3; ++a)  // the reference checks half_extents and translation (sdf_world.hpp:400)
+    if (!std::isfinite(in.pose_t[a]) || !std::isfinite(in.half_extents[a])) why = "stamp: non-finite cuboid";
+  if (!why.empty()) return false;
+  Rigid pose;
+  std::memcpy(pose.r, in.pose_R, sizeof pose.r);
+  std::memcpy(pose.t, in.pose_t, sizeof pose.t);
+  P.inv = rigid_inverse(pose);
+  for (int a = 0; a < 3; ++a) P.he[a] = in.half_extents[a], lo[a] = INFINITY, hi[a] = -INFINITY;
+  for (int corner = 0; corner < 8; ++corner) {  // world AABB over the eight corners (sdf_world.hpp:402-411)
+    const double sx = (corner & 1) ? 1.0 : -1.0, sy = (corner & 2) ? 1.0 : -1.0, sz = (corner & 4) ? 1.0 : -1.0;
+    double w[3];
+    rigid_apply(pose, sx * in.half_extents[0], sy * in.half_extents[1], sz * in.half_extents[2], w);
+    for (int a = 0; a < 3; ++a) lo[a] = std::min(lo[a], w[a]), hi[a] = std::max(hi[a], w[a]);
+  }
+  return true;
+}
+
+// one group of at most kMaxBatch primitives: candidates, allocation, voxels
+static int stamp_group_async(ks_tsdf* t, const ks_primitive* prims, int n, bool last_group) {
+  const bool prof = profiling(t);
+  t->generation.fetch_add(1, std::memory_order_relaxed);
+  wait_for_readers(t);
+  KS_MARK(t, 4);
+  const double v = t->cfg.voxel_size, trunc = t->cfg.truncation;
+  BatchPrims PB{};
+  PB.n = n;
+  PB.offset[0] = 0;
+  bool legal = true;
+  for (int k = 0; k < n; ++k) {
+    double lo_in[3], hi_in[3];
+    std::string why;
+    if (!fill_primitive(prims[k], PB.prim[k], lo_in, hi_in, why)) return fail(KS_ERR_INVALID, why);
+    BlockBox& B = PB.box[k];
+    B.count = 1;
+    for (int a = 0; a < 3; ++a) {  // AABB grown by the truncation band -> block range (sdf_world.hpp:418-425)
+      const int blo = voxel_index(lo_in[a] - trunc, v) >> 3, bhi = voxel_index(hi_in[a] + trunc, v) >> 3;
+      B.lo[a] = blo;
+      B.n[a] = std::max(bhi - blo + 1, 0);
+      B.count *= B.n[a];
+      if (B.lo[a] <= -kKeyBias || B.lo[a] + B.n[a] >= kKeyBias) legal = false;
+    }
+    PB.offset[k + 1] = PB.offset[k] + B.count;
+  }
+  const long long total = PB.offset[n];
+  if (total > t->lists.cap) {  // a batch may touch more blocks than any single call: the op lists grow to hold all candidates
+    const int rc = ensure_lists(t, static_cast<size_t>(total), 1);
+    if (rc != KS_OK) return rc;
+  }
+  {  // at most `total` blocks are new: can this batch fail on the device at all?
+    const bool safe = legal && t->bounds_valid && total <= t->known_avail && total <= t->known_room && total <= t->lists.cap;
+    if (safe) t->known_avail -= total, t->known_room -= total;
+    else t->bounds_valid = false;
+    t->last_stamp_safe = safe;
+  }
+  const double reach = trunc + 0.5 * kBlockEdge * v * std::sqrt(3.0);  // sdf_world.hpp:288-290, :425
+  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 8 * kSmCount)));
+  KS_LAUNCH(k_batch_candidates, grid, 256, 0, t->stream, t->view, t->lists, PB, reach);
+  KS_LAUNCH(k_batch_commit, 4 * kSmCount, 256, 0, t->stream, t->view, t->lists, n);
+  KS_MARK(t, 5);
+  KS_LAUNCH(k_batch_blocks, 3 * kSmCount, 512, 0, t->stream, t->view, t->lists, PB, last_group ? 1 : 0);
+  KS_MARK(t, 6);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
 }  // namespace ksb
 
 extern "C" {
+
+int ks_tsdf_stamp_batch_async(ks_tsdf* t, const ks_primitive* prims, int32_t n) {
+  if (!t || (n > 0 && !prims)) return fail(KS_ERR_INVALID, "null argument");
+  for (int32_t at = 0; at < n; at += kMaxBatch) {  // groups run in order; a failing group is reported like a failing call
+    const int rc = stamp_group_async(t, prims + at, std::min<int32_t>(kMaxBatch, n - at), at + kMaxBatch >= n);
+    if (rc != KS_OK) return rc;
+  }
+  return KS_OK;
+}
+
 
 static int tsdf_init(ks_tsdf* t, const ks_tsdf_config* cfg);
 
@@ -1007,6 +1344,8 @@ static int tsdf_init(ks_tsdf* t, const ks_tsdf_config* cfg) {
   KS_CUDA(cudaMallocHost(&t->h_verdict, sizeof(TsdfCtrl)));
   KS_CUDA(cudaEventCreateWithFlags(&t->ev_verdict, cudaEventDisableTiming));
   KS_CUDA(cudaMemsetAsync(V.ctrl, 0, sizeof(TsdfCtrl), t->stream));
+  static const int kNoAbort = 0x7FFFFFFF;
+  KS_CUDA(cudaMemcpyAsync(&V.ctrl->abort_prim, &kNoAbort, sizeof(int), cudaMemcpyHostToDevice, t->stream));
   KS_CUDA(cudaMemsetAsync(V.slot_pool, 0xFF, V.nslots * sizeof(int), t->stream));
   KS_CUDA(cudaMemsetAsync(V.digest, 0, cap * kDigestWords * sizeof(uint32_t), t->stream));
   KS_LAUNCH(k_fill_u64, 1024, 256, 0, t->stream, V.slot_key, static_cast<size_t>(V.nslots), kKeyEmpty);
@@ -1026,7 +1365,7 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.slot_claim), cudaFree(V.free_list), cudaFree(V.pool_key);
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset), cudaFree(L.fmask);
   cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
   cudaFreeHost(t->h_verdict);
@@ -1282,6 +1621,11 @@ static int finish_stamp(ks_tsdf* t) {
   cudaStreamIsCapturing(t->stream, &cap);
   if (cap == cudaStreamCaptureStatusNone && t->last_stamp_safe) return KS_OK;
   return ks_tsdf_sync(t, nullptr);
+}
+
+int ks_tsdf_stamp_batch(ks_tsdf* t, const ks_primitive* prims, int32_t n) {
+  int rc = ks_tsdf_stamp_batch_async(t, prims, n);
+  return rc != KS_OK ? rc : finish_stamp(t);
 }
 
 int ks_tsdf_stamp_cuboid(ks_tsdf* t, const double pose_R[9], const double pose_t[3], const double he[3]) {
