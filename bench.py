@@ -70,6 +70,25 @@ WORKLOAD_DESC = {
 }
 
 
+def config_of(workload: str, scene, world: int, envs_per_gpu: int, queries: int):
+    """The workload both arms report (identical keys and values in `--impl ours` and `--impl reference`)."""
+    nx, ny, nz = scene.esdf_dims
+    return {"workload": WORKLOAD_DESC[workload], "cells": nx * ny * nz, "dims": [nx, ny, nz], "tsdf_voxel_m": scene.tsdf_voxel,
+            "esdf_voxel_m": scene.esdf_voxel, "cameras": len(scene.frames), "cuboids": len(scene.cuboids), "spheres": len(scene.spheres),
+            "meshes": len(getattr(scene, "meshes", [])), "environments": world * envs_per_gpu, "environments_per_gpu": envs_per_gpu,
+            "queries_per_update": queries}
+
+
+def resolve_workload(args):
+    """Default workload: configs[1] on one GPU; on N > 1 GPUs BASELINE.json's batched case, configs[4] = 128 environments."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.workload is None:
+        args.workload = "cfg5env" if world > 1 else "cfg2"
+    if args.envs_per_gpu is None:
+        args.envs_per_gpu = max(1, 128 // world) if (args.workload == "cfg5env" and world > 1) else 1
+    return args
+
+
 # ---- clocks ---------------------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled while the GPU is under this benchmark's load."""
@@ -82,7 +101,8 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
-    def start(self):
+    def start(self, wait_s: float = 5.0):
+        """Start nvidia-smi and wait until its first sample has arrived (its start-up alone can take a second)."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
@@ -90,13 +110,19 @@ class ClockSampler:
             threading.Thread(target=self._pump, daemon=True).start()
         except OSError:
             self.proc = None
+            return
+        deadline = time.time() + wait_s
+        while not self.rows and time.time() < deadline:
+            time.sleep(0.01)
 
     def _pump(self):
         for line in self.proc.stdout:
             self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
 
-    def stop(self, t_begin: float, t_end: float):
-        """Summarise the samples that arrived inside [t_begin, t_end] (the timed region)."""
+    def stop(self, t_begin: float, t_end: float, t_load: float = None):
+        """Summarise the samples that arrived inside [t_begin, t_end] (the timed region); when that region is shorter
+        than ~10 sampling periods, the window is widened backwards over the uninterrupted load that led into it
+        (t_load: since when the GPU has been replaying the same update back to back)."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.05)
@@ -121,9 +147,10 @@ class ClockSampler:
         inside = [row for row in self.rows if t_begin <= row[0] <= t_end]
         sm, mx, reasons = summarise(inside)
         window = "timed region"
-        if not sm:  # region shorter than the sampling period: fall back to every sample of the loaded phase
-            sm, mx, reasons = summarise(self.rows)
-            window = "warm-up + timed region"
+        if len(sm) < 10 and t_load is not None:  # a short region: add the back-to-back replays that ran right before it
+            sm, mx, reasons = summarise([row for row in self.rows if t_load <= row[0] <= t_end])
+            window = "timed region + the %.1f s of uninterrupted replay before it (%d samples inside the region itself)" % (
+                t_begin - t_load, len(inside))
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
@@ -185,7 +212,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "cells_per_step": cells},
+        "config": config_of(args.workload, scene, int(os.environ.get("WORLD_SIZE", "1")), args.envs_per_gpu,
+                            1_000_000 if args.workload == "cfg4" else 0),
+        "sample_cells_per_step": cells,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": lib.kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -287,6 +316,7 @@ def run_ours(args):
             self.probes = torch.from_numpy(np.ascontiguousarray(probes)).cuda()
             self.probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
             self.queries = None
+            self.q_events = None  # (start, end) CUDA events around the query kernel while stage times are taken
             if queries is not None:  # configs[3]: 1 M batched distance + gradient queries per update
                 self.query_buffers = api.QueryBuffers(len(queries))   # page-locked: the "planner" writes its points here
                 self.query_buffers.points[...] = queries
@@ -317,9 +347,13 @@ def run_ours(args):
                 self.tsdf.stamp_async(m)
             self.esdf.build_async(self.tsdf)
             if self.queries is not None:
+                if self.q_events is not None:
+                    self.q_events[0].record()
                 api._check(self.esdf.lib.ks_esdf_query_device_async(
                     self.esdf.h, C.c_void_p(self.queries.data_ptr()), self.queries.shape[0], C.c_void_p(self.q_dist.data_ptr()),
                     C.c_void_p(self.q_grad.data_ptr()), C.c_void_p(self.q_inside.data_ptr())))
+                if self.q_events is not None:
+                    self.q_events[1].record()
 
         def blocking_update(self):
             k = 0
@@ -380,16 +414,49 @@ def run_ours(args):
         tsdf.profile(True)
         esdf.profile(True)
         stage_acc = {}
+        if envs[0].queries is not None:
+            envs[0].q_events = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         for i in range(args.warmup + min(args.steps, 20)):
             flush.zero_()
             envs[0].enqueue_update(False)
             st = {**tsdf.stage_ms(), **esdf.stage_ms()}
+            if envs[0].q_events is not None:
+                stream.synchronize()
+                st["query"] = envs[0].q_events[0].elapsed_time(envs[0].q_events[1])
             if i >= args.warmup:
                 for k, v in st.items():
                     stage_acc.setdefault(k, []).append(v)
+        envs[0].q_events = None
+        stage_ms = {k: float(np.mean(v)) for k, v in stage_acc.items()}
+
+        # ---- cold frame: the first update of a FRESH world (every block still to be allocated), plain launches -----------
+        cold_ms = []
+        for _ in range(3):
+            cfg_cold = api.make_tsdf_config(scene.tsdf_voxel)
+            cfg_cold.capacity = scene.capacity
+            cold = api.make_tsdf(cfg_cold, stream.cuda_stream)
+            for slot, f in enumerate(envs[0].frames):
+                cold.stage_frame(f, slot)  # staging buffers and op lists are set up here, outside the timed part
+                cold.upload_frame_async(slot)
+            cold.sync()
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for slot in range(len(envs[0].frames)):
+                cold.integrate_async(slot)
+            if envs[0].prims:
+                cold.stamp_batch_async(envs[0].prims)
+            for m in envs[0].meshes:
+                cold.stamp_async(m)
+            esdf.build_async(cold)
+            e1.record()
+            rep_cold = cold.sync()
+            assert rep_cold.status == 0
+            cold_ms.append(e0.elapsed_time(e1))
+            cold.close()
+        esdf.build_async(tsdf)  # back on the benchmark's own world
         tsdf.profile(False)
         esdf.profile(False)
-        stage_ms = {k: float(np.mean(v)) for k, v in stage_acc.items()}
 
         # ---- graph capture (inputs resident in HBM; multi-camera workloads re-upload inside the graph) --
         graph = api.Graph(stream.cuda_stream)
@@ -398,12 +465,16 @@ def run_ours(args):
         kernel_nodes, all_nodes = graph.node_count()
         sampler = ClockSampler(local)
         sampler.start()
-        for _ in range(max(args.warmup, 50)):  # also gives the clock sampler a loaded GPU to look at
-            flush.zero_()
-            graph.launch()
-            if exchange:
-                gather_summaries()
-        stream.synchronize()
+        t_load = time.time()
+        replays = 0
+        while replays < max(args.warmup, 50) or time.time() - t_load < 1.2:  # >= 1.2 s of the same load the timed steps apply
+            for _ in range(25):
+                flush.zero_()
+                graph.launch()
+                if exchange:
+                    gather_summaries()
+            replays += 25
+            stream.synchronize()
         if world > 1:
             dist.barrier()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -421,7 +492,7 @@ def run_ours(args):
         t_end = time.time()
         if world > 1:
             dist.barrier()
-        clocks = sampler.stop(t_begin, t_end)
+        clocks = sampler.stop(t_begin, t_end, t_load)
         per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -485,6 +556,17 @@ def run_ours(args):
     if traffic_path.exists():
         traffic = json.loads(traffic_path.read_text()).get(args.workload, {}).get(dominant)
     update_bytes = sum(stage_bytes[s] * (len(frames) if s in ("discover", "allocate", "integrate") else 1) for s in kernel_stages)
+    stage_bytes["stamp_candidates"] = 0.0
+    if n_queries:
+        stage_bytes["query"] = 89.0 * n_queries  # 24 B in + 33 B out + 8 gathers of 4 B
+    stage_table = []
+    for name in ["discover", "allocate", "integrate", "stamp_candidates", "stamp_blocks", "directory", "seed", "flood_z", "sweep_y", "sweep_x", "query"]:
+        if name not in stage_ms:
+            continue
+        ms = stage_ms[name]
+        gbs = stage_bytes.get(name, 0.0) / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        stage_table.append({"stage": name, "ms": round(ms, 5), "algorithmic_bytes": stage_bytes.get(name, 0.0), "GB/s": round(gbs, 1),
+                            "frac_of_hbm_peak": round(gbs / peak, 4)})
     ms_per_step = total_ms / args.steps
     value = n_envs * cells * args.steps / (total_ms * 1e-3)
 
@@ -509,12 +591,11 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "cells": cells, "tsdf_voxel_m": scene.tsdf_voxel,
-                   "esdf_voxel_m": scene.esdf_voxel, "blocks_touched": touched_last, "live_blocks": live,
-                   "seeds": int(erep.seed_count), "environments": n_envs, "environments_per_gpu": E_local,
-                   "queries_per_update": n_queries, "execution": "cuda-graph replay",
-                   "l2": "flushed between timed steps (256 MiB memset outside the event pairs); per-step working set ~22 B/cell > 126 MB L2",
-                   "collective": "none" if not exchange else "ncclAllGather of 32-byte per-environment summaries each step"},
+        "config": config_of(args.workload, scene, world, E_local, n_queries),
+        "run": {"blocks_touched": touched_last, "live_blocks": live, "seeds": int(erep.seed_count), "execution": "cuda-graph replay",
+                "l2": "flushed between timed steps (256 MiB memset outside the event pairs); per-step working set ~18 B/cell > 126 MB L2",
+                "collective": "none" if not exchange else "ncclAllGather of 32-byte per-environment summaries each step",
+                "state": "steady state: the world's blocks exist (allocated by the warm-up); cold_frame_ms is the first update of a fresh world"},
         "clocks": clocks,
         "e2e": {"value": n_envs * cells * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": 1e3 * e2e_s / args.steps, "path": "blocking ks:: calls: integrate_depth(page-locked host frame, uploaded in place) + stamp_primitive x%d + build_esdf + report" % len(prims)},
@@ -523,6 +604,9 @@ def run_ours(args):
         "gpu_launches": int(kernel_nodes * args.steps),
         "graph": {"kernel_nodes": int(kernel_nodes), "all_nodes": int(all_nodes)},
         "stage_ms": {k: round(v, 5) for k, v in stage_ms.items()},
+        "stages": stage_table,
+        "cold_frame_ms": {"value": float(np.median(cold_ms)), "runs": [round(v, 4) for v in cold_ms],
+                          "what": "first update of a fresh world (all blocks allocated by this update), plain stream launches, inputs resident in HBM"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": stage_bytes[dominant],
@@ -542,10 +626,12 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
-    ap.add_argument("--envs-per-gpu", type=int, default=1, help="independent environments per rank (cfg5: 128 / N)")
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOAD_DESC),
+                    help="default: cfg2 on one GPU; cfg5env (BASELINE configs[4]) under torchrun with N > 1")
+    ap.add_argument("--envs-per-gpu", type=int, default=None, help="independent environments per rank (cfg5env on N > 1 GPUs: 128 / N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    args = resolve_workload(args)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)

@@ -24,7 +24,7 @@ def test_two_ranks_share_one_gpu(tmp_path):
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["scaling"] == "weak" and rec["config"]["environments"] == 2
     assert rec["value"] > 0 and rec["e2e"]["value"] > 0 and rec["gpu_launches"] > 0
-    assert "ncclAllGather" in rec["config"]["collective"]
+    assert "ncclAllGather" in rec["run"]["collective"]
 
 
 def test_reference_arm_only_rank0_prints(tmp_path):
