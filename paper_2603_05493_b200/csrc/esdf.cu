@@ -2038,7 +2038,9 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
     e->none_x = KeysX::none_offset(E.nx, gmax_x);
     // warps per tile: 8 (y) and 16 (x) measured best while several tiles share an SM (tools/ab_sweeps.sh); long rows
     // leave room for fewer tiles, which then get more warps each
-    e->dc_wl_y = dc_smem_bytes_y(E.ny) > 56 * 1024 ? 4 : 3;
+    // y sweep, measured per row length (tools/gpu_env_sweep.sh KS_DC_WARPS_Y): 100 rows 8 warps, 200 rows 4 warps (93 vs 98 us),
+    // 500 rows 8 warps (703 vs 759 us with 16)
+    e->dc_wl_y = dc_smem_bytes_y(E.ny) > 16 * 1024 && dc_smem_bytes_y(E.ny) <= 48 * 1024 ? 2 : 3;
     e->dc_wl_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) > 113 * 1024 ? 5 : 4;
     if (const char* v = std::getenv("KS_DC_WARPS_Y")) e->dc_wl_y = std::min(4, std::max(0, std::atoi(v)));
     if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(5, std::max(0, std::atoi(v)));
