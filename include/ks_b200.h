@@ -280,6 +280,59 @@ KS_API int ks_esdf_scene_collision_swept(ks_esdf* e, const double* centers_host,
                                          ks_collision_report* reports, double* center_gradient,
                                          double* next_center_gradient, double* velocity_gradient);
 
+/* ---- batched environments (BASELINE configs[4]) ------------------------- */
+/* The reference has no batch API ("no batched-environment API"; PAPER.md's batched planning runs one
+ * SparseTsdf + DenseEsdf per environment through the functions above).  A ks_batch owns n_envs such pairs with one
+ * configuration and runs an update of all of them -- per environment: upload the staged frames, integrate_depth per
+ * camera (sdf_world.hpp:340-389), stamp_primitive for its primitives / meshes (sdf_world.hpp:394-444), build_esdf
+ * (esdf.hpp:323-327), one 32-byte summary {environment id, min distance over its probe points, probes closer than
+ * near_distance, seed count} -- as one enqueue on ks_batch_stream(), capturable, or as the batch's own graph
+ * (ks_batch_update).  Environments are independent: no data-path collective.  The environments are dealt round-robin
+ * onto `lanes` (1..8) streams forked from / joined into the batch stream, so one environment's short kernels overlap
+ * another's sweeps.  Each world is exactly what the per-handle calls produce; ks_batch_tsdf / ks_batch_esdf hand out
+ * the handles (owned by the batch) for staging frames (ks_tsdf_stage_frame_slot, ks_tsdf_frame_buffer), queries,
+ * collision checks and downloads. */
+typedef struct ks_batch ks_batch;
+KS_API int ks_batch_create(int32_t n_envs, const ks_tsdf_config* tsdf_config, const ks_esdf_config* esdf_config,
+                           int32_t lanes, ks_batch** out);
+KS_API void ks_batch_destroy(ks_batch* b);
+KS_API int32_t ks_batch_size(const ks_batch* b);
+KS_API int32_t ks_batch_lanes(const ks_batch* b);
+KS_API ks_tsdf* ks_batch_tsdf(ks_batch* b, int32_t env);
+KS_API ks_esdf* ks_batch_esdf(ks_batch* b, int32_t env);
+KS_API ks_stream ks_batch_stream(ks_batch* b);
+/* what an update applies to environment `env`: the first n_cameras staging slots, these primitives (copied), these
+ * meshes (borrowed: keep them alive) */
+KS_API int ks_batch_set_inputs(ks_batch* b, int32_t env, int32_t n_cameras, const ks_primitive* prims, int32_t n_prims,
+                               const ks_mesh* const* meshes, int32_t n_meshes);
+/* probe points of the environment's summary (n xyz triples, copied to the device); n = 0: no summary row */
+KS_API int ks_batch_set_probes(ks_batch* b, int32_t env, const double* points_host, int64_t n, double near_distance);
+/* global id of environment 0 (multi-rank: the rank's first environment), written into the summaries */
+KS_API int ks_batch_set_first_env(ks_batch* b, int32_t first_env);
+/* enqueue one update of every environment (+ the all-gather when a communicator is attached); never synchronises */
+KS_API int ks_batch_update_async(ks_batch* b, int32_t upload_frames);
+/* the same through a private CUDA graph: captured at the first call and after inputs changed, replayed otherwise */
+KS_API int ks_batch_update(ks_batch* b, int32_t upload_frames);
+KS_API int64_t ks_batch_graph_kernels(const ks_batch* b);
+/* wait; per-environment reports (any pointer may be NULL): reports[n_envs], esdf_reports[n_envs],
+ * summaries_host[n_envs][4].  Returns the first failing environment's status, its text prefixed "environment <id>: " */
+KS_API int ks_batch_sync(ks_batch* b, ks_tsdf_report* reports, ks_esdf_report* esdf_reports, double* summaries_host);
+KS_API double* ks_batch_summary_device(ks_batch* b);   /* [max_local][4] doubles, rows >= n_envs stay NaN */
+/* Multi-GPU: one process per GPU, each with its own batch over a contiguous range of environments. */
+KS_API int ks_partition_envs(int32_t n_envs, int32_t world, int32_t rank, int32_t* lo, int32_t* hi);
+/* NCCL is resolved at run time (dlopen of libnccl.so.2, or KS_NCCL_LIB): the library does not link it.
+ * ks_nccl_unique_id: 128 bytes from ncclGetUniqueId, to be broadcast by the host's own means;
+ * ks_batch_attach_nccl: ncclCommInitRank (collective over all ranks) + gather buffers; from then on every update ends
+ * with ncclAllGather(summary rows) on the batch stream -- a node of the captured graph.  A host that already owns a
+ * communicator passes it to ks_batch_attach_nccl_comm instead (borrowed).  max_local_envs = the largest batch size of
+ * any rank (every rank contributes that many rows; missing ones are NaN). */
+KS_API int ks_nccl_unique_id(void* out128);
+KS_API int ks_batch_attach_nccl(ks_batch* b, const void* unique_id128, int32_t world, int32_t rank, int32_t max_local_envs);
+KS_API int ks_batch_attach_nccl_comm(ks_batch* b, void* nccl_comm, int32_t world, int32_t rank, int32_t max_local_envs);
+KS_API double* ks_batch_gathered_device(ks_batch* b);  /* [world][max_local][4]; == the summary buffer on one rank */
+KS_API int32_t ks_batch_gathered_rows(const ks_batch* b);
+KS_API int ks_batch_gathered(ks_batch* b, double* host_out);  /* wait + download of the gathered rows */
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,10 @@ ABI_SYMBOLS = [
     "ks_esdf_download", "ks_esdf_query", "ks_esdf_query_device_async", "ks_esdf_scene_collision_static",
     "ks_esdf_scene_collision_swept", "ks_tsdf_export_slots", "ks_tsdf_generation", "ks_esdf_generation",
     "ks_tsdf_stamp_batch", "ks_tsdf_stamp_batch_async",
+    "ks_batch_create", "ks_batch_destroy", "ks_batch_size", "ks_batch_lanes", "ks_batch_tsdf", "ks_batch_esdf", "ks_batch_stream",
+    "ks_batch_set_inputs", "ks_batch_set_probes", "ks_batch_set_first_env", "ks_batch_update_async", "ks_batch_update",
+    "ks_batch_graph_kernels", "ks_batch_sync", "ks_batch_summary_device", "ks_partition_envs", "ks_nccl_unique_id",
+    "ks_batch_attach_nccl", "ks_batch_attach_nccl_comm", "ks_batch_gathered_device", "ks_batch_gathered_rows", "ks_batch_gathered",
 ]
 
 
@@ -174,6 +178,28 @@ def load_library() -> C.CDLL:
         "ks_esdf_generation": (C.c_uint64, [VP]),
         "ks_tsdf_stamp_batch": (C.c_int, [VP, P(PrimitiveC), I32]),
         "ks_tsdf_stamp_batch_async": (C.c_int, [VP, P(PrimitiveC), I32]),
+        "ks_batch_create": (C.c_int, [I32, P(TsdfConfigC), P(EsdfConfigC), I32, P(VP)]),
+        "ks_batch_destroy": (None, [VP]),
+        "ks_batch_size": (I32, [VP]),
+        "ks_batch_lanes": (I32, [VP]),
+        "ks_batch_tsdf": (VP, [VP, I32]),
+        "ks_batch_esdf": (VP, [VP, I32]),
+        "ks_batch_stream": (VP, [VP]),
+        "ks_batch_set_inputs": (C.c_int, [VP, I32, I32, P(PrimitiveC), I32, P(VP), I32]),
+        "ks_batch_set_probes": (C.c_int, [VP, I32, VP, I64, D]),
+        "ks_batch_set_first_env": (C.c_int, [VP, I32]),
+        "ks_batch_update_async": (C.c_int, [VP, I32]),
+        "ks_batch_update": (C.c_int, [VP, I32]),
+        "ks_batch_graph_kernels": (I64, [VP]),
+        "ks_batch_sync": (C.c_int, [VP, P(TsdfReportC), P(EsdfReportC), VP]),
+        "ks_batch_summary_device": (VP, [VP]),
+        "ks_partition_envs": (C.c_int, [I32, I32, I32, P(I32), P(I32)]),
+        "ks_nccl_unique_id": (C.c_int, [VP]),
+        "ks_batch_attach_nccl": (C.c_int, [VP, VP, I32, I32, I32]),
+        "ks_batch_attach_nccl_comm": (C.c_int, [VP, VP, I32, I32, I32]),
+        "ks_batch_gathered_device": (VP, [VP]),
+        "ks_batch_gathered_rows": (I32, [VP]),
+        "ks_batch_gathered": (C.c_int, [VP, VP]),
     }
     assert sorted(sig) == sorted(ABI_SYMBOLS)
     for name, (res, args) in sig.items():
@@ -325,9 +351,17 @@ class SparseTsdf:
         if stream is not None:
             _check(self.lib.ks_tsdf_set_stream(self.h, C.c_void_p(stream)))
 
+    @classmethod
+    def _borrowed(cls, handle, config: "TsdfConfig", owner) -> "SparseTsdf":
+        """A view of a world owned by something else (an EnvBatch): same methods, never destroyed from here."""
+        self = cls.__new__(cls)
+        self.lib, self.config, self.h, self._owner = load_library(), config, C.c_void_p(handle), owner
+        return self
+
     def close(self):
         if getattr(self, "h", None):
-            self.lib.ks_tsdf_destroy(self.h)
+            if getattr(self, "_owner", None) is None:
+                self.lib.ks_tsdf_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -433,9 +467,16 @@ class DenseEsdf:
         if stream is not None:
             _check(self.lib.ks_esdf_set_stream(self.h, C.c_void_p(stream)))
 
+    @classmethod
+    def _borrowed(cls, handle, config: "EsdfConfig", owner) -> "DenseEsdf":
+        self = cls.__new__(cls)
+        self.lib, self.config, self.h, self._owner = load_library(), config, C.c_void_p(handle), owner
+        return self
+
     def close(self):
         if getattr(self, "h", None):
-            self.lib.ks_esdf_destroy(self.h)
+            if getattr(self, "_owner", None) is None:
+                self.lib.ks_esdf_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -753,3 +794,104 @@ class Graph:
         if self.h:
             self.lib.ks_graph_destroy(self.h)
             self.h = C.c_void_p()
+
+
+# ---- batched environments (BASELINE configs[4]; include/ks_b200.h "batched environments") ---------------------------------
+
+SUMMARY_FIELDS = ("env", "min_distance", "colliding", "seeds")  # 4 x float64 per environment
+
+
+def partition_envs(n_envs: int, world: int, rank: int) -> Tuple[int, int]:
+    """ks_partition_envs: the contiguous range [lo, hi) of environments `rank` owns (earlier ranks take the remainder)."""
+    lo, hi = C.c_int32(), C.c_int32()
+    if load_library().ks_partition_envs(n_envs, world, rank, C.byref(lo), C.byref(hi)) != KS_OK:
+        raise ValueError(last_error())
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(load_library().ks_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class EnvBatch:
+    """ks_batch: n independent (SparseTsdf, DenseEsdf) pairs of one configuration updated by one enqueue / one graph."""
+
+    def __init__(self, n_envs: int, tsdf_config: TsdfConfig, esdf_config: EsdfConfig, lanes: int = 2, first_env: int = 0):
+        self.lib = load_library()
+        tc = TsdfConfigC(tsdf_config.voxel_size, tsdf_config.truncation, tsdf_config.alpha_time, tsdf_config.alpha_frustum,
+                         tsdf_config.weight_threshold, int(tsdf_config.capacity), int(tsdf_config.slot_count))
+        ec = EsdfConfigC()
+        ec.origin[:] = [float(v) for v in esdf_config.origin]
+        ec.nx, ec.ny, ec.nz = int(esdf_config.nx), int(esdf_config.ny), int(esdf_config.nz)
+        ec.voxel_size = float(esdf_config.voxel_size)
+        ec.seeding = 1 if esdf_config.seeding == "gather" else 0
+        h = C.c_void_p()
+        _check(self.lib.ks_batch_create(n_envs, C.byref(tc), C.byref(ec), lanes, C.byref(h)))
+        self.h = h
+        self.n = n_envs
+        self.first_env = first_env
+        _check(self.lib.ks_batch_set_first_env(self.h, first_env))
+        self.tsdf = [SparseTsdf._borrowed(self.lib.ks_batch_tsdf(self.h, i), tsdf_config, self) for i in range(n_envs)]
+        self.esdf = [DenseEsdf._borrowed(self.lib.ks_batch_esdf(self.h, i), esdf_config, self) for i in range(n_envs)]
+        self._meshes = {}
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.ks_batch_stream(self.h) or 0)
+
+    @property
+    def lanes(self) -> int:
+        return int(self.lib.ks_batch_lanes(self.h))
+
+    def set_inputs(self, env: int, n_cameras: int, primitives=(), meshes=()):
+        prims = [p for p in primitives]
+        arr = _primitive_array(prims)
+        self._meshes[env] = list(meshes)  # borrowed by the library: keep them alive
+        marr = (C.c_void_p * max(1, len(meshes)))(*[m.h for m in meshes])
+        _check(self.lib.ks_batch_set_inputs(self.h, env, n_cameras, arr, len(prims), marr, len(meshes)))
+
+    def set_probes(self, env: int, points, near_distance: float):
+        pts = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 3))
+        _check(self.lib.ks_batch_set_probes(self.h, env, _ptr(pts), pts.shape[0], float(near_distance)))
+
+    def update_async(self, upload_frames: bool = True):
+        _check(self.lib.ks_batch_update_async(self.h, int(upload_frames)))
+
+    def update(self, upload_frames: bool = True):
+        _check(self.lib.ks_batch_update(self.h, int(upload_frames)))
+
+    def graph_kernels(self) -> int:
+        return int(self.lib.ks_batch_graph_kernels(self.h))
+
+    def sync(self):
+        """(tsdf reports, esdf reports, summaries [n, 4]) after waiting for the batch stream."""
+        reps = (TsdfReportC * self.n)()
+        ereps = (EsdfReportC * self.n)()
+        summ = np.empty((self.n, 4), np.float64)
+        _check(self.lib.ks_batch_sync(self.h, reps, ereps, _ptr(summ)))
+        return list(reps), list(ereps), summ
+
+    def attach_nccl(self, unique_id: bytes, world: int, rank: int, max_local_envs: int):
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(self.lib.ks_batch_attach_nccl(self.h, buf, world, rank, max_local_envs))
+
+    def gathered(self) -> np.ndarray:
+        rows = int(self.lib.ks_batch_gathered_rows(self.h))
+        out = np.empty((rows, 4), np.float64)
+        _check(self.lib.ks_batch_gathered(self.h, _ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            for w in self.tsdf + self.esdf:
+                w.h = None
+            self.lib.ks_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libks_b200.so"
-SOURCES = ["capi.cu", "tsdf.cu", "esdf.cu"]
+SOURCES = ["capi.cu", "tsdf.cu", "esdf.cu", "batch.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write("\n".join(log))
             raise RuntimeError(f"nvcc failed on {src}")
     (build_dir / "ptxas.log").write_text("\n".join(log))
-    link = [NVCC, "-shared", "-o", str(LIB), *objs, "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static"]
+    link = [NVCC, "-shared", "-o", str(LIB), *objs, "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-ldl"]
     subprocess.run(link, check=True)
     if verbose:
         print("\n".join(log))
