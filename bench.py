@@ -277,17 +277,15 @@ def run_ours(args):
         else:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
-    from paper_2603_05493_b200 import multi_env
-
     stream = torch.cuda.Stream()
     E_local = max(1, args.envs_per_gpu)
     n_envs = world * E_local
-    env_lo, env_hi = multi_env.partition_envs(n_envs, world, rank)
+    env_lo, env_hi = api.partition_envs(n_envs, world, rank)
 
     class Environment:
         """One independent scene: its own TSDF + ESDF handles, all on this rank's stream."""
 
-        def __init__(self, env_id):
+        def __init__(self, env_id, handles=None):
             self.env_id = env_id
             queries = None
             if args.workload == "cfg4":
@@ -308,13 +306,15 @@ def run_ours(args):
             self.meshes = [api.TriangleMesh(m.vertices, m.triangles) for m in sc.meshes]  # uploaded once (static geometry)
             cfg = api.make_tsdf_config(sc.tsdf_voxel)
             cfg.capacity = sc.capacity
-            self.tsdf = api.make_tsdf(cfg, stream.cuda_stream)
+            self.tcfg = cfg
             self.ecfg = api.EsdfConfig(tuple(sc.esdf_origin), *sc.esdf_dims, sc.esdf_voxel, "gather")
-            self.esdf = api.DenseEsdf(self.ecfg, stream.cuda_stream)
+            if handles is None:
+                self.tsdf = api.make_tsdf(cfg, stream.cuda_stream)
+                self.esdf = api.DenseEsdf(self.ecfg, stream.cuda_stream)
+            else:  # worlds owned by the C-ABI batch (ks_batch_*)
+                self.tsdf, self.esdf = handles
             ext = np.array(sc.esdf_dims) * sc.esdf_voxel
-            probes = sc.esdf_origin + np.random.RandomState(3 + env_id).random_sample((4096, 3)) * ext
-            self.probes = torch.from_numpy(np.ascontiguousarray(probes)).cuda()
-            self.probe_d = torch.empty(4096, dtype=torch.float64, device="cuda")
+            self.probes_host = np.ascontiguousarray(sc.esdf_origin + np.random.RandomState(3 + env_id).random_sample((4096, 3)) * ext)
             self.queries = None
             self.q_events = None  # (start, end) CUDA events around the query kernel while stage times are taken
             if queries is not None:  # configs[3]: 1 M batched distance + gradient queries per update
@@ -369,13 +369,28 @@ def run_ours(args):
                 api.query(self.esdf, self.queries_host, self.query_buffers)  # H2D points, D2H distance + gradient + inside (page-locked)
             return k, r.seed_count
 
-        def summary_into(self, row):
-            """collision summary of this environment (env id, probe-sphere minimum distance, near-contact count, seeds):
-            one kernel, written straight into this environment's row of the exchange buffer"""
-            api._check(self.esdf.lib.ks_esdf_probe_summary_device_async(
-                self.esdf.h, C.c_void_p(self.probes.data_ptr()), 4096, 0.02, float(self.env_id), C.c_void_p(row.data_ptr())))
-
-    envs = [Environment(e) for e in range(env_lo, env_hi)]
+    # Several environments (configs[4]) go through the C-ABI batch: ks_batch_create owns the worlds, one update of all of
+    # them is one enqueue / one private graph, the per-environment summaries are written by the update itself and
+    # all-gathered by ncclAllGather as the last node of that graph.
+    exchange = world > 1 or E_local > 1
+    batch = None
+    if exchange:
+        sc0 = make_scene(args.workload, env=env_lo)
+        cfg0 = api.make_tsdf_config(sc0.tsdf_voxel)
+        cfg0.capacity = sc0.capacity
+        ecfg0 = api.EsdfConfig(tuple(sc0.esdf_origin), *sc0.esdf_dims, sc0.esdf_voxel, "gather")
+        batch = api.EnvBatch(env_hi - env_lo, cfg0, ecfg0, lanes=args.lanes, first_env=env_lo)
+        stream = torch.cuda.ExternalStream(batch.stream)
+        envs = [Environment(e, (batch.tsdf[e - env_lo], batch.esdf[e - env_lo])) for e in range(env_lo, env_hi)]
+        for i, env in enumerate(envs):
+            batch.set_inputs(i, len(env.frames), env.prims, env.meshes)
+            batch.set_probes(i, env.probes_host, 0.02)
+        if world > 1 and not share_gpu:  # the batch's own communicator: 128-byte id from rank 0, ncclCommInitRank on every rank
+            uid = [api.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            batch.attach_nccl(uid[0], world, rank, E_local)
+    else:
+        envs = [Environment(e) for e in range(env_lo, env_hi)]
     scene = envs[0].scene
     nx, ny, nz = scene.esdf_dims
     cells = nx * ny * nz
@@ -383,26 +398,24 @@ def run_ours(args):
     tsdf, esdf, ecfg = envs[0].tsdf, envs[0].esdf, envs[0].ecfg
     pixels = sum(f.width * f.height for f in frames)
     n_queries = 0 if envs[0].queries is None else int(envs[0].queries.shape[0])
-    exchange = world > 1 or E_local > 1
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    summary_local, summary_all, _valid_rows = multi_env.summary_buffers(n_envs, world, rank, "cuda")
 
     def enqueue_update(upload: bool):
-        for i, env in enumerate(envs):
-            env.enqueue_update(upload)
-            if exchange:  # the environment's collision summary is one more kernel of the same (captured) update
-                env.summary_into(summary_local[i])
-
-    def gather_summaries():
-        """per-environment collision summaries (written by the update itself), all-gathered over NCCL -- the only
-        collective on this path."""
-        if world > 1 and share_gpu:
-            host_all = torch.empty(summary_all.shape, dtype=torch.float64)
-            dist.all_gather_into_tensor(host_all, summary_local.cpu())
-            summary_all.copy_(host_all)
+        if batch is not None:
+            batch.update_async(upload)
         else:
-            multi_env.gather_summaries(summary_local, summary_all, world)
+            envs[0].enqueue_update(upload)
+
+    def gather_summaries_shared_gpu():
+        """test mode only (KS_BENCH_SHARE_GPU=1, every rank on device 0, NCCL impossible): the summaries the update
+        wrote are exchanged through gloo from the host.  The real multi-GPU run gathers inside the batch graph."""
+        _, _, mine = batch.sync()
+        pad = np.full((E_local, 4), np.nan)
+        pad[:mine.shape[0]] = mine
+        host_all = torch.empty((world * E_local, 4), dtype=torch.float64)
+        dist.all_gather_into_tensor(host_all, torch.from_numpy(pad))
+        return host_all.numpy()
 
     with torch.cuda.stream(stream):
         # ---- eager warm-up (allocates blocks, binds the directory), then stage timings ---------------
@@ -459,10 +472,18 @@ def run_ours(args):
         esdf.profile(False)
 
         # ---- graph capture (inputs resident in HBM; multi-camera workloads re-upload inside the graph) --
-        graph = api.Graph(stream.cuda_stream)
-        with graph:
-            enqueue_update(upload=False)
-        kernel_nodes, all_nodes = graph.node_count()
+        if batch is not None:  # the batch's private graph (ks_batch_update): first call captures, later calls replay
+            class _BatchGraph:
+                def launch(self):
+                    batch.update(False)
+            graph = _BatchGraph()
+            graph.launch()
+            kernel_nodes = all_nodes = batch.graph_kernels()
+        else:
+            graph = api.Graph(stream.cuda_stream)
+            with graph:
+                enqueue_update(upload=False)
+            kernel_nodes, all_nodes = graph.node_count()
         sampler = ClockSampler(local)
         sampler.start()
         t_load = time.time()
@@ -471,8 +492,6 @@ def run_ours(args):
             for _ in range(25):
                 flush.zero_()
                 graph.launch()
-                if exchange:
-                    gather_summaries()
             replays += 25
             stream.synchronize()
         if world > 1:
@@ -485,8 +504,6 @@ def run_ours(args):
             flush.zero_()  # L2 flush between timed iterations (outside the event pair)
             starts[i].record(stream)
             graph.launch()
-            if exchange:
-                gather_summaries()
             ends[i].record(stream)
         torch.cuda.synchronize()
         t_end = time.time()
@@ -504,8 +521,15 @@ def run_ours(args):
 
         # ---- e2e: blocking drop-in calls with host buffers ------------------------------------------------
         def blocking_update():
+            if batch is None:
+                envs[0].blocking_update()
+                return
+            # batch: every camera's pixels are written into its slot's page-locked staging area (zero-copy staging),
+            # the update graph uploads them (H2D inside the timed region), sync reads back reports + summaries (D2H)
             for env in envs:
-                env.blocking_update()
+                env.stage()
+            batch.update(True)
+            batch.sync()
 
         for _ in range(args.warmup):
             blocking_update()
@@ -524,6 +548,9 @@ def run_ours(args):
         # ---- e2e through the graph API (stage + upload + replay + report), informational ----------------
         t0 = time.perf_counter()
         for _ in range(args.steps):
+            if batch is not None:
+                blocking_update()
+                continue
             for env in envs:
                 env.stage()
                 for slot in range(len(env.frames)):
@@ -533,6 +560,15 @@ def run_ours(args):
                 env.tsdf.sync()
                 env.esdf.report()
         e2e_graph_s = time.perf_counter() - t0
+
+        # ---- the exchanged summaries: every environment of every rank must be there -----------------------------------
+        gathered_rows = None
+        if batch is not None:
+            rows = gather_summaries_shared_gpu() if (world > 1 and share_gpu) else batch.gathered()
+            ids = sorted(int(r[0]) for r in rows if not np.isnan(r[0]))
+            assert ids == list(range(n_envs)), f"summary exchange incomplete: {ids}"
+            assert all(r[3] > 0 for r in rows if not np.isnan(r[0])), "an environment reported no seeds"
+            gathered_rows = len(ids)
 
     if rank != 0:
         if world > 1:
@@ -587,6 +623,8 @@ def run_ours(args):
 
     h2d = E_local * (sum(f.width * f.height * 4 + 248 for f in frames) + 24 * n_queries)
     d2h = E_local * (48 * (len(frames) + len(prims)) + 16 + 33 * n_queries)
+    if batch is not None:  # per environment: the control block (ks_tsdf_sync), the ESDF report, its 32-byte summary row
+        d2h = E_local * (48 + 16 + 32)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -594,11 +632,16 @@ def run_ours(args):
         "config": config_of(args.workload, scene, world, E_local, n_queries),
         "run": {"blocks_touched": touched_last, "live_blocks": live, "seeds": int(erep.seed_count), "execution": "cuda-graph replay",
                 "l2": "flushed between timed steps (256 MiB memset outside the event pairs); per-step working set ~18 B/cell > 126 MB L2",
-                "collective": "none" if not exchange else "ncclAllGather of 32-byte per-environment summaries each step",
+                "collective": "none" if not exchange else
+                              ("ncclAllGather of 32-byte per-environment summaries, last node of the batch graph (ks_batch_attach_nccl)" if world > 1 and not share_gpu
+                               else "ncclAllGather path not taken on one rank: summaries written by the update, read from the batch buffer"
+                               if world == 1 else "test mode (ranks share one GPU): summaries exchanged through gloo; the multi-GPU run uses ncclAllGather inside the batch graph"),
+                "summary_rows_gathered": gathered_rows, "lanes": None if batch is None else batch.lanes,
                 "state": "steady state: the world's blocks exist (allocated by the warm-up); cold_frame_ms is the first update of a fresh world"},
         "clocks": clocks,
         "e2e": {"value": n_envs * cells * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": 1e3 * e2e_s / args.steps, "path": "blocking ks:: calls: integrate_depth(page-locked host frame, uploaded in place) + stamp_primitive x%d + build_esdf + report" % len(prims)},
+                "ms_per_step": 1e3 * e2e_s / args.steps, "path": ("blocking ks:: calls: integrate_depth(page-locked host frame, uploaded in place) + stamp_primitive x%d + build_esdf + report" % len(prims))
+                        if batch is None else "ks_batch: stage every frame in its pinned slot + ks_batch_update(upload) [H2D inside the graph] + ks_batch_sync (reports + summaries D2H)"},
         "e2e_graph": {"value": E_local * cells * args.steps / e2e_graph_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_graph_s / args.steps,
                       "path": "stage_frame (frame written in the slot's pinned staging area) + upload_frame_async + graph replay + sync/report"},
         "gpu_launches": int(kernel_nodes * args.steps),
@@ -629,6 +672,7 @@ def main():
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOAD_DESC),
                     help="default: cfg2 on one GPU; cfg5env (BASELINE configs[4]) under torchrun with N > 1")
     ap.add_argument("--envs-per-gpu", type=int, default=None, help="independent environments per rank (cfg5env on N > 1 GPUs: 128 / N)")
+    ap.add_argument("--lanes", type=int, default=2, help="streams a batch of environments is dealt onto (ks_batch_create)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args = resolve_workload(args)

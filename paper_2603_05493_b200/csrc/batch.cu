@@ -96,10 +96,9 @@ struct ks_batch {
   int world = 1, rank = 0, max_local = 0;
   void* comm = nullptr;
   bool own_comm = false;
-  cudaGraphExec_t exec = nullptr;  // private graph of one update
-  int exec_upload = -1;
-  int64_t exec_nodes = 0;
-  bool dirty = true;               // inputs changed since the capture
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // private graphs of one update: [0] frames resident, [1] frames uploaded first
+  int64_t exec_nodes[2] = {0, 0};
+  bool dirty = true;                             // inputs changed since the captures
 };
 
 namespace {
@@ -145,10 +144,11 @@ int enqueue_update(ks_batch* b, bool upload) {
   return KS_OK;
 }
 
-void drop_graph(ks_batch* b) {
-  if (b->exec) cudaGraphExecDestroy(b->exec);
-  b->exec = nullptr;
-  b->exec_upload = -1;
+void drop_graphs(ks_batch* b) {
+  for (int k = 0; k < 2; ++k) {
+    if (b->exec[k]) cudaGraphExecDestroy(b->exec[k]);
+    b->exec[k] = nullptr;
+  }
 }
 
 }  // namespace
@@ -217,7 +217,7 @@ void ks_batch_destroy(ks_batch* b) {
   if (b->main) cudaStreamSynchronize(b->main);
   for (size_t l = 1; l < b->lane.size(); ++l)
     if (b->lane[l]) cudaStreamSynchronize(b->lane[l]);
-  drop_graph(b);
+  drop_graphs(b);
   if (b->comm && b->own_comm && nccl().CommDestroy) nccl().CommDestroy(b->comm);
   for (ks_esdf* e : b->esdf) ks_esdf_destroy(e);
   for (ks_tsdf* t : b->tsdf) ks_tsdf_destroy(t);
@@ -290,8 +290,8 @@ int ks_batch_update(ks_batch* b, int32_t upload_frames) {
   cudaStreamIsCapturing(b->main, &cap);
   if (cap != cudaStreamCaptureStatusNone) return enqueue_update(b, upload_frames != 0);  // inside the caller's own capture
   const int up = upload_frames != 0;
-  if (!b->exec || b->dirty || b->exec_upload != up) {
-    drop_graph(b);
+  if (b->dirty) drop_graphs(b), b->dirty = false;
+  if (!b->exec[up]) {
     // first bring every world to its steady shape outside the capture (directory binding, list growth, per-handle
     // attribute setup happen at the first enqueue and are not capturable)
     int rc = enqueue_update(b, up != 0);
@@ -307,22 +307,21 @@ int ks_batch_update(ks_batch* b, int32_t upload_frames) {
       cudaGetLastError();
       return rc != KS_OK ? rc : cuda_fail(end, "batch capture");
     }
-    b->exec_nodes = g_kernel_launches.load() - before;
-    const cudaError_t inst = cudaGraphInstantiate(&b->exec, graph, 0);
+    b->exec_nodes[up] = g_kernel_launches.load() - before;
+    const cudaError_t inst = cudaGraphInstantiate(&b->exec[up], graph, 0);
     cudaGraphDestroy(graph);
     if (inst != cudaSuccess) {
-      b->exec = nullptr;
+      b->exec[up] = nullptr;
       return cuda_fail(inst, "batch graph instantiate");
     }
-    b->exec_upload = up, b->dirty = false;
     return KS_OK;  // the warm-up enqueue above was this call's update
   }
-  KS_CUDA(cudaGraphLaunch(b->exec, b->main));
-  g_kernel_launches.fetch_add(b->exec_nodes, std::memory_order_relaxed);
+  KS_CUDA(cudaGraphLaunch(b->exec[up], b->main));
+  g_kernel_launches.fetch_add(b->exec_nodes[up], std::memory_order_relaxed);
   return KS_OK;
 }
 
-int64_t ks_batch_graph_kernels(const ks_batch* b) { return b && b->exec ? b->exec_nodes : 0; }
+int64_t ks_batch_graph_kernels(const ks_batch* b) { return !b ? 0 : b->exec[0] ? b->exec_nodes[0] : b->exec[1] ? b->exec_nodes[1] : 0; }
 
 int ks_batch_sync(ks_batch* b, ks_tsdf_report* reports, ks_esdf_report* esdf_reports, double* summaries_host) {
   if (!b) return fail(KS_ERR_INVALID, "null batch");

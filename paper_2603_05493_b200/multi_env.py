@@ -18,11 +18,8 @@ SUMMARY_FIELDS = ("env", "min_distance", "colliding", "seeds")  # 4 x float64 = 
 
 def partition_envs(n_envs: int, world: int, rank: int) -> Tuple[int, int]:
     """Contiguous range [lo, hi) of environments owned by `rank`; earlier ranks take the remainder."""
-    if n_envs < 0 or world < 1 or not 0 <= rank < world:
-        raise ValueError("bad partition arguments")
-    base, extra = divmod(n_envs, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+    from . import api
+    return api.partition_envs(n_envs, world, rank)  # ks_partition_envs: the C ABI owns the rule (host code, no device needed)
 
 
 def owner_of(env: int, n_envs: int, world: int) -> int:
