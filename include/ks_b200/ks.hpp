@@ -329,15 +329,27 @@ struct SphereShape {  // sdf_world.hpp:217-220
 };
 using Primitive = std::variant<Cuboid, SphereShape>;
 
+namespace b200_detail {
+inline ks_tsdf_config to_c(const TsdfConfig& config) {
+  return ks_tsdf_config{config.voxel_size, config.truncation, config.alpha_time, config.alpha_frustum,
+                        config.weight_threshold, config.capacity, config.slot_count};
+}
+inline SparseTsdf wrap_tsdf(std::shared_ptr<ks_tsdf> handle, const TsdfConfig& config);
+}  // namespace b200_detail
+
 inline SparseTsdf make_tsdf(const TsdfConfig& config) {  // sdf_world.hpp:327-334
   config.validate();
-  ks_tsdf_config c{config.voxel_size, config.truncation, config.alpha_time, config.alpha_frustum,
-                   config.weight_threshold, config.capacity, config.slot_count};
+  const ks_tsdf_config c = b200_detail::to_c(config);
   ks_tsdf* raw = nullptr;
   b200_detail::check(ks_tsdf_create(&c, &raw));
+  return b200_detail::wrap_tsdf(std::shared_ptr<ks_tsdf>(raw, ks_tsdf_destroy), config);
+}
+
+// the ks::SparseTsdf view (config + host mirrors) of a device world, whoever owns it
+inline SparseTsdf b200_detail::wrap_tsdf(std::shared_ptr<ks_tsdf> handle, const TsdfConfig& config) {
   SparseTsdf tsdf;
   tsdf.config = config;
-  tsdf.handle = std::shared_ptr<ks_tsdf>(raw, ks_tsdf_destroy);
+  tsdf.handle = std::move(handle);
   const std::shared_ptr<ks_tsdf> h = tsdf.handle;
   using Slot = BlockHashTableMirror::Slot;
   tsdf.table.slots = b200_detail::HostMirror<Slot>([h] { return ks_tsdf_generation(h.get()); }, [h](std::vector<Slot>& out) {
@@ -519,18 +531,30 @@ using SeedMask = std::vector<std::uint8_t>;  // esdf.hpp:66
 
 inline double seed_threshold(const SparseTsdf& tsdf) { return 0.9 * tsdf.config.voxel_size; }  // esdf.hpp:69
 
-inline DenseEsdf make_esdf(const EsdfConfig& config) {
-  config.validate();
+namespace b200_detail {
+inline ks_esdf_config to_c(const EsdfConfig& config) {
   ks_esdf_config c{};
   for (int a = 0; a < 3; ++a) c.origin[a] = config.origin[a];
   c.nx = config.nx, c.ny = config.ny, c.nz = config.nz;
   c.voxel_size = config.voxel_size;
   c.seeding = config.seeding == SeedingMode::kGather ? 1 : 0;
+  return c;
+}
+inline DenseEsdf wrap_esdf(std::shared_ptr<ks_esdf> handle, const EsdfConfig& config);
+}  // namespace b200_detail
+
+inline DenseEsdf make_esdf(const EsdfConfig& config) {
+  config.validate();
+  const ks_esdf_config c = b200_detail::to_c(config);
   ks_esdf* raw = nullptr;
   b200_detail::check(ks_esdf_create(&c, &raw));
+  return b200_detail::wrap_esdf(std::shared_ptr<ks_esdf>(raw, ks_esdf_destroy), config);
+}
+
+inline DenseEsdf b200_detail::wrap_esdf(std::shared_ptr<ks_esdf> handle, const EsdfConfig& config) {
   DenseEsdf esdf;
   esdf.config = config;
-  esdf.handle = std::shared_ptr<ks_esdf>(raw, ks_esdf_destroy);
+  esdf.handle = std::move(handle);
   const std::shared_ptr<ks_esdf> h = esdf.handle;
   const std::size_t cells = config.cell_count();
   using Site = std::array<std::int32_t, 3>;
@@ -611,6 +635,94 @@ inline void query_batch(const DenseEsdf& esdf, const std::vector<double>& points
   inside.resize(n);
   b200_detail::check(ks_esdf_query(esdf.get(), points_xyz.data(), n, distance.data(), gradient_xyz.data(), inside.data()));
 }
+
+
+// ---- batched environments (addition: the reference has no batch API; BASELINE configs[4]) ---------------
+/// n independent (SparseTsdf, DenseEsdf) pairs of one configuration, updated by one enqueue / one CUDA graph
+/// (ks_batch_* in ks_b200.h).  tsdf(i) / esdf(i) are ordinary ks:: worlds -- every function above works on them
+/// (query, scene_collision_static, host mirrors ...) -- owned by the batch.
+class EnvironmentBatch {
+ public:
+  struct Summary {  // one row per environment, written by the update itself
+    int env = -1;
+    double min_distance = kInf;  // over the environment's probe points
+    long colliding = 0;          // probes closer than near_distance
+    long seeds = 0;
+  };
+
+  EnvironmentBatch(int n_envs, const TsdfConfig& tsdf_config, const EsdfConfig& esdf_config, int lanes = 4, int first_env = 0) {
+    tsdf_config.validate();
+    esdf_config.validate();
+    const ks_tsdf_config tc = b200_detail::to_c(tsdf_config);
+    const ks_esdf_config ec = b200_detail::to_c(esdf_config);
+    ks_batch* raw = nullptr;
+    b200_detail::check(ks_batch_create(n_envs, &tc, &ec, lanes, &raw));
+    handle_ = std::shared_ptr<ks_batch>(raw, ks_batch_destroy);
+    b200_detail::check(ks_batch_set_first_env(raw, first_env));
+    for (int i = 0; i < n_envs; ++i) {  // aliasing pointers: a world handed out keeps the whole batch alive
+      tsdf_.push_back(b200_detail::wrap_tsdf(std::shared_ptr<ks_tsdf>(handle_, ks_batch_tsdf(raw, i)), tsdf_config));
+      esdf_.push_back(b200_detail::wrap_esdf(std::shared_ptr<ks_esdf>(handle_, ks_batch_esdf(raw, i)), esdf_config));
+    }
+  }
+  int size() const { return static_cast<int>(tsdf_.size()); }
+  ks_batch* get() const { return handle_.get(); }
+  SparseTsdf& tsdf(int env) { return tsdf_.at(static_cast<std::size_t>(env)); }
+  DenseEsdf& esdf(int env) { return esdf_.at(static_cast<std::size_t>(env)); }
+
+  /// the frame camera `slot` of environment `env` integrates at the next update (copied into page-locked staging)
+  void stage_frame(int env, int slot, const DepthFrame& frame) {
+    frame.validate();
+    const ks_camera cam = frame.camera();
+    b200_detail::check(ks_tsdf_stage_frame_slot(tsdf(env).get(), slot, &cam, frame.depth.data()));
+  }
+  void set_inputs(int env, int n_cameras, std::span<const Primitive> primitives, std::span<const DeviceMesh> meshes = {}) {
+    std::vector<ks_primitive> prims(primitives.size());
+    for (std::size_t i = 0; i < primitives.size(); ++i) {
+      ks_primitive& out = prims[i];
+      out = ks_primitive{};
+      if (const auto* cuboid = std::get_if<Cuboid>(&primitives[i])) {
+        out.kind = 0;
+        b200_detail::fill_pose(cuboid->pose, out.pose_R, out.pose_t);
+        for (int a = 0; a < 3; ++a) out.half_extents[a] = cuboid->half_extents[a];
+      } else {
+        const auto& sphere = std::get<SphereShape>(primitives[i]);
+        out.kind = 1;
+        for (int a = 0; a < 3; ++a) out.center[a] = sphere.center[a];
+        out.radius = sphere.radius;
+      }
+    }
+    std::vector<const ks_mesh*> raw;
+    for (const DeviceMesh& m : meshes) raw.push_back(m.handle.get()), meshes_.push_back(m.handle);  // kept alive
+    b200_detail::check(ks_batch_set_inputs(get(), env, n_cameras, prims.data(), static_cast<std::int32_t>(prims.size()), raw.data(),
+                                           static_cast<std::int32_t>(raw.size())));
+  }
+  void set_probes(int env, std::span<const Vec3> points, double near_distance) {
+    std::vector<double> xyz;
+    for (const Vec3& p : points) xyz.insert(xyz.end(), {p[0], p[1], p[2]});
+    b200_detail::check(ks_batch_set_probes(get(), env, xyz.data(), static_cast<std::int64_t>(points.size()), near_distance));
+  }
+  /// one update of every environment through the batch's own graph; returns without waiting
+  void update(bool upload_frames = true) { b200_detail::check(ks_batch_update(get(), upload_frames ? 1 : 0)); }
+  /// wait; throws ValidationError("environment <id>: <the reference's text>") for the first failing environment
+  std::vector<Summary> sync() {
+    std::vector<double> rows(4 * static_cast<std::size_t>(size()));
+    std::vector<ks_esdf_report> ereps(static_cast<std::size_t>(size()));
+    b200_detail::check(ks_batch_sync(get(), nullptr, ereps.data(), rows.data()));
+    std::vector<Summary> out(static_cast<std::size_t>(size()));
+    for (int i = 0; i < size(); ++i) {
+      esdf_[i].has_sites = ereps[i].has_sites != 0, esdf_[i].signs_recovered = ereps[i].signs_recovered != 0;
+      const double* r = &rows[4 * static_cast<std::size_t>(i)];
+      if (r[0] == r[0]) out[i] = Summary{static_cast<int>(r[0]), r[1], static_cast<long>(r[2]), static_cast<long>(r[3])};
+    }
+    return out;
+  }
+
+ private:
+  std::shared_ptr<ks_batch> handle_;
+  std::vector<SparseTsdf> tsdf_;
+  std::vector<DenseEsdf> esdf_;
+  std::vector<std::shared_ptr<ks_mesh>> meshes_;
+};
 
 // ---- collision.hpp, scene part (collision.hpp:30-52, :130-239) ---------------------------------------
 }  // namespace ks

@@ -171,3 +171,32 @@ def test_mixed_program_prints_the_reference_output_on_the_gpu():
         pytest.skip("tests/cpp/_built/mixed_b200 was not prebuilt (needs /root/reference at build time) and no reference tree here")
     out = subprocess.run([str(MIXED_EXE)], check=True, capture_output=True, text=True).stdout
     assert out == MIXED_GOLD.read_text()
+
+
+# ---- ks::EnvironmentBatch (the batch API the reference lacks) against the free functions of the same header ------
+BATCH = ROOT / "tests" / "cpp" / "batch_program.cpp"
+
+
+def _build_batch_program(out: Path):
+    from paper_2603_05493_b200 import build
+    build.build()
+    lib_dir = ROOT / "paper_2603_05493_b200"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{STANDIN}", str(BATCH), "-o", str(out),
+                    f"-L{lib_dir}", "-lks_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+
+
+def test_batch_program_compiles(tmp_path):
+    _build_batch_program(tmp_path / "batch_b200")
+
+
+@pytest.mark.gpu
+def test_batch_program_every_environment_equals_its_own_world(tmp_path):
+    exe = tmp_path / "batch_b200"
+    _build_batch_program(exe)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines()
+    assert len(out) == 4, out
+    for k, line in enumerate(out[:3]):
+        f = line.split()
+        assert f[:4] == ["env", str(100 + k), "same", "1"] and f[4:6] == ["cells", "60000"], line
+        assert f[8:] == ["summary", "1", "1", "1", "flags", "1", "1"], line
+    assert out[3] == "ValidationError: environment 8: tsdf: pool exhausted, frame r"
