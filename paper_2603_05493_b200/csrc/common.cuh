@@ -141,6 +141,7 @@ struct TsdfCtrl {  // device control block, mirrored to pinned host memory on sy
   int abort_prim;       // lowest primitive of the batch with a block outside the key range (0x7FFFFFFF: none)
   int batch_kstar, batch_alloc, batch_status, batch_required, batch_available;  // verdict of the batch in flight
   int batch_stop;       // a group of the call in flight failed: its later groups do nothing
+  int sort_ticket, sort_done;  // large allocations: tiles of new keys handed out / sorted (reset by the op tail)
 };
 
 struct TsdfView {
@@ -157,6 +158,7 @@ struct TsdfView {
   uint8_t* pool_geom;   // [capacity] 1 when the block holds stamped geometry
   TsdfCtrl* ctrl;
   double voxel, trunc, seed_thr;
+  int rank_direct;      // new blocks per call up to which ranks are counted directly (above: sorted tiles)
 };
 
 // BlockHashTable::find (sdf_world.hpp:132-142)

@@ -36,6 +36,8 @@ struct OpLists {  // scratch of the op in flight (discover -> rank -> commit -> 
   int* fresh_idx;      // [cap] indices into key[] of blocks that must be allocated
   int* fresh_rank;     // [cap] rank of that key among the new keys (lexicographic = insertion order)
   uint64_t* rank_key;  // [cap] key of each rank (published before the key claims any slot)
+  uint64_t* sorted_key;  // [cap rounded up to kSortTile] the new keys as sorted tiles (large allocations only, see fresh ranks)
+  uint8_t* sorted_prim;  //   "   first primitive of each (batched stamps; 0 otherwise), 255 = padding
   int cap;
   uint64_t* fset;      // per-frame dedup set, open addressing
   uint32_t fset_mask;  // slots - 1
@@ -344,53 +346,170 @@ __device__ void finalize_slots(const TsdfView& T, const OpLists& L, int n_fresh)
   }
 }
 
-// ---- phase 3: allocation.  One CTA per new block: its rank among the new keys (= its place in the
-// sorted order allocate_keys inserts in, sdf_world.hpp:308-322) is counted by the whole CTA, the pool
-// index follows (free list LIFO first, then fresh), warp 0 claims the key's slot with a
-// warp-cooperative probe (32 slots per step, ballot, one atomicMin; see claim_slot) and the CTA
-// resets the block (VoxelBlock::reset :70-74). ----
+// ---- ranks of the new keys ----
+// A new block's rank is its place in the order the reference inserts in: sorted by key (allocate_keys,
+// sdf_world.hpp:308-322), for a batch of stamps by (first primitive, key).  Up to T.rank_direct (kRankDirect) new keys every CTA counts
+// the smaller ones directly.  Above that (a cold start: tens of thousands of new blocks in one call) the direct count is
+// quadratic, so the kernel first sorts the new keys in tiles of kSortTile -- tiles are handed out by ticket to whichever
+// CTAs are running, a CTA only waits once every ticket is taken, so the wait cannot starve a sorter -- and a rank is the
+// sum of one binary search per tile: n * (n / 1024) * 10 probes instead of n * n comparisons.
+constexpr int kSortTile = 1024;
+constexpr int kRankDirect = 8192;  // default of TsdfView::rank_direct: measured break-even ~12 K new keys (the sort costs ~20 us whatever n)
+constexpr int kRankChunk = 8;  // new blocks a CTA ranks together
+
+__device__ __forceinline__ bool rank_less(int pa, uint64_t ka, int pb, uint64_t kb) { return pa < pb || (pa == pb && ka < kb); }
+
+template <bool kBatch>
+__device__ void sort_fresh_tiles(const TsdfView& T, const OpLists& L, int n, uint64_t* s_k, uint8_t* s_p) {
+  __shared__ int s_ticket;
+  const int ntiles = (n + kSortTile - 1) / kSortTile;
+  const int tid = threadIdx.x;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) s_ticket = atomicAdd(&T.ctrl->sort_ticket, 1);
+    __syncthreads();
+    const int tile = s_ticket;
+    if (tile >= ntiles) break;
+    for (int q = tid; q < kSortTile; q += blockDim.x) {
+      const int j = tile * kSortTile + q;
+      uint64_t k = ~0ull;
+      int p = 255;
+      if (j < n) {
+        const int idx = L.fresh_idx[j];
+        k = L.key[idx];
+        p = kBatch ? __ffs(static_cast<int>(L.fmask[L.slot[idx]])) - 1 : 0;
+      }
+      s_k[q] = k, s_p[q] = static_cast<uint8_t>(p);
+    }
+    for (int span = 2; span <= kSortTile; span <<= 1)  // bitonic network, ascending by (primitive, key)
+      for (int step = span >> 1; step > 0; step >>= 1) {
+        __syncthreads();
+        for (int q = tid; q < kSortTile; q += blockDim.x) {
+          const int other = q ^ step;
+          if (other > q) {
+            const uint64_t ka = s_k[q], kb = s_k[other];
+            const int pa = s_p[q], pb = s_p[other];
+            const bool up = (q & span) == 0;
+            if (rank_less(pb, kb, pa, ka) == up) s_k[q] = kb, s_k[other] = ka, s_p[q] = static_cast<uint8_t>(pb), s_p[other] = static_cast<uint8_t>(pa);
+          }
+        }
+      }
+    __syncthreads();
+    for (int q = tid; q < kSortTile; q += blockDim.x) {
+      L.sorted_key[tile * kSortTile + q] = s_k[q];
+      L.sorted_prim[tile * kSortTile + q] = s_p[q];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(&T.ctrl->sort_done, 1);
+  }
+  if (tid == 0) {
+    while (*reinterpret_cast<volatile int*>(&T.ctrl->sort_done) < ntiles) __nanosleep(200);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Allocation proper, shared by integrate and stamps: a CTA takes kRankChunk new blocks at a time, ranks them, and for each
+// one picks the pool index (free list LIFO first, then fresh), lets warp 0 claim the key's hash slot with a
+// warp-cooperative probe (32 slots per step, ballot, one atomicMin; see claim_slot) and resets the block
+// (VoxelBlock::reset, sdf_world.hpp:70-74).  Blocks whose first primitive is >= kstar are not allocated (batched stamps).
+template <bool kBatch>
+__device__ void allocate_fresh(const TsdfView& T, const OpLists& L, int n, int kstar, int free_count, int next_fresh) {
+  __shared__ uint64_t s_k[kSortTile];
+  __shared__ uint8_t s_p[kSortTile];
+  __shared__ uint64_t s_ckey[kRankChunk];
+  __shared__ int s_cprim[kRankChunk], s_cidx[kRankChunk], s_below[kRankChunk];
+  const int tid = threadIdx.x;
+  const bool direct = n <= T.rank_direct;
+  const int ntiles = (n + kSortTile - 1) / kSortTile;
+  if (!direct) sort_fresh_tiles<kBatch>(T, L, n, s_k, s_p);
+  for (int base = blockIdx.x * kRankChunk; base < n; base += gridDim.x * kRankChunk) {
+    const int m = min(kRankChunk, n - base);
+    __syncthreads();  // the previous chunk is done with the arrays below
+    if (tid < kRankChunk) {
+      s_below[tid] = 0;
+      if (tid < m) {
+        const int idx = L.fresh_idx[base + tid];
+        s_cidx[tid] = idx;
+        s_ckey[tid] = L.key[idx];
+        s_cprim[tid] = kBatch ? __ffs(static_cast<int>(L.fmask[L.slot[idx]])) - 1 : 0;
+      }
+    }
+    __syncthreads();
+    if (direct) {
+      int cnt[kRankChunk];
+#pragma unroll
+      for (int e = 0; e < kRankChunk; ++e) cnt[e] = 0;
+      for (int j = tid; j < n; j += blockDim.x) {
+        const int jdx = L.fresh_idx[j];
+        const uint64_t kj = L.key[jdx];
+        const int pj = kBatch ? __ffs(static_cast<int>(L.fmask[L.slot[jdx]])) - 1 : 0;
+#pragma unroll
+        for (int e = 0; e < kRankChunk; ++e) cnt[e] += e < m && rank_less(pj, kj, s_cprim[e], s_ckey[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < kRankChunk; ++e) {
+        int c = cnt[e];
+        for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xFFFFFFFFu, c, d);
+        if ((tid & 31) == 0 && c) atomicAdd(&s_below[e], c);
+      }
+    } else {
+      for (int pair = tid; pair < m * ntiles; pair += blockDim.x) {  // one binary search per (block, tile)
+        const int e = pair / ntiles, tile = pair - e * ntiles;
+        const uint64_t key = s_ckey[e];
+        const int mine = s_cprim[e];
+        const uint64_t* tk = L.sorted_key + static_cast<size_t>(tile) * kSortTile;
+        const uint8_t* tp = L.sorted_prim + static_cast<size_t>(tile) * kSortTile;
+        int lo = 0, hi = kSortTile;  // first element that is not smaller
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (rank_less(__ldcg(&tp[mid]), __ldcg(&tk[mid]), mine, key)) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo) atomicAdd(&s_below[e], lo);
+      }
+    }
+    __syncthreads();
+    for (int e = 0; e < m; ++e) {
+      const int i = base + e, idx = s_cidx[e];
+      if (s_cprim[e] >= kstar) {  // its primitive is not applied: the block is not allocated
+        if (tid == 0) L.fresh_rank[i] = -1;
+        continue;
+      }
+      const uint64_t key = s_ckey[e];
+      const int r = s_below[e];
+      const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
+      if (tid < 32) {
+        if (tid == 0) {
+          L.fresh_rank[i] = r;
+          L.rank_key[r] = key;
+          L.pool[idx] = pool;
+          T.pool_key[pool] = key;
+          __threadfence();  // the key of a rank is visible before that rank can be seen in a claim
+        }
+        __syncwarp();
+        claim_slot(T, key, static_cast<uint32_t>(r), L.rank_key, tid);
+      }
+      // reset the block: sum = wt = 0, geom = +inf, digest = 0
+      double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
+      double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
+      for (int q = tid; q < kBlockVoxels; q += blockDim.x) {
+        sw[q] = make_double2(0.0, 0.0);
+        g[q] = CUDART_INF;
+      }
+      if (tid < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + tid] = 0;
+      if (tid == 0) T.pool_geom[pool] = 0;
+    }
+  }
+}
+
+// ---- phase 3: allocation of the frame's new blocks (allocate_keys, sdf_world.hpp:307-323) ----
 __global__ void __launch_bounds__(256) k_commit(TsdfView T, OpLists L) {
   pdl_enter();
   if (op_blocked(T)) return;
   const TsdfCtrl* c = T.ctrl;
-  const int n = min(c->fresh, L.cap);
-  const int free_count = c->free_count, next_fresh = c->next_fresh;
-  __shared__ int s_count[8];
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int idx = L.fresh_idx[i];
-    const uint64_t key = L.key[idx];
-    int below = 0;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) below += L.key[L.fresh_idx[j]] < key;
-    for (int d = 16; d > 0; d >>= 1) below += __shfl_down_sync(0xFFFFFFFFu, below, d);
-    __syncthreads();  // s_count free again
-    if ((threadIdx.x & 31) == 0) s_count[threadIdx.x >> 5] = below;
-    __syncthreads();
-    int r = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) r += s_count[w];
-    const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      if (lane == 0) {
-        L.fresh_rank[i] = r;
-        L.rank_key[r] = key;
-        L.pool[idx] = pool;
-        T.pool_key[pool] = key;
-        __threadfence();  // the key of a rank is visible before that rank can be seen in a claim
-      }
-      __syncwarp();
-      claim_slot(T, key, static_cast<uint32_t>(r), L.rank_key, lane);
-    }
-    // reset the block: sum = wt = 0, geom = +inf, digest = 0
-    double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
-    double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
-    for (int q = threadIdx.x; q < kBlockVoxels; q += blockDim.x) {
-      sw[q] = make_double2(0.0, 0.0);
-      g[q] = CUDART_INF;
-    }
-    if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
-    if (threadIdx.x == 0) T.pool_geom[pool] = 0;
-  }
+  allocate_fresh<false>(T, L, min(c->fresh, L.cap), 0x7FFFFFFF, c->free_count, c->next_fresh);
 }
 
 // Op tail, run by the last CTA of the apply kernel: commit the counters or surface the error
@@ -420,6 +539,7 @@ __device__ void finish_op(const TsdfView& T, int list_cap, int is_integrate) {
   c->touched = 0;
   c->fresh = 0;
   c->abort_op = 0;
+  c->sort_ticket = 0, c->sort_done = 0;
 }
 // Every CTA calls this after its last block; the final arrival runs finish_op.
 __device__ __forceinline__ void arrive_and_finish(const TsdfView& T, int list_cap, int is_integrate) {
@@ -640,7 +760,6 @@ __global__ void __launch_bounds__(256) k_batch_commit(TsdfView T, OpLists L, int
   const int n = min(c->fresh, L.cap);
   if (n == 0 && blockIdx.x != 0) return;
   __shared__ int s_hist[kMaxBatch];
-  __shared__ int s_count[8];
   __shared__ BatchVerdict s_v;
   if (threadIdx.x < kMaxBatch) s_hist[threadIdx.x] = 0;
   __syncthreads();
@@ -656,50 +775,7 @@ __global__ void __launch_bounds__(256) k_batch_commit(TsdfView T, OpLists L, int
   }
   __syncthreads();
   const BatchVerdict v = s_v;
-  const int free_count = c->free_count, next_fresh = c->next_fresh;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int idx = L.fresh_idx[i];
-    const uint64_t key = L.key[idx];
-    const int mine = first_prim(L, idx);
-    if (mine >= v.kstar) {  // its primitive is not applied: the block is not allocated
-      if (threadIdx.x == 0) L.fresh_rank[i] = -1;
-      continue;
-    }
-    int below = 0;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const int jdx = L.fresh_idx[j];
-      const int fj = first_prim(L, jdx);
-      below += fj < mine || (fj == mine && L.key[jdx] < key);
-    }
-    for (int d = 16; d > 0; d >>= 1) below += __shfl_down_sync(0xFFFFFFFFu, below, d);
-    __syncthreads();  // s_count free again
-    if ((threadIdx.x & 31) == 0) s_count[threadIdx.x >> 5] = below;
-    __syncthreads();
-    int r = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) r += s_count[w];
-    const int pool = r < free_count ? T.free_list[free_count - 1 - r] : next_fresh + (r - free_count);
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      if (lane == 0) {
-        L.fresh_rank[i] = r;
-        L.rank_key[r] = key;
-        L.pool[idx] = pool;
-        T.pool_key[pool] = key;
-        __threadfence();  // the key of a rank is visible before that rank can be seen in a claim
-      }
-      __syncwarp();
-      claim_slot(T, key, static_cast<uint32_t>(r), L.rank_key, lane);
-    }
-    double2* sw = T.sumwt + static_cast<size_t>(pool) * kBlockVoxels;
-    double* g = T.geom + static_cast<size_t>(pool) * kBlockVoxels;
-    for (int q = threadIdx.x; q < kBlockVoxels; q += blockDim.x) {
-      sw[q] = make_double2(0.0, 0.0);
-      g[q] = CUDART_INF;
-    }
-    if (threadIdx.x < kDigestWords) T.digest[static_cast<size_t>(pool) * kDigestWords + threadIdx.x] = 0;
-    if (threadIdx.x == 0) T.pool_geom[pool] = 0;
-  }
+  allocate_fresh<true>(T, L, n, v.kstar, c->free_count, c->next_fresh);
 }
 
 __device__ void finish_batch(const TsdfView& T, int last_group) {
@@ -717,6 +793,7 @@ __device__ void finish_batch(const TsdfView& T, int last_group) {
   c->touched = 0;
   c->fresh = 0;
   c->abort_prim = 0x7FFFFFFF;
+  c->sort_ticket = 0, c->sort_done = 0;
 }
 
 // Voxels of a batch: one CTA per touched block, the per-voxel min (sdf_world.hpp:437-443) over the applied
@@ -1078,7 +1155,7 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset), cudaFree(L.fmask);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.sorted_key), cudaFree(L.sorted_prim), cudaFree(L.fset), cudaFree(L.fmask);
   L.cap = static_cast<int>(want);
   KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
@@ -1086,6 +1163,9 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
   KS_CUDA(cudaMalloc(&L.fresh_idx, want * sizeof(int)));
   KS_CUDA(cudaMalloc(&L.fresh_rank, want * sizeof(int)));
   KS_CUDA(cudaMalloc(&L.rank_key, want * sizeof(uint64_t)));
+  const size_t tiles = (want + kSortTile - 1) / kSortTile * kSortTile;
+  KS_CUDA(cudaMalloc(&L.sorted_key, tiles * sizeof(uint64_t)));
+  KS_CUDA(cudaMalloc(&L.sorted_prim, tiles));
   uint32_t slots = 1u << 16;
   while (slots < 2 * want) slots <<= 1;
   L.fset_mask = slots - 1;
@@ -1323,6 +1403,8 @@ static int tsdf_init(ks_tsdf* t, const ks_tsdf_config* cfg) {
   V.voxel = cfg->voxel_size;
   V.trunc = cfg->truncation;
   V.seed_thr = 0.9 * cfg->voxel_size;  // seed_threshold (esdf.hpp:69)
+  V.rank_direct = kRankDirect;
+  if (const char* v = std::getenv("KS_RANK_DIRECT")) V.rank_direct = std::max(0, std::atoi(v));  // tests: force the sorted-tile ranks
   const size_t cap = static_cast<size_t>(cfg->capacity);
   KS_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
   t->own_stream = true;
@@ -1365,7 +1447,7 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.slot_key), cudaFree(V.slot_pool), cudaFree(V.slot_claim), cudaFree(V.free_list), cudaFree(V.pool_key);
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.fset), cudaFree(L.fmask);
+  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.sorted_key), cudaFree(L.sorted_prim), cudaFree(L.fset), cudaFree(L.fmask);
   cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
   cudaFreeHost(t->h_verdict);
