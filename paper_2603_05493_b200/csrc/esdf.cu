@@ -94,6 +94,7 @@ struct EsdfView {
   uint2* field;      // wide path: [cells] y-fastest: {site (x | y << 10 | z << 20), squared distance | sign << 31}
   // fast path
   int fast;          // 1: the field is f32[ctrl->front], phase 2's result is gimg / himg
+  int xpay;          // 1: gimg words are Keys<1> (in-plane d2 << 11 | x << 1 | the site has a sign table), 0: Keys<0>
   uint32_t* zgbits;  // like zbits, for gbits: bit b of word w = the seed at z = 32w + b has a sign table
   uint32_t* gimg;    // [nzt][nyt][nx][32 rows] the x sweep's tiles as they sit in shared memory: row = (y & 7) + 8 (z & 3),
                      //   word = in-plane d2 << 10 | x  (KeysX candidate; none_x << 10 | x without candidate)
@@ -1080,7 +1081,7 @@ constexpr int kTopShiftY = 4, kTopShiftX = 3;
 constexpr int kTileA = 8, kTileZ = 4;
 
 template <int kPay, int kTopShift>
-__device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, int n, int warp, int lane, int warps_log2) {
+__device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, int n, int warp, int lane, int nwarps, int warps_log2) {
   constexpr int kTopStep = 1 << kTopShift;
   const edt_dc::Plan plan = edt_dc::make_plan(n);
   for (int level = 0; level < plan.levels; ++level) {
@@ -1088,7 +1089,7 @@ __device__ __forceinline__ void dc_top_levels(const uint32_t* G, uint32_t* Kt, i
     if (s < kTopStep) break;
     const int parts_log2 = warps_log2 > level ? warps_log2 - level : 0;
     const int items = edt_dc::level_visits(plan, level) << parts_log2;
-    for (int item = warp; item < items; item += 1 << warps_log2) {
+    for (int item = warp; item < items; item += nwarps) {
       const int tp = s * (2 * (item >> parts_log2) + 1);
       int lo, len;
       edt_dc::top_window<kPay>(Kt, n, kTopShift, tp, s, item & ((1 << parts_log2) - 1), parts_log2, lane, lo, len);
@@ -1118,8 +1119,8 @@ __device__ __forceinline__ void dc_stretch_into(const uint32_t* G, const uint32_
 
 static size_t dc_top_bytes(int n, int top_shift) { return static_cast<size_t>((n >> top_shift) + 1) * 32 * sizeof(uint32_t); }
 static size_t dc_smem_bytes_y(int n) { return static_cast<size_t>(n) * 32 * sizeof(uint32_t) + dc_top_bytes(n, kTopShiftY); }
-static size_t dc_smem_bytes_x(int n, int total) {  // G (u32), H (u16), Kt and the per-axis fraction table of the sign tables
-  return static_cast<size_t>(n) * 32 * (sizeof(uint32_t) + sizeof(uint16_t)) + dc_top_bytes(n, kTopShiftX) + static_cast<size_t>(total) * sizeof(float);
+static size_t dc_smem_bytes_x(int n, int total, bool with_h = true) {  // G (u32), H (u16, kPX = 0), Kt and the per-axis fraction table of the sign tables
+  return static_cast<size_t>(n) * 32 * (sizeof(uint32_t) + (with_h ? sizeof(uint16_t) : 0)) + dc_top_bytes(n, kTopShiftX) + static_cast<size_t>(total) * sizeof(float);
 }
 
 // root of a perfect square below 2^24 (one MUFU; its error of a few ulp cannot reach the next integer)
@@ -1135,12 +1136,13 @@ __device__ __forceinline__ int exact_root(int sq) {
 // himg): a lane's 8 consecutive y of one x-sweep tile are 8 consecutive words, so a stretch of 16 positions leaves as
 // four 16-byte stores of candidates + two of payload, and the x sweep fills its tile with two bulk copies.
 constexpr int kLoadBatch = 8;
-template <int kPay>
+template <int kPay, int kPX>
 __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, uint32_t none_y, uint32_t none_x) {
   pdl_enter();
   using KY = edt_dc::Keys<kPay>;
+  using KX = edt_dc::Keys<kPX>;  // kPX = 1: phase 3's candidate carries "site has a sign table" below its position
   extern __shared__ __align__(16) unsigned char s_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;  // any warp count; windows are cut into 2^warps_log2 slices
   const int x = blockIdx.x * kTileA + (lane & (kTileA - 1)), z = blockIdx.y * kTileZ + lane / kTileA;
   const int ny = E.ny, nx = E.nx;
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
@@ -1183,7 +1185,7 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   }
   for (int i = warp; i <= ny >> kTopShiftY; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   __syncthreads();
-  dc_top_levels<kPay, kTopShiftY>(G, Kt, ny, warp, lane, warps_log2);
+  dc_top_levels<kPay, kTopShiftY>(G, Kt, ny, warp, lane, nwarps, warps_log2);
   // tile images: tile (yt, zt = blockIdx.y), position x, row (y & 7) + 8 (z & 3) = yy + 8 zz
   const size_t zt_base = static_cast<size_t>(blockIdx.y) * E.nyt;
   const int zz = lane / kTileA;
@@ -1203,8 +1205,8 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
         const uint32_t k = keys.k[8 * h + i];
         const uint32_t c = KY::cost(k);
         const bool none = c >= none_y;
-        gw[i] = KeysX::pack(none ? none_x : c, x, 0);
         const uint32_t low = k & KY::kLowMask;  // site_y and the payload
+        gw[i] = none ? KX::pack(none_x, x, 0) : KX::pack(c, x, kPX ? (kPay == 2 ? (low & 1u) : 1u) : 0u);
         hw[i] = none ? 0u : (kPay == 2 ? low : (low << 1 | 1u));
       }
       const size_t at = ((zt_base + yt) * nx + x) * 32 + 8 * zz;
@@ -1243,8 +1245,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // site_y, site_z of the winner `u` of row (y, z) from a tile image word pair (gimg / himg or their shared-memory copies)
+template <int kPX>
 __device__ __forceinline__ void decode_site(uint32_t gword, uint32_t hword, int y, int z, int& sy, int& sz) {
-  const int r2 = static_cast<int>(KeysX::cost(gword));
+  const int r2 = static_cast<int>(edt_dc::Keys<kPX>::cost(gword));
   sy = static_cast<int>(hword >> 2);
   const int dy = y - sy;
   const int dz = exact_root(r2 - dy * dy);
@@ -1259,27 +1262,33 @@ __device__ __forceinline__ void decode_site(uint32_t gword, uint32_t hword, int 
 // table fetch; only cells whose site lies next to stamped geometry go through the probe.  One lane stores its 8
 // cells with two 16-byte stores (x-fastest field).
 // kBig: rows so long that only one tile fits an SM -- then the tile gets 32 warps instead of 16
-template <int kSigns, bool kBig>
+// kPX = 1 (whenever the keys have a spare bit): the candidate word itself says whether its site has a sign table, so the
+// payload image H is not staged at all -- the tile is G alone (a third less shared memory: three tiles per SM at
+// cfg2 instead of two), a position costs no H lookup, and only the few cells next to stamped geometry fetch their
+// site's payload word from the image in L2.
+template <int kSigns, bool kBig, int kPX>
 __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(EsdfView E, TsdfView Tw, int warps_log2, uint32_t none_x) {
+  using KX = edt_dc::Keys<kPX>;
   pdl_wait();
   extern __shared__ __align__(128) unsigned char s_raw[];
   __shared__ __align__(8) uint64_t s_bar;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 1 << warps_log2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int y0 = blockIdx.x * kTileA, z0 = blockIdx.y * kTileZ;
   const int nx = E.nx, ny = E.ny;
   uint32_t* G = reinterpret_cast<uint32_t*>(s_raw);
-  uint16_t* H = reinterpret_cast<uint16_t*>(G + nx * 32);
-  uint32_t* Kt = reinterpret_cast<uint32_t*>(H + nx * 32);
+  uint16_t* H = reinterpret_cast<uint16_t*>(G + nx * 32);  // kPX = 0 only
+  uint32_t* Kt = kPX ? G + nx * 32 : reinterpret_cast<uint32_t*>(H + nx * 32);
   constexpr int kTopShift = kTopShiftX, kTopStep = 1 << kTopShift;
   float* s_qsf = reinterpret_cast<float*>(Kt + ((nx >> kTopShift) + 1) * 32);
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
+  const size_t tile = static_cast<size_t>(blockIdx.y) * E.nyt + blockIdx.x;
+  const uint16_t* Hsrc = kPX ? E.himg + tile * nx * 32 : H;  // where a slow cell reads its site's payload word
   if (threadIdx.x == 0) {
-    const size_t tile = static_cast<size_t>(blockIdx.y) * E.nyt + blockIdx.x;
-    const uint32_t gbytes = static_cast<uint32_t>(nx) * 32u * 4u, hbytes = static_cast<uint32_t>(nx) * 32u * 2u;
+    const uint32_t gbytes = static_cast<uint32_t>(nx) * 32u * 4u, hbytes = kPX ? 0u : static_cast<uint32_t>(nx) * 32u * 2u;
     mbar_expect_tx(&s_bar, gbytes + hbytes);
     bulk_g2s(G, E.gimg + tile * nx * 32, gbytes, &s_bar);
-    bulk_g2s(H, E.himg + tile * nx * 32, hbytes, &s_bar);
+    if (!kPX) bulk_g2s(H, E.himg + tile * nx * 32, hbytes, &s_bar);
   }
   for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   if constexpr (kSigns == 3)
@@ -1287,7 +1296,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   const int back = 1 - E.ctrl->front;
   mbar_wait(&s_bar, 0);
   __syncthreads();
-  dc_top_levels<0, kTopShift>(G, Kt, nx, warp, lane, warps_log2);
+  dc_top_levels<kPX, kTopShift>(G, Kt, nx, warp, lane, nwarps, warps_log2);
   const int y = min(y0 + (lane & (kTileA - 1)), ny - 1), z = min(z0 + lane / kTileA, E.nz - 1);
   const bool live = y0 + (lane & (kTileA - 1)) < ny && z0 + lane / kTileA < E.nz;
   auto make_probe = [&]() {
@@ -1305,7 +1314,7 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
     edt_dc::KeySink<8> keys;
 #pragma unroll
     for (int i = 0; i < 8; ++i) keys.k[i] = 0xFFFFFFFFu;
-    dc_stretch_into<0, kTopShift>(G, Kt, nx, j, lane, keys);
+    dc_stretch_into<kPX, kTopShift>(G, Kt, nx, j, lane, keys);
     if (!live) continue;
     uint32_t w[8];
     uint32_t slow = 0;  // positions that need the site: bit i
@@ -1315,24 +1324,26 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint32_t k = keys.k[i];
-        const bool none = KeysX::cost(k) >= none_x;  // the grid holds no seed at all
-        const uint32_t h = H[edt_dc::at(none ? 0 : KeysX::winner(k), lane)];  // (a position beyond the row carries key ~0)
-        w[i] = none ? 0xFFFFFFFFu : (k | ((own >> i) & 1u) << 31);
-        slow |= (none ? 0u : (h & 1u)) << i;
+        const bool none = KX::cost(k) >= none_x;  // the grid holds no seed at all
+        uint32_t table;  // the winner's site has a sign table
+        if constexpr (kPX) table = k & 1u;
+        else table = H[edt_dc::at(none ? 0 : KX::winner(k), lane)] & 1u;  // (a position beyond the row carries key ~0)
+        w[i] = none ? 0xFFFFFFFFu : ((k >> kPX) | ((own >> i) & 1u) << 31);
+        slow |= (none ? 0u : table) << i;
       }
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const bool none = KeysX::cost(keys.k[i]) >= none_x;
-        w[i] = none ? 0xFFFFFFFFu : keys.k[i];
+        const bool none = KX::cost(keys.k[i]) >= none_x;
+        w[i] = none ? 0xFFFFFFFFu : keys.k[i] >> kPX;
         if (kSigns != 0 && !none) slow |= 1u << i;
       }
     }
     if (slow != 0) {  // cells whose site may resolve a geometry probe: the reference's decision from the site's table / the directory
       // the eight winners, 10 bits each, in three registers (a run-time index into keys.k would put it in local memory)
-      const uint32_t p0 = (keys.k[0] & 1023u) | (keys.k[1] & 1023u) << 10 | (keys.k[2] & 1023u) << 20;
-      const uint32_t p1 = (keys.k[3] & 1023u) | (keys.k[4] & 1023u) << 10 | (keys.k[5] & 1023u) << 20;
-      const uint32_t p2 = (keys.k[6] & 1023u) | (keys.k[7] & 1023u) << 10;
+      const uint32_t p0 = (w[0] & 1023u) | (w[1] & 1023u) << 10 | (w[2] & 1023u) << 20;
+      const uint32_t p1 = (w[3] & 1023u) | (w[4] & 1023u) << 10 | (w[5] & 1023u) << 20;
+      const uint32_t p2 = (w[6] & 1023u) | (w[7] & 1023u) << 10;
       uint32_t flip = 0;
       int last = -1;
       for (uint32_t m = slow; m != 0; m &= m - 1) {
@@ -1343,7 +1354,8 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
         if (u != last) {
           last = u;
           int sy, sz;
-          decode_site(G[edt_dc::at(u, lane)], H[edt_dc::at(u, lane)], y, z, sy, sz);
+          const uint32_t hword = kPX ? __ldg(Hsrc + edt_dc::at(u, lane)) : Hsrc[edt_dc::at(u, lane)];
+          decode_site<kPX>(G[edt_dc::at(u, lane)], hword, y, z, sy, sz);
           if constexpr (kSigns == 3) probe.set_site(u, sy, sz, __ldg(E.gtab + (u + nx * (sy + ny * sz))));
           else if constexpr (kSigns != 0) probe.template set_site<kSigns == 2>(u, sy, sz);
         }
@@ -1392,7 +1404,8 @@ __device__ __forceinline__ const uint32_t* front_field(const EsdfView& E) {  // 
 __device__ __forceinline__ void fast_site(const EsdfView& E, uint32_t w, int y, int z, int& sx, int& sy, int& sz) {
   sx = static_cast<int>(w & 1023u);
   const size_t at = ((static_cast<size_t>(z >> 2) * E.nyt + (y >> 3)) * E.nx + sx) * 32 + (y & 7) + 8 * (z & 3);
-  decode_site(E.gimg[at], E.himg[at], y, z, sy, sz);
+  if (E.xpay) decode_site<1>(E.gimg[at], E.himg[at], y, z, sy, sz);
+  else decode_site<0>(E.gimg[at], E.himg[at], y, z, sy, sz);
 }
 
 // ---- recover_signs as its own pass (esdf.hpp:288-320), for the stage-by-stage API (no hints) ----
@@ -1754,7 +1767,8 @@ struct ks_esdf {
   int64_t build_nodes;
   bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
-  int dc_wl_y, dc_wl_x;    // log2(warps per tile)
+  int dc_wl_y, dc_wl_x;    // floor(log2(warps per tile)): slices a top-level window is cut into
+  int dc_nw_y, dc_nw_x;    // warps per tile
   int pay_y;               // payload bits of the y keys: 2 = {seed above z, site has a sign table}, 1 = the first only
   uint32_t none_y, none_x; // offsets of positions without candidate
   int sticky_err;
@@ -1940,8 +1954,10 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
   if (e->dc) {
     const dim3 ygrid((E.nx + kTileA - 1) / kTileA, (E.nz + kTileZ - 1) / kTileZ);
-    if (e->pay_y == 2) KS_LAUNCH(k_sweep_y_dc<2>, ygrid, 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y, e->none_x);
-    else KS_LAUNCH(k_sweep_y_dc<1>, ygrid, 32 << e->dc_wl_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y, e->none_x);
+#define KS_Y_DC(P, X) KS_LAUNCH((k_sweep_y_dc<P, X>), ygrid, 32 * e->dc_nw_y, e->smem_y, e->stream, E, e->dc_wl_y, e->none_y, e->none_x)
+    if (e->pay_y == 2) { if (E.xpay) KS_Y_DC(2, 1); else KS_Y_DC(2, 0); }
+    else { if (E.xpay) KS_Y_DC(1, 1); else KS_Y_DC(1, 0); }
+#undef KS_Y_DC
   } else KS_LAUNCH(k_sweep_y, dim3((E.nx + 31) / 32, E.nz), 32 * e->bands_y, e->smem_y, e->stream, E, e->band_y, e->bands_y);
   if (e->profile_stages) cudaEventRecord(e->ev[4], e->stream);
   if (e->side_pending) {  // the site tables must be complete before the sweep that reads them
@@ -1950,17 +1966,24 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   }
   const dim3 xgrid((E.ny + 31) / 32, E.nz);
   if (e->dc) {
-    const unsigned threads = 32u << e->dc_wl_x;
+    const unsigned threads = 32u * e->dc_nw_x;
     const int mode = t && bits && fast_build(e) ? 3 : (t && bits ? 2 : (t ? 1 : 0));
     const TsdfView tv = t ? tsdf_view(t) : TsdfView{};
     const dim3 xgrid(E.nyt, E.nzt);
-#define KS_X_DC(M, B) KS_LAUNCH((k_sweep_x_dc<M, B>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_x)
+#define KS_X_DC(M, B) KS_LAUNCH((k_sweep_x_dc<M, B, 0>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_x)
+#define KS_X_DC1(M) KS_LAUNCH((k_sweep_x_dc<M, false, 1>), xgrid, threads, e->smem_x, e->stream, E, tv, e->dc_wl_x, e->none_x)
 #define KS_X_DC_MODE(B)        \
   if (mode == 3) KS_X_DC(3, B);      \
   else if (mode == 2) KS_X_DC(2, B); \
   else if (mode == 1) KS_X_DC(1, B); \
   else KS_X_DC(0, B)
-    if (e->dc_wl_x == 5) { KS_X_DC_MODE(true); } else { KS_X_DC_MODE(false); }
+    if (E.xpay) {
+      if (mode == 3) KS_X_DC1(3);
+      else if (mode == 2) KS_X_DC1(2);
+      else if (mode == 1) KS_X_DC1(1);
+      else KS_X_DC1(0);
+    } else if (e->dc_nw_x > 16) { KS_X_DC_MODE(true); } else { KS_X_DC_MODE(false); }
+#undef KS_X_DC1
 #undef KS_X_DC_MODE
 #undef KS_X_DC
   } else if (t && bits) {  // hint planes are fresh only when this build gathered into the bit planes
@@ -2044,7 +2067,33 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
     e->dc_wl_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) > 113 * 1024 ? 5 : 4;
     if (const char* v = std::getenv("KS_DC_WARPS_Y")) e->dc_wl_y = std::min(4, std::max(0, std::atoi(v)));
     if (const char* v = std::getenv("KS_DC_WARPS_X")) e->dc_wl_x = std::min(5, std::max(0, std::atoi(v)));
-    if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz);
+    e->dc_nw_y = 1 << e->dc_wl_y, e->dc_nw_x = 1 << e->dc_wl_x;
+    // x sweep with the table bit inside the candidate (no payload image in shared memory) whenever the keys have the bit to spare
+    E.xpay = e->dc && edt_dc::Keys<1>::fits(E.nx, gmax_x) ? 1 : 0;
+    if (const char* v = std::getenv("KS_XPAY")) E.xpay = E.xpay && std::atoi(v) != 0;
+    if (E.xpay) {
+      // tiles per SM by shared memory, warps per tile so that tiles x warps stays within the 32 warps 64 registers allow,
+      // preferring a count that deals the row's stretches out evenly (score = resident warps x (1 + evenness) / 2)
+      const size_t bytes = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz, false) + 1024;
+      const int stretches = (E.nx + (1 << kTopShiftX) - 1) >> kTopShiftX;
+      double best = 0.0;
+      for (int tiles = 1; tiles <= 4; ++tiles) {
+        if (tiles * bytes > 227 * 1024) break;
+        const int wmax = std::min(16, 32 / tiles);
+        for (int w = std::max(4, wmax - 3); w <= wmax; ++w) {
+          const double even = static_cast<double>(stretches) / (w * ((stretches + w - 1) / w));
+          const double score = tiles * w * (1.0 + even) / 2.0;
+          if (score > best) best = score, e->dc_nw_x = w;
+        }
+      }
+    }
+    // any warp count works (KS_DC_NWARPS_*): the stretches of a row are dealt round-robin to the warps, so a count that
+    // divides them evenly leaves no warp idle at the end of a tile
+    auto floor_log2 = [](int v) { int l = 0; while ((2 << l) <= v) ++l; return l; };
+    if (const char* v = std::getenv("KS_DC_NWARPS_Y")) e->dc_nw_y = std::min(16, std::max(1, std::atoi(v))), e->dc_wl_y = floor_log2(e->dc_nw_y);
+    if (const char* v = std::getenv("KS_DC_NWARPS_X")) e->dc_nw_x = std::min(E.xpay ? 16 : 32, std::max(1, std::atoi(v)));
+    e->dc_wl_x = floor_log2(e->dc_nw_x);
+    if (e->dc) e->smem_y = dc_smem_bytes_y(E.ny), e->smem_x = dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz, !E.xpay);
   }
   if (e->smem_y > 227 * 1024 || e->smem_x > 227 * 1024) {
     return fail(KS_ERR_UNSUPPORTED, "esdf: row length exceeds the shared-memory tile of this build (ny <= 1024, nx <= 900)");
@@ -2056,12 +2105,17 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_sweep_x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
-  KS_CUDA(cudaFuncSetAttribute(k_sweep_y_dc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute((k_sweep_y_dc<1, 0>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute((k_sweep_y_dc<2, 0>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute((k_sweep_y_dc<1, 1>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
+  KS_CUDA(cudaFuncSetAttribute((k_sweep_y_dc<2, 1>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn));
   KS_CUDA(cudaFuncSetAttribute(k_flood_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-#define KS_X_ATTR(M, B) KS_CUDA(cudaFuncSetAttribute(k_sweep_x_dc<M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
+#define KS_X_ATTR(M, B) KS_CUDA(cudaFuncSetAttribute((k_sweep_x_dc<M, B, 0>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
 #define KS_X_ATTR4(B) KS_X_ATTR(0, B); KS_X_ATTR(1, B); KS_X_ATTR(2, B); KS_X_ATTR(3, B)
   KS_X_ATTR4(false); KS_X_ATTR4(true);
+#define KS_X_ATTR1(M) KS_CUDA(cudaFuncSetAttribute((k_sweep_x_dc<M, false, 1>), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptIn))
+  KS_X_ATTR1(0); KS_X_ATTR1(1); KS_X_ATTR1(2); KS_X_ATTR1(3);
+#undef KS_X_ATTR1
 #undef KS_X_ATTR4
 #undef KS_X_ATTR
   KS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
