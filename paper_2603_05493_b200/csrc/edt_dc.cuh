@@ -74,9 +74,14 @@ struct Plan {
 KS_DC_HD Plan make_plan(int n) {
   Plan p;
   p.n = n;
+#if defined(__CUDA_ARCH__)
+  p.levels = 32 - __clz(n);  // smallest power of two > n, without the loop (n >= 1)
+  p.P = 1 << p.levels;
+#else
   p.P = 1;
   p.levels = 0;
   while (p.P <= n) p.P <<= 1, ++p.levels;
+#endif
   return p;
 }
 KS_DC_HD int level_step(const Plan& p, int level) { return p.P >> (level + 1); }

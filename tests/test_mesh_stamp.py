@@ -235,3 +235,60 @@ def test_config4_mixed_scene_full_size_against_the_restatement(oracle):
     c = np.array([0.35, 0.8, 0.7])
     inside = api.query(e, np.array([c, c + [0.0, 0.0, 0.2]]))
     assert inside.distance[0] < 0 < inside.distance[1]
+
+
+# ---- an independent checker on non-convex meshes (tests/mesh_independent.py: segment-clamp distance + winding-number sign) ----
+def _nonconvex_cases():
+    import mesh_independent as mi
+    return {"torus": mi.torus((0.4, 0.4, 0.3), 0.2, 0.07), "l_prism": mi.l_prism((0.15, 0.2, 0.1))}
+
+
+@pytest.mark.parametrize("name", ["torus", "l_prism"])
+def test_restatement_agrees_with_the_independent_checker_on_nonconvex_meshes(oracle, name):
+    """Different distance algorithm, different sign principle (tests/mesh_independent.py), same answer: magnitudes
+    to 1e-12, signs everywhere except within 1e-9 of the surface."""
+    import mesh_independent as mi
+    verts, tris = _nonconvex_cases()[name]
+    rng = np.random.RandomState(11)
+    lo, hi = verts.min(axis=0) - 0.15, verts.max(axis=0) + 0.15
+    pts = lo + rng.random_sample((6000, 3)) * (hi - lo)
+    d = oracle.mesh_sdf(verts, tris, pts)
+    ref, wind = mi.signed_distance(verts, tris, pts)
+    assert np.abs(np.minimum(np.abs(wind - 1.0), np.abs(wind))).max() < 1e-6, "the test mesh is not closed / consistently oriented"
+    np.testing.assert_allclose(np.abs(d), np.abs(ref), rtol=0, atol=1e-12)
+    off = np.abs(ref) > 1e-9
+    assert np.array_equal(d[off] < 0, ref[off] < 0)
+    assert (ref < 0).sum() > 100 and (ref > 0).sum() > 100
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["torus", "l_prism"])
+def test_gpu_stamp_of_nonconvex_meshes_against_the_independent_checker(name):
+    """ks_tsdf_stamp_mesh on a torus and an L-shaped prism: every stamped voxel's geometry value equals the independent
+    signed distance at its centre (1e-12; sign included), blocks = those whose centre lies within truncation + block radius."""
+    import mesh_independent as mi
+    from paper_2603_05493_b200 import api
+    verts, tris = _nonconvex_cases()[name]
+    voxel = 0.01
+    cfg = api.make_tsdf_config(voxel)
+    cfg.capacity = 8192
+    t = api.make_tsdf(cfg)
+    api.stamp_mesh(t, api.TriangleMesh(verts, tris))
+    keys, pools = t.export_blocks()
+    assert len(keys) > 200
+    _, _, geom = t.download_blocks(pools)
+    idx = np.arange(512)
+    local = np.stack([idx & 7, (idx >> 3) & 7, idx >> 6], axis=1)
+    rng = np.random.RandomState(5)
+    pick = rng.choice(len(keys), size=min(len(keys), 120), replace=False)
+    centres = np.concatenate([((keys[k][None, :] * 8 + local) + 0.5) * voxel for k in pick])
+    ref, _ = mi.signed_distance(verts, tris, centres)
+    got = geom[pick].reshape(-1)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12)
+    off = np.abs(ref) > 1e-9
+    assert np.array_equal(np.signbit(got[off]), ref[off] < 0)
+    # candidate rule (stamp_primitive's, sdf_world.hpp:425-431): |sdf(block centre)| <= truncation + half the block diagonal
+    bc = (keys * 8 + 4.0) * voxel
+    dref, _ = mi.signed_distance(verts, tris, bc)
+    reach = cfg.truncation + 0.5 * 8 * voxel * np.sqrt(3.0)
+    assert (np.abs(dref) <= reach + 1e-12).all()
