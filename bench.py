@@ -233,7 +233,7 @@ def algorithmic_bytes(stage: str, C_: int, P: int, K: int, Kp: int, L: int, dcou
         "seed": 3.0 * C_ / 8.0 + 6.0 * C_ / 8.0 + 2.0 * C_ / 8.0 + 128.0 * L + 5.0 * dcount,  # 3 resampled planes out; 5 rows + near row in, seed + near planes out; digest rows + directory in
         "flood_z": 2.0 * C_ / 8.0 + 3.0 * C_ / 8.0,                   # seed + table bit planes in; column bit strings (seeds, tables) + per-word info out
         "sweep_y": 3.0 * C_ / 8.0 + 6.0 * C_,                         # column words + info in; tile images out: candidate u32 + payload u16
-        "sweep_x": 6.0 * C_ + 4.0 * C_ + C_ / 8.0,                    # tile images in (u32 + u16), field word u32 out, own-sign plane
+        "sweep_x": 4.0 * C_ + 4.0 * C_ + C_ / 8.0,                    # candidate image in (u32; the u16 payload image is only touched next to stamped geometry), field word u32 out, own-sign plane
         "signs": 0.0,                                                 # fused into sweep_x
     }[stage]
 
@@ -592,6 +592,8 @@ def run_ours(args):
     if traffic_path.exists():
         traffic = json.loads(traffic_path.read_text()).get(args.workload, {}).get(dominant)
     update_bytes = sum(stage_bytes[s] * (len(frames) if s in ("discover", "allocate", "integrate") else 1) for s in kernel_stages)
+    survey_bytes = (len(frames) * 4.0 * (pixels / max(1, len(frames))) + 2 * 16 * 512 * K * len(frames) + 2 * 8 * 512 * max(live - K, 0)
+                    + 30.0 * cells + 16384.0 * live + 20.0 * 2 * scene.capacity)
     stage_bytes["stamp_candidates"] = 0.0
     if n_queries:
         stage_bytes["query"] = 89.0 * n_queries  # 24 B in + 33 B out + 8 gathers of 4 B
@@ -654,8 +656,11 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": stage_bytes[dominant],
                      "update_bytes": update_bytes, "update_frac_of_peak": update_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
+                     # SURVEY.md 8(d)'s formulas with ITS assumed formats (byte mask, 4-byte site + f32 distance fields, 21 B/cell of propagate passes):
+                     "survey_update_bytes": survey_bytes, "survey_update_frac_of_peak": survey_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
                      "note": "HBM is the nominal roof of every stage (no contraction on this path), but the sweeps are "
-                             "instruction-issue bound: see profiles/README.md and profiles/r1/p_ncu_k_sweep_x_dc.txt"},
+                             "instruction-issue bound: see profiles/README.md and profiles/r2/e_ncu_cfg2_k_sweep_x_dc.txt. The device formats move fewer bytes "
+                             "than SURVEY 8(d) assumed (bit-packed masks, 4-byte field, phase 1 as bit strings), so frac is quoted on the smaller figure"},
         "cpu_baseline": cpu_base,
     }
     print(json.dumps(line))
