@@ -368,10 +368,14 @@ static int attach(ks_batch* b, void* comm, bool own, int world, int rank, int ma
   // every rank contributes max_local rows (ranks with fewer environments pad with NaN rows), so the local buffer is regrown
   double* local = nullptr;
   double* all = nullptr;
-  KS_CUDA(cudaMalloc(&local, sizeof(double) * 4 * max_local));
-  KS_CUDA(cudaMemset(local, 0xFF, sizeof(double) * 4 * max_local));
-  KS_CUDA(cudaMalloc(&all, sizeof(double) * 4 * max_local * world));
-  KS_CUDA(cudaMemset(all, 0xFF, sizeof(double) * 4 * max_local * world));
+  cudaError_t err = cudaMalloc(&local, sizeof(double) * 4 * max_local);
+  if (err == cudaSuccess) err = cudaMemset(local, 0xFF, sizeof(double) * 4 * max_local);
+  if (err == cudaSuccess) err = cudaMalloc(&all, sizeof(double) * 4 * max_local * world);
+  if (err == cudaSuccess) err = cudaMemset(all, 0xFF, sizeof(double) * 4 * max_local * world);
+  if (err != cudaSuccess) {
+    cudaFree(local), cudaFree(all);
+    return cuda_fail(err, "batch gather buffers");
+  }
   if (b->gathered_dev && b->gathered_dev != b->summary_dev) cudaFree(b->gathered_dev);
   cudaFree(b->summary_dev);
   b->summary_dev = local, b->gathered_dev = all;

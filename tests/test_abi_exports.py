@@ -52,6 +52,19 @@ def test_compute_fails_loudly_without_a_device(lib):
         api.DenseEsdf(api.EsdfConfig(nx=4, ny=4, nz=4))
 
 
+def test_batch_fails_loudly_without_a_device_and_partitions_on_the_host(lib):
+    """ks_batch_create has no CPU path either; ks_partition_envs is host code (the N > 1 launcher calls it before any GPU work)."""
+    from paper_2603_05493_b200 import api
+    assert [api.partition_envs(128, 8, r) for r in (0, 7)] == [(0, 16), (112, 128)]
+    assert [api.partition_envs(5, 3, r) for r in range(3)] == [(0, 2), (2, 4), (4, 5)]
+    with pytest.raises(ValueError, match="bad partition arguments"):
+        api.partition_envs(4, 2, 2)
+    if lib.ks_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(api.CudaError):
+        api.EnvBatch(2, api.make_tsdf_config(0.01), api.EsdfConfig(nx=4, ny=4, nz=4))
+
+
 def test_validation_messages_match_the_reference(lib):
     from paper_2603_05493_b200 import api
     cases = [
