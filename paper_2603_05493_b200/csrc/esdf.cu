@@ -88,7 +88,7 @@ struct EsdfView {
   uint16_t* near_z;  // [cells] x-fastest phase-1 result (banded-stack fallback only)
   // phase 1 of the divide-and-conquer path (aliases near_z): every column's seeds as a bit string along z
   uint32_t* zbits;   // [ny][nzw][nx] word w of column (x, y): bit b = cell z = 32w + b is a seed
-  uint32_t* zinfo;   // same layout: nearest seed z in the words below w | the words above w << 16 (0xFFFF: none)
+  uint32_t* zinfo;   // same layout: distance from the word to the nearest seed in the words below w | above w << 16 (k_flood_cols)
   int nzw;           // words per column
   uint32_t* yz;      // [cells] x-fastest phase-2 result  site_y | site_z << 16
   uint2* field;      // wide path: [cells] y-fastest: {site (x | y << 10 | z << 20), squared distance | sign << 31}
@@ -687,8 +687,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t v, int lane) {
 // words below and above.  Phase 2 resolves "nearest seed along z" from one word + one info word per
 // candidate, so the 2-byte-per-cell nearest-z field is never written or read.  The "seed has a sign table" plane
 // (gbits) is transposed alongside: phase 2 hands that bit on, and the x sweep needs no site decode where it is 0.
-// zinfo half = z (15 bits, 0x7FFF: none) | table bit << 15.
-constexpr uint32_t kZNone = 0x7FFFu;
+// zinfo half = distance (15 bits) | table bit << 15: the low half counts from the word's bit 0 down to the nearest seed in
+// the words below, the high half from its bit 31 up to the nearest seed in the words above; kZNone (farther than any
+// grid is long) when there is none, so "no seed at all" falls out of the minimum without a flag of its own.
+constexpr uint32_t kZNone = 0x4000u;
 __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
   pdl_enter();
   extern __shared__ uint32_t s_words[];  // [nzw][32] seeds, then [nzw][32] table bits
@@ -711,7 +713,7 @@ __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
     const uint32_t m = s_words[k * 32 + lane];
     if (m != 0) {
       const int b = 31 - __clz(static_cast<int>(m));
-      below = (32 * k + b) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
+      below = static_cast<uint32_t>(32 * w - (32 * k + b)) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
       break;
     }
   }
@@ -719,7 +721,7 @@ __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
     const uint32_t m = s_words[k * 32 + lane];
     if (m != 0) {
       const int b = __ffs(static_cast<int>(m)) - 1;
-      above = (32 * k + b) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
+      above = static_cast<uint32_t>((32 * k + b) - (32 * w + 31)) | ((s_tab[k * 32 + lane] >> b) & 1u) << 15;
       break;
     }
   }
@@ -1151,8 +1153,7 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
   {  // candidates: the nearest seed along z of every column (esdf.hpp:213-233; ties keep the lower z, strict '<' :229)
     const int zc = min(z, E.nz - 1);
     const int col = (zc >> 5) * nx + min(x, nx - 1), stride = E.nzw * nx;
-    const int zbase = zc & ~31, zb = zc & 31;
-    const uint32_t le = 0xFFFFFFFFu >> (31 - zb), ge = 0xFFFFFFFFu << zb;
+    const int zb = zc & 31;
     for (int yb = warp * kLoadBatch; yb < ny; yb += nwarps * kLoadBatch) {
       uint32_t wd[kLoadBatch], inf[kLoadBatch], tb[kLoadBatch];
 #pragma unroll
@@ -1164,21 +1165,20 @@ __global__ void __launch_bounds__(512) k_sweep_y_dc(EsdfView E, int warps_log2, 
 #pragma unroll
       for (int i = 0; i < kLoadBatch; ++i) {
         const int y = yb + i;
-        const uint32_t lo_m = wd[i] & le, hi_m = wd[i] & ge;
-        const int bb = 31 - __clz(static_cast<int>(lo_m)), ba = __ffs(static_cast<int>(hi_m)) - 1;
-        const uint32_t ib = inf[i] & 0xFFFFu, ia = inf[i] >> 16;
-        const int below = lo_m ? zbase + bb : static_cast<int>(ib & kZNone);
-        const int above = hi_m ? zbase + ba : static_cast<int>(ia & kZNone);
-        const bool has_b = below != static_cast<int>(kZNone), has_a = above != static_cast<int>(kZNone);
-        const int db = zc - below, da = above - zc;
-        const bool up = has_a && (!has_b || da < db);
+        // distance to the nearest seed at or below z / at or above z: inside the word by a bit scan, else the word's info
+        const uint32_t t_lo = wd[i] << (31 - zb), t_hi = wd[i] >> zb;  // bit z at position 31 / 0
+        const int db = t_lo ? __clz(static_cast<int>(t_lo)) : zb + static_cast<int>(inf[i] & 0x7FFFu);
+        const int da = t_hi ? __ffs(static_cast<int>(t_hi)) - 1 : (31 - zb) + static_cast<int>((inf[i] >> 16) & 0x7FFFu);
+        const bool up = da < db;  // a tie keeps the lower z (strict '<', esdf.hpp:229); up implies dz > 0
         const int dz = up ? da : db;
-        uint32_t pay = up && dz > 0 ? 1u : 0u;
+        uint32_t pay = up ? 1u : 0u;
         if constexpr (kPay == 2) {
-          const uint32_t fb = lo_m ? (tb[i] >> bb) & 1u : ib >> 15, fa = hi_m ? (tb[i] >> ba) & 1u : ia >> 15;
-          pay = pay << 1 | (up ? fa : fb);
+          const bool inword = up ? t_hi != 0 : t_lo != 0;
+          const int pos = up ? zb + da : zb - db;  // the chosen seed's bit inside the word (meaningless when it lies outside)
+          const uint32_t flag = inword ? (tb[i] >> (pos & 31)) & 1u : (up ? inf[i] >> 31 : (inf[i] >> 15) & 1u);
+          pay = pay << 1 | flag;
         }
-        const uint32_t g = (!(has_a || has_b) || !live) ? KY::pack(none_y, y, 0) : KY::pack(static_cast<uint32_t>(dz * dz), y, pay);
+        const uint32_t g = (dz >= static_cast<int>(kZNone) || !live) ? KY::pack(none_y, y, 0) : KY::pack(static_cast<uint32_t>(dz * dz), y, pay);
         if (y < ny) G[edt_dc::at(y, lane)] = g;
       }
     }
