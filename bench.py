@@ -587,10 +587,11 @@ def run_ours(args):
     dominant = max(kernel_stages, key=lambda s: stage_ms.get(s, 0.0))
     stage_bytes = {s: algorithmic_bytes(s, cells, pixels, K, max(live - K, 0), live, dcount) for s in kernel_stages}
     achieved = stage_bytes[dominant] / (stage_ms[dominant] * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_all = None, {}
     traffic_path = ROOT / "profiles" / "dram_traffic.json"
-    if traffic_path.exists():
-        traffic = json.loads(traffic_path.read_text()).get(args.workload, {}).get(dominant)
+    if traffic_path.exists():  # per-launch DRAM bytes from committed ncu captures of the same command (not measurable without ncu)
+        traffic_all = json.loads(traffic_path.read_text()).get(args.workload, {})
+        traffic = traffic_all.get(dominant)
     update_bytes = sum(stage_bytes[s] * (len(frames) if s in ("discover", "allocate", "integrate") else 1) for s in kernel_stages)
     survey_bytes = (len(frames) * 4.0 * (pixels / max(1, len(frames))) + 2 * 16 * 512 * K * len(frames) + 2 * 8 * 512 * max(live - K, 0)
                     + 30.0 * cells + 16384.0 * live + 20.0 * 2 * scene.capacity)
@@ -604,7 +605,7 @@ def run_ours(args):
         ms = stage_ms[name]
         gbs = stage_bytes.get(name, 0.0) / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
         stage_table.append({"stage": name, "ms": round(ms, 5), "algorithmic_bytes": stage_bytes.get(name, 0.0), "GB/s": round(gbs, 1),
-                            "frac_of_hbm_peak": round(gbs / peak, 4)})
+                            "frac_of_hbm_peak": round(gbs / peak, 4), "dram_traffic_bytes": traffic_all.get(name)})
     ms_per_step = total_ms / args.steps
     value = n_envs * cells * args.steps / (total_ms * 1e-3)
 
