@@ -56,6 +56,7 @@ struct EsdfView {
   double origin[3];
   double ve;
   float ratio;   // ve / tsdf voxel (fast-path sign probe)
+  int iprobe;    // 1: ve == tsdf voxel and every cell centre sits at the middle of its voxel -> the probe offset is an integer test (SignTable)
   int* vox;      // [kVoxRows][nx+ny+nz]: offsets {0, +ve/2, -ve/2, +ve, -ve} (esdf.hpp:106-108, :303)
   double* ctr;   // [nx+ny+nz]    cell centre coordinate per axis position (esdf.hpp:51-53)
   float* qsf;    // [nx+ny+nz]    fractional part of centre / tsdf voxel
@@ -897,11 +898,27 @@ struct SignTable {
   }
   __device__ __forceinline__ void set_site(int sx_, int sy_, int sz_, uint2 tab_) {
     sx = sx_, sy = sy_, sz = sz_, tab = tab_;
-    if (tab.x != 0) qx = qsf[sx], qy = qsf[E.nx + sy], qz = qsf[E.nx + E.ny + sz];
+    if (tab.x != 0 && !E.iprobe) qx = qsf[sx], qy = qsf[E.nx + sy], qz = qsf[E.nx + E.ny + sz];
   }
   // own: the cell's bit of the own-sign plane
   __device__ __forceinline__ bool negative(int x, bool own) const {
     const int dx = x - sx, dy = y - sy, dz = z - sz;
+    if (E.iprobe) {
+      // Grids in step (ve == v, cell centres at voxel centres): the probe site + ve * d / |d| leaves the site's voxel along
+      // an axis exactly when |d_a| / |d| > 1/2, i.e. 4 d_a^2 > |d|^2 -- integers.  Equality would need 3 a^2 = b^2 + c^2,
+      // which has no integer solution but 0, so the nearest the real quantity comes to the voxel face is 1 / (6 |d|^2)
+      // >= 8e-8 voxels: five orders of magnitude beyond what the reference's fp64 rounding (or the 1e-9 the centres may
+      // be off, checked at bind time) can move it.  Same voxel as esdf.hpp:303-304, no square root, no certificate.
+      if (tab.x != 0 && (dx | dy | dz) != 0) {
+        const int d2 = dx * dx + dy * dy + dz * dz;
+        int idx = 13;
+        if (4 * dx * dx > d2) idx += dx > 0 ? 1 : -1;
+        if (4 * dy * dy > d2) idx += dy > 0 ? 3 : -3;
+        if (4 * dz * dz > d2) idx += dz > 0 ? 9 : -9;
+        if ((tab.x >> idx) & 1u) return ((tab.y >> idx) & 1u) != 0;  // query_tsdf_geom has a value: its sign decides
+      }
+      return own;
+    }
     if (tab.x != 0 && (dx | dy | dz) != 0) {
       const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
       const float rinv = rsqrtf(fx * fx + fy * fy + fz * fz) * E.ratio;
@@ -1865,6 +1882,16 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
     bool in_step = voxe[0] >= 0;
     for (int i = 0; i < E.nx + 2; ++i) in_step = in_step && voxe[i] == i + voxe[0];
     E.xshift = in_step ? voxe[0] : -1;
+    {  // integer sign probe (SignTable::negative): same voxel size and every cell centre within 1e-9 voxels of its voxel's middle
+      bool centred = E.ve == T.voxel;
+      for (int a = 0; a < 3 && centred; ++a)
+        for (int k = 0; k < dims[a] && centred; ++k) {
+          const double q = (E.origin[a] + (k + 0.5) * E.ve) / T.voxel;
+          centred = std::fabs(q - std::floor(q) - 0.5) < 1e-9 && std::fabs(q) < 1e7;
+        }
+      E.iprobe = centred ? 1 : 0;
+      if (const char* v = std::getenv("KS_IPROBE")) E.iprobe = E.iprobe && std::atoi(v) != 0;
+    }
     if (ok && e->dc && !E.gtab) {  // the site tables (8 B per cell, touched at the seeds only) exist once the fast path is known to apply
       KS_CUDA(cudaMalloc(&E.gtab, static_cast<size_t>(E.cells) * sizeof(uint2)));
       KS_CUDA(cudaMalloc(&E.seedw, static_cast<size_t>(E.cells) * sizeof(int)));

@@ -154,13 +154,17 @@ def test_scene_scatter_mode_against_oracle(oracle_lib):
     _compare_scene(oracle_lib, scenes.small_scene(41, ratio=2.0, dims=(24, 20, 18)), seeding="scatter")
 
 
-@pytest.mark.parametrize("env", [{"KS_SWEEP": "stack"}, {"KS_SEED": "bricks"}, {"KS_SWEEP": "stack", "KS_SEED": "bricks"}],
-                         ids=["stack-sweeps", "brick-gather", "round-1-path"])
+@pytest.mark.parametrize("env", [{"KS_SWEEP": "stack"}, {"KS_SEED": "bricks"}, {"KS_SWEEP": "stack", "KS_SEED": "bricks"},
+                                 {"KS_IPROBE": "0"}, {"KS_XPAY": "0"}, {"KS_IPROBE": "0", "KS_XPAY": "0"}],
+                         ids=["stack-sweeps", "brick-gather", "round-1-path", "fp32-certified-probe", "payload-image-in-smem", "round-2a-x-sweep"])
 @pytest.mark.parametrize("name", ["small1", "ratio0.5-offset"])
 def test_fallback_kernels_against_oracle(oracle_lib, monkeypatch, env, name):
     """The library picks the divide-and-conquer sweeps / resampled seeding whenever they apply; the banded-stack
     sweeps (grids whose keys do not fit 32 bits) and the brick gather (ESDF coarser than the TSDF) are the
-    fallbacks.  The knobs are read when the ESDF is created / bound, so this forces them for one scene."""
+    fallbacks.  Likewise the x sweep variants: the integer sign probe applies when the grids are in step (KS_IPROBE=0:
+    the fp32-certified offset instead), the table bit rides in the candidate word when the keys have a bit to spare
+    (KS_XPAY=0: payload image staged in shared memory).  The knobs are read when the ESDF is created / bound, so this
+    forces them for one scene."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _compare_scene(oracle_lib, SCENES[name]())
