@@ -1309,7 +1309,8 @@ __global__ void __launch_bounds__(kBig ? 1024 : 512, kBig ? 1 : 2) k_sweep_x_dc(
   }
   for (int i = warp; i <= nx >> kTopShift; i += nwarps) Kt[edt_dc::at(i, lane)] = 0xFFFFFFFFu;
   if constexpr (kSigns == 3)
-    for (int i = threadIdx.x; i < nx + ny + E.nz; i += blockDim.x) s_qsf[i] = E.qsf[i];
+    if (!E.iprobe)  // the fp32 probe's per-axis fractions; the integer probe needs none
+      for (int i = threadIdx.x; i < nx + ny + E.nz; i += blockDim.x) s_qsf[i] = E.qsf[i];
   const int back = 1 - E.ctrl->front;
   mbar_wait(&s_bar, 0);
   __syncthreads();
