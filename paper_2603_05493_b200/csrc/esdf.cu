@@ -56,6 +56,7 @@ struct EsdfView {
   double origin[3];
   double ve;
   float ratio;   // ve / tsdf voxel (fast-path sign probe)
+  int tab_all;   // 1: the sweeps carry no table bit (y keys too wide): every site's table is read, so every seed needs one
   int iprobe;    // 1: ve == tsdf voxel and every cell centre sits at the middle of its voxel -> the probe offset is an integer test (SignTable)
   int* vox;      // [kVoxRows][nx+ny+nz]: offsets {0, +ve/2, -ve/2, +ve, -ve} (esdf.hpp:106-108, :303)
   double* ctr;   // [nx+ny+nz]    cell centre coordinate per axis position (esdf.hpp:51-53)
@@ -500,7 +501,9 @@ __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
     E.gbits[i] = near;
   }
   // seeds with no stamped block in reach resolve no sign probe: their table is all zero
-  for (uint32_t m = seed & ~near; m != 0; m &= m - 1) E.gtab[32 * xw + __ffs(static_cast<int>(m)) - 1 + E.nx * row] = make_uint2(0u, 0u);
+  // (only read when the y sweep's keys cannot carry the "site has a table" bit and every site counts as having one)
+  if (E.tab_all)
+    for (uint32_t m = seed & ~near; m != 0; m &= m - 1) E.gtab[32 * xw + __ffs(static_cast<int>(m)) - 1 + E.nx * row] = make_uint2(0u, 0u);
   // the others go on the work list of k_site_tables (one atomic per warp)
   const int mine = __popc(near);
   int before = mine;
@@ -2084,6 +2087,7 @@ static int esdf_init(ks_esdf* e, const ks_esdf_config* cfg) {
             dc_smem_bytes_x(E.nx, E.nx + E.ny + E.nz) <= 226 * 1024 && dc_smem_bytes_y(E.ny) <= 226 * 1024;
     e->pay_y = edt_dc::Keys<2>::fits(E.ny, gmax_y) ? 2 : 1;
     if (const char* v = std::getenv("KS_PAY_Y")) e->pay_y = std::atoi(v) == 1 ? 1 : e->pay_y;
+    E.tab_all = e->pay_y == 2 ? 0 : 1;
     if (const char* v = std::getenv("KS_SWEEP")) e->dc = e->dc && std::strcmp(v, "stack") != 0;
     e->none_y = KeysY::none_offset(E.ny, gmax_y);
     e->none_x = KeysX::none_offset(E.nx, gmax_x);
