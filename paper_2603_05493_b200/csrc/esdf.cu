@@ -83,6 +83,7 @@ struct EsdfView {
   uint32_t* xminus;    // [wpr] ... and the -ve/2 probe
   uint8_t* yzflags;    // [ny | nz] bit0 / bit1: the same for the y and z probes of that row
   int xshift;          // voxe[i] == i + xshift along x (cell and voxel grids in step), else -1
+  int yshift, zshift;  // the same along y and z
   int* seedw;          // compacted cell indices of the seeds whose sign table is not all zero (count in ctrl->seed_words)
   uint8_t* dirg;       // [dcount] 1 when a stamped block lies in the 3x3x3 blocks around this directory entry
   uint2* gtab;         // [cells] x-fastest, valid at the seeds: {has value, negative} of the geometry channel
@@ -465,6 +466,76 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_rows(EsdfView 
     }
     const uint32_t cw = __ballot_sync(0xFFFFFFFFu, c), ow = __ballot_sync(0xFFFFFFFFu, o), nw = __ballot_sync(0xFFFFFFFFu, n);
     if (lane == 0) out[w] = cw, out[plane + w] = ow, out[2 * plane + w] = nw;
+  }
+}
+
+// The same three planes when the grids are in step along all three axes (every BASELINE config): one warp per block row
+// and lz, i.e. the 8 voxel rows ly = 0 .. 7 that share a directory row and six digest words per block.  Step 1, lane <->
+// block: one directory read and six digest reads serve eight rows (k_resample_rows: one + two per row).  Step 2, lane <->
+// (row, word): a cell word is 32 consecutive bits of the row's byte string -- two aligned 4-byte reads and a funnel
+// shift -- with all 32 lanes busy (k_resample_rows: 13 of 32 for a 400-cell row).
+constexpr int kRowBytes = (kMaxDirX + 8 + 3) & ~3;
+__global__ void __launch_bounds__(kResampleWarps * 32) k_resample_blockrows(EsdfView E, TsdfView T) {
+  pdl_enter();
+  __shared__ __align__(4) uint8_t s_c[kResampleWarps][8][kRowBytes];  // surface bits, one byte per block
+  __shared__ __align__(4) uint8_t s_o[kResampleWarps][8][kRowBytes];  // own-sign bits
+  __shared__ __align__(4) uint8_t s_n[kResampleWarps][kRowBytes];     // stamped geometry within one block: 0xFF / 0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int item = blockIdx.x * kResampleWarps + warp;  // (directory-relative voxel z) * dn[1] + block y
+  if (item >= E.dn[1] * E.dn[2] * 8) return;
+  const int by = item % E.dn[1], vz = item / E.dn[1];
+  const int lz = vz & 7, bz = vz >> 3;
+  const int ey = E.ny + 2, ez = E.nz + 2;
+  const int zi = vz - E.zshift, yi0 = 8 * by - E.yshift;  // extended row indices of (ly = 0, this vz)
+  if (zi < 0 || zi >= ez || yi0 + 7 < 0 || yi0 >= ey) return;
+  const int drow = E.dn[0] * (by + E.dn[1] * bz);
+  const int padded = min(kRowBytes, (E.dn[0] + 8 + 3) & ~3);  // bytes step 2 may read: zero beyond the last block
+  bool any = false;
+  for (int b = lane; b < padded; b += 32) {
+    uint32_t sw[2] = {0u, 0u}, cw[4] = {0u, 0u, 0u, 0u};
+    uint8_t nb = 0;
+    if (b < E.dn[0]) {
+      const int pool = __ldg(E.dir + drow + b);
+      if (pool >= 0) {
+        const uint32_t* dg = T.digest + pool * kDigestWords;
+        sw[0] = __ldg(dg + 2 * lz), sw[1] = __ldg(dg + 2 * lz + 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cw[j] = __ldg(dg + kDigestComb + 4 * lz + j);
+      }
+      nb = E.dirg[drow + b] ? 0xFFu : 0u;
+    }
+#pragma unroll
+    for (int ly = 0; ly < 8; ++ly) {
+      const uint32_t pairs = (cw[ly >> 1] >> (16 * (ly & 1))) & 0xFFFFu;
+      uint32_t both = pairs & (pairs >> 1) & 0x5555u;  // bit 2k: voxel k has a value and it is negative
+      both = (both | both >> 1) & 0x3333u;
+      both = (both | both >> 2) & 0x0F0Fu;
+      s_c[warp][ly][b] = static_cast<uint8_t>(sw[ly >> 2] >> (8 * (ly & 3)));
+      s_o[warp][ly][b] = static_cast<uint8_t>((both | both >> 4) & 0xFFu);
+    }
+    s_n[warp][b] = nb;
+    any |= (sw[0] | sw[1] | cw[0] | cw[1] | cw[2] | cw[3] | nb) != 0;
+  }
+  any = __any_sync(0xFFFFFFFFu, any);
+  __syncwarp();
+  const size_t plane = static_cast<size_t>(E.wpr2) * ey * ez;
+  for (int p = lane; p < 8 * E.wpr2; p += 32) {
+    const int ly = p / E.wpr2, w = p - ly * E.wpr2;
+    const int yi = yi0 + ly;
+    if (yi < 0 || yi >= ey) continue;
+    uint32_t wc = 0u, wo = 0u, wn = 0u;
+    if (any) {
+      const int o = 32 * w + E.xshift;
+      const int at = (o >> 3) & ~3, sh = 8 * ((o >> 3) & 3) + (o & 7);
+      auto word = [&](const uint8_t* bytes) {
+        return __funnelshift_r(*reinterpret_cast<const uint32_t*>(bytes + at), *reinterpret_cast<const uint32_t*>(bytes + at + 4), sh);
+      };
+      const int rest = E.nx + 2 - 32 * w;
+      const uint32_t keep = rest < 32 ? (1u << rest) - 1u : 0xFFFFFFFFu;
+      wc = word(s_c[warp][ly]) & keep, wo = word(s_o[warp][ly]) & keep, wn = word(s_n[warp]) & keep;
+    }
+    uint32_t* out = E.cbits + static_cast<size_t>(zi * ey + yi) * E.wpr2 + w;
+    out[0] = wc, out[plane] = wo, out[2 * plane] = wn;
   }
 }
 
@@ -1788,6 +1859,7 @@ struct ks_esdf {
   int64_t build_nodes;
   bool resample_ok;        // the dilation identity of the resampled seeding holds for the bound TSDF voxel size
   bool dc;                 // sweeps by divide and conquer (keys fit 32 bits), else the banded stacks
+  bool resample_by_rows;   // KS_RESAMPLE=rows: the per-row resampling kernel even when the grids are in step
   int dc_wl_y, dc_wl_x;    // floor(log2(warps per tile)): slices a top-level window is cut into
   int dc_nw_y, dc_nw_x;    // warps per tile
   int pay_y;               // payload bits of the y keys: 2 = {seed above z, site has a sign table}, 1 = the first only
@@ -1886,6 +1958,16 @@ static int bind_tsdf(ks_esdf* e, const ks_tsdf* t) {
     bool in_step = voxe[0] >= 0;
     for (int i = 0; i < E.nx + 2; ++i) in_step = in_step && voxe[i] == i + voxe[0];
     E.xshift = in_step ? voxe[0] : -1;
+    {  // the same along y and z (k_resample_blockrows needs all three)
+      const int* vy = voxe.data() + E.nx + 2;
+      const int* vz = vy + E.ny + 2;
+      bool ys = vy[0] >= 0, zs = vz[0] >= 0;
+      for (int i = 0; i < E.ny + 2; ++i) ys = ys && vy[i] == i + vy[0];
+      for (int i = 0; i < E.nz + 2; ++i) zs = zs && vz[i] == i + vz[0];
+      E.yshift = ys ? vy[0] : -1, E.zshift = zs ? vz[0] : -1;
+      e->resample_by_rows = false;
+      if (const char* v = std::getenv("KS_RESAMPLE")) e->resample_by_rows = std::strcmp(v, "rows") == 0;
+    }
     {  // integer sign probe (SignTable::negative): same voxel size and every cell centre within 1e-9 voxels of its voxel's middle
       bool centred = E.ve == T.voxel;
       for (int a = 0; a < 3 && centred; ++a)
@@ -1945,7 +2027,10 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
     if (bits && fast_build(e)) {
       const int words = E.wpr * E.ny * E.nz;
       const int ext_rows = (E.ny + 2) * (E.nz + 2);
-      KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
+      if (E.xshift >= 0 && E.yshift >= 0 && E.zshift >= 0 && !e->resample_by_rows)
+        KS_LAUNCH(k_resample_blockrows, (E.dn[1] * E.dn[2] * 8 + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
+      else
+        KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
       if (e->profile_stages) {  // stage timing: everything in line
         KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));

@@ -155,8 +155,8 @@ def test_scene_scatter_mode_against_oracle(oracle_lib):
 
 
 @pytest.mark.parametrize("env", [{"KS_SWEEP": "stack"}, {"KS_SEED": "bricks"}, {"KS_SWEEP": "stack", "KS_SEED": "bricks"},
-                                 {"KS_IPROBE": "0"}, {"KS_XPAY": "0"}, {"KS_IPROBE": "0", "KS_XPAY": "0"}, {"KS_PAY_Y": "1"}],
-                         ids=["stack-sweeps", "brick-gather", "round-1-path", "fp32-certified-probe", "payload-image-in-smem", "round-2a-x-sweep", "y-keys-without-table-bit"])
+                                 {"KS_IPROBE": "0"}, {"KS_XPAY": "0"}, {"KS_IPROBE": "0", "KS_XPAY": "0"}, {"KS_PAY_Y": "1"}, {"KS_RESAMPLE": "rows"}],
+                         ids=["stack-sweeps", "brick-gather", "round-1-path", "fp32-certified-probe", "payload-image-in-smem", "round-2a-x-sweep", "y-keys-without-table-bit", "resample-row-by-row"])
 @pytest.mark.parametrize("name", ["small1", "ratio0.5-offset"])
 def test_fallback_kernels_against_oracle(oracle_lib, monkeypatch, env, name):
     """The library picks the divide-and-conquer sweeps / resampled seeding whenever they apply; the banded-stack
