@@ -131,7 +131,9 @@ KS_API int ks_tsdf_integrate_async(ks_tsdf* t);
 #define KS_MAX_FRAME_SLOTS 8
 KS_API int ks_tsdf_stage_frame_slot(ks_tsdf* t, int32_t slot, const ks_camera* cam, const float* depth_host);
 /* Zero-copy staging.  ks_tsdf_frame_buffer returns the pinned staging area of a slot (width*height floats,
- * owned by the handle, stable until a larger frame is requested): a producer that writes its pixels there and
+ * owned by the handle, stable until a larger frame is requested; once a graph was captured on the world's stream a
+ * larger frame gets NEW buffers and the old ones stay alive until ks_tsdf_destroy, so a graph captured earlier keeps
+ * reading the memory it was captured with -- re-capture after growing): a producer that writes its pixels there and
  * passes the same pointer to ks_tsdf_stage_frame_slot skips the staging copy.  ks_tsdf_integrate_depth does
  * the same for ANY page-locked depth_host (e.g. from ks_host_alloc): it is uploaded in place. */
 KS_API int ks_tsdf_frame_buffer(ks_tsdf* t, int32_t slot, int32_t width, int32_t height, float** out);

@@ -100,6 +100,11 @@ struct ks_tsdf {
     bool staged;
   } slots[KS_MAX_FRAME_SLOTS];
   OpLists lists;
+  // Buffers whose addresses are baked into kernel / copy nodes of graphs captured on this world's stream.  Once anything
+  // was captured, growing the op lists or a frame slot RETIRES the old buffers (freed with the handle) instead of freeing
+  // them: a graph captured earlier keeps running on the memory it was captured with (re-capture to use the new buffers).
+  bool ever_captured;
+  std::vector<void*> retired_dev, retired_host;
   int* d_flags;  // [capacity] recycle flags
   bool profile;
   cudaEvent_t ev[7];  // integrate: 0..3, stamp: 4..6
@@ -117,12 +122,18 @@ void tsdf_reader_enqueued(const ks_tsdf* t_const, cudaStream_t reader) {
   if (cudaEventRecord(t->ev_reader, reader) == cudaSuccess) t->reader_pending = true;
   else cudaGetLastError();
 }
-static void wait_for_readers(ks_tsdf* t) {
-  if (!t->reader_pending) return;
-  t->reader_pending = false;
+// every enqueue passes here: remember that a graph now holds this world's buffer addresses (see ks_tsdf::ever_captured)
+static bool note_capture(ks_tsdf* t) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(t->stream, &cap);
-  if (cap != cudaStreamCaptureStatusNone) return;  // inside a capture the caller orders the two handles (one stream)
+  if (cap != cudaStreamCaptureStatusNone) t->ever_captured = true;
+  return cap != cudaStreamCaptureStatusNone;
+}
+static void wait_for_readers(ks_tsdf* t) {
+  const bool in_capture = note_capture(t);
+  if (!t->reader_pending) return;
+  t->reader_pending = false;
+  if (in_capture) return;  // inside a capture the caller orders the two handles (one stream)
   if (cudaStreamWaitEvent(t->stream, t->ev_reader, 0) != cudaSuccess) cudaGetLastError();
 }
 
@@ -1147,6 +1158,17 @@ static bool capturing(cudaStream_t stream) {
   cudaStreamIsCapturing(stream, &cap);
   return cap != cudaStreamCaptureStatusNone;
 }
+// free now, or -- when a captured graph may still hold the address -- with the handle
+static void release_dev(ks_tsdf* t, void* p) {
+  if (!p) return;
+  if (t->ever_captured) t->retired_dev.push_back(p);
+  else cudaFree(p);
+}
+static void release_host(ks_tsdf* t, void* p) {
+  if (!p) return;
+  if (t->ever_captured) t->retired_host.push_back(p);
+  else cudaFreeHost(p);
+}
 
 static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
   const size_t want = std::max<size_t>(pixels * samples, 2 * static_cast<size_t>(t->cfg.capacity) + 1);
@@ -1155,7 +1177,11 @@ static int ensure_lists(ks_tsdf* t, size_t pixels, int samples) {
     return fail(KS_ERR_INVALID, "tsdf: frame larger than the staged buffers; stage a frame of this size before capture");
   KS_CUDA(cudaStreamSynchronize(t->stream));
   OpLists& L = t->lists;
-  cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.sorted_key), cudaFree(L.sorted_prim), cudaFree(L.fset), cudaFree(L.fmask);
+  for (void* old : {static_cast<void*>(L.key), static_cast<void*>(L.pool), static_cast<void*>(L.slot), static_cast<void*>(L.fresh_idx),
+                    static_cast<void*>(L.fresh_rank), static_cast<void*>(L.rank_key), static_cast<void*>(L.sorted_key),
+                    static_cast<void*>(L.sorted_prim), static_cast<void*>(L.fset), static_cast<void*>(L.fmask)})
+    release_dev(t, old);
+  L = OpLists{};
   L.cap = static_cast<int>(want);
   KS_CUDA(cudaMalloc(&L.key, want * sizeof(uint64_t)));
   KS_CUDA(cudaMalloc(&L.pool, want * sizeof(int)));
@@ -1187,8 +1213,15 @@ static int ensure_slot(ks_tsdf* t, int slot, size_t pixels) {
     KS_CUDA(cudaMalloc(&S.d_frame, sizeof(FrameParams)));
   }
   if (S.depth_cap < pixels) {
-    if (S.h_depth) cudaFreeHost(S.h_depth);
-    if (S.d_depth) cudaFree(S.d_depth);
+    if (t->ever_captured && S.depth_cap > 0) {  // the camera parameters a captured graph uploads stay with its pixels
+      release_host(t, S.h_frame);
+      release_dev(t, S.d_frame);
+      S.h_frame = nullptr, S.d_frame = nullptr;
+      KS_CUDA(cudaMallocHost(&S.h_frame, sizeof(FrameParams)));
+      KS_CUDA(cudaMalloc(&S.d_frame, sizeof(FrameParams)));
+    }
+    release_host(t, S.h_depth);
+    release_dev(t, S.d_depth);
     S.h_depth = nullptr, S.d_depth = nullptr;
     KS_CUDA(cudaMallocHost(&S.h_depth, pixels * sizeof(float)));
     KS_CUDA(cudaMalloc(&S.d_depth, pixels * sizeof(float)));
@@ -1448,6 +1481,8 @@ void ks_tsdf_destroy(ks_tsdf* t) {
   cudaFree(V.sumwt), cudaFree(V.geom), cudaFree(V.digest), cudaFree(V.pool_geom), cudaFree(V.ctrl), cudaFree(t->d_flags);
   OpLists& L = t->lists;
   cudaFree(L.key), cudaFree(L.pool), cudaFree(L.slot), cudaFree(L.fresh_idx), cudaFree(L.fresh_rank), cudaFree(L.rank_key), cudaFree(L.sorted_key), cudaFree(L.sorted_prim), cudaFree(L.fset), cudaFree(L.fmask);
+  for (void* p : t->retired_dev) cudaFree(p);
+  for (void* p : t->retired_host) cudaFreeHost(p);
   cudaFree(t->query_scratch);
   cudaFreeHost(t->h_ctrl);
   cudaFreeHost(t->h_verdict);
@@ -1551,6 +1586,7 @@ int ks_tsdf_upload_frame_slot_async(ks_tsdf* t, int32_t slot) {
   if (!t || slot < 0 || slot >= KS_MAX_FRAME_SLOTS || !t->slots[slot].staged) return fail(KS_ERR_INVALID, "tsdf: no frame staged");
   ks_tsdf::FrameSlot& S = t->slots[slot];
   const size_t pixels = static_cast<size_t>(S.h_frame->width) * S.h_frame->height;
+  note_capture(t);
   KS_CUDA(cudaMemcpyAsync(S.d_frame, S.h_frame, sizeof(FrameParams), cudaMemcpyHostToDevice, t->stream));
   KS_CUDA(cudaMemcpyAsync(S.d_depth, S.h_depth, pixels * sizeof(float), cudaMemcpyHostToDevice, t->stream));
   return KS_OK;

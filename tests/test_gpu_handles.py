@@ -85,3 +85,43 @@ def test_async_build_and_world_updates_on_separate_streams(oracle_lib):
         assert np.array_equal(site, fields[-1][0]) and np.array_equal(dist, fields[-1][1]), k
     tsdf.sync()
     assert_world_parity(tsdf, cpu)
+
+
+def test_graph_captured_before_a_larger_frame_keeps_its_buffers(oracle_lib):
+    """A graph captured with a small frame stays valid after a larger frame grew the staging slot and the op lists:
+    the old buffers are retired, not freed, so replaying the old graph integrates the OLD frame again (the memory it
+    was captured with) -- no use after free, and the world equals the oracle's for that sequence of frames."""
+    import ctypes as C
+    small = scenes.small_scene(71, width=48, height=36, n_cuboids=0, n_spheres=0)
+    large = scenes.small_scene(72, width=160, height=120, n_cuboids=0, n_spheres=0)
+    lib = api.load_library()
+    stream = C.c_void_p()
+    assert lib.ks_stream_create(C.byref(stream)) == 0
+    cfg = api.make_tsdf_config(small.tsdf_voxel)
+    cfg.capacity = 8192
+    t = api.make_tsdf(cfg, stream.value)
+    fs, fl = small.frames[0], large.frames[0]
+    t.stage_frame(frame_of(fs))
+    t.upload_frame_async()
+    t.integrate_async()
+    t.sync()
+    g = api.Graph(stream.value)
+    with g:
+        t.upload_frame_async()
+        t.integrate_async()
+    g.launch()
+    t.sync()
+    t.stage_frame(frame_of(fl))  # 11x the pixels: slot and op lists grow
+    t.upload_frame_async()
+    t.integrate_async()
+    rep = t.sync()
+    assert rep.status == 0
+    for _ in range(2):
+        g.launch()  # the old graph: the small frame once more, from the retired buffers
+    rep = t.sync()
+    assert rep.status == 0
+    cpu = oracle_lib.make_tsdf(small.tsdf_voxel, capacity=8192)
+    for f in (fs, fs, fl, fs, fs):
+        cpu.integrate_depth(f.depth, f.width, f.height, f.intr, f.R, f.t)
+    assert assert_world_parity(t, cpu)
+    g.close()
