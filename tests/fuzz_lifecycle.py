@@ -18,7 +18,7 @@ for p in (str(ROOT), str(ROOT / "tests")):
 
 import cpu_checkers  # noqa: E402
 from paper_2603_05493_b200 import api, scenes  # noqa: E402
-from parity_util import assert_world_parity  # noqa: E402
+from parity_util import assert_world_parity, esdf_config, same_bits  # noqa: E402
 
 
 def both(gpu_call, cpu_call, what):
@@ -37,7 +37,7 @@ def both(gpu_call, cpu_call, what):
     return got
 
 
-def one_world(oracle, rng):
+def one_world(oracle, rng, esdf_every=0.5):
     sc = scenes.small_scene(int(rng.randint(1, 10**6)), dims=(24, 20, 18), n_cuboids=0, n_spheres=0)
     f = sc.frames[0]
     capacity = int(rng.choice([60, 150, 400, 2000]))
@@ -48,6 +48,9 @@ def one_world(oracle, rng):
     cpu = oracle.make_tsdf(sc.tsdf_voxel, capacity=capacity, weight_threshold=wt, alpha_time=alpha)
     steps = 0
     t = f.t.copy()
+    # ONE DenseEsdf for the world's whole life, rebuilt into after some of the operations: its directory, planes, site
+    # tables, double-buffered field and private graph must follow every allocation / recycling / stamp
+    esdf = api.DenseEsdf(esdf_config(sc)) if esdf_every else None
     for _ in range(int(rng.randint(4, 12))):
         op = rng.choice(["integrate", "integrate", "sphere", "cuboid", "mesh", "decay", "recycle"])
         if op == "integrate":
@@ -79,6 +82,12 @@ def one_world(oracle, rng):
         rep = tsdf.sync()
         assert rep.live_blocks == cpu.allocated_block_count() and rep.next_fresh == cpu.next_fresh(), op
         assert np.array_equal(tsdf.free_list(), cpu.free_list()), op
+        if esdf is not None and rng.random_sample() < esdf_every:
+            api.build_esdf(tsdf, esdf.config, esdf)
+            site, dist, _ = esdf.download(d2=False)
+            mask0, has0, site0, dist0 = cpu.build_esdf(sc.esdf_origin, sc.esdf_dims, sc.esdf_voxel)
+            assert esdf.has_sites == has0 and int(esdf.report().seed_count) == int(mask0.sum()), op
+            assert np.array_equal(site, site0) and same_bits(dist, dist0), f"ESDF rebuilt after {op} differs"
         steps += 1
     return steps
 
