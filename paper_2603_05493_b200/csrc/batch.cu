@@ -325,15 +325,26 @@ int64_t ks_batch_graph_kernels(const ks_batch* b) { return !b ? 0 : b->exec[0] ?
 
 int ks_batch_sync(ks_batch* b, ks_tsdf_report* reports, ks_esdf_report* esdf_reports, double* summaries_host) {
   if (!b) return fail(KS_ERR_INVALID, "null batch");
-  KS_CUDA(cudaStreamSynchronize(b->main));
+  // every environment's control blocks are requested first (each on its own lane), then the lanes are waited for once:
+  // one round trip for the whole batch instead of two per environment
+  if (b->lanes > 1) {  // a replayed update ran on the batch stream: the lanes' copies must come after it
+    KS_CUDA(cudaEventRecord(b->fork, b->main));
+    for (int l = 1; l < b->lanes; ++l) KS_CUDA(cudaStreamWaitEvent(b->lane[l], b->fork, 0));
+  }
+  for (int i = 0; i < b->n; ++i) {
+    int rc = tsdf_report_enqueue(b->tsdf[i]);
+    if (rc == KS_OK) rc = esdf_report_enqueue(b->esdf[i]);
+    if (rc != KS_OK) return rc;
+  }
+  for (cudaStream_t lane : b->lane) KS_CUDA(cudaStreamSynchronize(lane));
   int first = KS_OK;
   std::string why;
   for (int i = 0; i < b->n; ++i) {
     ks_tsdf_report r;
     ks_esdf_report er;
-    int rc = ks_tsdf_sync(b->tsdf[i], &r);
+    int rc = tsdf_report_collect(b->tsdf[i], &r);
     if (rc != KS_OK && first == KS_OK) first = rc, why = "environment " + std::to_string(b->first_env + i) + ": " + ks_last_error();
-    rc = ks_esdf_sync(b->esdf[i], &er);
+    rc = esdf_report_collect(b->esdf[i], &er);
     if (rc != KS_OK && first == KS_OK) first = rc, why = "environment " + std::to_string(b->first_env + i) + ": " + ks_last_error();
     if (reports) reports[i] = r;
     if (esdf_reports) esdf_reports[i] = er;

@@ -183,5 +183,11 @@ const TsdfView& tsdf_view(const ks_tsdf* t);
 cudaStream_t tsdf_stream(const ks_tsdf* t);
 uint64_t tsdf_uid(const ks_tsdf* t);  // unique per created handle (a recycled address is not the same world)
 void tsdf_reader_enqueued(const ks_tsdf* t, cudaStream_t reader);  // an ESDF build on another stream now reads this world
+// ks_tsdf_sync / ks_esdf_sync in two halves, so that a batch reads every environment's control block back with ONE wait:
+// enqueue the copy on the handle's stream; after that stream has been synchronised, turn the copy into the report
+int tsdf_report_enqueue(ks_tsdf* t);
+int tsdf_report_collect(ks_tsdf* t, ks_tsdf_report* report);
+int esdf_report_enqueue(ks_esdf* e);
+int esdf_report_collect(ks_esdf* e, ks_esdf_report* report);
 
 }  // namespace ksb

@@ -2417,10 +2417,13 @@ int ks_esdf_stage_ms(ks_esdf* e, float out[6]) {
   return KS_OK;
 }
 
-int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {
-  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+}  // extern "C"
+namespace ksb {
+int esdf_report_enqueue(ks_esdf* e) {
   KS_CUDA(cudaMemcpyAsync(e->h_ctrl, e->view.ctrl, sizeof(EsdfCtrl), cudaMemcpyDeviceToHost, e->stream));
-  KS_CUDA(cudaStreamSynchronize(e->stream));
+  return KS_OK;
+}
+int esdf_report_collect(ks_esdf* e, ks_esdf_report* report) {
   if (report) {
     report->status = KS_OK;
     report->has_sites = e->h_ctrl->seed_count > 0;
@@ -2428,6 +2431,16 @@ int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {
     report->seed_count = static_cast<int64_t>(e->h_ctrl->seed_count);
   }
   return KS_OK;
+}
+}  // namespace ksb
+extern "C" {
+
+int ks_esdf_sync(ks_esdf* e, ks_esdf_report* report) {
+  if (!e) return fail(KS_ERR_INVALID, "null esdf");
+  const int rc = esdf_report_enqueue(e);
+  if (rc != KS_OK) return rc;
+  KS_CUDA(cudaStreamSynchronize(e->stream));
+  return esdf_report_collect(e, report);
 }
 
 int ks_esdf_last_report(const ks_esdf* e, ks_esdf_report* report) {

@@ -1625,10 +1625,26 @@ int ks_tsdf_stage_frame(ks_tsdf* t, const ks_camera* cam, const float* depth_hos
 int ks_tsdf_upload_frame_async(ks_tsdf* t) { return ks_tsdf_upload_frame_slot_async(t, 0); }
 int ks_tsdf_integrate_async(ks_tsdf* t) { return ks_tsdf_integrate_slot_async(t, 0); }
 
+}  // extern "C"
+namespace ksb {
+int tsdf_report_enqueue(ks_tsdf* t) {
+  KS_CUDA(cudaMemcpyAsync(t->h_ctrl, t->view.ctrl, sizeof(TsdfCtrl), cudaMemcpyDeviceToHost, t->stream));
+  return KS_OK;
+}
+}  // namespace ksb
+extern "C" {
+
 int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
   if (!t) return fail(KS_ERR_INVALID, "null tsdf");
-  KS_CUDA(cudaMemcpyAsync(t->h_ctrl, t->view.ctrl, sizeof(TsdfCtrl), cudaMemcpyDeviceToHost, t->stream));
+  const int rc = tsdf_report_enqueue(t);
+  if (rc != KS_OK) return rc;
   KS_CUDA(cudaStreamSynchronize(t->stream));
+  return tsdf_report_collect(t, report);
+}
+
+}  // extern "C"
+namespace ksb {
+int tsdf_report_collect(ks_tsdf* t, ks_tsdf_report* report) {
   const TsdfCtrl c = *t->h_ctrl;
   if (c.err != 0) {  // errors are sticky until collected
     KS_CUDA(cudaMemsetAsync(&t->view.ctrl->err, 0, sizeof(int), t->stream));
@@ -1649,6 +1665,8 @@ int ks_tsdf_sync(ks_tsdf* t, ks_tsdf_report* report) {
   }
   return report_status(c);
 }
+}  // namespace ksb
+extern "C" {
 
 int ks_tsdf_integrate_depth(ks_tsdf* t, const ks_camera* cam, const float* depth_host, int32_t* blocks_touched) {
   if (!t) return fail(KS_ERR_INVALID, "null argument");

@@ -537,6 +537,7 @@ def test_probe_summary_matches_the_batched_query():
         want = api.query(e, pts).distance
         d_pts = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
         out = torch.full((4,), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()  # torch fills on ITS stream; the summary kernel runs on the handle's
         near = 0.03
         api._check(e.lib.ks_esdf_probe_summary_device_async(e.h, C.c_void_p(d_pts.data_ptr()), n, near, 7.0, C.c_void_p(out.data_ptr())))
         e.report()  # waits for the handle's stream
