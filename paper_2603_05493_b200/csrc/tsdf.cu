@@ -183,32 +183,22 @@ __device__ __forceinline__ uint32_t voxel_bits(double sum, double wt, double geo
   return bits;
 }
 
-__device__ __forceinline__ uint32_t spread16(uint32_t v) {  // bit i -> bit 2i
-  v &= 0xFFFFu;
-  v = (v | (v << 8)) & 0x00FF00FFu;
-  v = (v | (v << 4)) & 0x0F0F0F0Fu;
-  v = (v | (v << 2)) & 0x33333333u;
-  v = (v | (v << 1)) & 0x55555555u;
-  return v;
-}
-// One warp = 32 consecutive voxels = one surface word and two words of each 2-bit pair plane.
+// One warp = 32 consecutive voxels = one surface word and two words of each 2-bit pair plane.  A pair word interleaves
+// {has value, negative} of 16 voxels: lane j fetches the predicate bits of voxel (j >> 1) of its half and votes with the
+// bit it stands for (even lanes: has value, odd lanes: negative) -- the ballot IS the interleaved word.
 __device__ __forceinline__ void store_digest(uint32_t* digest, int pool, int tid, uint32_t bits) {
   const int word = tid >> 5, lane = tid & 31;
   const uint32_t surf = __ballot_sync(0xFFFFFFFFu, (bits >> kSurface) & 1u);
-  const uint32_t gv = __ballot_sync(0xFFFFFFFFu, (bits >> kGeomValid) & 1u);
-  const uint32_t gn = __ballot_sync(0xFFFFFFFFu, (bits >> kGeomNeg) & 1u);
-  const uint32_t cv = __ballot_sync(0xFFFFFFFFu, (bits >> kCombValid) & 1u);
-  const uint32_t cn = __ballot_sync(0xFFFFFFFFu, (bits >> kCombNeg) & 1u);
+  const uint32_t lo = __shfl_sync(0xFFFFFFFFu, bits, lane >> 1), hi = __shfl_sync(0xFFFFFFFFu, bits, 16 + (lane >> 1));
+  const int odd = lane & 1;
+  const uint32_t g0 = __ballot_sync(0xFFFFFFFFu, (lo >> (kGeomValid + odd)) & 1u), g1 = __ballot_sync(0xFFFFFFFFu, (hi >> (kGeomValid + odd)) & 1u);
+  const uint32_t c0 = __ballot_sync(0xFFFFFFFFu, (lo >> (kCombValid + odd)) & 1u), c1 = __ballot_sync(0xFFFFFFFFu, (hi >> (kCombValid + odd)) & 1u);
   uint32_t* d = digest + static_cast<size_t>(pool) * kDigestWords;
   if (lane == 0) d[word] = surf;
-  if (lane == 1 || lane == 2) {
-    const int half = lane - 1;
-    d[kDigestGeom + 2 * word + half] = spread16(gv >> (16 * half)) | (spread16(gn >> (16 * half)) << 1);
-  }
-  if (lane == 3 || lane == 4) {
-    const int half = lane - 3;
-    d[kDigestComb + 2 * word + half] = spread16(cv >> (16 * half)) | (spread16(cn >> (16 * half)) << 1);
-  }
+  if (lane == 1) d[kDigestGeom + 2 * word] = g0;
+  if (lane == 2) d[kDigestGeom + 2 * word + 1] = g1;
+  if (lane == 3) d[kDigestComb + 2 * word] = c0;
+  if (lane == 4) d[kDigestComb + 2 * word + 1] = c1;
 }
 
 __device__ __forceinline__ bool op_blocked(const TsdfView& T) {
