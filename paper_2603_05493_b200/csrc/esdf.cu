@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_blockrows(Esdf
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int item = blockIdx.x * kResampleWarps + warp;  // (directory-relative voxel z) * dn[1] + block y
   if (item >= E.dn[1] * E.dn[2] * 8) return;
-  const int by = item % E.dn[1], vz = item / E.dn[1];
+  const int vz = __float2int_rz((static_cast<float>(item) + 0.5f) * (1.0f / static_cast<float>(E.dn[1]))), by = item - vz * E.dn[1];  // item < 2^17: exact
   const int lz = vz & 7, bz = vz >> 3;
   const int ey = E.ny + 2, ez = E.nz + 2;
   const int zi = vz - E.zshift, yi0 = 8 * by - E.yshift;  // extended row indices of (ly = 0, this vz)
@@ -519,8 +519,9 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_blockrows(Esdf
   any = __any_sync(0xFFFFFFFFu, any);
   __syncwarp();
   const size_t plane = static_cast<size_t>(E.wpr2) * ey * ez;
+  const float rcp_wpr2 = 1.0f / static_cast<float>(E.wpr2);
   for (int p = lane; p < 8 * E.wpr2; p += 32) {
-    const int ly = p / E.wpr2, w = p - ly * E.wpr2;
+    const int ly = __float2int_rz((static_cast<float>(p) + 0.5f) * rcp_wpr2), w = p - ly * E.wpr2;
     const int yi = yi0 + ly;
     if (yi < 0 || yi >= ey) continue;
     uint32_t wc = 0u, wo = 0u, wn = 0u;
@@ -542,14 +543,17 @@ __global__ void __launch_bounds__(kResampleWarps * 32) k_resample_blockrows(Esdf
 // one thread per word of the seed plane
 __global__ void __launch_bounds__(256) k_seed_dilate(EsdfView E) {
   pdl_enter();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // grid = (words of a z slice / 256, nz): the slice index splits into (xw, y) by a float reciprocal (exact: the
+  // quotient is never closer than 1 / (2 wpr) >= 0.015 to an integer, the product is off by < 1e-2 for < 2^15 words)
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, z = blockIdx.y;
+  const int slice = E.wpr * E.ny;
   const int lane = threadIdx.x & 31;
-  const int words = E.wpr * E.ny * E.nz;
   uint32_t seed = 0, near = 0;
   int row = 0, xw = 0;
-  if (i < words) {
-    xw = i % E.wpr, row = i / E.wpr;
-    const int y = row % E.ny, z = row / E.ny;
+  const int i = z * slice + j;
+  if (j < slice) {
+    const int y = __float2int_rz((static_cast<float>(j) + 0.5f) * (1.0f / static_cast<float>(E.wpr)));
+    xw = j - y * E.wpr, row = z * E.ny + y;
     const int ey = E.ny + 2;
     auto ext = [&](const uint32_t* plane, int yy, int zz) -> uint64_t {  // extended bits 32xw .. 32xw+63 of row (yy, zz)
       const uint32_t* r = plane + ((zz + 1) * ey + (yy + 1)) * E.wpr2 + xw;
@@ -771,7 +775,7 @@ __global__ void __launch_bounds__(1024) k_flood_cols(EsdfView E) {
   extern __shared__ uint32_t s_words[];  // [nzw][32] seeds, then [nzw][32] table bits
   uint32_t* s_tab = s_words + E.nzw * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int xw = blockIdx.x % E.wpr, y = blockIdx.x / E.wpr;
+  const int xw = blockIdx.x, y = blockIdx.y;  // grid = (words per row, ny): no division
   const int x = xw * 32 + lane;
   {
     const int z = 32 * w + lane;
@@ -2031,7 +2035,7 @@ static int seed_async(ks_esdf* e, const ks_tsdf* t, int mode, bool bits) {
         KS_LAUNCH(k_resample_blockrows, (E.dn[1] * E.dn[2] * 8 + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
       else
         KS_LAUNCH(k_resample_rows, (ext_rows + kResampleWarps - 1) / kResampleWarps, kResampleWarps * 32, 0, e->stream, E, tsdf_view(t));
-      KS_LAUNCH(k_seed_dilate, (words + 255) / 256, 256, 0, e->stream, E);
+      KS_LAUNCH(k_seed_dilate, dim3((E.wpr * E.ny + 255) / 256, E.nz), 256, 0, e->stream, E);
       if (e->profile_stages) {  // stage timing: everything in line
         KS_LAUNCH(k_site_tables, 4 * kSmCount, 256, 0, e->stream, E, tsdf_view(t));
       } else {
@@ -2064,7 +2068,7 @@ static int propagate_async(ks_esdf* e, bool bits, const ks_tsdf* t) {
   (void)plane;
   if (e->dc) {
     if (!bits) KS_LAUNCH(k_pack_mask, (E.wpr * E.ny * E.nz + 7) / 8, 256, 0, e->stream, E);  // the reference's byte mask -> bit plane
-    KS_LAUNCH(k_flood_cols, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 2 * 32 * sizeof(uint32_t), e->stream, E);
+    KS_LAUNCH(k_flood_cols, dim3(E.wpr, E.ny), 32 * nwords, static_cast<size_t>(nwords) * 2 * 32 * sizeof(uint32_t), e->stream, E);
   } else if (bits) KS_LAUNCH(k_flood_z_chunks, E.wpr * E.ny, 32 * nwords, static_cast<size_t>(nwords) * 32 * sizeof(uint32_t), e->stream, E);
   else KS_LAUNCH(k_flood_z<false>, fgrid, kFloodWarps * 32, fsmem, e->stream, E);
   if (e->profile_stages) cudaEventRecord(e->ev[3], e->stream);
